@@ -1,0 +1,172 @@
+/* include/nlsp_gpu.h — C-ABI of the B200 (sm_100a) two-level PCG library
+ * (paper_2601_20174_b200/libnlsp_gpu.so).
+ *
+ * This is the drop-in boundary for the reference's solver/preconditioner
+ * interface (/root/reference/proj/include/nlsp/, header-only C++). Every entry
+ * point names the reference symbol it replaces. Plain pointers and sizes only;
+ * host pointers are borrowed for the duration of the call, device buffers are
+ * owned by the opaque handles. One context per host thread; handles other than
+ * the context are immutable after creation and may be shared read-only between
+ * contexts on the same device (the reference: objects immutable after
+ * construction).
+ *
+ * Errors: the reference throws (errors.hpp:10-49); here every call returns an
+ * nlsp_status and leaves a message in nlsp_last_error(ctx). include/nlsp_gpu.hpp
+ * maps the codes back onto the nlsp:: exception types.
+ *
+ * There is no CPU fallback: without a usable sm_100 device every compute entry
+ * point returns NLSP_E_CUDA.
+ */
+#ifndef NLSP_GPU_H
+#define NLSP_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    NLSP_OK = 0,
+    NLSP_E_VALIDATION = 1,     /* nlsp::ValidationError (CLI exit 1)           */
+    NLSP_E_NUMERIC = 2,        /* nlsp::NumericError                           */
+    NLSP_E_NOT_SPD = 3,        /* nlsp::NotSpdError                            */
+    NLSP_E_RANK_DEFICIENT = 4, /* nlsp::RankDeficiencyError                    */
+    NLSP_E_CONVERGENCE = 5,    /* nlsp::ConvergenceError                       */
+    NLSP_E_CUDA = 6,           /* device missing / CUDA failure                */
+    NLSP_E_OOM = 7             /* device allocation failed                     */
+} nlsp_status;
+
+typedef enum {
+    NLSP_PRECOND_IDENTITY = 0, /* IdentityPreconditioner, two_level.hpp:103-106 */
+    NLSP_PRECOND_JACOBI = 1,   /* JacobiPreconditioner, two_level.hpp:107-118   */
+    NLSP_PRECOND_TWOLEVEL = 2  /* TwoLevelPreconditioner, two_level.hpp:22-89   */
+} nlsp_precond_kind;
+
+typedef struct nlsp_ctx nlsp_ctx;
+typedef struct nlsp_csr nlsp_csr;
+typedef struct nlsp_dense nlsp_dense;
+typedef struct nlsp_twolevel nlsp_twolevel;
+
+/* Mirrors SolveReport (two_level.hpp:121-132); the residual history is
+ * returned through the separate residual_history argument of nlsp_pcg. */
+typedef struct {
+    uint64_t iterations;           /* completed x/r updates                          */
+    int32_t converged;             /* recurrence ||r||/||b|| < delta reached         */
+    int32_t precond_kind;          /* nlsp_precond_kind                              */
+    double true_relative_residual; /* ||b - A x|| / ||b|| recomputed at exit         */
+    double final_relative_residual;/* last recurrence entry (history back())         */
+    double solve_ms;               /* device time of the solve (CUDA events)         */
+    double total_ms;               /* solve incl. host<->device copies of b, x      */
+    uint64_t coarse_dim;           /* k for the two-level preconditioner, else 0     */
+    uint64_t kernel_launches;      /* this library's kernels launched by the solve   */
+    uint64_t h2d_bytes;            /* host->device bytes copied by the call          */
+    uint64_t d2h_bytes;            /* device->host bytes copied by the call          */
+} nlsp_solve_report;
+
+/* ------------------------------------------------------------ context ---- */
+nlsp_status nlsp_ctx_create(int device, nlsp_ctx** out);
+void nlsp_ctx_destroy(nlsp_ctx* ctx);
+const char* nlsp_last_error(const nlsp_ctx* ctx);
+/* the cudaStream_t every call of this context is ordered on */
+void* nlsp_ctx_stream(nlsp_ctx* ctx);
+nlsp_status nlsp_ctx_synchronize(nlsp_ctx* ctx);
+const char* nlsp_version(void);
+/* number of kernels this library has launched on ctx since creation */
+uint64_t nlsp_ctx_kernel_launches(const nlsp_ctx* ctx);
+
+/* ---------------------------------------------------------------- CSR ---- */
+/* SparseCsrMatrix (sparse.hpp:19-113): size_t row_ptr/col_idx, fp64 values;
+ * columns sorted, no duplicates. Stored on the device with int32 indices;
+ * NLSP_E_VALIDATION for nnz >= 2^31, n >= 2^31, or a violated invariant. */
+nlsp_status nlsp_csr_upload(nlsp_ctx* ctx, uint64_t n, uint64_t nnz, const uint64_t* row_ptr,
+                            const uint64_t* col_idx, const double* values, nlsp_csr** out);
+void nlsp_csr_destroy(nlsp_csr* a);
+void nlsp_csr_dims(const nlsp_csr* a, uint64_t* n, uint64_t* nnz);
+/* spmv (sparse.hpp:116-128), y = A x; host buffers of length n */
+nlsp_status nlsp_spmv(nlsp_ctx* ctx, const nlsp_csr* a, const double* x, double* y);
+/* device-buffer variant (x, y device pointers of length n) */
+nlsp_status nlsp_spmv_device(nlsp_ctx* ctx, const nlsp_csr* a, const double* x, double* y);
+/* diagonal() (sparse.hpp:74-78), host buffer of length n */
+nlsp_status nlsp_csr_diagonal(nlsp_ctx* ctx, const nlsp_csr* a, double* d);
+
+/* -------------------------------------------------------------- dense ---- */
+/* DenseMatrix (dense.hpp:17-50): row-major fp64 */
+nlsp_status nlsp_dense_upload(nlsp_ctx* ctx, uint64_t rows, uint64_t cols, const double* host,
+                              nlsp_dense** out);
+nlsp_status nlsp_dense_export(nlsp_ctx* ctx, const nlsp_dense* d, double* host);
+void nlsp_dense_dims(const nlsp_dense* d, uint64_t* rows, uint64_t* cols);
+void nlsp_dense_destroy(nlsp_dense* d);
+/* device address of the row-major data (for the *_device entry points) */
+void* nlsp_dense_data(const nlsp_dense* d);
+
+/* ----------------------------------------------------------- smoothing ---- */
+/* `sweeps` weighted-Jacobi sweeps x <- x + w D^-1 (b - A x)
+ * (JacobiSmoother::sweep, smoothing.hpp:34-41); x in/out, b host, length n. */
+nlsp_status nlsp_jacobi_sweeps(nlsp_ctx* ctx, const nlsp_csr* a, double omega, uint64_t sweeps,
+                               double* x, const double* b);
+/* homogeneous block sweeps on s in place (smoothing.hpp:50-60) */
+nlsp_status nlsp_smooth_vectors(nlsp_ctx* ctx, const nlsp_csr* a, nlsp_dense* s, uint64_t sweeps,
+                                double omega);
+/* generate_smoothed_vectors (smoothing.hpp:81-100): S^(0) drawn on the host
+ * from the reference's Rng stream (bit-identical), uploaded, then swept on the
+ * device. mask may be NULL (no Dirichlet rows). */
+nlsp_status nlsp_generate_smoothed_vectors(nlsp_ctx* ctx, const nlsp_csr* a, const uint8_t* mask,
+                                           uint64_t k, uint64_t sweeps, double omega,
+                                           uint64_t seed, nlsp_dense** out);
+
+/* ----------------------------------------------------------- SVD basis ---- */
+/* first_cols(svd_oracle(S).left_vectors, k) (svd.hpp:155-227, dense.hpp:158-164)
+ * for a tall S (rows >= cols): Gram S^T S, Jacobi eigensolve, U_k = S V_k / sigma_k,
+ * largest-|entry|-nonnegative sign convention. sigma (length cols) and
+ * eigh_sweeps may be NULL. */
+nlsp_status nlsp_svd_basis(nlsp_ctx* ctx, const nlsp_dense* s, uint64_t k, nlsp_dense** p_out,
+                           double* sigma, int32_t* eigh_sweeps);
+
+/* --------------------------------------------------- two-level operator ---- */
+/* TwoLevelPreconditioner(a, basis_any, omega, nu1, nu2) (two_level.hpp:24-53):
+ * orthonormalise the basis (CholeskyQR2 in place of qr_thin's MGS), form the
+ * Galerkin operator P^T A P, symmetrise exactly, Cholesky-factor it. */
+nlsp_status nlsp_twolevel_build(nlsp_ctx* ctx, const nlsp_csr* a, const nlsp_dense* basis,
+                                double omega, uint64_t nu1, uint64_t nu2, nlsp_twolevel** out);
+void nlsp_twolevel_destroy(nlsp_twolevel* m);
+void nlsp_twolevel_dims(const nlsp_twolevel* m, uint64_t* n, uint64_t* k);
+/* basis_ (n x k), Cholesky factor L (k x k, lower), A_c (k x k); any may be NULL */
+nlsp_status nlsp_twolevel_export(nlsp_ctx* ctx, const nlsp_twolevel* m, double* basis,
+                                 double* chol, double* coarse);
+/* apply (two_level.hpp:60-81): z = M^-1 r, host buffers of length n */
+nlsp_status nlsp_twolevel_apply(nlsp_ctx* ctx, const nlsp_twolevel* m, const nlsp_csr* a,
+                                const double* r, double* z);
+
+/* ------------------------------------------------------------------ PCG ---- */
+/* pcg<Preconditioner> (two_level.hpp:141-191) with x0 = 0. m must be non-NULL
+ * for NLSP_PRECOND_TWOLEVEL and is ignored otherwise. b, x host buffers of
+ * length n; residual_history (may be NULL) receives rep->iterations entries and
+ * must hold max_iters. The whole iteration loop runs on the device. */
+nlsp_status nlsp_pcg(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twolevel* m,
+                     const double* b, double delta, uint64_t max_iters, double* x,
+                     nlsp_solve_report* rep, double* residual_history);
+/* device-resident variant: b, x device pointers (length n); residual_history is
+ * a HOST pointer (may be NULL). */
+nlsp_status nlsp_pcg_device(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twolevel* m,
+                            const double* b_dev, double delta, uint64_t max_iters, double* x_dev,
+                            nlsp_solve_report* rep, double* residual_history);
+
+/* ------------------------------------------------------------ profiling ---- */
+/* Runs `iters` PCG iterations kernel by kernel (no graph) on device-resident b
+ * and records CUDA events around every launch. Fills, for up to `cap` kernel
+ * kinds, the name, the number of launches and the summed device ms. Returns the
+ * number of kinds written. */
+typedef struct {
+    char name[32];
+    uint64_t launches;
+    double total_ms;
+    double bytes_per_launch; /* algorithmic bytes (DESIGN.md byte model) */
+} nlsp_kernel_stat;
+int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twolevel* m,
+                     const double* b_dev, uint64_t iters, nlsp_kernel_stat* stats, int cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

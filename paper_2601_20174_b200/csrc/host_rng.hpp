@@ -1,0 +1,114 @@
+// paper_2601_20174_b200/csrc/host_rng.hpp — restatement of the reference's
+// random streams (rng.hpp:12-73) for host-side input generation: splitmix64
+// mix_seed, std::mt19937_64, top-53-bit uniforms and Box–Muller with the cached
+// sine value. normal_stream() is bit-identical to a serial loop over
+// Rng(seed).normal(); only the transcendental part runs on several threads.
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <random>
+#include <thread>
+#include <vector>
+
+namespace nlsp_host {
+
+inline std::uint64_t mix_seed(std::uint64_t seed, std::uint64_t tag) {
+    std::uint64_t z = seed + 0x9e3779b97f4a7c15ULL * (tag + 1);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+class Rng {
+public:
+    explicit Rng(std::uint64_t seed) : gen_(seed) {}
+    std::uint64_t u64() { return gen_(); }
+    double uniform() { return static_cast<double>(gen_() >> 11) * 0x1.0p-53; }
+    double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+    double normal() {
+        if (has_cached_) {
+            has_cached_ = false;
+            return cached_;
+        }
+        double u1 = uniform();
+        double u2 = uniform();
+        while (u1 <= 0.0) u1 = uniform();
+        const double r = std::sqrt(-2.0 * std::log(u1));
+        const double a = 2.0 * 3.141592653589793 * u2;
+        cached_ = r * std::sin(a);
+        has_cached_ = true;
+        return r * std::cos(a);
+    }
+
+private:
+    std::mt19937_64 gen_;
+    double cached_ = 0.0;
+    bool has_cached_ = false;
+};
+
+inline void normal_stream(std::uint64_t seed, std::uint64_t count, double* out) {
+    std::mt19937_64 gen(seed);
+    auto uni = [&]() { return static_cast<double>(gen() >> 11) * 0x1.0p-53; };
+    const std::uint64_t pairs_total = (count + 1) / 2;
+    const std::uint64_t chunk = 1ull << 22;
+    std::vector<double> u1(std::min(chunk, pairs_total)), u2(std::min(chunk, pairs_total));
+    const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    for (std::uint64_t base = 0; base < pairs_total; base += chunk) {
+        const std::uint64_t np = std::min(chunk, pairs_total - base);
+        for (std::uint64_t p = 0; p < np; ++p) {
+            double a = uni();
+            const double b = uni();
+            while (a <= 0.0) a = uni();
+            u1[p] = a;
+            u2[p] = b;
+        }
+        auto work = [&, base](std::uint64_t lo, std::uint64_t hi) {
+            for (std::uint64_t p = lo; p < hi; ++p) {
+                const double r = std::sqrt(-2.0 * std::log(u1[p]));
+                const double a = 2.0 * 3.141592653589793 * u2[p];
+                const std::uint64_t o = 2 * (base + p);
+                out[o] = r * std::cos(a);
+                if (o + 1 < count) out[o + 1] = r * std::sin(a);
+            }
+        };
+        if (np < 65536 || hw == 1) {
+            work(0, np);
+        } else {
+            std::vector<std::thread> th;
+            const std::uint64_t per = (np + hw - 1) / hw;
+            for (unsigned t = 0; t < hw; ++t) {
+                const std::uint64_t lo = t * per, hi = std::min(np, lo + per);
+                if (lo < hi) th.emplace_back(work, lo, hi);
+            }
+            for (auto& x : th) x.join();
+        }
+    }
+}
+
+// S^(0) of generate_smoothed_vectors before the sweeps (smoothing.hpp:84-92)
+inline void smoothed_s0(std::uint64_t seed, std::uint64_t n, std::uint64_t m,
+                        const std::uint8_t* mask, double* out) {
+    std::uint64_t live = 0;
+    for (std::uint64_t i = 0; i < n; ++i) live += (mask && mask[i]) ? 0 : 1;
+    const std::uint64_t s = mix_seed(seed, 0x736d6f6f);
+    if (live == n) {
+        normal_stream(s, n * m, out);
+        return;
+    }
+    std::vector<double> tmp(live * m);
+    normal_stream(s, tmp.size(), tmp.data());
+    std::uint64_t k = 0;
+    for (std::uint64_t i = 0; i < n; ++i) {
+        double* row = out + i * m;
+        if (mask && mask[i]) {
+            std::fill(row, row + m, 0.0);
+        } else {
+            std::copy(tmp.begin() + k * m, tmp.begin() + (k + 1) * m, row);
+            ++k;
+        }
+    }
+}
+
+}  // namespace nlsp_host

@@ -1,0 +1,102 @@
+// paper_2601_20174_b200/csrc/internal.cuh — shared internals of libnlsp_gpu.so.
+//
+// Layout in HBM:
+//   CSR A      int32 row_ptr[n+1], int32 col_idx[nnz], fp64 values[nnz]  (12 B/nnz)
+//   basis P    fp64 n x k row-major, leading dimension k (even k keeps 16-B rows)
+//   vectors    fp64 n each: x, r, q, z, p[2] (ping-pong), zt[2] (sweep temps), b
+//   state      one PcgState (scalars + flags) + per-CTA reduction partials
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace nlsp {
+
+constexpr int kThreads = 256;      // CTA size of the row kernels
+constexpr int kGroup = 8;          // lanes per CSR row / basis row
+constexpr int kRowsPerWarp = 32 / kGroup;
+constexpr int kMaxGrid = 148 * 8;  // upper bound on row-kernel grids (partials sizing)
+constexpr int kMaxCoarse = 1024;   // largest supported coarse dimension k
+
+enum DevError : int {
+    kErrNone = 0,
+    kErrValidation = 1,
+    kErrNumeric = 2,
+    kErrNotSpd = 3,
+    kErrRank = 4,
+    kErrConvergence = 5,
+};
+
+// Device-resident PCG scalars (two_level.hpp:141-191 locals).
+struct PcgState {
+    double rz, rz_new, pap, alpha, beta, rr, bnorm, delta, true_res, last_rel;
+    long long it, max_it, iterations;
+    int done, converged, error, first;
+    unsigned int counter[16];  // last-CTA tickets, one slot per kernel kind
+};
+
+// Ticket slots (each kernel kind reuses its own counter; counters return to 0).
+enum Ticket : int {
+    kTkBnorm = 0, kTkSpmvP, kTkUpdate, kTkSweep, kTkRestrict, kTkProlong, kTkTrue,
+    kTkInit, kTkGeneric
+};
+
+// Everything a solve kernel needs, passed by value.
+struct SolveArgs {
+    int n;
+    const int* rp;
+    const int* ci;
+    const double* v;
+    const double* wd;    // omega * (1 / A_ii)    (two-level smoother)
+    const double* diag;  // A_ii                   (Jacobi preconditioner)
+    const double* P;     // basis, n x k row-major, ld = k
+    const double* L;     // Cholesky factor of A_c, k x k row-major
+    int k;
+    double* x;
+    double* r;
+    double* q;
+    double* z;
+    double* p0;
+    double* p1;
+    double* zt0;
+    double* zt1;
+    const double* b;
+    double* hist;        // device residual history (max_it entries)
+    PcgState* st;
+    double* partials;    // kMaxGrid * max(k, 4)
+    double* e;           // coarse correction, k
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ double group_sum(double v) {
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    return v;
+}
+
+// Streaming 16-B load that does not allocate in L1 (basis rows, CSR arrays).
+__device__ __forceinline__ double2 ld_stream2(const double* p) {
+    double2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+                 : "=d"(r.x), "=d"(r.y)
+                 : "l"(p));
+    return r;
+}
+
+}  // namespace nlsp
+
+// Host-side launch helpers (defined in the .cu files).
+namespace nlsp {
+struct LaunchCtx {
+    cudaStream_t s;
+    int num_sms;
+    unsigned long long* launches;  // incremented per kernel launch
+};
+}  // namespace nlsp

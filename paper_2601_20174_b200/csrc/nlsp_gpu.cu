@@ -1,0 +1,1126 @@
+// paper_2601_20174_b200/csrc/nlsp_gpu.cu — the C-ABI (include/nlsp_gpu.h):
+// handles, device memory, setup orchestration and the device-resident PCG loop
+// (one CUDA graph per solve: prologue, a WHILE conditional node whose body is
+// one PCG iteration, epilogue). Reference interface cited per entry point.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "host_rng.hpp"
+#include "internal.cuh"
+#include "nlsp_gpu.h"
+
+namespace nlsp {
+// solve_kernels.cu
+void launch_state_init(const LaunchCtx&, PcgState*, double, long long);
+void launch_bnorm(const LaunchCtx&, const SolveArgs&);
+void launch_init_simple(const LaunchCtx&, const SolveArgs&, int);
+void launch_init_ctl(const LaunchCtx&, PcgState*);
+void launch_spmv_p(const LaunchCtx&, const SolveArgs&);
+void launch_update(const LaunchCtx&, const SolveArgs&, int);
+void launch_loop_ctl(const LaunchCtx&, PcgState*, cudaGraphConditionalHandle, int);
+void launch_true_res(const LaunchCtx&, const SolveArgs&);
+void launch_spmv(const LaunchCtx&, int, const int*, const int*, const double*, const double*,
+                 double*);
+void launch_sweep(const LaunchCtx&, const SolveArgs&, bool, const double*, double*, bool);
+void launch_restrict(const LaunchCtx&, const SolveArgs&, int, const double*);
+void launch_prolong(const LaunchCtx&, const SolveArgs&, int, bool, const double*, double*);
+void launch_twolevel_apply(const LaunchCtx&, const SolveArgs&, unsigned long long,
+                           unsigned long long);
+int ppl_for(int k);
+// setup_kernels.cu
+void launch_csr_import(const LaunchCtx&, int, long long, const unsigned long long*,
+                       const unsigned long long*, const double*, int*, int*, double*, int*, int*);
+void launch_wd(const LaunchCtx&, int, const double*, double, double*, int*);
+void launch_block_op(const LaunchCtx&, int, int, const int*, const int*, const double*,
+                     const double*, int, const double*, double*);
+int gram_grid(const LaunchCtx&, long long);
+void launch_gram(const LaunchCtx&, long long, int, int, const double*, const double*, double*,
+                 double*);
+void launch_eigh(const LaunchCtx&, int, const double*, double*, double*, double*, double*, int*,
+                 int*);
+void launch_dense_mm(const LaunchCtx&, long long, int, int, const double*, const double*,
+                     const double*, double*);
+void launch_colsign(const LaunchCtx&, long long, int, double*, double*, long long*, double*,
+                    double*);
+void launch_chol(const LaunchCtx&, int, const double*, double*, double, int*);
+void launch_tri_inv_t(const LaunchCtx&, int, const double*, double*);
+void launch_symmetrize(const LaunchCtx&, int, double*);
+void launch_sigma(const LaunchCtx&, int, int, const double*, const double*, double*, double*,
+                  int*);
+}  // namespace nlsp
+
+using namespace nlsp;
+
+namespace {
+std::atomic<unsigned long long> g_next_id{1};
+}
+
+struct nlsp_csr {
+    unsigned long long id;
+    int device;
+    int n;
+    long long nnz;
+    int* rp;
+    int* ci;
+    double* v;
+    double* diag;
+    int diag_ok;  // all A_ii > 0
+    int max_row;
+};
+
+struct nlsp_dense {
+    unsigned long long id;
+    int device;
+    unsigned long long rows, cols;
+    double* d;
+};
+
+struct nlsp_twolevel {
+    unsigned long long id;
+    int device;
+    int n, k, ld;
+    unsigned long long nu1, nu2;
+    double omega;
+    double* basis;   // n x ld
+    double* L;       // k x k
+    double* coarse;  // k x k
+    double* wd;      // n
+};
+
+struct GraphKey {
+    unsigned long long a = 0, m = 0;
+    int kind = -1;
+    long long ws_gen = -1;
+    bool operator==(const GraphKey& o) const {
+        return a == o.a && m == o.m && kind == o.kind && ws_gen == o.ws_gen;
+    }
+};
+
+struct nlsp_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t s = nullptr;
+    cudaStream_t s_body = nullptr;
+    std::string err;
+    unsigned long long launches = 0;
+    LaunchCtx lc{};
+    PcgState* st = nullptr;      // device
+    PcgState* st_host = nullptr; // pinned
+    int* flags = nullptr;        // device int[16]
+    int* flags_host = nullptr;   // pinned
+    // workspace (sized for ws_n rows, ws_ld coarse columns, ws_hist history)
+    long long ws_n = 0, ws_hist = 0;
+    long long ws_gen = 0;
+    double *x = nullptr, *r = nullptr, *q = nullptr, *z = nullptr, *p0 = nullptr, *p1 = nullptr,
+           *zt0 = nullptr, *zt1 = nullptr, *b = nullptr, *e = nullptr, *partials = nullptr,
+           *hist = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    GraphKey gkey;
+    bool use_graph = true;
+};
+
+// ------------------------------------------------------------------ helpers --
+namespace {
+
+nlsp_status set_err(nlsp_ctx* c, nlsp_status st, const std::string& msg) {
+    if (c) c->err = msg;
+    return st;
+}
+
+nlsp_status cuda_fail(nlsp_ctx* c, cudaError_t e, const char* what) {
+    const nlsp_status st = (e == cudaErrorMemoryAllocation) ? NLSP_E_OOM : NLSP_E_CUDA;
+    cudaGetLastError();
+    return set_err(c, st, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CU(expr)                                                  \
+    do {                                                          \
+        cudaError_t e_ = (expr);                                  \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #expr);  \
+    } while (0)
+
+#define CHECK_LAUNCH()                                                   \
+    do {                                                                 \
+        cudaError_t e_ = cudaGetLastError();                             \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, "kernel launch"); \
+    } while (0)
+
+nlsp_status map_dev_error(nlsp_ctx* c, int code, const char* where) {
+    switch (code) {
+        case kErrNone: return NLSP_OK;
+        case kErrValidation: return set_err(c, NLSP_E_VALIDATION, std::string(where) + ": validation error");
+        case kErrNumeric: return set_err(c, NLSP_E_NUMERIC, std::string(where) + ": numeric error");
+        case kErrNotSpd: return set_err(c, NLSP_E_NOT_SPD, std::string(where) + ": operator not SPD");
+        case kErrRank: return set_err(c, NLSP_E_RANK_DEFICIENT, std::string(where) + ": rank-deficient basis");
+        case kErrConvergence: return set_err(c, NLSP_E_CONVERGENCE, std::string(where) + ": no convergence");
+        default: return set_err(c, NLSP_E_NUMERIC, std::string(where) + ": device error");
+    }
+}
+
+template <class T>
+cudaError_t dalloc(T** p, size_t count) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+}
+
+void dfree(void* p) {
+    if (p) cudaFree(p);
+}
+
+nlsp_status bind(nlsp_ctx* ctx) {
+    if (!ctx) return NLSP_E_VALIDATION;
+    CU(cudaSetDevice(ctx->device));
+    return NLSP_OK;
+}
+
+void free_ws(nlsp_ctx* c) {
+    for (double** p : {&c->x, &c->r, &c->q, &c->z, &c->p0, &c->p1, &c->zt0, &c->zt1, &c->b,
+                       &c->e, &c->partials, &c->hist}) {
+        dfree(*p);
+        *p = nullptr;
+    }
+    c->ws_n = 0;
+    c->ws_hist = 0;
+}
+
+// vectors for n rows, coarse vector and partials, history of hist entries
+nlsp_status ensure_ws(nlsp_ctx* ctx, long long n, long long hist) {
+    if (n > ctx->ws_n) {
+        const long long hist_keep = ctx->ws_hist;
+        free_ws(ctx);
+        for (double** p : {&ctx->x, &ctx->r, &ctx->q, &ctx->z, &ctx->p0, &ctx->p1, &ctx->zt0,
+                           &ctx->zt1, &ctx->b})
+            CU(dalloc(p, (size_t)n));
+        CU(dalloc(&ctx->e, (size_t)kMaxCoarse + 2));
+        CU(dalloc(&ctx->partials, (size_t)kMaxGrid * 256));
+        ctx->ws_n = n;
+        ctx->ws_gen++;
+        hist = hist > hist_keep ? hist : hist_keep;
+    }
+    if (hist > ctx->ws_hist || !ctx->hist) {
+        dfree(ctx->hist);
+        ctx->hist = nullptr;
+        const long long cap = hist > 1 ? hist : 1;
+        CU(dalloc(&ctx->hist, (size_t)cap));
+        ctx->ws_hist = cap;
+        ctx->ws_gen++;
+    }
+    return NLSP_OK;
+}
+
+SolveArgs make_args(nlsp_ctx* c, const nlsp_csr* a, const nlsp_twolevel* m) {
+    SolveArgs s{};
+    s.n = a->n;
+    s.rp = a->rp;
+    s.ci = a->ci;
+    s.v = a->v;
+    s.diag = a->diag;
+    s.wd = m ? m->wd : nullptr;
+    s.P = m ? m->basis : nullptr;
+    s.L = m ? m->L : nullptr;
+    s.k = m ? m->k : 0;
+    s.x = c->x;
+    s.r = c->r;
+    s.q = c->q;
+    s.z = c->z;
+    s.p0 = c->p0;
+    s.p1 = c->p1;
+    s.zt0 = c->zt0;
+    s.zt1 = c->zt1;
+    s.b = c->b;
+    s.hist = c->hist;
+    s.st = c->st;
+    s.partials = c->partials;
+    s.e = c->e;
+    return s;
+}
+
+// One PCG iteration (the WHILE body). mode: 0 two-level, 1 identity, 2 Jacobi.
+void enqueue_iteration(const LaunchCtx& lc, const SolveArgs& a, int mode, const nlsp_twolevel* m,
+                       cudaGraphConditionalHandle h, int use_cond) {
+    launch_spmv_p(lc, a);
+    launch_update(lc, a, mode);
+    if (mode == 0) launch_twolevel_apply(lc, a, m->nu1, m->nu2);
+    launch_loop_ctl(lc, a.st, h, use_cond);
+}
+
+// prologue: state, r = b, x = 0, ||b||, z = M r, rz
+void enqueue_prologue(const LaunchCtx& lc, const SolveArgs& a, int mode, const nlsp_twolevel* m,
+                      const double* params_dev) {
+    (void)params_dev;
+    launch_bnorm(lc, a);
+    if (mode == 0) launch_twolevel_apply(lc, a, m->nu1, m->nu2);
+    else launch_init_simple(lc, a, mode == 2 ? 1 : 0);
+    launch_init_ctl(lc, a.st);
+}
+
+int kind_mode(int kind) { return kind == NLSP_PRECOND_TWOLEVEL ? 0 : (kind == NLSP_PRECOND_JACOBI ? 2 : 1); }
+
+nlsp_status build_graph(nlsp_ctx* ctx, const SolveArgs& a, int mode, const nlsp_twolevel* m) {
+    if (ctx->gexec) {
+        cudaGraphExecDestroy(ctx->gexec);
+        ctx->gexec = nullptr;
+    }
+    cudaGraph_t g = nullptr;
+    LaunchCtx lc = ctx->lc;
+    unsigned long long dummy = 0;
+    lc.launches = &dummy;
+    CU(cudaStreamBeginCapture(ctx->s, cudaStreamCaptureModeThreadLocal));
+    enqueue_prologue(lc, a, mode, m, nullptr);
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t cg = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    cudaError_t e = cudaStreamGetCaptureInfo(ctx->s, &cs, nullptr, &cg, &deps, &ndeps);
+    cudaGraphConditionalHandle h{};
+    cudaGraphNode_t cnode{};
+    cudaGraph_t body = nullptr;
+    if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&h, cg, 1, cudaGraphCondAssignDefault);
+    if (e == cudaSuccess) {
+        cudaGraphNodeParams cp{};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        e = cudaGraphAddNode(&cnode, cg, deps, ndeps, &cp);
+        if (e == cudaSuccess) body = cp.conditional.phGraph_out[0];
+    }
+    if (e == cudaSuccess)
+        e = cudaStreamUpdateCaptureDependencies(ctx->s, &cnode, 1, cudaStreamSetCaptureDependencies);
+    if (e == cudaSuccess)
+        e = cudaStreamBeginCaptureToGraph(ctx->s_body, body, nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+        LaunchCtx lb = lc;
+        lb.s = ctx->s_body;
+        enqueue_iteration(lb, a, mode, m, h, 1);
+        e = cudaStreamEndCapture(ctx->s_body, &body);
+    }
+    if (e == cudaSuccess) launch_true_res(lc, a);
+    cudaError_t e2 = cudaStreamEndCapture(ctx->s, &g);
+    if (e != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        return cuda_fail(ctx, e, "graph build");
+    }
+    if (e2 != cudaSuccess) return cuda_fail(ctx, e2, "graph capture");
+    e = cudaGraphInstantiate(&ctx->gexec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "graph instantiate");
+    return NLSP_OK;
+}
+
+// number of kernels one iteration / the prologue launch (for the report)
+unsigned long long iteration_kernels(int mode, const nlsp_twolevel* m) {
+    unsigned long long c = 3;  // spmv_p, update, loop_ctl
+    if (mode == 0) {
+        const unsigned long long pre = m->nu1 >= 2 ? m->nu1 - 1 : 0;
+        c += pre + 1 + 1 + m->nu2;  // sweeps, restrict, prolong, post sweeps
+    }
+    return c;
+}
+
+unsigned long long prologue_kernels(int mode, const nlsp_twolevel* m) {
+    unsigned long long c = 2 + 1;  // bnorm, init_ctl, (state_init outside)
+    if (mode == 0) c += iteration_kernels(0, m) - 3;
+    else c += 1;
+    return c;
+}
+
+// Runs the solve on ctx->b -> ctx->x. Caller has ensured the workspace.
+nlsp_status run_pcg(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twolevel* m,
+                    double delta, unsigned long long max_iters, nlsp_solve_report* rep,
+                    double* hist_host) {
+    const int mode = kind_mode(kind);
+    const SolveArgs args = make_args(ctx, a, m);
+    launch_state_init(ctx->lc, ctx->st, delta, (long long)max_iters);
+    CHECK_LAUNCH();
+    CU(cudaEventRecord(ctx->ev0, ctx->s));
+    unsigned long long klaunch = 1;
+    bool graph_ok = false;
+    if (ctx->use_graph) {
+        GraphKey key{a->id, m ? m->id : 0, kind, ctx->ws_gen};
+        if (!ctx->gexec || !(ctx->gkey == key)) {
+            if (build_graph(ctx, args, mode, m) == NLSP_OK) {
+                ctx->gkey = key;
+            } else {
+                ctx->use_graph = false;  // fall back to stream-ordered launches
+                ctx->gexec = nullptr;
+                ctx->gkey = GraphKey{};
+            }
+        }
+        if (ctx->gexec) {
+            CU(cudaGraphLaunch(ctx->gexec, ctx->s));
+            graph_ok = true;
+        }
+    }
+    if (!graph_ok) {
+        // stream-ordered loop: chunks of iterations, converged kernels exit early
+        enqueue_prologue(ctx->lc, args, mode, m, nullptr);
+        CHECK_LAUNCH();
+        unsigned long long done_iters = 0;
+        const unsigned long long chunk = 16;
+        for (;;) {
+            for (unsigned long long i = 0; i < chunk && done_iters < max_iters; ++i, ++done_iters)
+                enqueue_iteration(ctx->lc, args, mode, m, cudaGraphConditionalHandle{}, 0);
+            CHECK_LAUNCH();
+            CU(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(PcgState), cudaMemcpyDeviceToHost, ctx->s));
+            CU(cudaStreamSynchronize(ctx->s));
+            if (ctx->st_host->done || done_iters >= max_iters) break;
+        }
+        launch_true_res(ctx->lc, args);
+        CHECK_LAUNCH();
+    }
+    CU(cudaEventRecord(ctx->ev1, ctx->s));
+    CU(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(PcgState), cudaMemcpyDeviceToHost, ctx->s));
+    CU(cudaStreamSynchronize(ctx->s));
+    const PcgState& st = *ctx->st_host;
+    if (graph_ok) {
+        const unsigned long long its = st.it + (st.done && st.it < (long long)max_iters ? 1 : 0);
+        klaunch += prologue_kernels(mode, m) + iteration_kernels(mode, m) * (its ? its : 1) + 1;
+        ctx->launches += klaunch;
+    }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    if (rep) {
+        rep->iterations = (unsigned long long)st.iterations;
+        rep->converged = st.converged;
+        rep->precond_kind = kind;
+        rep->true_relative_residual = st.true_res;
+        rep->final_relative_residual = st.last_rel;
+        rep->solve_ms = ms;
+        rep->coarse_dim = m ? (unsigned long long)m->k : 0;
+        rep->kernel_launches = klaunch;
+    }
+    if (st.error) return map_dev_error(ctx, st.error, "pcg");
+    if (hist_host && st.iterations > 0)
+        CU(cudaMemcpy(hist_host, ctx->hist, sizeof(double) * (size_t)st.iterations,
+                      cudaMemcpyDeviceToHost));
+    return NLSP_OK;
+}
+
+nlsp_status check_pcg_args(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twolevel* m) {
+    if (!a) return set_err(ctx, NLSP_E_VALIDATION, "pcg: null matrix");
+    if (kind < 0 || kind > 2) return set_err(ctx, NLSP_E_VALIDATION, "pcg: unknown preconditioner");
+    if (kind == NLSP_PRECOND_TWOLEVEL) {
+        if (!m) return set_err(ctx, NLSP_E_VALIDATION, "pcg: two-level preconditioner is NULL");
+        if (m->n != a->n) return set_err(ctx, NLSP_E_VALIDATION, "pcg: dimension mismatch");
+    }
+    if (kind == NLSP_PRECOND_JACOBI && !a->diag_ok)
+        return set_err(ctx, NLSP_E_NUMERIC, "jacobi preconditioner: non-positive diagonal");
+    return NLSP_OK;
+}
+
+}  // namespace
+
+// ==================================================================== C-ABI ==
+extern "C" {
+
+const char* nlsp_version(void) { return "nlsp-b200 0.1 (sm_100a)"; }
+
+nlsp_status nlsp_ctx_create(int device, nlsp_ctx** out) {
+    if (!out) return NLSP_E_VALIDATION;
+    *out = nullptr;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return NLSP_E_CUDA;
+    }
+    if (device < 0 || device >= count) return NLSP_E_VALIDATION;
+    cudaDeviceProp prop{};
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10) return NLSP_E_CUDA;
+    auto* ctx = new nlsp_ctx();
+    ctx->device = device;
+    ctx->num_sms = prop.multiProcessorCount;
+    if (cudaSetDevice(device) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->s_body, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMalloc(&ctx->st, sizeof(PcgState)) != cudaSuccess ||
+        cudaMallocHost(&ctx->st_host, sizeof(PcgState)) != cudaSuccess ||
+        cudaMalloc(&ctx->flags, 16 * sizeof(int)) != cudaSuccess ||
+        cudaMallocHost(&ctx->flags_host, 16 * sizeof(int)) != cudaSuccess ||
+        cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
+        cudaEventCreate(&ctx->ev2) != cudaSuccess || cudaEventCreate(&ctx->ev3) != cudaSuccess) {
+        cudaGetLastError();
+        nlsp_ctx_destroy(ctx);
+        return NLSP_E_CUDA;
+    }
+    cudaMemset(ctx->st, 0, sizeof(PcgState));
+    ctx->lc.s = ctx->s;
+    ctx->lc.num_sms = ctx->num_sms;
+    ctx->lc.launches = &ctx->launches;
+    const char* loop = std::getenv("NLSP_LOOP");
+    ctx->use_graph = !(loop && std::strcmp(loop, "host") == 0);
+    *out = ctx;
+    return NLSP_OK;
+}
+
+void nlsp_ctx_destroy(nlsp_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->s) cudaStreamSynchronize(ctx->s);
+    if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+    free_ws(ctx);
+    dfree(ctx->st);
+    dfree(ctx->flags);
+    if (ctx->st_host) cudaFreeHost(ctx->st_host);
+    if (ctx->flags_host) cudaFreeHost(ctx->flags_host);
+    for (cudaEvent_t ev : {ctx->ev0, ctx->ev1, ctx->ev2, ctx->ev3})
+        if (ev) cudaEventDestroy(ev);
+    if (ctx->s_body) cudaStreamDestroy(ctx->s_body);
+    if (ctx->s) cudaStreamDestroy(ctx->s);
+    delete ctx;
+}
+
+const char* nlsp_last_error(const nlsp_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+void* nlsp_ctx_stream(nlsp_ctx* ctx) { return ctx ? static_cast<void*>(ctx->s) : nullptr; }
+
+uint64_t nlsp_ctx_kernel_launches(const nlsp_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+nlsp_status nlsp_ctx_synchronize(nlsp_ctx* ctx) {
+    nlsp_status b = bind(ctx);
+    if (b) return b;
+    CU(cudaStreamSynchronize(ctx->s));
+    return NLSP_OK;
+}
+
+// ---------------------------------------------------------------------- CSR --
+nlsp_status nlsp_csr_upload(nlsp_ctx* ctx, uint64_t n, uint64_t nnz, const uint64_t* row_ptr,
+                            const uint64_t* col_idx, const double* values, nlsp_csr** out) {
+    if (!out) return set_err(ctx, NLSP_E_VALIDATION, "csr_upload: null out");
+    *out = nullptr;
+    nlsp_status b = bind(ctx);
+    if (b) return b;
+    if (n >= (1ull << 31) || nnz >= (1ull << 31))
+        return set_err(ctx, NLSP_E_VALIDATION, "csr_upload: n and nnz must be < 2^31");
+    if (!row_ptr || (nnz && (!col_idx || !values)))
+        return set_err(ctx, NLSP_E_VALIDATION, "csr_upload: null array");
+    if (row_ptr[0] != 0 || row_ptr[n] != nnz)
+        return set_err(ctx, NLSP_E_VALIDATION, "csr_upload: row_ptr must start at 0 and end at nnz");
+    auto* a = new nlsp_csr();
+    a->id = g_next_id++;
+    a->device = ctx->device;
+    a->n = (int)n;
+    a->nnz = (long long)nnz;
+    unsigned long long *rp64 = nullptr, *ci64 = nullptr;
+    auto fail = [&](cudaError_t e, const char* w) {
+        dfree(rp64);
+        dfree(ci64);
+        nlsp_csr_destroy(a);
+        return cuda_fail(ctx, e, w);
+    };
+    cudaError_t e;
+    if ((e = dalloc(&a->rp, n + 1)) || (e = dalloc(&a->ci, nnz)) || (e = dalloc(&a->v, nnz)) ||
+        (e = dalloc(&a->diag, n)) || (e = dalloc(&rp64, n + 1)) || (e = dalloc(&ci64, nnz)))
+        return fail(e, "csr_upload alloc");
+    if ((e = cudaMemcpyAsync(rp64, row_ptr, (n + 1) * 8, cudaMemcpyHostToDevice, ctx->s)) ||
+        (nnz && (e = cudaMemcpyAsync(ci64, col_idx, nnz * 8, cudaMemcpyHostToDevice, ctx->s))) ||
+        (nnz && (e = cudaMemcpyAsync(a->v, values, nnz * 8, cudaMemcpyHostToDevice, ctx->s))) ||
+        (e = cudaMemsetAsync(ctx->flags, 0, 16 * sizeof(int), ctx->s)))
+        return fail(e, "csr_upload copy");
+    if (n == 0) {
+        cudaMemsetAsync(a->rp, 0, sizeof(int), ctx->s);
+    } else {
+        launch_csr_import(ctx->lc, (int)n, (long long)nnz, rp64, ci64, a->v, a->rp, a->ci, a->diag,
+                          ctx->flags, ctx->flags + 1);
+    }
+    if ((e = cudaGetLastError())) return fail(e, "csr_import launch");
+    if ((e = cudaMemcpyAsync(ctx->flags_host, ctx->flags, 16 * sizeof(int), cudaMemcpyDeviceToHost,
+                             ctx->s)) ||
+        (e = cudaStreamSynchronize(ctx->s)))
+        return fail(e, "csr_upload sync");
+    dfree(rp64);
+    dfree(ci64);
+    rp64 = ci64 = nullptr;
+    const int fl = ctx->flags_host[0];
+    if (fl) {
+        nlsp_csr_destroy(a);
+        return set_err(ctx, NLSP_E_VALIDATION,
+                       (fl & 1) ? "csr_upload: row_ptr not monotone"
+                       : (fl & 2) ? "csr_upload: column index out of range"
+                                  : "csr_upload: columns must be sorted without duplicates");
+    }
+    a->max_row = ctx->flags_host[1];
+    // diag_ok: any A_ii <= 0 ?
+    {
+        int* f = ctx->flags + 2;
+        double* tmp = nullptr;
+        if ((e = dalloc(&tmp, n)) || (e = cudaMemsetAsync(f, 0, sizeof(int), ctx->s))) {
+            dfree(tmp);
+            return fail(e, "csr_upload diag");
+        }
+        launch_wd(ctx->lc, (int)n, a->diag, 1.0, tmp, f);
+        e = cudaMemcpyAsync(ctx->flags_host + 2, f, sizeof(int), cudaMemcpyDeviceToHost, ctx->s);
+        if (!e) e = cudaStreamSynchronize(ctx->s);
+        dfree(tmp);
+        if (e) return fail(e, "csr_upload diag sync");
+        a->diag_ok = ctx->flags_host[2] == 0;
+    }
+    *out = a;
+    return NLSP_OK;
+}
+
+void nlsp_csr_destroy(nlsp_csr* a) {
+    if (!a) return;
+    cudaSetDevice(a->device);
+    dfree(a->rp);
+    dfree(a->ci);
+    dfree(a->v);
+    dfree(a->diag);
+    delete a;
+}
+
+void nlsp_csr_dims(const nlsp_csr* a, uint64_t* n, uint64_t* nnz) {
+    if (n) *n = a ? (uint64_t)a->n : 0;
+    if (nnz) *nnz = a ? (uint64_t)a->nnz : 0;
+}
+
+nlsp_status nlsp_spmv_device(nlsp_ctx* ctx, const nlsp_csr* a, const double* x, double* y) {
+    nlsp_status b = bind(ctx);
+    if (b) return b;
+    if (!a) return set_err(ctx, NLSP_E_VALIDATION, "spmv: null matrix");
+    if (a->n) launch_spmv(ctx->lc, a->n, a->rp, a->ci, a->v, x, y);
+    CHECK_LAUNCH();
+    CU(cudaStreamSynchronize(ctx->s));
+    return NLSP_OK;
+}
+
+nlsp_status nlsp_spmv(nlsp_ctx* ctx, const nlsp_csr* a, const double* x, double* y) {
+    nlsp_status b = bind(ctx);
+    if (b) return b;
+    if (!a || !x || !y) return set_err(ctx, NLSP_E_VALIDATION, "spmv: null argument");
+    b = ensure_ws(ctx, a->n, 1);
+    if (b) return b;
+    const size_t bytes = (size_t)a->n * 8;
+    CU(cudaMemcpyAsync(ctx->zt0, x, bytes, cudaMemcpyHostToDevice, ctx->s));
+    if (a->n) launch_spmv(ctx->lc, a->n, a->rp, a->ci, a->v, ctx->zt0, ctx->zt1);
+    CHECK_LAUNCH();
+    CU(cudaMemcpyAsync(y, ctx->zt1, bytes, cudaMemcpyDeviceToHost, ctx->s));
+    CU(cudaStreamSynchronize(ctx->s));
+    return NLSP_OK;
+}
+
+nlsp_status nlsp_csr_diagonal(nlsp_ctx* ctx, const nlsp_csr* a, double* d) {
+    nlsp_status b = bind(ctx);
+    if (b) return b;
+    if (!a || !d) return set_err(ctx, NLSP_E_VALIDATION, "diagonal: null argument");
+    CU(cudaMemcpy(d, a->diag, (size_t)a->n * 8, cudaMemcpyDeviceToHost));
+    return NLSP_OK;
+}
+
+// -------------------------------------------------------------------- dense --
+static nlsp_status dense_alloc(nlsp_ctx* ctx, uint64_t rows, uint64_t cols, nlsp_dense** out) {
+    auto* d = new nlsp_dense();
+    d->id = g_next_id++;
+    d->device = ctx->device;
+    d->rows = rows;
+    d->cols = cols;
+    cudaError_t e = dalloc(&d->d, rows * cols);
+    if (e) {
+        delete d;
+        return cuda_fail(ctx, e, "dense alloc");
+    }
+    *out = d;
+    return NLSP_OK;
+}
+
+nlsp_status nlsp_dense_upload(nlsp_ctx* ctx, uint64_t rows, uint64_t cols, const double* host,
+                              nlsp_dense** out) {
+    if (!out) return set_err(ctx, NLSP_E_VALIDATION, "dense_upload: null out");
+    *out = nullptr;
+    nlsp_status b = bind(ctx);
+    if (b) return b;
+    if (rows * cols && !host) return set_err(ctx, NLSP_E_VALIDATION, "dense_upload: null data");
+    nlsp_dense* d = nullptr;
+    b = dense_alloc(ctx, rows, cols, &d);
+    if (b) return b;
+    if (rows * cols) {
+        cudaError_t e = cudaMemcpy(d->d, host, rows * cols * 8, cudaMemcpyHostToDevice);
+        if (e) {
+            nlsp_dense_destroy(d);
+            return cuda_fail(ctx, e, "dense_upload copy");
+        }
+    }
+    *out = d;
+    return NLSP_OK;
+}
+
+nlsp_status nlsp_dense_export(nlsp_ctx* ctx, const nlsp_dense* d, double* host) {
+    nlsp_status b = bind(ctx);
+    if (b) return b;
+    if (!d || (!host && d->rows * d->cols)) return set_err(ctx, NLSP_E_VALIDATION, "dense_export: null");
+    CU(cudaStreamSynchronize(ctx->s));
+    if (d->rows * d->cols) CU(cudaMemcpy(host, d->d, d->rows * d->cols * 8, cudaMemcpyDeviceToHost));
+    return NLSP_OK;
+}
+
+void nlsp_dense_dims(const nlsp_dense* d, uint64_t* rows, uint64_t* cols) {
+    if (rows) *rows = d ? d->rows : 0;
+    if (cols) *cols = d ? d->cols : 0;
+}
+
+void* nlsp_dense_data(const nlsp_dense* d) { return d ? d->d : nullptr; }
+
+void nlsp_dense_destroy(nlsp_dense* d) {
+    if (!d) return;
+    cudaSetDevice(d->device);
+    dfree(d->d);
+    delete d;
+}
+
+// ---------------------------------------------------------------- smoothing --
+nlsp_status nlsp_jacobi_sweeps(nlsp_ctx* ctx, const nlsp_csr* a, double omega, uint64_t sweeps,
+                               double* x, const double* b) {
+    nlsp_status st = bind(ctx);
+    if (st) return st;
+    if (!a || !x || !b) return set_err(ctx, NLSP_E_VALIDATION, "jacobi sweep: null argument");
+    if (omega < 0.0 || omega > 1.0)
+        return set_err(ctx, NLSP_E_VALIDATION, "jacobi: omega must lie in [0, 1]");
+    if (!a->diag_ok) return set_err(ctx, NLSP_E_NUMERIC, "jacobi: non-positive diagonal");
+    st = ensure_ws(ctx, a->n, 1);
+    if (st) return st;
+    double* wd = nullptr;
+    CU(dalloc(&wd, a->n));
+    launch_wd(ctx->lc, a->n, a->diag, omega, wd, ctx->flags + 3);
+    const size_t bytes = (size_t)a->n * 8;
+    CU(cudaMemcpyAsync(ctx->zt0, x, bytes, cudaMemcpyHostToDevice, ctx->s));
+    CU(cudaMemcpyAsync(ctx->r, b, bytes, cudaMemcpyHostToDevice, ctx->s));
+    CU(cudaMemsetAsync(ctx->st, 0, sizeof(PcgState), ctx->s));
+    nlsp_twolevel fake{};
+    fake.wd = wd;
+    SolveArgs args = make_args(ctx, a, &fake);
+    double* cur = ctx->zt0;
+    for (uint64_t s = 0; s < sweeps; ++s) {
+        double* nxt = (cur == ctx->zt0) ? ctx->zt1 : ctx->zt0;
+        launch_sweep(ctx->lc, args, false, cur, nxt, false);
+        cur = nxt;
+    }
+    CHECK_LAUNCH();
+    CU(cudaMemcpyAsync(x, cur, bytes, cudaMemcpyDeviceToHost, ctx->s));
+    CU(cudaStreamSynchronize(ctx->s));
+    dfree(wd);
+    return NLSP_OK;
+}
+
+static nlsp_status smooth_impl(nlsp_ctx* ctx, const nlsp_csr* a, nlsp_dense* s, uint64_t sweeps,
+                               double omega) {
+    if (omega < 0.0 || omega > 1.0)
+        return set_err(ctx, NLSP_E_VALIDATION, "jacobi: omega must lie in [0, 1]");
+    if (!a->diag_ok) return set_err(ctx, NLSP_E_NUMERIC, "jacobi: non-positive diagonal");
+    if (s->rows != (uint64_t)a->n)
+        return set_err(ctx, NLSP_E_VALIDATION, "jacobi sweep: dimension mismatch");
+    if (sweeps == 0 || s->cols == 0 || a->n == 0) return NLSP_OK;
+    double *wd = nullptr, *tmp = nullptr;
+    CU(dalloc(&wd, a->n));
+    cudaError_t e = dalloc(&tmp, s->rows * s->cols);
+    if (e) {
+        dfree(wd);
+        return cuda_fail(ctx, e, "smooth alloc");
+    }
+    launch_wd(ctx->lc, a->n, a->diag, omega, wd, ctx->flags + 3);
+    double* cur = s->d;
+    double* other = tmp;
+    for (uint64_t k = 0; k < sweeps; ++k) {
+        launch_block_op(ctx->lc, 0, a->n, a->rp, a->ci, a->v, wd, (int)s->cols, cur, other);
+        double* t = cur;
+        cur = other;
+        other = t;
+    }
+    e = cudaGetLastError();
+    if (!e && cur != s->d)
+        e = cudaMemcpyAsync(s->d, cur, s->rows * s->cols * 8, cudaMemcpyDeviceToDevice, ctx->s);
+    if (!e) e = cudaStreamSynchronize(ctx->s);
+    dfree(wd);
+    dfree(tmp);
+    if (e) return cuda_fail(ctx, e, "smooth");
+    return NLSP_OK;
+}
+
+nlsp_status nlsp_smooth_vectors(nlsp_ctx* ctx, const nlsp_csr* a, nlsp_dense* s, uint64_t sweeps,
+                                double omega) {
+    nlsp_status st = bind(ctx);
+    if (st) return st;
+    if (!a || !s) return set_err(ctx, NLSP_E_VALIDATION, "smooth: null argument");
+    return smooth_impl(ctx, a, s, sweeps, omega);
+}
+
+nlsp_status nlsp_generate_smoothed_vectors(nlsp_ctx* ctx, const nlsp_csr* a, const uint8_t* mask,
+                                           uint64_t k, uint64_t sweeps, double omega,
+                                           uint64_t seed, nlsp_dense** out) {
+    if (!out) return set_err(ctx, NLSP_E_VALIDATION, "generate_smoothed_vectors: null out");
+    *out = nullptr;
+    nlsp_status st = bind(ctx);
+    if (st) return st;
+    if (!a) return set_err(ctx, NLSP_E_VALIDATION, "generate_smoothed_vectors: null matrix");
+    if (k < 1) return set_err(ctx, NLSP_E_VALIDATION, "generate_smoothed_vectors: K must be positive");
+    std::vector<double> s0((size_t)a->n * k);
+    nlsp_host::smoothed_s0(seed, (uint64_t)a->n, k, mask, s0.data());
+    nlsp_dense* d = nullptr;
+    st = nlsp_dense_upload(ctx, a->n, k, s0.data(), &d);
+    if (st) return st;
+    st = smooth_impl(ctx, a, d, sweeps, omega);
+    if (st) {
+        nlsp_dense_destroy(d);
+        return st;
+    }
+    *out = d;
+    return NLSP_OK;
+}
+
+// ---------------------------------------------------------------- SVD basis --
+nlsp_status nlsp_svd_basis(nlsp_ctx* ctx, const nlsp_dense* s, uint64_t k, nlsp_dense** p_out,
+                           double* sigma, int32_t* eigh_sweeps) {
+    if (!p_out) return set_err(ctx, NLSP_E_VALIDATION, "svd_basis: null out");
+    *p_out = nullptr;
+    nlsp_status st = bind(ctx);
+    if (st) return st;
+    if (!s) return set_err(ctx, NLSP_E_VALIDATION, "svd_basis: null matrix");
+    const long long n = (long long)s->rows;
+    const int m = (int)s->cols;
+    if (m == 0 || n == 0) return set_err(ctx, NLSP_E_VALIDATION, "svd_oracle: empty matrix");
+    if ((long long)m > n) return set_err(ctx, NLSP_E_VALIDATION, "svd_basis: requires rows >= cols");
+    if (k > (uint64_t)m) return set_err(ctx, NLSP_E_VALIDATION, "first_cols: k exceeds column count");
+    if (m > 1024) return set_err(ctx, NLSP_E_VALIDATION, "svd_basis: at most 1024 columns");
+    if (k == 0) {
+        nlsp_dense* d = nullptr;
+        st = dense_alloc(ctx, n, 0, &d);
+        if (!st) *p_out = d;
+        return st;
+    }
+    const int g = gram_grid(ctx->lc, n);
+    double *part = nullptr, *G = nullptr, *ev = nullptr, *V = nullptr, *sa = nullptr, *sv = nullptr,
+           *sig = nullptr, *W = nullptr, *pmag = nullptr, *pval = nullptr, *sign = nullptr;
+    long long* pidx = nullptr;
+    nlsp_dense* P = nullptr;
+    nlsp_status ret = NLSP_OK;
+    auto cleanup = [&]() {
+        for (double* p : {part, G, ev, V, sa, sv, sig, W, pmag, pval, sign}) dfree(p);
+        dfree(pidx);
+    };
+    cudaError_t e;
+    const size_t mm = (size_t)m * m;
+    if ((e = dalloc(&part, (size_t)g * mm)) || (e = dalloc(&G, mm)) || (e = dalloc(&ev, m)) ||
+        (e = dalloc(&V, mm)) || (e = dalloc(&sa, mm)) || (e = dalloc(&sv, mm)) ||
+        (e = dalloc(&sig, m)) || (e = dalloc(&W, (size_t)m * k)) ||
+        (e = dalloc(&pmag, (size_t)ctx->num_sms * k)) || (e = dalloc(&pval, (size_t)ctx->num_sms * k)) ||
+        (e = dalloc(&pidx, (size_t)ctx->num_sms * k)) || (e = dalloc(&sign, k))) {
+        cleanup();
+        return cuda_fail(ctx, e, "svd_basis alloc");
+    }
+    CU(cudaMemsetAsync(ctx->flags, 0, 16 * sizeof(int), ctx->s));
+    // Gram S^T S (svd.hpp:162-166), eigensolve (:167), sigma + W = V_k (:174-183)
+    launch_gram(ctx->lc, n, m, m, s->d, s->d, part, G);
+    launch_eigh(ctx->lc, m, G, ev, V, sa, sv, ctx->flags + 4, ctx->flags + 5);
+    launch_sigma(ctx->lc, m, (int)k, ev, V, sig, W, ctx->flags + 6);
+    e = cudaGetLastError();
+    if (!e) e = cudaMemcpyAsync(ctx->flags_host, ctx->flags, 16 * sizeof(int), cudaMemcpyDeviceToHost, ctx->s);
+    if (!e) e = cudaStreamSynchronize(ctx->s);
+    if (e) {
+        cleanup();
+        return cuda_fail(ctx, e, "svd_basis");
+    }
+    if (eigh_sweeps) *eigh_sweeps = ctx->flags_host[5];
+    if (ctx->flags_host[4] == kErrValidation) {
+        cleanup();
+        return set_err(ctx, NLSP_E_VALIDATION, "svd_oracle: non-finite entries");
+    }
+    if (ctx->flags_host[4]) {
+        cleanup();
+        return set_err(ctx, NLSP_E_CONVERGENCE, "jacobi_eigh: no convergence after 30 sweeps");
+    }
+    if (sigma) cudaMemcpy(sigma, sig, sizeof(double) * m, cudaMemcpyDeviceToHost);
+    if (ctx->flags_host[6]) {
+        cleanup();
+        return set_err(ctx, NLSP_E_NUMERIC,
+                       "svd_basis: S has numerical rank below k (sigma_j <= 1e-13 sigma_max)");
+    }
+    ret = dense_alloc(ctx, n, k, &P);
+    if (ret) {
+        cleanup();
+        return ret;
+    }
+    // U_k = S V_k / sigma_k (svd.hpp:189-202), sign convention (:209-225)
+    launch_dense_mm(ctx->lc, n, m, (int)k, s->d, W, sig, P->d);
+    launch_colsign(ctx->lc, n, (int)k, P->d, pmag, pidx, pval, sign);
+    e = cudaGetLastError();
+    if (!e) e = cudaStreamSynchronize(ctx->s);
+    cleanup();
+    if (e) {
+        nlsp_dense_destroy(P);
+        return cuda_fail(ctx, e, "svd_basis products");
+    }
+    *p_out = P;
+    return NLSP_OK;
+}
+
+// -------------------------------------------------------- two-level operator --
+nlsp_status nlsp_twolevel_build(nlsp_ctx* ctx, const nlsp_csr* a, const nlsp_dense* basis,
+                                double omega, uint64_t nu1, uint64_t nu2, nlsp_twolevel** out) {
+    if (!out) return set_err(ctx, NLSP_E_VALIDATION, "two-level: null out");
+    *out = nullptr;
+    nlsp_status st = bind(ctx);
+    if (st) return st;
+    if (!a || !basis) return set_err(ctx, NLSP_E_VALIDATION, "two-level: null argument");
+    // smoother_ is constructed first (two_level.hpp:25), then the basis checks
+    if (omega < 0.0 || omega > 1.0)
+        return set_err(ctx, NLSP_E_VALIDATION, "jacobi: omega must lie in [0, 1]");
+    if (!a->diag_ok) return set_err(ctx, NLSP_E_NUMERIC, "jacobi: non-positive diagonal");
+    if (basis->cols == 0) return set_err(ctx, NLSP_E_VALIDATION, "two-level: empty coarse space");
+    if (basis->rows != (uint64_t)a->n)
+        return set_err(ctx, NLSP_E_VALIDATION, "two-level: basis row count must match matrix dimension");
+    const int k = (int)basis->cols;
+    const long long n = a->n;
+    if (k > 256) return set_err(ctx, NLSP_E_VALIDATION, "two-level: coarse dimension above 256 unsupported");
+    if ((long long)k > n) return set_err(ctx, NLSP_E_VALIDATION, "qr_thin: requires rows >= cols");
+    auto* m = new nlsp_twolevel();
+    m->id = g_next_id++;
+    m->device = ctx->device;
+    m->n = (int)n;
+    m->k = k;
+    m->ld = k + (k & 1);
+    m->nu1 = nu1;
+    m->nu2 = nu2;
+    m->omega = omega;
+    const size_t kk = (size_t)k * k;
+    const int g = gram_grid(ctx->lc, n);
+    double *part = nullptr, *G = nullptr, *U = nullptr, *Q1 = nullptr, *Q = nullptr, *Y = nullptr;
+    auto cleanup = [&]() {
+        for (double* p : {part, G, U, Q1, Q, Y}) dfree(p);
+    };
+    auto fail_cuda = [&](cudaError_t e, const char* w) {
+        cleanup();
+        nlsp_twolevel_destroy(m);
+        return cuda_fail(ctx, e, w);
+    };
+    cudaError_t e;
+    if ((e = dalloc(&m->basis, (size_t)n * m->ld)) || (e = dalloc(&m->L, kk)) ||
+        (e = dalloc(&m->coarse, kk)) || (e = dalloc(&m->wd, n)) || (e = dalloc(&part, (size_t)g * kk)) ||
+        (e = dalloc(&G, kk)) || (e = dalloc(&U, kk)) || (e = dalloc(&Q1, (size_t)n * k)) ||
+        (e = dalloc(&Q, (size_t)n * k)) || (e = dalloc(&Y, (size_t)n * k)))
+        return fail_cuda(e, "two-level alloc");
+    if ((e = cudaMemsetAsync(ctx->flags, 0, 16 * sizeof(int), ctx->s))) return fail_cuda(e, "memset");
+    launch_wd(ctx->lc, (int)n, a->diag, omega, m->wd, ctx->flags + 7);
+    // qr_thin (qr.hpp:18-45) as CholeskyQR2: R1 = chol(B^T B) with the rank
+    // test, Q1 = B R1^-1; R2 = chol(Q1^T Q1), Q = Q1 R2^-1.
+    launch_gram(ctx->lc, n, k, k, basis->d, basis->d, part, G);
+    launch_chol(ctx->lc, k, G, m->L, 1e-12, ctx->flags + 8);
+    launch_tri_inv_t(ctx->lc, k, m->L, U);
+    launch_dense_mm(ctx->lc, n, k, k, basis->d, U, nullptr, Q1);
+    launch_gram(ctx->lc, n, k, k, Q1, Q1, part, G);
+    launch_chol(ctx->lc, k, G, m->L, 0.0, ctx->flags + 9);
+    launch_tri_inv_t(ctx->lc, k, m->L, U);
+    launch_dense_mm(ctx->lc, n, k, k, Q1, U, nullptr, Q);
+    // Galerkin A_c = Q^T (A Q), exact symmetrisation, Cholesky (two_level.hpp:33-52)
+    launch_block_op(ctx->lc, 1, (int)n, a->rp, a->ci, a->v, nullptr, k, Q, Y);
+    launch_gram(ctx->lc, n, k, k, Q, Y, part, m->coarse);
+    launch_symmetrize(ctx->lc, k, m->coarse);
+    launch_chol(ctx->lc, k, m->coarse, m->L, 0.0, ctx->flags + 10);
+    // basis with an even leading dimension (zero pad column for odd k)
+    if (!(e = cudaGetLastError()))
+        e = cudaMemcpy2DAsync(m->basis, (size_t)m->ld * 8, Q, (size_t)k * 8, (size_t)k * 8, n,
+                              cudaMemcpyDeviceToDevice, ctx->s);
+    if (!e && m->ld != k)
+        e = cudaMemset2DAsync(m->basis + k, (size_t)m->ld * 8, 0, 8, n, ctx->s);
+    if (!e) e = cudaMemcpyAsync(ctx->flags_host, ctx->flags, 16 * sizeof(int), cudaMemcpyDeviceToHost, ctx->s);
+    if (!e) e = cudaStreamSynchronize(ctx->s);
+    if (e) return fail_cuda(e, "two-level build");
+    cleanup();
+    const int* f = ctx->flags_host;
+    if (f[7]) {
+        nlsp_twolevel_destroy(m);
+        return set_err(ctx, NLSP_E_NUMERIC, "jacobi: non-positive diagonal");
+    }
+    if (f[8] || f[9]) {
+        nlsp_twolevel_destroy(m);
+        return set_err(ctx, NLSP_E_RANK_DEFICIENT, "qr_thin: rank-deficient basis");
+    }
+    if (f[10]) {
+        nlsp_twolevel_destroy(m);
+        return map_dev_error(ctx, f[10], "cholesky");
+    }
+    *out = m;
+    return NLSP_OK;
+}
+
+void nlsp_twolevel_destroy(nlsp_twolevel* m) {
+    if (!m) return;
+    cudaSetDevice(m->device);
+    for (double* p : {m->basis, m->L, m->coarse, m->wd}) dfree(p);
+    delete m;
+}
+
+void nlsp_twolevel_dims(const nlsp_twolevel* m, uint64_t* n, uint64_t* k) {
+    if (n) *n = m ? (uint64_t)m->n : 0;
+    if (k) *k = m ? (uint64_t)m->k : 0;
+}
+
+nlsp_status nlsp_twolevel_export(nlsp_ctx* ctx, const nlsp_twolevel* m, double* basis, double* chol,
+                                 double* coarse) {
+    nlsp_status st = bind(ctx);
+    if (st) return st;
+    if (!m) return set_err(ctx, NLSP_E_VALIDATION, "two-level export: null handle");
+    CU(cudaStreamSynchronize(ctx->s));
+    const size_t kk = (size_t)m->k * m->k * 8;
+    if (basis)
+        CU(cudaMemcpy2D(basis, (size_t)m->k * 8, m->basis, (size_t)m->ld * 8, (size_t)m->k * 8,
+                        (size_t)m->n, cudaMemcpyDeviceToHost));
+    if (chol) CU(cudaMemcpy(chol, m->L, kk, cudaMemcpyDeviceToHost));
+    if (coarse) CU(cudaMemcpy(coarse, m->coarse, kk, cudaMemcpyDeviceToHost));
+    return NLSP_OK;
+}
+
+nlsp_status nlsp_twolevel_apply(nlsp_ctx* ctx, const nlsp_twolevel* m, const nlsp_csr* a,
+                                const double* r, double* z) {
+    nlsp_status st = bind(ctx);
+    if (st) return st;
+    if (!m || !a || !r || !z) return set_err(ctx, NLSP_E_VALIDATION, "two-level apply: null argument");
+    if (a->n != m->n) return set_err(ctx, NLSP_E_VALIDATION, "two-level apply: dimension mismatch");
+    st = ensure_ws(ctx, a->n, 1);
+    if (st) return st;
+    const size_t bytes = (size_t)a->n * 8;
+    CU(cudaMemcpyAsync(ctx->r, r, bytes, cudaMemcpyHostToDevice, ctx->s));
+    CU(cudaMemsetAsync(ctx->st, 0, sizeof(PcgState), ctx->s));
+    const SolveArgs args = make_args(ctx, a, m);
+    launch_twolevel_apply(ctx->lc, args, m->nu1, m->nu2);
+    CHECK_LAUNCH();
+    CU(cudaMemcpyAsync(z, ctx->z, bytes, cudaMemcpyDeviceToHost, ctx->s));
+    CU(cudaStreamSynchronize(ctx->s));
+    return NLSP_OK;
+}
+
+// ---------------------------------------------------------------------- PCG --
+nlsp_status nlsp_pcg(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twolevel* m,
+                     const double* b, double delta, uint64_t max_iters, double* x,
+                     nlsp_solve_report* rep, double* residual_history) {
+    nlsp_status st = bind(ctx);
+    if (st) return st;
+    st = check_pcg_args(ctx, a, kind, m);
+    if (st) return st;
+    if (!b || !x) return set_err(ctx, NLSP_E_VALIDATION, "pcg: null vector");
+    st = ensure_ws(ctx, a->n, (long long)max_iters);
+    if (st) return st;
+    const size_t bytes = (size_t)a->n * 8;
+    CU(cudaEventRecord(ctx->ev2, ctx->s));
+    CU(cudaMemcpyAsync(ctx->b, b, bytes, cudaMemcpyHostToDevice, ctx->s));
+    nlsp_solve_report local{};
+    nlsp_solve_report* r = rep ? rep : &local;
+    std::memset(r, 0, sizeof(*r));
+    st = run_pcg(ctx, a, kind, m, delta, max_iters, r, residual_history);
+    if (st) return st;
+    CU(cudaMemcpyAsync(x, ctx->x, bytes, cudaMemcpyDeviceToHost, ctx->s));
+    CU(cudaEventRecord(ctx->ev3, ctx->s));
+    CU(cudaStreamSynchronize(ctx->s));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev2, ctx->ev3);
+    r->total_ms = ms;
+    r->h2d_bytes = bytes;
+    r->d2h_bytes = bytes + sizeof(PcgState) + (residual_history ? r->iterations * 8 : 0);
+    return NLSP_OK;
+}
+
+nlsp_status nlsp_pcg_device(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twolevel* m,
+                            const double* b_dev, double delta, uint64_t max_iters, double* x_dev,
+                            nlsp_solve_report* rep, double* residual_history) {
+    nlsp_status st = bind(ctx);
+    if (st) return st;
+    st = check_pcg_args(ctx, a, kind, m);
+    if (st) return st;
+    if (!b_dev || !x_dev) return set_err(ctx, NLSP_E_VALIDATION, "pcg: null vector");
+    st = ensure_ws(ctx, a->n, (long long)max_iters);
+    if (st) return st;
+    const size_t bytes = (size_t)a->n * 8;
+    CU(cudaEventRecord(ctx->ev2, ctx->s));
+    CU(cudaMemcpyAsync(ctx->b, b_dev, bytes, cudaMemcpyDeviceToDevice, ctx->s));
+    nlsp_solve_report local{};
+    nlsp_solve_report* r = rep ? rep : &local;
+    std::memset(r, 0, sizeof(*r));
+    st = run_pcg(ctx, a, kind, m, delta, max_iters, r, residual_history);
+    if (st) return st;
+    CU(cudaMemcpyAsync(x_dev, ctx->x, bytes, cudaMemcpyDeviceToDevice, ctx->s));
+    CU(cudaEventRecord(ctx->ev3, ctx->s));
+    CU(cudaStreamSynchronize(ctx->s));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev2, ctx->ev3);
+    r->total_ms = ms;
+    r->h2d_bytes = 0;
+    r->d2h_bytes = sizeof(PcgState) + (residual_history ? r->iterations * 8 : 0);
+    return NLSP_OK;
+}
+
+// ---------------------------------------------------------------- profiling --
+int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twolevel* m,
+                     const double* b_dev, uint64_t iters, nlsp_kernel_stat* stats, int cap) {
+    if (bind(ctx) || check_pcg_args(ctx, a, kind, m) || !b_dev || !stats || cap <= 0) return -1;
+    if (ensure_ws(ctx, a->n, (long long)iters + 1)) return -1;
+    const int mode = kind_mode(kind);
+    const SolveArgs args = make_args(ctx, a, m);
+    cudaMemcpyAsync(ctx->b, b_dev, (size_t)a->n * 8, cudaMemcpyDeviceToDevice, ctx->s);
+    launch_state_init(ctx->lc, ctx->st, 0.0, (long long)iters);
+    enqueue_prologue(ctx->lc, args, mode, m, nullptr);
+    struct Acc {
+        const char* name;
+        double bytes;
+        unsigned long long launches = 0;
+        double ms = 0.0;
+    };
+    const double n = a->n, nnz = (double)a->nnz, k = m ? m->k : 0;
+    const double csr = 12.0 * nnz + 4.0 * (n + 1);
+    std::vector<Acc> acc = {
+        {"spmv_p", csr + 32.0 * n},          // reads z, p; writes p, q
+        {"update", (mode == 0 ? 48.0 : (mode == 1 ? 56.0 : 64.0)) * n},
+        {"restrict", csr + 8.0 * n * k + 16.0 * n},  // P, r, w (implicit z1)
+        {"prolong", 8.0 * n * k + 24.0 * n},         // P, r, w; writes z2
+        {"post_sweep", csr + 32.0 * n},              // z2, r, w; writes z
+        {"loop_ctl", 0.0},
+    };
+    std::vector<cudaEvent_t> evs(2 * 8);
+    for (auto& e : evs) cudaEventCreate(&e);
+    auto timed = [&](int slot, auto&& fn) {
+        cudaEventRecord(evs[0], ctx->s);
+        fn();
+        cudaEventRecord(evs[1], ctx->s);
+        cudaEventSynchronize(evs[1]);
+        float t = 0.f;
+        cudaEventElapsedTime(&t, evs[0], evs[1]);
+        acc[slot].ms += t;
+        acc[slot].launches++;
+    };
+    const bool simple_apply = mode == 0 && m->nu1 == 1 && m->nu2 == 1;
+    for (uint64_t it = 0; it < iters; ++it) {
+        timed(0, [&] { launch_spmv_p(ctx->lc, args); });
+        timed(1, [&] { launch_update(ctx->lc, args, mode); });
+        if (mode == 0) {
+            if (simple_apply) {
+                timed(2, [&] { launch_restrict(ctx->lc, args, 1, nullptr); });
+                timed(3, [&] { launch_prolong(ctx->lc, args, 1, false, nullptr, ctx->zt0); });
+                timed(4, [&] { launch_sweep(ctx->lc, args, false, ctx->zt0, ctx->z, true); });
+            } else {
+                timed(2, [&] { launch_twolevel_apply(ctx->lc, args, m->nu1, m->nu2); });
+            }
+        }
+        timed(5, [&] { launch_loop_ctl(ctx->lc, ctx->st, cudaGraphConditionalHandle{}, 0); });
+    }
+    for (auto& e : evs) cudaEventDestroy(e);
+    cudaStreamSynchronize(ctx->s);
+    int w = 0;
+    for (auto& x : acc) {
+        if (!x.launches || w >= cap) continue;
+        std::snprintf(stats[w].name, sizeof(stats[w].name), "%s", x.name);
+        stats[w].launches = x.launches;
+        stats[w].total_ms = x.ms;
+        stats[w].bytes_per_launch = x.bytes;
+        ++w;
+    }
+    return w;
+}
+
+}  // extern "C"

@@ -1,0 +1,754 @@
+// paper_2601_20174_b200/csrc/setup_kernels.cu — setup path on sm_100a:
+//
+//   k_csr_import     size_t CSR -> int32 CSR, invariant checks, diagonal
+//   k_block_sweep    S <- S + w D^-1 (0 - A S)   (smoothing.hpp:50-60), also plain Y = A X
+//   k_gram_partial   C = X^T Y per CTA (+ k_gram_reduce), register-tiled fp64
+//   k_eigh           cyclic-by-rounds parallel Jacobi on the m x m Gram (svd.hpp:23-88)
+//   k_dense_mm       Y = X W (/ sigma) for the tall-skinny basis products
+//   k_colsign_*      largest-|entry|-nonnegative column signs (svd.hpp:209-225)
+//   k_chol / k_tri_inv_lower / k_symmetrize   single-CTA k x k kernels
+#include <cfloat>
+
+#include "internal.cuh"
+
+namespace nlsp {
+
+// ------------------------------------------------------------ CSR import --
+// flags bit 0: bad row_ptr, bit 1: column out of range, bit 2: unsorted or
+// duplicate column
+__global__ void k_csr_import(int n, long long nnz, const unsigned long long* rp64,
+                             const unsigned long long* ci64, const double* v, int* rp, int* ci,
+                             double* diag, int* flags, int* max_row) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long b = rp64[i], e = rp64[i + 1];
+        rp[i] = static_cast<int>(b);
+        if (i == n - 1) rp[n] = static_cast<int>(e);
+        if (e < b || e > (unsigned long long)nnz) {
+            atomicOr(flags, 1);
+            diag[i] = 0.0;
+            continue;
+        }
+        atomicMax(max_row, static_cast<int>(e - b));
+        double d = 0.0;
+        long long prev = -1;
+        for (unsigned long long k = b; k < e; ++k) {
+            const unsigned long long c = ci64[k];
+            if (c >= (unsigned long long)n) {
+                atomicOr(flags, 2);
+                ci[k] = 0;
+                continue;
+            }
+            if ((long long)c <= prev) atomicOr(flags, 4);
+            prev = (long long)c;
+            ci[k] = static_cast<int>(c);
+            if ((long long)c == i) d = v[k];
+        }
+        diag[i] = d;
+    }
+}
+
+// w_i = omega * (1 / A_ii) (JacobiSmoother ctor, smoothing.hpp:19-29, then the
+// sweep's omega_ * inv_diag_[i]); flag NumericError on A_ii <= 0
+__global__ void k_wd(int n, const double* diag, double omega, double* wd, int* flag) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double d = diag[i];
+        if (d <= 0.0) {
+            atomicOr(flag, 1);
+            wd[i] = 0.0;
+        } else {
+            wd[i] = omega * (1.0 / d);
+        }
+    }
+}
+
+// ----------------------------------------------------------- block sweep --
+// L lanes per row, columns j = lane + L t. Each output entry accumulates the
+// row's nonzeros in column order with one fma per term (the -O3 -march build of
+// spmm, sparse.hpp:131-146), then x + w (0 - ax) (smoothing.hpp:50-60).
+// MODE 0: sweep (out = fma(w, -acc, in)); MODE 1: plain out = acc.
+template <int L, int T, int MODE>
+__global__ void __launch_bounds__(256) k_block_sweep(int n, const int* __restrict__ rp,
+                                                     const int* __restrict__ ci,
+                                                     const double* __restrict__ v,
+                                                     const double* __restrict__ wd, int m,
+                                                     const double* __restrict__ in,
+                                                     double* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int lr = lane % L;
+    const int sub = lane / L;
+    constexpr int RPW = 32 / L;
+    const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+    for (int c0 = 0; c0 < m; c0 += L * T) {
+        for (long long base = wid * RPW; base < n; base += nw * RPW) {
+            const long long row = base + sub;
+            if (row >= n) continue;
+            double acc[T];
+#pragma unroll
+            for (int t = 0; t < T; ++t) acc[t] = 0.0;
+            const int b = rp[row], e = rp[row + 1];
+            for (int k = b; k < e; ++k) {
+                const double aik = v[k];
+                const double* xr = in + (long long)ci[k] * m;
+#pragma unroll
+                for (int t = 0; t < T; ++t) {
+                    const int j = c0 + lr + L * t;
+                    if (j < m) acc[t] = fma(aik, xr[j], acc[t]);
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+                const int j = c0 + lr + L * t;
+                if (j < m) {
+                    const long long o = row * m + j;
+                    if (MODE == 0) out[o] = fma(wd[row], 0.0 - acc[t], in[o]);
+                    else out[o] = acc[t];
+                }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ Gram --
+// C = X^T Y for tall X (rows x ca), Y (rows x cb), row-major. 256 threads as a
+// 16 x 16 grid; thread (ti, tj) owns a TI x TJ block of C. Row tiles of X and Y
+// are staged in shared memory; each CTA writes its partial C.
+template <int TI>
+__global__ void __launch_bounds__(256) k_gram_partial(long long rows, int ca, int cb,
+                                                      const double* __restrict__ X,
+                                                      const double* __restrict__ Y,
+                                                      double* __restrict__ part) {
+    constexpr int RB = 16;
+    extern __shared__ double sm[];
+    double* xs = sm;                 // RB x (16*TI)
+    double* ys = sm + RB * 16 * TI;  // RB x (16*TI)
+    const int W = 16 * TI;
+    const int ti = threadIdx.x / 16, tj = threadIdx.x % 16;
+    double acc[TI][TI];
+#pragma unroll
+    for (int a = 0; a < TI; ++a)
+#pragma unroll
+        for (int b = 0; b < TI; ++b) acc[a][b] = 0.0;
+    const long long tiles = (rows + RB - 1) / RB;
+    for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const long long r0 = tile * RB;
+        for (int idx = threadIdx.x; idx < RB * W; idx += blockDim.x) {
+            const int rr = idx / W, cc = idx % W;
+            const long long row = r0 + rr;
+            xs[idx] = (row < rows && cc < ca) ? X[row * ca + cc] : 0.0;
+            ys[idx] = (row < rows && cc < cb) ? Y[row * cb + cc] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int rr = 0; rr < RB; ++rr) {
+            double xa[TI], yb[TI];
+#pragma unroll
+            for (int a = 0; a < TI; ++a) xa[a] = xs[rr * W + ti * TI + a];
+#pragma unroll
+            for (int b = 0; b < TI; ++b) yb[b] = ys[rr * W + tj * TI + b];
+#pragma unroll
+            for (int a = 0; a < TI; ++a)
+#pragma unroll
+                for (int b = 0; b < TI; ++b) acc[a][b] = fma(xa[a], yb[b], acc[a][b]);
+        }
+        __syncthreads();
+    }
+    double* out = part + (long long)blockIdx.x * ca * cb;
+#pragma unroll
+    for (int a = 0; a < TI; ++a)
+#pragma unroll
+        for (int b = 0; b < TI; ++b) {
+            const int i = ti * TI + a, j = tj * TI + b;
+            if (i < ca && j < cb) out[i * cb + j] = acc[a][b];
+        }
+}
+
+// fixed-order sum of the CTA partials
+__global__ void k_gram_reduce(int nparts, int count, const double* part, double* c) {
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < count;
+         idx += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int p = 0; p < nparts; ++p) s += part[(long long)p * count + idx];
+        c[idx] = s;
+    }
+}
+
+// ------------------------------------------------------------- eigensolve --
+// Jacobi eigensolver for a symmetric m x m matrix in one CTA. A sweep visits
+// every (p, q) pair once, as m-1 rounds of m/2 disjoint rotations (round-robin
+// tournament), each rotation formed with the reference's formulas
+// (svd.hpp:44-65) and applied as A <- J^T A J, V <- V J. Same convergence test
+// (off-norm <= 1e-12 ||A||_F, at most 30 sweeps) and stable descending sort as
+// svd.hpp:29-40,70-87. A is held as its packed upper triangle.
+struct EighArgs {
+    int m;
+    double* a_packed;  // m(m+1)/2, shared or global scratch
+    double* v;         // m x m, shared or global scratch
+    const double* g;   // input m x m (global)
+    double* evals;     // out m (descending)
+    double* evecs;     // out m x m, columns
+    int* status;       // out: 0 ok, kErrConvergence
+    int* sweeps_out;
+};
+
+__device__ __forceinline__ int pidx(int i, int j, int m) {  // i <= j
+    return i * m - (i * (i - 1)) / 2 + (j - i);
+}
+__device__ __forceinline__ double& pel(double* a, int i, int j, int m) {
+    return i <= j ? a[pidx(i, j, m)] : a[pidx(j, i, m)];
+}
+
+__global__ void __launch_bounds__(1024) k_eigh(EighArgs args, int use_shared) {
+    extern __shared__ double sm[];
+    const int m = args.m;
+    const int mp = m + (m & 1);  // even number of tournament players
+    double* a = use_shared ? sm : args.a_packed;
+    double* v = use_shared ? sm + (m * (m + 1)) / 2 : args.v;
+    __shared__ double cs_c[512], cs_s[512];
+    __shared__ int pp[512], pq[512];
+    __shared__ double red[32];
+    __shared__ double total_s, off_s;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int idx = tid; idx < m * m; idx += nt) {
+        const int i = idx / m, j = idx % m;
+        v[idx] = (i == j) ? 1.0 : 0.0;
+        if (i <= j) a[pidx(i, j, m)] = args.g[idx];
+    }
+    __syncthreads();
+    // ||A||_F over the full matrix (frobenius_norm, dense.hpp:129)
+    auto block_sum = [&](double t) {
+        t = warp_sum(t);
+        if ((tid & 31) == 0) red[tid >> 5] = t;
+        __syncthreads();
+        double r = 0.0;
+        if (tid < 32) {
+            r = tid < (nt >> 5) ? red[tid] : 0.0;
+            r = warp_sum(r);
+        }
+        __syncthreads();
+        return r;  // valid in thread 0 (and warp 0)
+    };
+    double t = 0.0;
+    for (int idx = tid; idx < m * m; idx += nt) {
+        const int i = idx / m, j = idx % m;
+        const double x = pel(a, i, j, m);
+        t = fma(x, x, t);
+    }
+    t = block_sum(t);
+    if (tid == 0) total_s = sqrt(t);
+    __syncthreads();
+    const double total = total_s;
+    int sweeps = 0;
+    int status = isfinite(total) ? 0 : kErrValidation;  // svd.hpp:156 all_finite gate
+    for (; status == 0;) {
+        double o = 0.0;
+        for (int idx = tid; idx < m * m; idx += nt) {
+            const int i = idx / m, j = idx % m;
+            if (i < j) {
+                const double x = a[pidx(i, j, m)];
+                o = fma(2.0 * x, x, o);
+            }
+        }
+        o = block_sum(o);
+        if (tid == 0) off_s = sqrt(o);
+        __syncthreads();
+        if (!(off_s > 1e-12 * total && total > 0.0)) break;
+        if (sweeps >= 30) {
+            status = kErrConvergence;
+            break;
+        }
+        ++sweeps;
+        for (int round = 0; round < mp - 1; ++round) {
+            // pairing (circle method) and rotation parameters
+            for (int w = tid; w < mp / 2; w += nt) {
+                auto player = [&](int pos) {
+                    return pos == 0 ? 0 : 1 + ((pos - 1 + round) % (mp - 1));
+                };
+                int p = player(w), q = player(mp - 1 - w);
+                if (p > q) { const int tmp = p; p = q; q = tmp; }
+                pp[w] = p;
+                pq[w] = q;
+                double c = 1.0, s = 0.0;
+                if (q < m) {
+                    const double apq = a[pidx(p, q, m)];
+                    if (apq != 0.0) {
+                        const double theta = (a[pidx(q, q, m)] - a[pidx(p, p, m)]) / (2.0 * apq);
+                        const double tt = (theta >= 0.0 ? 1.0 : -1.0) /
+                                          (fabs(theta) + sqrt(theta * theta + 1.0));
+                        c = 1.0 / sqrt(tt * tt + 1.0);
+                        s = tt * c;
+                    }
+                }
+                cs_c[w] = c;
+                cs_s[w] = s;
+            }
+            __syncthreads();
+            // A <- J^T A J on 2x2 blocks (pair u rows, pair w cols), u <= w
+            const int np = mp / 2;
+            const int nblocks = np * (np + 1) / 2;
+            for (int bi = tid; bi < nblocks; bi += nt) {
+                // decode bi -> (u, w) with u <= w
+                int u = 0, rem = bi;
+                while (rem >= np - u) {
+                    rem -= np - u;
+                    ++u;
+                }
+                const int w = u + rem;
+                const int p1 = pp[u], q1 = pq[u], p2 = pp[w], q2 = pq[w];
+                const double c1 = cs_c[u], s1 = cs_s[u], c2 = cs_c[w], s2 = cs_s[w];
+                const bool q1v = q1 < m, q2v = q2 < m;
+                if (u == w) {
+                    if (!q1v) continue;
+                    const double xpp = a[pidx(p1, p1, m)], xpq = a[pidx(p1, q1, m)],
+                                 xqq = a[pidx(q1, q1, m)];
+                    // columns: y(., p) = c x(., p) - s x(., q); y(., q) = s x(., p) + c x(., q)
+                    const double ypp = c1 * xpp - s1 * xpq, ypq = s1 * xpp + c1 * xpq;
+                    const double yqp = c1 * xpq - s1 * xqq, yqq = s1 * xpq + c1 * xqq;
+                    // rows: z(p, .) = c y(p, .) - s y(q, .); z(q, .) = s y(p, .) + c y(q, .)
+                    a[pidx(p1, p1, m)] = c1 * ypp - s1 * yqp;
+                    a[pidx(p1, q1, m)] = c1 * ypq - s1 * yqq;
+                    a[pidx(q1, q1, m)] = s1 * ypq + c1 * yqq;
+                } else {
+                    // rows {p1, q1} (rotation 1), cols {p2, q2} (rotation 2)
+                    const double xpp = pel(a, p1, p2, m);
+                    const double xpq = q2v ? pel(a, p1, q2, m) : 0.0;
+                    const double xqp = q1v ? pel(a, q1, p2, m) : 0.0;
+                    const double xqq = (q1v && q2v) ? pel(a, q1, q2, m) : 0.0;
+                    const double ypp = c2 * xpp - s2 * xpq, ypq = s2 * xpp + c2 * xpq;
+                    const double yqp = c2 * xqp - s2 * xqq, yqq = s2 * xqp + c2 * xqq;
+                    pel(a, p1, p2, m) = c1 * ypp - s1 * yqp;
+                    if (q2v) pel(a, p1, q2, m) = c1 * ypq - s1 * yqq;
+                    if (q1v) pel(a, q1, p2, m) = s1 * ypp + c1 * yqp;
+                    if (q1v && q2v) pel(a, q1, q2, m) = s1 * ypq + c1 * yqq;
+                }
+            }
+            // V <- V J (svd.hpp:61-65)
+            for (int idx = tid; idx < m * np; idx += nt) {
+                const int i = idx / np, w = idx % np;
+                const int p = pp[w], q = pq[w];
+                if (q >= m) continue;
+                const double c = cs_c[w], s = cs_s[w];
+                const double vip = v[i * m + p], viq = v[i * m + q];
+                v[i * m + p] = c * vip - s * viq;
+                v[i * m + q] = s * vip + c * viq;
+            }
+            __syncthreads();
+        }
+    }
+    // stable descending order: rank_i = #{j : ev_j > ev_i} + #{j < i : ev_j == ev_i}
+    for (int i = tid; i < m; i += nt) {
+        const double ei = a[pidx(i, i, m)];
+        int rank = 0;
+        for (int j = 0; j < m; ++j) {
+            const double ej = a[pidx(j, j, m)];
+            rank += (ej > ei) || (ej == ei && j < i);
+        }
+        args.evals[rank] = ei;
+        for (int r = 0; r < m; ++r) args.evecs[r * m + rank] = v[r * m + i];
+    }
+    if (tid == 0) {
+        *args.status = status;
+        *args.sweeps_out = sweeps;
+    }
+}
+
+// ------------------------------------------------------------- dense mm --
+// Y[i, j] = (sum_l X[i, l] W[l, j]) (/ sigma[j]) for j < kout, accumulated in
+// l order (svd.hpp:193-199). One warp per row; W staged in shared memory.
+template <int T>
+__global__ void __launch_bounds__(256) k_dense_mm(long long rows, int m, int kout,
+                                                  const double* __restrict__ X,
+                                                  const double* __restrict__ Wg,
+                                                  const double* __restrict__ sigma,
+                                                  double* __restrict__ Y, int use_shared) {
+    extern __shared__ double sw[];
+    const double* W = Wg;
+    if (use_shared) {
+        for (int idx = threadIdx.x; idx < m * kout; idx += blockDim.x) sw[idx] = Wg[idx];
+        __syncthreads();
+        W = sw;
+    }
+    const int lane = threadIdx.x & 31;
+    const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+    for (long long row = wid; row < rows; row += nw) {
+        const double* xr = X + row * m;
+        double acc[T];
+#pragma unroll
+        for (int t = 0; t < T; ++t) acc[t] = 0.0;
+        for (int l0 = 0; l0 < m; l0 += 32) {
+            const double xl = (l0 + lane < m) ? xr[l0 + lane] : 0.0;
+            const int lim = min(32, m - l0);
+            for (int u = 0; u < lim; ++u) {
+                const double s = __shfl_sync(0xffffffffu, xl, u);
+                const double* wr = W + (long long)(l0 + u) * kout;
+#pragma unroll
+                for (int t = 0; t < T; ++t) {
+                    const int j = lane + 32 * t;
+                    if (j < kout) acc[t] = fma(s, wr[j], acc[t]);
+                }
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+            const int j = lane + 32 * t;
+            if (j < kout) Y[row * kout + j] = sigma ? acc[t] / sigma[j] : acc[t];
+        }
+    }
+}
+
+// -------------------------------------------------------------- col signs --
+// per CTA: for each column, (max |x|, first row attaining it, x at that row)
+__global__ void k_colmax_partial(long long rows, int k, const double* __restrict__ P,
+                                 double* pmag, long long* pidx_out, double* pval) {
+    extern __shared__ unsigned char smraw[];
+    double* bm = reinterpret_cast<double*>(smraw);
+    long long* bi = reinterpret_cast<long long*>(bm + blockDim.x);
+    double* bv = reinterpret_cast<double*>(bi + blockDim.x);
+    for (int j = 0; j < k; ++j) {
+        double best = -1.0, val = 0.0;
+        long long arg = -1;
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < rows;
+             i += (long long)gridDim.x * blockDim.x) {
+            const double x = P[i * k + j];
+            const double mag = fabs(x);
+            if (mag > best) {  // rows visited in increasing order per thread
+                best = mag;
+                arg = i;
+                val = x;
+            }
+        }
+        bm[threadIdx.x] = best;
+        bi[threadIdx.x] = arg;
+        bv[threadIdx.x] = val;
+        __syncthreads();
+        for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+            if (threadIdx.x < s) {
+                const double m2 = bm[threadIdx.x + s];
+                const long long i2 = bi[threadIdx.x + s];
+                const bool take = (m2 > bm[threadIdx.x]) ||
+                                  (m2 == bm[threadIdx.x] && i2 >= 0 &&
+                                   (bi[threadIdx.x] < 0 || i2 < bi[threadIdx.x]));
+                if (take) {
+                    bm[threadIdx.x] = m2;
+                    bi[threadIdx.x] = i2;
+                    bv[threadIdx.x] = bv[threadIdx.x + s];
+                }
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            pmag[(long long)blockIdx.x * k + j] = bm[0];
+            pidx_out[(long long)blockIdx.x * k + j] = bi[0];
+            pval[(long long)blockIdx.x * k + j] = bv[0];
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_colsign_final(int nparts, int k, const double* pmag, const long long* pidx_in,
+                                const double* pval, double* sign) {
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+        double best = -1.0, val = 0.0;
+        long long arg = -1;
+        for (int p = 0; p < nparts; ++p) {
+            const double m2 = pmag[(long long)p * k + j];
+            const long long i2 = pidx_in[(long long)p * k + j];
+            if (i2 < 0) continue;
+            if (m2 > best || (m2 == best && (arg < 0 || i2 < arg))) {
+                best = m2;
+                arg = i2;
+                val = pval[(long long)p * k + j];
+            }
+        }
+        sign[j] = (arg >= 0 && val < 0.0) ? -1.0 : 1.0;
+    }
+}
+
+__global__ void k_colscale(long long rows, int k, double* P, const double* sign) {
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < rows * k;
+         idx += (long long)gridDim.x * blockDim.x) {
+        if (sign[idx % k] < 0.0) P[idx] = -P[idx];
+    }
+}
+
+// ------------------------------------------------------- small k x k ops --
+// Cholesky with the reference's symmetry gate (1e-10 max|a|) and pivot test
+// (cholesky.hpp:15-37). rank_tol > 0 additionally flags pivots below it as
+// rank deficiency (qr_thin's 1e-12 ||M||_F test on R_jj, qr.hpp:38-40), with
+// rank_tol computed here from the trace when rank_rel > 0.
+__global__ void __launch_bounds__(256) k_chol(int k, const double* __restrict__ A,
+                                              double* __restrict__ L, double rank_rel,
+                                              int* status) {
+    __shared__ double red[256];
+    __shared__ double djj;
+    __shared__ int fail;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    double mx = 0.0, tr = 0.0;
+    for (int idx = tid; idx < k * k; idx += nt) {
+        mx = fmax(mx, fabs(A[idx]));
+        L[idx] = 0.0;
+    }
+    for (int i = tid; i < k; i += nt) tr += A[i * k + i];
+    red[tid] = mx;
+    __syncthreads();
+    for (int s = nt / 2; s > 0; s >>= 1) {
+        if (tid < s) red[tid] = fmax(red[tid], red[tid + s]);
+        __syncthreads();
+    }
+    const double scale = red[0] > 0.0 ? red[0] : 1.0;
+    __syncthreads();
+    red[tid] = tr;
+    __syncthreads();
+    for (int s = nt / 2; s > 0; s >>= 1) {
+        if (tid < s) red[tid] += red[tid + s];
+        __syncthreads();
+    }
+    const double rank_tol = rank_rel > 0.0 ? rank_rel * sqrt(fmax(red[0], 0.0)) : 0.0;
+    if (tid == 0) fail = 0;
+    __syncthreads();
+    for (int idx = tid; idx < k * k; idx += nt) {
+        const int i = idx / k, j = idx % k;
+        if (j > i && fabs(A[i * k + j] - A[j * k + i]) > 1e-10 * scale) atomicOr(&fail, 1);
+    }
+    __syncthreads();
+    if (fail) {
+        if (tid == 0) *status = kErrNotSpd;
+        return;
+    }
+    for (int j = 0; j < k; ++j) {
+        if (tid == 0) {
+            double d = A[j * k + j];
+            for (int q = 0; q < j; ++q) d = fma(-L[j * k + q], L[j * k + q], d);
+            if (d <= 0.0) {
+                fail = rank_rel > 0.0 ? 2 : 1;
+            } else {
+                const double sd = sqrt(d);
+                if (rank_rel > 0.0 && sd < rank_tol) fail = 2;
+                djj = sd;
+                L[j * k + j] = sd;
+            }
+        }
+        __syncthreads();
+        if (fail) break;
+        const double lj = djj;
+        for (int i = j + 1 + tid; i < k; i += nt) {
+            double s = A[i * k + j];
+            for (int q = 0; q < j; ++q) s = fma(-L[i * k + q], L[j * k + q], s);
+            L[i * k + j] = s / lj;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) *status = fail == 0 ? 0 : (fail == 2 ? kErrRank : kErrNotSpd);
+}
+
+// U = L^-T (upper triangular), column j of L^-1 by forward substitution
+__global__ void k_tri_inv_lower_t(int k, const double* __restrict__ L, double* __restrict__ U) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+        // x = L^-1 e_j ; x_i = 0 for i < j
+        for (int i = 0; i < k; ++i) {
+            double xi;
+            if (i < j) {
+                xi = 0.0;
+            } else {
+                double s = (i == j) ? 1.0 : 0.0;
+                for (int q = j; q < i; ++q) s = fma(-L[i * k + q], U[j * k + q], s);
+                xi = s / L[i * k + i];
+            }
+            U[j * k + i] = xi;  // row j of U^T... U stored as (L^-1)^T: U[j][i] = (L^-1)[i][j]
+        }
+    }
+}
+
+// c_ij = c_ji = (c_ij + c_ji) / 2 (two_level.hpp:46-51)
+__global__ void k_symmetrize(int k, double* C) {
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < k * k;
+         idx += gridDim.x * blockDim.x) {
+        const int i = idx / k, j = idx % k;
+        if (i < j) {
+            const double v = 0.5 * (C[i * k + j] + C[j * k + i]);
+            C[i * k + j] = v;
+            C[j * k + i] = v;
+        }
+    }
+}
+
+// sigma_i = sqrt(max(0, lambda_i <= floor ? 0 : lambda_i)), floor = 64 eps lambda_0
+// (svd.hpp:174-179); W[:, :k] = V[:, :k]; flag if any sigma_j (j < k) <= 1e-13 sigma_0
+__global__ void k_sigma(int m, int k, const double* evals, const double* evecs, double* sigma,
+                        double* W, int* status) {
+    __shared__ double smax;
+    if (threadIdx.x == 0) {
+        const double fl = evals[0] * 64.0 * DBL_EPSILON;
+        for (int i = 0; i < m; ++i) {
+            const double lam = evals[i] <= fl ? 0.0 : evals[i];
+            sigma[i] = sqrt(fmax(0.0, lam));
+        }
+        smax = sigma[0];
+        int bad = 0;
+        for (int j = 0; j < k; ++j)
+            if (!(sigma[j] > smax * 1e-13)) bad = 1;
+        *status = bad ? kErrNumeric : 0;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < m * k; idx += blockDim.x) {
+        const int l = idx / k, j = idx % k;
+        W[idx] = evecs[l * m + j];
+    }
+}
+
+// =========================================================== launchers ==
+
+namespace {
+inline void count(const LaunchCtx& c) { ++*c.launches; }
+int grid_for(const LaunchCtx& c, long long work, int threads, int per_sm = 4) {
+    long long g = (work + threads - 1) / threads;
+    const long long cap = (long long)c.num_sms * per_sm;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return static_cast<int>(g);
+}
+}  // namespace
+
+void launch_csr_import(const LaunchCtx& c, int n, long long nnz, const unsigned long long* rp64,
+                       const unsigned long long* ci64, const double* v, int* rp, int* ci,
+                       double* diag, int* flags, int* max_row) {
+    k_csr_import<<<grid_for(c, n, 256, 8), 256, 0, c.s>>>(n, nnz, rp64, ci64, v, rp, ci, diag,
+                                                          flags, max_row);
+    count(c);
+}
+
+void launch_wd(const LaunchCtx& c, int n, const double* diag, double omega, double* wd, int* flag) {
+    k_wd<<<grid_for(c, n, 256), 256, 0, c.s>>>(n, diag, omega, wd, flag);
+    count(c);
+}
+
+// mode 0: sweep, 1: plain product
+void launch_block_op(const LaunchCtx& c, int mode, int n, const int* rp, const int* ci,
+                     const double* v, const double* wd, int m, const double* in, double* out) {
+    const int g = grid_for(c, (long long)n * 32, 256, 8);
+#define NLSP_BS(L, T)                                                                         \
+    do {                                                                                      \
+        if (mode == 0) k_block_sweep<L, T, 0><<<g, 256, 0, c.s>>>(n, rp, ci, v, wd, m, in, out); \
+        else k_block_sweep<L, T, 1><<<g, 256, 0, c.s>>>(n, rp, ci, v, wd, m, in, out);        \
+    } while (0)
+    if (m <= 8) NLSP_BS(8, 1);
+    else if (m <= 16) NLSP_BS(16, 1);
+    else if (m <= 32) NLSP_BS(32, 1);
+    else if (m <= 64) NLSP_BS(32, 2);
+    else if (m <= 96) NLSP_BS(32, 3);
+    else NLSP_BS(32, 4);
+#undef NLSP_BS
+    count(c);
+}
+
+// C (ca x cb) = X^T Y; part must hold grid * ca * cb doubles (grid <= kMaxGrid)
+int gram_grid(const LaunchCtx& c, long long rows) {
+    long long g = (rows + 15) / 16;
+    const long long cap = (long long)c.num_sms * 2;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return static_cast<int>(g);
+}
+
+void launch_gram(const LaunchCtx& c, long long rows, int ca, int cb, const double* X,
+                 const double* Y, double* part, double* C) {
+    const int g = gram_grid(c, rows);
+    const int w = ca > cb ? ca : cb;
+    const int ti = (w + 15) / 16;
+#define NLSP_G(T)                                                                       \
+    do {                                                                                \
+        const size_t smem = 2 * 16 * 16 * (T) * sizeof(double);                         \
+        k_gram_partial<T><<<g, 256, smem, c.s>>>(rows, ca, cb, X, Y, part);             \
+    } while (0)
+    switch (ti) {
+        case 1: NLSP_G(1); break;
+        case 2: NLSP_G(2); break;
+        case 3: NLSP_G(3); break;
+        case 4: NLSP_G(4); break;
+        case 5: NLSP_G(5); break;
+        case 6: NLSP_G(6); break;
+        case 7: NLSP_G(7); break;
+        default: NLSP_G(8); break;
+    }
+#undef NLSP_G
+    count(c);
+    k_gram_reduce<<<grid_for(c, (long long)ca * cb, 256), 256, 0, c.s>>>(g, ca * cb, part, C);
+    count(c);
+}
+
+void launch_eigh(const LaunchCtx& c, int m, const double* g, double* evals, double* evecs,
+                 double* scratch_a, double* scratch_v, int* status, int* sweeps) {
+    EighArgs a{m, scratch_a, scratch_v, g, evals, evecs, status, sweeps};
+    const size_t need = (size_t)(m * (m + 1) / 2 + m * m) * sizeof(double);
+    const int use_shared = need <= 200 * 1024;
+    if (use_shared) {
+        cudaFuncSetAttribute(k_eigh, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need);
+        k_eigh<<<1, 1024, need, c.s>>>(a, 1);
+    } else {
+        k_eigh<<<1, 1024, 0, c.s>>>(a, 0);
+    }
+    count(c);
+}
+
+void launch_dense_mm(const LaunchCtx& c, long long rows, int m, int kout, const double* X,
+                     const double* W, const double* sigma, double* Y) {
+    const size_t wbytes = (size_t)m * kout * sizeof(double);
+    const int use_shared = wbytes <= 96 * 1024;
+    const int g = grid_for(c, rows * 32, 256, 8);
+#define NLSP_MM(T)                                                                          \
+    do {                                                                                    \
+        if (use_shared) {                                                                   \
+            cudaFuncSetAttribute(k_dense_mm<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                 (int)wbytes);                                              \
+            k_dense_mm<T><<<g, 256, wbytes, c.s>>>(rows, m, kout, X, W, sigma, Y, 1);       \
+        } else {                                                                            \
+            k_dense_mm<T><<<g, 256, 0, c.s>>>(rows, m, kout, X, W, sigma, Y, 0);            \
+        }                                                                                   \
+    } while (0)
+    const int t = (kout + 31) / 32;
+    if (t <= 1) NLSP_MM(1);
+    else if (t == 2) NLSP_MM(2);
+    else if (t <= 4) NLSP_MM(4);
+    else NLSP_MM(8);
+#undef NLSP_MM
+    count(c);
+}
+
+void launch_colsign(const LaunchCtx& c, long long rows, int k, double* P, double* pmag,
+                    long long* pidx_buf, double* pval, double* sign) {
+    const int g = grid_for(c, rows, 256, 1);
+    const size_t smem = 256 * (sizeof(double) * 2 + sizeof(long long));
+    k_colmax_partial<<<g, 256, smem, c.s>>>(rows, k, P, pmag, pidx_buf, pval);
+    count(c);
+    k_colsign_final<<<1, 256, 0, c.s>>>(g, k, pmag, pidx_buf, pval, sign);
+    count(c);
+    k_colscale<<<grid_for(c, rows * k, 256), 256, 0, c.s>>>(rows, k, P, sign);
+    count(c);
+}
+
+void launch_chol(const LaunchCtx& c, int k, const double* A, double* L, double rank_rel,
+                 int* status) {
+    k_chol<<<1, 256, 0, c.s>>>(k, A, L, rank_rel, status);
+    count(c);
+}
+
+void launch_tri_inv_t(const LaunchCtx& c, int k, const double* L, double* U) {
+    k_tri_inv_lower_t<<<(k + 127) / 128, 128, 0, c.s>>>(k, L, U);
+    count(c);
+}
+
+void launch_symmetrize(const LaunchCtx& c, int k, double* C) {
+    k_symmetrize<<<(k * k + 255) / 256, 256, 0, c.s>>>(k, C);
+    count(c);
+}
+
+void launch_sigma(const LaunchCtx& c, int m, int k, const double* evals, const double* evecs,
+                  double* sigma, double* W, int* status) {
+    k_sigma<<<1, 256, 0, c.s>>>(m, k, evals, evecs, sigma, W, status);
+    count(c);
+}
+
+}  // namespace nlsp

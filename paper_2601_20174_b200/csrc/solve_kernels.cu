@@ -1,0 +1,678 @@
+// paper_2601_20174_b200/csrc/solve_kernels.cu — the PCG hot loop on sm_100a.
+//
+// One PCG iteration of two_level.hpp:141-191 with the two-level operator of
+// two_level.hpp:60-81 (nu1 = nu2 = 1) is five kernels, each a single pass over
+// HBM with its reductions finished by the last CTA to arrive (deterministic
+// fixed-order sums, no fp64 atomics):
+//
+//   k_spmv_p    p = z + beta p  (fused into the gather), q = A p, p.q -> alpha
+//   k_update    x += alpha p, r -= alpha q, ||r|| -> history, convergence test
+//   k_restrict  res = r - A (w D^-1 r), c = P^T res, last CTA: L L^T e = c
+//   k_prolong   z2 = w D^-1 r + P e
+//   k_sweep     z = z2 + w D^-1 (r - A z2), r.z -> beta            (post-sweep)
+//
+// plus a one-thread k_loop_ctl that advances the iteration and drives the CUDA
+// graph WHILE node. CSR rows and basis rows are handled by groups of 8 lanes
+// (4 rows per warp): the 8 lanes read a row's nonzeros as one coalesced run and
+// the row's k basis entries as 16-B loads, so the SpMV result of a row is
+// already in the registers of the lanes that stream that row of P.
+#include "internal.cuh"
+
+namespace nlsp {
+
+// ----------------------------------------------------------------- gathers --
+struct GPlain {
+    const double* x;
+    __device__ __forceinline__ double operator()(int j) const { return x[j]; }
+};
+// p_j = z_j + beta p_j (two_level.hpp:182, contracted to one fma), or z_j when
+// p is first formed (two_level.hpp:154)
+struct GPupd {
+    const double* z;
+    const double* pp;
+    double beta;
+    bool first;
+    __device__ __forceinline__ double operator()(int j) const {
+        return first ? z[j] : fma(beta, pp[j], z[j]);
+    }
+};
+// first pre-sweep from z = 0: z_j = (w dinv_j)(r_j - 0) (smoothing.hpp:40 with x = 0)
+struct GWdr {
+    const double* wd;
+    const double* r;
+    __device__ __forceinline__ double operator()(int j) const { return wd[j] * r[j]; }
+};
+
+// y_row = sum_k v_k g(col_k) by an 8-lane group; every lane of the group returns
+// the full sum.
+template <class Gat>
+__device__ __forceinline__ double group_dot(const int* __restrict__ rp, const int* __restrict__ ci,
+                                            const double* __restrict__ v, int row, bool valid,
+                                            const Gat& g, int l) {
+    double s = 0.0;
+    if (valid) {
+        const int b = __ldg(rp + row), e = __ldg(rp + row + 1);
+        for (int k = b + l; k < e; k += kGroup) s = fma(__ldg(v + k), g(__ldg(ci + k)), s);
+    }
+    return group_sum(s);
+}
+
+// CTA sum of NV values, partial per CTA, and the last-arriving CTA reduces all
+// partials in a fixed order. Returns true (in every thread) only in the last
+// CTA, where tot[] holds the grid-wide sums (valid in all threads).
+template <int NV>
+__device__ __forceinline__ bool grid_reduce(double (&v)[NV], double* part, unsigned int* counter,
+                                            double (&tot)[NV]) {
+    __shared__ double sm[NV][32];
+    __shared__ double fin[NV];
+    __shared__ int is_last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        const double t = warp_sum(v[j]);
+        if (lane == 0) sm[j][warp] = t;
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            double t = lane < nw ? sm[j][lane] : 0.0;
+            t = warp_sum(t);
+            if (lane == 0) part[blockIdx.x * NV + j] = t;
+        }
+        if (lane == 0) {
+            __threadfence();
+            const unsigned int tk = atomicAdd(counter, 1u);
+            is_last = (tk == gridDim.x - 1);
+        }
+    }
+    __syncthreads();
+    if (!is_last) return false;
+    __threadfence();
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        double t = 0.0;
+        for (int b = threadIdx.x; b < gridDim.x; b += blockDim.x) t += __ldcg(part + b * NV + j);
+        t = warp_sum(t);
+        if (lane == 0) sm[j][warp] = t;
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            double t = lane < nw ? sm[j][lane] : 0.0;
+            t = warp_sum(t);
+            if (lane == 0) fin[j] = t;
+        }
+        if (lane == 0) *counter = 0u;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NV; ++j) tot[j] = fin[j];
+    return true;
+}
+
+#define ROW_LOOP_BEGIN(n)                                                          \
+    const int lane_ = threadIdx.x & 31;                                            \
+    const int l = lane_ & (kGroup - 1);                                            \
+    const int grp = lane_ >> 3;                                                    \
+    const long long wid_ = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; \
+    const long long nwarps_ = (gridDim.x * (long long)blockDim.x) >> 5;            \
+    for (long long base_ = wid_ * kRowsPerWarp; base_ < (n); base_ += nwarps_ * kRowsPerWarp) { \
+        const int row = static_cast<int>(base_) + grp;                             \
+        const bool valid = row < (n);
+
+#define ROW_LOOP_END }
+
+// ------------------------------------------------------------------ state --
+struct PcgParamsHost {
+    double delta;
+    long long max_it;
+};
+
+__global__ void k_state_init(PcgState* st, double delta, long long max_it) {
+    st->rz = st->rz_new = st->pap = st->alpha = st->beta = st->rr = 0.0;
+    st->bnorm = 0.0;
+    st->delta = delta;
+    st->true_res = 0.0;
+    st->last_rel = 0.0;
+    st->it = 0;
+    st->max_it = max_it;
+    st->iterations = 0;
+    st->done = 0;
+    st->converged = 0;
+    st->error = 0;
+    st->first = 1;
+}
+
+// ||b||_2 (two_level.hpp:143-146) and r = b, x = 0; zero rhs -> ValidationError
+__global__ void __launch_bounds__(kThreads) k_bnorm(SolveArgs a) {
+    double s[1] = {0.0};
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double bi = a.b[i];
+        a.r[i] = bi;
+        a.x[i] = 0.0;
+        s[0] = fma(bi, bi, s[0]);
+    }
+    double tot[1];
+    if (grid_reduce<1>(s, a.partials, &a.st->counter[kTkBnorm], tot) && threadIdx.x == 0) {
+        const double bn = sqrt(tot[0]);
+        a.st->bnorm = bn;
+        if (bn == 0.0) {
+            a.st->error = kErrValidation;
+            a.st->done = 1;
+        }
+    }
+}
+
+// z = r (identity) or z = r / A_ii (Jacobi, two_level.hpp:107-118); r.z
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) k_init_simple(SolveArgs a) {
+    if (a.st->done) return;
+    double s[1] = {0.0};
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double ri = a.r[i];
+        const double zi = MODE == 1 ? ri / a.diag[i] : ri;
+        a.z[i] = zi;
+        s[0] = fma(ri, zi, s[0]);
+    }
+    double tot[1];
+    if (grid_reduce<1>(s, a.partials, &a.st->counter[kTkInit], tot) && threadIdx.x == 0)
+        a.st->rz_new = tot[0];
+}
+
+// rz = r.z of the initial apply; the loop starts with p = z (two_level.hpp:153-156)
+__global__ void k_init_ctl(PcgState* st) {
+    st->rz = st->rz_new;
+    st->first = 1;
+    st->it = 0;
+    if (st->max_it <= 0) st->done = 1;
+}
+
+// -------------------------------------------------------------- k_spmv_p --
+// p = z + beta p (written to the other ping-pong buffer), q = A p, p.q;
+// last CTA: p^T A p <= 0 -> NotSpdError (two_level.hpp:159-163), alpha = rz / pap
+__global__ void __launch_bounds__(kThreads) k_spmv_p(SolveArgs a) {
+    PcgState* st = a.st;
+    if (st->done) return;
+    const bool odd = st->it & 1;
+    const double* pp = odd ? a.p0 : a.p1;
+    double* pc = odd ? a.p1 : a.p0;
+    const GPupd g{a.z, pp, st->beta, st->first != 0};
+    double s[1] = {0.0};
+    ROW_LOOP_BEGIN(a.n)
+        const double y = group_dot(a.rp, a.ci, a.v, row, valid, g, l);
+        if (valid && l == 0) {
+            const double pi = g(row);
+            pc[row] = pi;
+            a.q[row] = y;
+            s[0] = fma(pi, y, s[0]);
+        }
+    ROW_LOOP_END
+    double tot[1];
+    if (grid_reduce<1>(s, a.partials, &st->counter[kTkSpmvP], tot) && threadIdx.x == 0) {
+        const double pap = tot[0];
+        st->pap = pap;
+        if (pap <= 0.0) {
+            st->error = kErrNotSpd;
+            st->done = 1;
+        } else {
+            st->alpha = st->rz / pap;
+        }
+    }
+}
+
+// -------------------------------------------------------------- k_update --
+// x += alpha p, r -= alpha q (two_level.hpp:164-167), ||r|| / ||b|| into the
+// history, convergence test on the recurrence residual (:168-176). MODE 1/2:
+// identity / Jacobi preconditioner fused (z and r.z in the same pass).
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) k_update(SolveArgs a) {
+    PcgState* st = a.st;
+    if (st->done) return;
+    const double alpha = st->alpha;
+    const double* p = (st->it & 1) ? a.p1 : a.p0;
+    double s[2] = {0.0, 0.0};
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.n;
+         i += (long long)gridDim.x * blockDim.x) {
+        a.x[i] = fma(alpha, p[i], a.x[i]);
+        const double ri = fma(-alpha, a.q[i], a.r[i]);
+        a.r[i] = ri;
+        s[0] = fma(ri, ri, s[0]);
+        if (MODE != 0) {
+            const double zi = MODE == 2 ? ri / a.diag[i] : ri;
+            a.z[i] = zi;
+            s[1] = fma(ri, zi, s[1]);
+        }
+    }
+    double tot[2];
+    if (grid_reduce<2>(s, a.partials, &st->counter[kTkUpdate], tot) && threadIdx.x == 0) {
+        const double rel = sqrt(tot[0]) / st->bnorm;
+        st->rr = tot[0];
+        st->last_rel = rel;
+        a.hist[st->it] = rel;
+        st->iterations = st->it + 1;
+        if (rel < st->delta) {
+            st->converged = 1;
+            st->done = 1;
+        }
+        if (MODE != 0) st->rz_new = tot[1];
+    }
+}
+
+// beta = rz' / rz, p-update bookkeeping, iteration advance, graph WHILE control
+__global__ void k_loop_ctl(PcgState* st, cudaGraphConditionalHandle h, int use_cond) {
+    if (!st->done) {
+        st->beta = st->rz_new / st->rz;
+        st->rz = st->rz_new;
+        st->first = 0;
+        st->it += 1;
+        if (st->it >= st->max_it) st->done = 1;
+    }
+    if (use_cond && st->done) cudaGraphSetConditional(h, 0);
+}
+
+// --------------------------------------------------------------- k_sweep --
+// z_out = z_in + (w dinv)(r - A z_in) (smoothing.hpp:34-41, contracted), with
+// z_in given by the gather (implicit first sweep or a buffer); RZ: r.z_out
+template <class Gat, bool RZ>
+__global__ void __launch_bounds__(kThreads) k_sweep(SolveArgs a, Gat g, double* zout) {
+    PcgState* st = a.st;
+    if (st->done) return;
+    double s[1] = {0.0};
+    ROW_LOOP_BEGIN(a.n)
+        const double y = group_dot(a.rp, a.ci, a.v, row, valid, g, l);
+        if (valid && l == 0) {
+            const double ri = a.r[row];
+            const double zi = fma(a.wd[row], ri - y, g(row));
+            zout[row] = zi;
+            if (RZ) s[0] = fma(ri, zi, s[0]);
+        }
+    ROW_LOOP_END
+    if (RZ) {
+        double tot[1];
+        if (grid_reduce<1>(s, a.partials, &st->counter[kTkSweep], tot) && threadIdx.x == 0)
+            st->rz_new = tot[0];
+    }
+}
+
+// ----------------------------------------------------- coarse solve (1 warp) --
+// L y = c, L^T e = y (cholesky.hpp:41-57), column-oriented so each y_i keeps the
+// reference's left-to-right accumulation order in the forward sweep.
+__device__ void coarse_solve_warp(const double* __restrict__ L, int k, double* ys, double* e) {
+    const int lane = threadIdx.x & 31;
+    for (int j = 0; j < k; ++j) {
+        __syncwarp();
+        const double yj = ys[j] / L[j * k + j];
+        __syncwarp();
+        if (lane == 0) ys[j] = yj;
+        for (int i = j + 1 + lane; i < k; i += 32) ys[i] = fma(-L[i * k + j], yj, ys[i]);
+    }
+    for (int j = k - 1; j >= 0; --j) {
+        __syncwarp();
+        const double xj = ys[j] / L[j * k + j];
+        __syncwarp();
+        if (lane == 0) ys[j] = xj;
+        for (int i = lane; i < j; i += 32) ys[i] = fma(-L[j * k + i], xj, ys[i]);
+    }
+    __syncwarp();
+    for (int i = lane; i < k; i += 32) e[i] = ys[i];
+}
+
+// ------------------------------------------------------------ k_restrict --
+// res = r - A z_pre (two_level.hpp:63-67); c = P^T res (:69-72); the last CTA
+// sums the per-CTA c partials in a fixed order and solves A_c e = c (:73).
+// ZMODE 0: z_pre = 0 (nu1 = 0), 1: z_pre = w D^-1 r implicit (nu1 = 1), 2: buffer.
+template <int PPL, int ZMODE>
+__global__ void __launch_bounds__(kThreads) k_restrict(SolveArgs a, const double* zpre) {
+    PcgState* st = a.st;
+    if (st->done) return;
+    __shared__ double cs[kThreads / 32][2 * 8 * PPL];
+    __shared__ double red[kThreads];
+    __shared__ double ys[2 * 8 * PPL];
+    const int ld = a.k + (a.k & 1);
+    const int pairs = ld >> 1;
+    double acc[2 * PPL];
+#pragma unroll
+    for (int t = 0; t < 2 * PPL; ++t) acc[t] = 0.0;
+    const GWdr gw{a.wd, a.r};
+    const GPlain gp{zpre};
+    ROW_LOOP_BEGIN(a.n)
+        double y = 0.0;
+        if (ZMODE == 1) y = group_dot(a.rp, a.ci, a.v, row, valid, gw, l);
+        if (ZMODE == 2) y = group_dot(a.rp, a.ci, a.v, row, valid, gp, l);
+        if (valid) {
+            const double res = a.r[row] - y;
+            const double* prow = a.P + (long long)row * ld;
+#pragma unroll
+            for (int t = 0; t < PPL; ++t) {
+                const int pi = l + kGroup * t;
+                if (pi < pairs) {
+                    const double2 pv = ld_stream2(prow + 2 * pi);
+                    acc[2 * t] = fma(pv.x, res, acc[2 * t]);
+                    acc[2 * t + 1] = fma(pv.y, res, acc[2 * t + 1]);
+                }
+            }
+        }
+    ROW_LOOP_END
+    // groups of a warp -> lanes 0..7, warps -> shared, CTA partial -> global
+#pragma unroll
+    for (int t = 0; t < 2 * PPL; ++t) {
+        acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], 8);
+        acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], 16);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (lane < kGroup) {
+#pragma unroll
+        for (int t = 0; t < PPL; ++t) {
+            const int pi = lane + kGroup * t;
+            if (pi < pairs) {
+                cs[warp][2 * pi] = acc[2 * t];
+                cs[warp][2 * pi + 1] = acc[2 * t + 1];
+            }
+        }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < ld; c += blockDim.x) {
+        double t = 0.0;
+        for (int w = 0; w < nw; ++w) t += cs[w][c];
+        a.partials[(long long)blockIdx.x * ld + c] = t;
+    }
+    __shared__ int is_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned int tk = atomicAdd(&st->counter[kTkRestrict], 1u);
+        is_last = (tk == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    // fixed-order grid sum: S slices of CTAs per column, then slices in order
+    const int S = blockDim.x / ld;  // ld <= 256 enforced on the host
+    const int c = threadIdx.x % ld, sl = threadIdx.x / ld;
+    if (sl < S) {
+        double t = 0.0;
+        for (int b = sl; b < gridDim.x; b += S) t += __ldcg(a.partials + (long long)b * ld + c);
+        red[threadIdx.x] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x < ld) {
+        double t = 0.0;
+        for (int q = 0; q < S; ++q) t += red[q * ld + threadIdx.x];
+        ys[threadIdx.x] = t;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        coarse_solve_warp(a.L, a.k, ys, a.e);
+        if (lane == 0) {
+            if (a.k & 1) a.e[a.k] = 0.0;  // padded column
+            st->counter[kTkRestrict] = 0u;
+        }
+    }
+}
+
+// ------------------------------------------------------------- k_prolong --
+// z = z_pre + P e (two_level.hpp:74-78); RZ: r.z when no post-sweep follows
+template <int PPL, int ZMODE, bool RZ>
+__global__ void __launch_bounds__(kThreads) k_prolong(SolveArgs a, const double* zpre,
+                                                      double* zout) {
+    PcgState* st = a.st;
+    if (st->done) return;
+    const int ld = a.k + (a.k & 1);
+    const int pairs = ld >> 1;
+    double ev[2 * PPL];
+    {
+        const int l0 = threadIdx.x & (kGroup - 1);
+#pragma unroll
+        for (int t = 0; t < PPL; ++t) {
+            const int pi = l0 + kGroup * t;
+            ev[2 * t] = pi < pairs ? a.e[2 * pi] : 0.0;
+            ev[2 * t + 1] = pi < pairs ? a.e[2 * pi + 1] : 0.0;
+        }
+    }
+    double s[1] = {0.0};
+    ROW_LOOP_BEGIN(a.n)
+        double part = 0.0;
+        if (valid) {
+            const double* prow = a.P + (long long)row * ld;
+#pragma unroll
+            for (int t = 0; t < PPL; ++t) {
+                const int pi = l + kGroup * t;
+                if (pi < pairs) {
+                    const double2 pv = ld_stream2(prow + 2 * pi);
+                    part = fma(pv.x, ev[2 * t], part);
+                    part = fma(pv.y, ev[2 * t + 1], part);
+                }
+            }
+        }
+        const double sum = group_sum(part);
+        if (valid && l == 0) {
+            double zp;
+            if (ZMODE == 0) zp = 0.0;
+            else if (ZMODE == 1) zp = a.wd[row] * a.r[row];
+            else zp = zpre[row];
+            const double zi = zp + sum;
+            zout[row] = zi;
+            if (RZ) s[0] = fma(a.r[row], zi, s[0]);
+        }
+    ROW_LOOP_END
+    if (RZ) {
+        double tot[1];
+        if (grid_reduce<1>(s, a.partials, &st->counter[kTkProlong], tot) && threadIdx.x == 0)
+            st->rz_new = tot[0];
+    }
+}
+
+// ----------------------------------------------------------- k_true_res --
+// ||b - A x|| / ||b|| recomputed at exit (two_level.hpp:185-189)
+__global__ void __launch_bounds__(kThreads) k_true_res(SolveArgs a) {
+    PcgState* st = a.st;
+    if (st->error) return;
+    const GPlain g{a.x};
+    double s[1] = {0.0};
+    ROW_LOOP_BEGIN(a.n)
+        const double y = group_dot(a.rp, a.ci, a.v, row, valid, g, l);
+        if (valid && l == 0) {
+            const double d = a.b[row] - y;
+            s[0] = fma(d, d, s[0]);
+        }
+    ROW_LOOP_END
+    double tot[1];
+    if (grid_reduce<1>(s, a.partials, &st->counter[kTkTrue], tot) && threadIdx.x == 0)
+        st->true_res = sqrt(tot[0]) / st->bnorm;
+}
+
+// --------------------------------------------------------------- k_spmv --
+// plain y = A x (sparse.hpp:116-128)
+__global__ void __launch_bounds__(kThreads) k_spmv(int n, const int* rp, const int* ci,
+                                                   const double* v, const double* x, double* y) {
+    const GPlain g{x};
+    ROW_LOOP_BEGIN(n)
+        const double yy = group_dot(rp, ci, v, row, valid, g, l);
+        if (valid && l == 0) y[row] = yy;
+    ROW_LOOP_END
+}
+
+// ======================================================== host launchers ==
+
+namespace {
+int row_grid(const LaunchCtx& c, long long n) {
+    const long long rows_per_cta = (kThreads / 32) * kRowsPerWarp;
+    long long g = (n + rows_per_cta - 1) / rows_per_cta;
+    const long long cap = (long long)c.num_sms * 4;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return static_cast<int>(g);
+}
+int elem_grid(const LaunchCtx& c, long long n) {
+    long long g = (n + kThreads - 1) / kThreads;
+    const long long cap = (long long)c.num_sms * 4;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return static_cast<int>(g);
+}
+inline void count(const LaunchCtx& c) { ++*c.launches; }
+}  // namespace
+
+void launch_state_init(const LaunchCtx& c, PcgState* st, double delta, long long max_it) {
+    k_state_init<<<1, 1, 0, c.s>>>(st, delta, max_it);
+    count(c);
+}
+
+void launch_bnorm(const LaunchCtx& c, const SolveArgs& a) {
+    k_bnorm<<<elem_grid(c, a.n), kThreads, 0, c.s>>>(a);
+    count(c);
+}
+
+void launch_init_simple(const LaunchCtx& c, const SolveArgs& a, int mode) {
+    if (mode == 1)
+        k_init_simple<1><<<elem_grid(c, a.n), kThreads, 0, c.s>>>(a);
+    else
+        k_init_simple<0><<<elem_grid(c, a.n), kThreads, 0, c.s>>>(a);
+    count(c);
+}
+
+void launch_init_ctl(const LaunchCtx& c, PcgState* st) {
+    k_init_ctl<<<1, 1, 0, c.s>>>(st);
+    count(c);
+}
+
+void launch_spmv_p(const LaunchCtx& c, const SolveArgs& a) {
+    k_spmv_p<<<row_grid(c, a.n), kThreads, 0, c.s>>>(a);
+    count(c);
+}
+
+// mode: 0 two-level, 1 identity, 2 Jacobi
+void launch_update(const LaunchCtx& c, const SolveArgs& a, int mode) {
+    const int g = elem_grid(c, a.n);
+    if (mode == 0) k_update<0><<<g, kThreads, 0, c.s>>>(a);
+    else if (mode == 1) k_update<1><<<g, kThreads, 0, c.s>>>(a);
+    else k_update<2><<<g, kThreads, 0, c.s>>>(a);
+    count(c);
+}
+
+void launch_loop_ctl(const LaunchCtx& c, PcgState* st, cudaGraphConditionalHandle h, int use_cond) {
+    k_loop_ctl<<<1, 1, 0, c.s>>>(st, h, use_cond);
+    count(c);
+}
+
+void launch_true_res(const LaunchCtx& c, const SolveArgs& a) {
+    k_true_res<<<row_grid(c, a.n), kThreads, 0, c.s>>>(a);
+    count(c);
+}
+
+void launch_spmv(const LaunchCtx& c, int n, const int* rp, const int* ci, const double* v,
+                 const double* x, double* y) {
+    k_spmv<<<row_grid(c, n), kThreads, 0, c.s>>>(n, rp, ci, v, x, y);
+    count(c);
+}
+
+template <int PPL>
+static void restrict_ppl(const LaunchCtx& c, const SolveArgs& a, int zmode, const double* zpre) {
+    const int g = row_grid(c, a.n);
+    if (zmode == 0) k_restrict<PPL, 0><<<g, kThreads, 0, c.s>>>(a, zpre);
+    else if (zmode == 1) k_restrict<PPL, 1><<<g, kThreads, 0, c.s>>>(a, zpre);
+    else k_restrict<PPL, 2><<<g, kThreads, 0, c.s>>>(a, zpre);
+}
+
+template <int PPL>
+static void prolong_ppl(const LaunchCtx& c, const SolveArgs& a, int zmode, bool rz,
+                        const double* zpre, double* zout) {
+    const int g = row_grid(c, a.n);
+#define NLSP_PRO(Z, R) k_prolong<PPL, Z, R><<<g, kThreads, 0, c.s>>>(a, zpre, zout)
+    if (zmode == 0) { if (rz) NLSP_PRO(0, true); else NLSP_PRO(0, false); }
+    else if (zmode == 1) { if (rz) NLSP_PRO(1, true); else NLSP_PRO(1, false); }
+    else { if (rz) NLSP_PRO(2, true); else NLSP_PRO(2, false); }
+#undef NLSP_PRO
+}
+
+int ppl_for(int k) {
+    const int pairs = (k + (k & 1)) / 2;
+    const int need = (pairs + kGroup - 1) / kGroup;
+    const int opts[] = {1, 2, 3, 4, 6, 8, 12, 16};
+    for (int o : opts)
+        if (o >= need) return o;
+    return -1;
+}
+
+#define NLSP_PPL_SWITCH(ppl, CALL)     \
+    switch (ppl) {                     \
+        case 1: CALL(1); break;        \
+        case 2: CALL(2); break;        \
+        case 3: CALL(3); break;        \
+        case 4: CALL(4); break;        \
+        case 6: CALL(6); break;        \
+        case 8: CALL(8); break;        \
+        case 12: CALL(12); break;      \
+        default: CALL(16); break;      \
+    }
+
+void launch_restrict(const LaunchCtx& c, const SolveArgs& a, int zmode, const double* zpre) {
+#define CALL(P) restrict_ppl<P>(c, a, zmode, zpre)
+    NLSP_PPL_SWITCH(ppl_for(a.k), CALL)
+#undef CALL
+    count(c);
+}
+
+void launch_prolong(const LaunchCtx& c, const SolveArgs& a, int zmode, bool rz, const double* zpre,
+                    double* zout) {
+#define CALL(P) prolong_ppl<P>(c, a, zmode, rz, zpre, zout)
+    NLSP_PPL_SWITCH(ppl_for(a.k), CALL)
+#undef CALL
+    count(c);
+}
+
+// sweep with z_in = implicit w D^-1 r (first pre-sweep) or a buffer
+void launch_sweep(const LaunchCtx& c, const SolveArgs& a, bool implicit_in, const double* zin,
+                  double* zout, bool rz) {
+    const int g = row_grid(c, a.n);
+    if (implicit_in) {
+        const GWdr gw{a.wd, a.r};
+        if (rz) k_sweep<GWdr, true><<<g, kThreads, 0, c.s>>>(a, gw, zout);
+        else k_sweep<GWdr, false><<<g, kThreads, 0, c.s>>>(a, gw, zout);
+    } else {
+        const GPlain gp{zin};
+        if (rz) k_sweep<GPlain, true><<<g, kThreads, 0, c.s>>>(a, gp, zout);
+        else k_sweep<GPlain, false><<<g, kThreads, 0, c.s>>>(a, gp, zout);
+    }
+    count(c);
+}
+
+// One two-level cycle z = M^-1 r (two_level.hpp:60-81) on a.r -> a.z, with r.z
+// left in st->rz_new. Buffers: zt0/zt1 ping-pong, prolongation in place.
+void launch_twolevel_apply(const LaunchCtx& c, const SolveArgs& a, unsigned long long nu1,
+                           unsigned long long nu2) {
+    int zmode;
+    const double* zpre = nullptr;
+    if (nu1 == 0) {
+        zmode = 0;
+    } else if (nu1 == 1) {
+        zmode = 1;
+    } else {
+        double* cur = a.zt0;
+        launch_sweep(c, a, true, nullptr, cur, false);
+        for (unsigned long long s = 2; s < nu1; ++s) {
+            double* nxt = (cur == a.zt0) ? a.zt1 : a.zt0;
+            launch_sweep(c, a, false, cur, nxt, false);
+            cur = nxt;
+        }
+        zmode = 2;
+        zpre = cur;
+    }
+    launch_restrict(c, a, zmode, zpre);
+    double* pro_out;
+    if (nu2 == 0) pro_out = a.z;
+    else pro_out = (zmode == 2) ? const_cast<double*>(zpre) : a.zt0;
+    launch_prolong(c, a, zmode, nu2 == 0, zpre, pro_out);
+    double* cur = pro_out;
+    for (unsigned long long s = 1; s <= nu2; ++s) {
+        double* out = (s == nu2) ? a.z : ((cur == a.zt0) ? a.zt1 : a.zt0);
+        launch_sweep(c, a, false, cur, out, s == nu2);
+        cur = out;
+    }
+}
+
+}  // namespace nlsp
