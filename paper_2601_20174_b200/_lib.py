@@ -12,7 +12,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-GPU_LIB_PATH = os.path.join(HERE, "libnlsp_gpu.so")
+GPU_LIB_PATH = os.environ.get("NLSP_GPU_LIB") or os.path.join(HERE, "libnlsp_gpu.so")
 INPUTS_LIB_PATH = os.path.join(HERE, "libnlsp_inputs.so")
 
 c_u64 = C.c_uint64

@@ -16,9 +16,26 @@
 // (4 rows per warp): the 8 lanes read a row's nonzeros as one coalesced run and
 // the row's k basis entries as 16-B loads, so the SpMV result of a row is
 // already in the registers of the lanes that stream that row of P.
+#include <mutex>
+#include <unordered_map>
+#include <utility>
+
 #include "internal.cuh"
 
 namespace nlsp {
+
+// rows per 8-lane group in flight: SpMV kernels / kernels that also stream P
+#ifndef NLSP_KU
+#define NLSP_KU 4
+#endif
+#ifndef NLSP_KUP
+#define NLSP_KUP 2
+#endif
+#ifndef NLSP_BLOCKROWS
+#define NLSP_BLOCKROWS 0
+#endif
+constexpr int kU = NLSP_KU;
+constexpr int kUP = NLSP_KUP;
 
 // ----------------------------------------------------------------- gathers --
 struct GPlain {
@@ -43,18 +60,42 @@ struct GWdr {
     __device__ __forceinline__ double operator()(int j) const { return wd[j] * r[j]; }
 };
 
-// y_row = sum_k v_k g(col_k) by an 8-lane group; every lane of the group returns
-// the full sum.
-template <class Gat>
-__device__ __forceinline__ double group_dot(const int* __restrict__ rp, const int* __restrict__ ci,
-                                            const double* __restrict__ v, int row, bool valid,
-                                            const Gat& g, int l) {
-    double s = 0.0;
-    if (valid) {
-        const int b = __ldg(rp + row), e = __ldg(rp + row + 1);
-        for (int k = b + l; k < e; k += kGroup) s = fma(__ldg(v + k), g(__ldg(ci + k)), s);
+// y[u] = sum_k v_k g(col_k) for the U rows row[u] of this 8-lane group; every
+// lane of the group returns the full sums. All row_ptr loads, then all
+// value/column loads, then all gathers are issued before any use, so a warp
+// keeps 4*U rows of CSR traffic in flight.
+template <int U, class Gat>
+__device__ __forceinline__ void group_dot_batch(const int* __restrict__ rp,
+                                                const int* __restrict__ ci,
+                                                const double* __restrict__ v, const int (&row)[U],
+                                                const bool (&valid)[U], const Gat& g, int l,
+                                                double (&y)[U]) {
+    int b[U], e[U];
+    int len = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        b[u] = valid[u] ? __ldg(rp + row[u]) : 0;
+        e[u] = valid[u] ? __ldg(rp + row[u] + 1) : 0;
+        y[u] = 0.0;
     }
-    return group_sum(s);
+#pragma unroll
+    for (int u = 0; u < U; ++u) len = max(len, e[u] - b[u]);
+    for (int off = l; off < len; off += kGroup) {
+        double vv[U];
+        int cc[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int k = b[u] + off;
+            const bool ok = k < e[u];
+            vv[u] = ok ? __ldg(v + k) : 0.0;
+            cc[u] = ok ? __ldg(ci + k) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (cc[u] >= 0) y[u] = fma(vv[u], g(cc[u]), y[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) y[u] = group_sum(y[u]);
 }
 
 // CTA sum of NV values, partial per CTA, and the last-arriving CTA reduces all
@@ -112,17 +153,39 @@ __device__ __forceinline__ bool grid_reduce(double (&v)[NV], double* part, unsig
     return true;
 }
 
-#define ROW_LOOP_BEGIN(n)                                                          \
+// Rows are dealt to warps in runs of 4*U; group grp of a warp takes rows
+// base + grp + 4u (u < U), so at each u the four groups read one contiguous run
+// of nonzeros. With NLSP_BLOCKROWS each CTA owns one contiguous block of rows
+// and its warps sweep it in order, so stencil neighbours (i +- 1, i +- nx) of a
+// gather were usually just touched by the same CTA (L1 hits).
+#if NLSP_BLOCKROWS
+#define ROW_BATCH_RANGE(n, U)                                                           \
+    const long long step_ = (long long)(blockDim.x >> 5) * (kRowsPerWarp * (U));       \
+    const long long per_ = ((((long long)(n) + gridDim.x - 1) / gridDim.x) + step_ - 1) / step_ * step_; \
+    const long long beg_ = blockIdx.x * per_;                                           \
+    const long long end_ = min((long long)(n), beg_ + per_);                            \
+    for (long long base_ = beg_ + (threadIdx.x >> 5) * (kRowsPerWarp * (U)); base_ < end_; \
+         base_ += step_) {
+#else
+#define ROW_BATCH_RANGE(n, U)                                                           \
+    const long long wid_ = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;     \
+    const long long nwarps_ = (gridDim.x * (long long)blockDim.x) >> 5;                \
+    for (long long base_ = wid_ * (kRowsPerWarp * (U)); base_ < (n);                   \
+         base_ += nwarps_ * (kRowsPerWarp * (U))) {
+#endif
+#define ROW_BATCH_BEGIN(n, U)                                                      \
     const int lane_ = threadIdx.x & 31;                                            \
     const int l = lane_ & (kGroup - 1);                                            \
     const int grp = lane_ >> 3;                                                    \
-    const long long wid_ = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; \
-    const long long nwarps_ = (gridDim.x * (long long)blockDim.x) >> 5;            \
-    for (long long base_ = wid_ * kRowsPerWarp; base_ < (n); base_ += nwarps_ * kRowsPerWarp) { \
-        const int row = static_cast<int>(base_) + grp;                             \
-        const bool valid = row < (n);
+    ROW_BATCH_RANGE(n, U)                                                          \
+        int row[U];                                                                \
+        bool valid[U];                                                             \
+        _Pragma("unroll") for (int u = 0; u < (U); ++u) {                          \
+            row[u] = static_cast<int>(base_) + grp + kRowsPerWarp * u;             \
+            valid[u] = row[u] < (n);                                               \
+        }
 
-#define ROW_LOOP_END }
+#define ROW_BATCH_END }
 
 // ------------------------------------------------------------------ state --
 struct PcgParamsHost {
@@ -202,15 +265,20 @@ __global__ void __launch_bounds__(kThreads) k_spmv_p(SolveArgs a) {
     double* pc = odd ? a.p1 : a.p0;
     const GPupd g{a.z, pp, st->beta, st->first != 0};
     double s[1] = {0.0};
-    ROW_LOOP_BEGIN(a.n)
-        const double y = group_dot(a.rp, a.ci, a.v, row, valid, g, l);
-        if (valid && l == 0) {
-            const double pi = g(row);
-            pc[row] = pi;
-            a.q[row] = y;
-            s[0] = fma(pi, y, s[0]);
+    ROW_BATCH_BEGIN(a.n, kU)
+        double y[kU];
+        group_dot_batch<kU>(a.rp, a.ci, a.v, row, valid, g, l, y);
+        if (l == 0) {
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                if (!valid[u]) continue;
+                const double pi = g(row[u]);
+                pc[row[u]] = pi;
+                a.q[row[u]] = y[u];
+                s[0] = fma(pi, y[u], s[0]);
+            }
         }
-    ROW_LOOP_END
+    ROW_BATCH_END
     double tot[1];
     if (grid_reduce<1>(s, a.partials, &st->counter[kTkSpmvP], tot) && threadIdx.x == 0) {
         const double pap = tot[0];
@@ -235,17 +303,38 @@ __global__ void __launch_bounds__(kThreads) k_update(SolveArgs a) {
     const double alpha = st->alpha;
     const double* p = (st->it & 1) ? a.p1 : a.p0;
     double s[2] = {0.0, 0.0};
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.n;
-         i += (long long)gridDim.x * blockDim.x) {
-        a.x[i] = fma(alpha, p[i], a.x[i]);
-        const double ri = fma(-alpha, a.q[i], a.r[i]);
-        a.r[i] = ri;
-        s[0] = fma(ri, ri, s[0]);
+    auto one = [&](long long i, double pi, double qi, double xi, double ri0, double& xo,
+                   double& ro) {
+        xo = fma(alpha, pi, xi);
+        ro = fma(-alpha, qi, ri0);
+        s[0] = fma(ro, ro, s[0]);
         if (MODE != 0) {
-            const double zi = MODE == 2 ? ri / a.diag[i] : ri;
+            const double zi = MODE == 2 ? ro / a.diag[i] : ro;
             a.z[i] = zi;
-            s[1] = fma(ri, zi, s[1]);
+            s[1] = fma(ro, zi, s[1]);
         }
+    };
+    // 16-B vector loads over element pairs; the odd tail element separately
+    const long long npairs = a.n >> 1;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < npairs; t += stride) {
+        const long long i = 2 * t;
+        const double2 pv = *reinterpret_cast<const double2*>(p + i);
+        const double2 qv = *reinterpret_cast<const double2*>(a.q + i);
+        const double2 xv = *reinterpret_cast<const double2*>(a.x + i);
+        const double2 rv = *reinterpret_cast<const double2*>(a.r + i);
+        double2 xo, ro;
+        one(i, pv.x, qv.x, xv.x, rv.x, xo.x, ro.x);
+        one(i + 1, pv.y, qv.y, xv.y, rv.y, xo.y, ro.y);
+        *reinterpret_cast<double2*>(a.x + i) = xo;
+        *reinterpret_cast<double2*>(a.r + i) = ro;
+    }
+    if ((a.n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const long long i = a.n - 1;
+        double xo, ro;
+        one(i, p[i], a.q[i], a.x[i], a.r[i], xo, ro);
+        a.x[i] = xo;
+        a.r[i] = ro;
     }
     double tot[2];
     if (grid_reduce<2>(s, a.partials, &st->counter[kTkUpdate], tot) && threadIdx.x == 0) {
@@ -282,15 +371,20 @@ __global__ void __launch_bounds__(kThreads) k_sweep(SolveArgs a, Gat g, double* 
     PcgState* st = a.st;
     if (st->done) return;
     double s[1] = {0.0};
-    ROW_LOOP_BEGIN(a.n)
-        const double y = group_dot(a.rp, a.ci, a.v, row, valid, g, l);
-        if (valid && l == 0) {
-            const double ri = a.r[row];
-            const double zi = fma(a.wd[row], ri - y, g(row));
-            zout[row] = zi;
-            if (RZ) s[0] = fma(ri, zi, s[0]);
+    ROW_BATCH_BEGIN(a.n, kU)
+        double y[kU];
+        group_dot_batch<kU>(a.rp, a.ci, a.v, row, valid, g, l, y);
+        if (l == 0) {
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                if (!valid[u]) continue;
+                const double ri = a.r[row[u]];
+                const double zi = fma(a.wd[row[u]], ri - y[u], g(row[u]));
+                zout[row[u]] = zi;
+                if (RZ) s[0] = fma(ri, zi, s[0]);
+            }
         }
-    ROW_LOOP_END
+    ROW_BATCH_END
     if (RZ) {
         double tot[1];
         if (grid_reduce<1>(s, a.partials, &st->counter[kTkSweep], tot) && threadIdx.x == 0)
@@ -339,24 +433,33 @@ __global__ void __launch_bounds__(kThreads) k_restrict(SolveArgs a, const double
     for (int t = 0; t < 2 * PPL; ++t) acc[t] = 0.0;
     const GWdr gw{a.wd, a.r};
     const GPlain gp{zpre};
-    ROW_LOOP_BEGIN(a.n)
-        double y = 0.0;
-        if (ZMODE == 1) y = group_dot(a.rp, a.ci, a.v, row, valid, gw, l);
-        if (ZMODE == 2) y = group_dot(a.rp, a.ci, a.v, row, valid, gp, l);
-        if (valid) {
-            const double res = a.r[row] - y;
-            const double* prow = a.P + (long long)row * ld;
+    ROW_BATCH_BEGIN(a.n, kUP)
+        // basis rows first (independent of the SpMV), then the residuals
+        double2 pv[kUP][PPL];
+#pragma unroll
+        for (int u = 0; u < kUP; ++u) {
+            const double* prow = a.P + (long long)row[u] * ld;
 #pragma unroll
             for (int t = 0; t < PPL; ++t) {
                 const int pi = l + kGroup * t;
-                if (pi < pairs) {
-                    const double2 pv = ld_stream2(prow + 2 * pi);
-                    acc[2 * t] = fma(pv.x, res, acc[2 * t]);
-                    acc[2 * t + 1] = fma(pv.y, res, acc[2 * t + 1]);
-                }
+                pv[u][t] = (valid[u] && pi < pairs) ? ld_stream2(prow + 2 * pi) : make_double2(0.0, 0.0);
             }
         }
-    ROW_LOOP_END
+        double y[kUP];
+#pragma unroll
+        for (int u = 0; u < kUP; ++u) y[u] = 0.0;
+        if (ZMODE == 1) group_dot_batch<kUP>(a.rp, a.ci, a.v, row, valid, gw, l, y);
+        if (ZMODE == 2) group_dot_batch<kUP>(a.rp, a.ci, a.v, row, valid, gp, l, y);
+#pragma unroll
+        for (int u = 0; u < kUP; ++u) {
+            const double res = valid[u] ? a.r[row[u]] - y[u] : 0.0;
+#pragma unroll
+            for (int t = 0; t < PPL; ++t) {
+                acc[2 * t] = fma(pv[u][t].x, res, acc[2 * t]);
+                acc[2 * t + 1] = fma(pv[u][t].y, res, acc[2 * t + 1]);
+            }
+        }
+    ROW_BATCH_END
     // groups of a warp -> lanes 0..7, warps -> shared, CTA partial -> global
 #pragma unroll
     for (int t = 0; t < 2 * PPL; ++t) {
@@ -434,31 +537,43 @@ __global__ void __launch_bounds__(kThreads) k_prolong(SolveArgs a, const double*
         }
     }
     double s[1] = {0.0};
-    ROW_LOOP_BEGIN(a.n)
-        double part = 0.0;
-        if (valid) {
-            const double* prow = a.P + (long long)row * ld;
+    ROW_BATCH_BEGIN(a.n, kUP)
+        double2 pv[kUP][PPL];
+#pragma unroll
+        for (int u = 0; u < kUP; ++u) {
+            const double* prow = a.P + (long long)row[u] * ld;
 #pragma unroll
             for (int t = 0; t < PPL; ++t) {
                 const int pi = l + kGroup * t;
-                if (pi < pairs) {
-                    const double2 pv = ld_stream2(prow + 2 * pi);
-                    part = fma(pv.x, ev[2 * t], part);
-                    part = fma(pv.y, ev[2 * t + 1], part);
-                }
+                pv[u][t] = (valid[u] && pi < pairs) ? ld_stream2(prow + 2 * pi) : make_double2(0.0, 0.0);
             }
         }
-        const double sum = group_sum(part);
-        if (valid && l == 0) {
-            double zp;
-            if (ZMODE == 0) zp = 0.0;
-            else if (ZMODE == 1) zp = a.wd[row] * a.r[row];
-            else zp = zpre[row];
-            const double zi = zp + sum;
-            zout[row] = zi;
-            if (RZ) s[0] = fma(a.r[row], zi, s[0]);
+        double sum[kUP];
+#pragma unroll
+        for (int u = 0; u < kUP; ++u) {
+            double part = 0.0;
+#pragma unroll
+            for (int t = 0; t < PPL; ++t) {
+                part = fma(pv[u][t].x, ev[2 * t], part);
+                part = fma(pv[u][t].y, ev[2 * t + 1], part);
+            }
+            sum[u] = group_sum(part);
         }
-    ROW_LOOP_END
+        if (l == 0) {
+#pragma unroll
+            for (int u = 0; u < kUP; ++u) {
+                if (!valid[u]) continue;
+                const int rw = row[u];
+                double zp;
+                if (ZMODE == 0) zp = 0.0;
+                else if (ZMODE == 1) zp = a.wd[rw] * a.r[rw];
+                else zp = zpre[rw];
+                const double zi = zp + sum[u];
+                zout[rw] = zi;
+                if (RZ) s[0] = fma(a.r[rw], zi, s[0]);
+            }
+        }
+    ROW_BATCH_END
     if (RZ) {
         double tot[1];
         if (grid_reduce<1>(s, a.partials, &st->counter[kTkProlong], tot) && threadIdx.x == 0)
@@ -473,13 +588,18 @@ __global__ void __launch_bounds__(kThreads) k_true_res(SolveArgs a) {
     if (st->error) return;
     const GPlain g{a.x};
     double s[1] = {0.0};
-    ROW_LOOP_BEGIN(a.n)
-        const double y = group_dot(a.rp, a.ci, a.v, row, valid, g, l);
-        if (valid && l == 0) {
-            const double d = a.b[row] - y;
-            s[0] = fma(d, d, s[0]);
+    ROW_BATCH_BEGIN(a.n, kU)
+        double y[kU];
+        group_dot_batch<kU>(a.rp, a.ci, a.v, row, valid, g, l, y);
+        if (l == 0) {
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                if (!valid[u]) continue;
+                const double d = a.b[row[u]] - y[u];
+                s[0] = fma(d, d, s[0]);
+            }
         }
-    ROW_LOOP_END
+    ROW_BATCH_END
     double tot[1];
     if (grid_reduce<1>(s, a.partials, &st->counter[kTkTrue], tot) && threadIdx.x == 0)
         st->true_res = sqrt(tot[0]) / st->bnorm;
@@ -490,29 +610,53 @@ __global__ void __launch_bounds__(kThreads) k_true_res(SolveArgs a) {
 __global__ void __launch_bounds__(kThreads) k_spmv(int n, const int* rp, const int* ci,
                                                    const double* v, const double* x, double* y) {
     const GPlain g{x};
-    ROW_LOOP_BEGIN(n)
-        const double yy = group_dot(rp, ci, v, row, valid, g, l);
-        if (valid && l == 0) y[row] = yy;
-    ROW_LOOP_END
+    ROW_BATCH_BEGIN(n, kU)
+        double yy[kU];
+        group_dot_batch<kU>(rp, ci, v, row, valid, g, l, yy);
+        if (l == 0) {
+#pragma unroll
+            for (int u = 0; u < kU; ++u)
+                if (valid[u]) y[row[u]] = yy[u];
+        }
+    ROW_BATCH_END
 }
 
 // ======================================================== host launchers ==
 
 namespace {
-int row_grid(const LaunchCtx& c, long long n) {
-    const long long rows_per_cta = (kThreads / 32) * kRowsPerWarp;
-    long long g = (n + rows_per_cta - 1) / rows_per_cta;
-    const long long cap = (long long)c.num_sms * 4;
+// Persistent, occupancy-sized grids: min(work, resident CTAs on all SMs).
+int occ_blocks(const void* f) {
+    static std::mutex mu;
+    static std::unordered_map<const void*, int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(f);
+    if (it != cache.end()) return it->second;
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kThreads, 0) != cudaSuccess || nb < 1)
+        nb = 1;
+    cudaGetLastError();
+    cache[f] = nb;
+    return nb;
+}
+int occ_grid(const LaunchCtx& c, const void* f, long long units, long long per_cta) {
+    long long g = (units + per_cta - 1) / per_cta;
+    long long cap = (long long)c.num_sms * occ_blocks(f);
+    if (cap > kMaxGrid) cap = kMaxGrid;
     if (g > cap) g = cap;
     if (g < 1) g = 1;
     return static_cast<int>(g);
 }
-int elem_grid(const LaunchCtx& c, long long n) {
-    long long g = (n + kThreads - 1) / kThreads;
-    const long long cap = (long long)c.num_sms * 4;
-    if (g > cap) g = cap;
-    if (g < 1) g = 1;
-    return static_cast<int>(g);
+// row kernels: units = rows, per CTA = warps * 4 * U rows
+template <int U, class... KArgs, class... Args>
+void launch_rows(const LaunchCtx& c, void (*f)(KArgs...), long long n, Args&&... args) {
+    const int g = occ_grid(c, reinterpret_cast<const void*>(f), n, (kThreads / 32) * kRowsPerWarp * U);
+    f<<<g, kThreads, 0, c.s>>>(std::forward<Args>(args)...);
+}
+// element kernels: units = elements (2 per thread)
+template <class... KArgs, class... Args>
+void launch_elems(const LaunchCtx& c, void (*f)(KArgs...), long long n, Args&&... args) {
+    const int g = occ_grid(c, reinterpret_cast<const void*>(f), n, 2LL * kThreads);
+    f<<<g, kThreads, 0, c.s>>>(std::forward<Args>(args)...);
 }
 inline void count(const LaunchCtx& c) { ++*c.launches; }
 }  // namespace
@@ -523,15 +667,15 @@ void launch_state_init(const LaunchCtx& c, PcgState* st, double delta, long long
 }
 
 void launch_bnorm(const LaunchCtx& c, const SolveArgs& a) {
-    k_bnorm<<<elem_grid(c, a.n), kThreads, 0, c.s>>>(a);
+    launch_elems(c, k_bnorm, a.n, a);
     count(c);
 }
 
 void launch_init_simple(const LaunchCtx& c, const SolveArgs& a, int mode) {
     if (mode == 1)
-        k_init_simple<1><<<elem_grid(c, a.n), kThreads, 0, c.s>>>(a);
+        launch_elems(c, k_init_simple<1>, a.n, a);
     else
-        k_init_simple<0><<<elem_grid(c, a.n), kThreads, 0, c.s>>>(a);
+        launch_elems(c, k_init_simple<0>, a.n, a);
     count(c);
 }
 
@@ -541,16 +685,15 @@ void launch_init_ctl(const LaunchCtx& c, PcgState* st) {
 }
 
 void launch_spmv_p(const LaunchCtx& c, const SolveArgs& a) {
-    k_spmv_p<<<row_grid(c, a.n), kThreads, 0, c.s>>>(a);
+    launch_rows<kU>(c, k_spmv_p, a.n, a);
     count(c);
 }
 
 // mode: 0 two-level, 1 identity, 2 Jacobi
 void launch_update(const LaunchCtx& c, const SolveArgs& a, int mode) {
-    const int g = elem_grid(c, a.n);
-    if (mode == 0) k_update<0><<<g, kThreads, 0, c.s>>>(a);
-    else if (mode == 1) k_update<1><<<g, kThreads, 0, c.s>>>(a);
-    else k_update<2><<<g, kThreads, 0, c.s>>>(a);
+    if (mode == 0) launch_elems(c, k_update<0>, a.n, a);
+    else if (mode == 1) launch_elems(c, k_update<1>, a.n, a);
+    else launch_elems(c, k_update<2>, a.n, a);
     count(c);
 }
 
@@ -560,29 +703,27 @@ void launch_loop_ctl(const LaunchCtx& c, PcgState* st, cudaGraphConditionalHandl
 }
 
 void launch_true_res(const LaunchCtx& c, const SolveArgs& a) {
-    k_true_res<<<row_grid(c, a.n), kThreads, 0, c.s>>>(a);
+    launch_rows<kU>(c, k_true_res, a.n, a);
     count(c);
 }
 
 void launch_spmv(const LaunchCtx& c, int n, const int* rp, const int* ci, const double* v,
                  const double* x, double* y) {
-    k_spmv<<<row_grid(c, n), kThreads, 0, c.s>>>(n, rp, ci, v, x, y);
+    launch_rows<kU>(c, k_spmv, n, n, rp, ci, v, x, y);
     count(c);
 }
 
 template <int PPL>
 static void restrict_ppl(const LaunchCtx& c, const SolveArgs& a, int zmode, const double* zpre) {
-    const int g = row_grid(c, a.n);
-    if (zmode == 0) k_restrict<PPL, 0><<<g, kThreads, 0, c.s>>>(a, zpre);
-    else if (zmode == 1) k_restrict<PPL, 1><<<g, kThreads, 0, c.s>>>(a, zpre);
-    else k_restrict<PPL, 2><<<g, kThreads, 0, c.s>>>(a, zpre);
+    if (zmode == 0) launch_rows<kUP>(c, k_restrict<PPL, 0>, a.n, a, zpre);
+    else if (zmode == 1) launch_rows<kUP>(c, k_restrict<PPL, 1>, a.n, a, zpre);
+    else launch_rows<kUP>(c, k_restrict<PPL, 2>, a.n, a, zpre);
 }
 
 template <int PPL>
 static void prolong_ppl(const LaunchCtx& c, const SolveArgs& a, int zmode, bool rz,
                         const double* zpre, double* zout) {
-    const int g = row_grid(c, a.n);
-#define NLSP_PRO(Z, R) k_prolong<PPL, Z, R><<<g, kThreads, 0, c.s>>>(a, zpre, zout)
+#define NLSP_PRO(Z, R) launch_rows<kUP>(c, k_prolong<PPL, Z, R>, a.n, a, zpre, zout)
     if (zmode == 0) { if (rz) NLSP_PRO(0, true); else NLSP_PRO(0, false); }
     else if (zmode == 1) { if (rz) NLSP_PRO(1, true); else NLSP_PRO(1, false); }
     else { if (rz) NLSP_PRO(2, true); else NLSP_PRO(2, false); }
@@ -628,15 +769,14 @@ void launch_prolong(const LaunchCtx& c, const SolveArgs& a, int zmode, bool rz, 
 // sweep with z_in = implicit w D^-1 r (first pre-sweep) or a buffer
 void launch_sweep(const LaunchCtx& c, const SolveArgs& a, bool implicit_in, const double* zin,
                   double* zout, bool rz) {
-    const int g = row_grid(c, a.n);
     if (implicit_in) {
         const GWdr gw{a.wd, a.r};
-        if (rz) k_sweep<GWdr, true><<<g, kThreads, 0, c.s>>>(a, gw, zout);
-        else k_sweep<GWdr, false><<<g, kThreads, 0, c.s>>>(a, gw, zout);
+        if (rz) launch_rows<kU>(c, k_sweep<GWdr, true>, a.n, a, gw, zout);
+        else launch_rows<kU>(c, k_sweep<GWdr, false>, a.n, a, gw, zout);
     } else {
         const GPlain gp{zin};
-        if (rz) k_sweep<GPlain, true><<<g, kThreads, 0, c.s>>>(a, gp, zout);
-        else k_sweep<GPlain, false><<<g, kThreads, 0, c.s>>>(a, gp, zout);
+        if (rz) launch_rows<kU>(c, k_sweep<GPlain, true>, a.n, a, gp, zout);
+        else launch_rows<kU>(c, k_sweep<GPlain, false>, a.n, a, gp, zout);
     }
     count(c);
 }

@@ -159,10 +159,16 @@ class SparseCsrMatrix:
             new = np.ones(i.size, bool)
             new[1:] = (i[1:] != i[:-1]) | (j[1:] != j[:-1])
             starts = np.flatnonzero(new)
-            # duplicates summed left to right, as `v += ...` in the reference loop
-            sums = np.array([v[s:e].sum() if e - s > 1 else v[s]
-                             for s, e in zip(starts, list(starts[1:]) + [i.size])]) \
-                if (~new).any() else v[starts]
+            # duplicates summed left to right from 0.0, as the reference loop does
+            # (sparse.hpp:40-44); the sort above is stable, so input order holds
+            sums = 0.0 + v[starts]
+            if (~new).any():
+                ends = np.append(starts[1:], i.size)
+                for g in np.flatnonzero(ends - starts > 1):
+                    acc = 0.0
+                    for t in v[starts[g]:ends[g]]:
+                        acc += float(t)
+                    sums[g] = acc
             ui, uj = i[starts], j[starts]
             keep = sums != 0.0
             ui, uj, sums = ui[keep], uj[keep], sums[keep]

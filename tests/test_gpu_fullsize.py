@@ -1,0 +1,63 @@
+"""BASELINE.json configurations at full size on the GPU. The CPU reference needs
+tens of minutes to hours per solve here, so parity is checked
+through size-independent properties, each recomputed independently on the host
+(scipy.sparse): the recurrence stop and the true residual, the basis is
+orthonormal, A_c = P^T A P, the operator is linear / symmetric / positive, and
+repeated solves are bitwise deterministic."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from paper_2601_20174_b200 import problems
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def scipy_csr(pb):
+    return sp.csr_matrix((pb.values, pb.col_idx.astype(np.int64), pb.row_ptr.astype(np.int64)),
+                         shape=(pb.n, pb.n))
+
+
+@pytest.mark.parametrize("name", ["C2", "C4", "C5"])
+def test_full_size_solve_properties(nlsp, name):
+    cfg = problems.CONFIGS[name]
+    pb = problems.generate(cfg)
+    a = pb.csr()
+    mask = pb.mask if pb.mask.any() else None
+    sv = nlsp.generate_smoothed_vectors(a, mask, cfg.m, cfg.s1, cfg.omega, cfg.s0_seed)
+    p, sig, sweeps = nlsp.svd_basis(sv.s, cfg.k)
+    assert np.all(np.diff(sig) <= 0) and sweeps <= 30
+    m = nlsp.TwoLevelPreconditioner(a, p, cfg.omega, cfg.nu1, cfg.nu2)
+    basis, chol, coarse = m._export()
+    A = scipy_csr(pb)
+    # orthonormal basis, Galerkin operator, factor
+    g = basis.T @ basis
+    assert np.abs(g - np.eye(cfg.k)).max() <= 1e-10
+    ac = basis.T @ (A @ basis)
+    ac = 0.5 * (ac + ac.T)
+    assert np.abs(coarse - ac).max() <= 1e-10 * np.abs(ac).max()
+    assert np.abs(chol @ chol.T - coarse).max() <= 1e-12 * np.abs(coarse).max()
+    # solve
+    res = nlsp.pcg(a, pb.rhs, m, cfg.delta, 10 * pb.n)
+    rep = res.report
+    assert rep.converged and rep.residual_history[-1] < cfg.delta
+    assert len(rep.residual_history) == rep.iterations
+    true = np.linalg.norm(pb.rhs - A @ res.solution) / np.linalg.norm(pb.rhs)
+    assert abs(true - rep.true_relative_residual) <= 1e-3 * true
+    assert true < 10 * cfg.delta
+    # determinism
+    res2 = nlsp.pcg(a, pb.rhs, m, cfg.delta, 10 * pb.n)
+    assert res2.report.iterations == rep.iterations and np.array_equal(res2.solution, res.solution)
+    # operator: linear, symmetric, positive (two_level.hpp:17-20)
+    rng = np.random.default_rng(0)
+    x, y = rng.standard_normal(pb.n), rng.standard_normal(pb.n)
+    mx, my = m.apply(a, x), m.apply(a, y)
+    assert abs(mx @ y - x @ my) <= 1e-10 * np.linalg.norm(x) * np.linalg.norm(y)
+    assert mx @ x > 0.0
+    m2 = m.apply(a, -2.5 * x)
+    assert np.abs(m2 + 2.5 * mx).max() <= 1e-12 * np.abs(mx).max()
+    # the coarse correction must help: fewer iterations than plain CG
+    plain = nlsp.pcg(a, pb.rhs, nlsp.IdentityPreconditioner(), cfg.delta, 10 * pb.n)
+    assert rep.iterations < plain.report.iterations
