@@ -1,0 +1,472 @@
+#!/usr/bin/env python
+"""bench.py — two-level-preconditioned CG (NeuraLSP SVD-basis path) on B200.
+
+One step = one full PCG solve to ||r||/||b|| < 1e-8 of the workload's system
+(BASELINE.json config C4 by default: 3D 7-point Poisson 160^3, n = 4,096,000,
+k = 64, m = 128). The metric is PCG iterations per second over the timed solves
+(time-to-solution reported beside it).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1..C5]
+  python bench.py --impl reference ...   # the reference's own CPU solve
+
+Arms
+  ours       value: nlsp_pcg_device (b, x resident in HBM), CUDA events on the
+             library's stream; e2e: nlsp_pcg through the C-ABI with pinned HOST
+             b / x (H2D + D2H inside every timed step), wall clock.
+  reference  the reference's pcg<TwoLevelPreconditioner> (oracle/_ref, the
+             reference headers compiled unmodified) on all host cores: one
+             single-threaded solve per core, as the reference's own harness runs
+             instances in parallel (pipeline.hpp:356); each step is a bounded
+             sample of iterations (a full C4 solve is minutes per core).
+
+Multi-GPU: one process per GPU under torchrun, each rank solves its own
+instance (replicas, seed offset by rank; no data-path collective), timing is
+max over ranks, value = iterations of all ranks / that time ("scaling": "weak").
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PCG iters/s & time-to-1e-8 residual at n=4M; achieved HBM GB/s vs roofline"
+UNIT = "iters/s"
+
+
+# ------------------------------------------------------------- distributed --
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            if backend == "nccl":
+                torch.cuda.set_device(self.local_rank)
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group(backend=backend)
+            self.pg = dist
+            self.backend = backend
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, x: float) -> float:
+        return self._reduce(x, "max")
+
+    def sum(self, x: float) -> float:
+        return self._reduce(x, "sum")
+
+    def _reduce(self, x, op):
+        if not self.pg:
+            return x
+        import torch
+        dev = f"cuda:{self.local_rank}" if self.backend == "nccl" else "cpu"
+        t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX if op == "max" else self.pg.ReduceOp.SUM)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+def replica_seeds(cfg, rank: int):
+    """Independent instance per rank (replicas): offset both seed streams."""
+    return cfg.scaled(seed=cfg.seed + 1000 * rank, s0_seed=cfg.s0_seed + 1000 * rank)
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms while timing."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.device), "-f", self.path],
+                stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) >= 9:
+                    rows.append(f)
+        finally:
+            os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[5 + i]
+                          and "Not" not in r[5 + i]})
+        loaded = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+# --------------------------------------------------------------- byte model --
+def byte_model(n, nnz, k, nu1, nu2):
+    """Algorithmic HBM bytes per PCG iteration:
+    A streamed once per SpMV pass (first pre-sweep from 0 is free), P twice,
+    V*n fp64 vector bytes for the fused schedule."""
+    csr = 12.0 * nnz + 4.0 * (n + 1)
+    v = 160 + 32 * (nu1 - 1) + 32 * (nu2 - 1)
+    return (1 + nu1 + nu2) * csr + 16.0 * n * k + v * n
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic(kernel: str, workload: str):
+    """dram bytes per launch of `kernel` from the committed ncu summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    e = d.get(workload, {}).get(kernel)
+    return float(e) if e is not None else None
+
+
+# ---------------------------------------------------------------- our arm --
+def run_ours(args, dist: Dist):
+    import torch
+
+    from paper_2601_20174_b200 import _lib as L
+    from paper_2601_20174_b200 import nlsp, problems
+
+    dev = dist.local_rank
+    torch.cuda.set_device(dev)
+    cfg = replica_seeds(problems.CONFIGS[args.config], dist.rank)
+    ctx = nlsp.Context(dev)
+    nlsp._tls.ctx = ctx
+    lib = L.gpu_lib()
+
+    t0 = time.perf_counter()
+    pb = problems.generate(cfg)
+    gen_s = time.perf_counter() - t0
+    a = pb.csr()
+    dcsr = a.device(ctx)
+    mask = pb.mask if pb.mask.any() else None
+
+    # setup: S^(0) (host, reference RNG) + upload, then device sweeps / SVD / build
+    t0 = time.perf_counter()
+    s0 = problems.smoothed_s0(cfg.s0_seed, pb.n, cfg.m, mask)
+    s = nlsp.DeviceDense.upload(s0, ctx)
+    del s0
+    s0_s = time.perf_counter() - t0
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    ctx.synchronize()
+    ev[0].record(stream)
+    nlsp.smooth_vectors(a, s, cfg.s1, cfg.omega)
+    ev[1].record(stream)
+    p, sigma, sweeps = nlsp.svd_basis(s, cfg.k, ctx)
+    ev[2].record(stream)
+    m = nlsp.TwoLevelPreconditioner(a, p, cfg.omega, cfg.nu1, cfg.nu2)
+    ev[3].record(stream)
+    ctx.synchronize()
+    setup = {"smooth_ms": ev[0].elapsed_time(ev[1]), "svd_basis_ms": ev[1].elapsed_time(ev[2]),
+             "twolevel_build_ms": ev[2].elapsed_time(ev[3]), "s0_host_gen_upload_ms": s0_s * 1e3,
+             "input_gen_s": gen_s, "eigh_sweeps": sweeps}
+    setup["total_ms"] = setup["smooth_ms"] + setup["svd_basis_ms"] + setup["twolevel_build_ms"]
+    del s
+
+    bd = nlsp.DeviceDense.upload(pb.rhs.reshape(-1, 1), ctx)
+    xd = nlsp.DeviceDense.upload(np.zeros((pb.n, 1)), ctx)
+    max_iters = 10 * pb.n
+    rep = L.SolveReportC()
+
+    def solve_device():
+        st = lib.nlsp_pcg_device(ctx.handle, dcsr.handle, L.PRECOND_TWOLEVEL, m.handle, bd.data_ptr,
+                                 cfg.delta, max_iters, xd.data_ptr, C.byref(rep), None)
+        if st != 0:
+            raise RuntimeError(lib.nlsp_last_error(ctx.handle).decode())
+        if not rep.converged:
+            raise RuntimeError("solve did not converge")
+        return int(rep.iterations)
+
+    for _ in range(args.warmup):
+        solve_device()
+    # ---- timed region (device-resident inputs) ----
+    clocks = ClockSampler(dev)
+    clocks.start()
+    launches0 = ctx.kernel_launches()
+    dist.barrier()
+    ctx.synchronize()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    iters = 0
+    for _ in range(args.steps):
+        iters += solve_device()
+    e1.record(stream)
+    ctx.synchronize()
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches = ctx.kernel_launches() - launches0
+    clk = clocks.stop()
+    ms_local = e0.elapsed_time(e1)
+    ms = dist.max(ms_local)
+    iters_all = dist.sum(iters)
+    value = iters_all / (ms / 1e3)
+    iters_per_solve = iters // args.steps
+
+    # ---- end to end through the C-ABI with pinned host buffers ----
+    b_host = torch.from_numpy(pb.rhs.copy()).pin_memory()
+    x_host = torch.empty(pb.n, dtype=torch.float64).pin_memory()
+    P_dbl = C.POINTER(C.c_double)
+    e2e_iters = 0
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        st = lib.nlsp_pcg(ctx.handle, dcsr.handle, L.PRECOND_TWOLEVEL, m.handle,
+                          C.cast(b_host.data_ptr(), P_dbl), cfg.delta, max_iters,
+                          C.cast(x_host.data_ptr(), P_dbl), C.byref(rep), None)
+        if st != 0:
+            raise RuntimeError(lib.nlsp_last_error(ctx.handle).decode())
+        e2e_iters += int(rep.iterations)
+    e2e_s = dist.max(time.perf_counter() - t0)
+    e2e_value = dist.sum(e2e_iters) / e2e_s
+    h2d = int(rep.h2d_bytes)
+    d2h = int(rep.d2h_bytes)
+    x_gpu = x_host.numpy().copy()
+
+    # ---- per-kernel profile (CUDA events around each launch, same stream) ----
+    stats = (L.KernelStatC * 8)()
+    nk = lib.nlsp_pcg_profile(ctx.handle, dcsr.handle, L.PRECOND_TWOLEVEL, m.handle, bd.data_ptr,
+                              args.profile_iters, stats, 8)
+    kernels = {}
+    for i in range(max(nk, 0)):
+        s_ = stats[i]
+        avg = s_.total_ms / max(s_.launches, 1)
+        kernels[s_.name.decode()] = {"avg_us": avg * 1e3, "bytes_per_launch": s_.bytes_per_launch,
+                                     "gbs": s_.bytes_per_launch / (avg * 1e-3) / 1e9 if avg > 0 else 0.0,
+                                     "launches": int(s_.launches)}
+    peak, peak_kind = measured_peaks()
+    dominant = max((k for k in kernels if kernels[k]["bytes_per_launch"] > 0),
+                   key=lambda k: kernels[k]["avg_us"] * kernels[k]["launches"])
+    dk = kernels[dominant]
+    bytes_iter = byte_model(pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2)
+    iter_gbs = bytes_iter * iters / (ms_local / 1e3) / 1e9
+    traffic = ncu_traffic(dominant, args.config)
+    roofline = {"bound": "hbm", "kernel": dominant, "achieved": round(dk["gbs"], 1),
+                "peak": peak, "unit": "GB/s", "frac": round(dk["gbs"] / peak, 4),
+                "traffic": traffic, "peak_source": peak_kind,
+                "bytes_per_launch": dk["bytes_per_launch"], "avg_launch_us": round(dk["avg_us"], 2),
+                "iteration": {"bytes_per_iter": bytes_iter, "achieved": round(iter_gbs, 1),
+                              "frac": round(iter_gbs / peak, 4)}}
+
+    # ---- CPU baseline: the reference's own pcg, 1 core, bounded sample ----
+    cpu = None
+    if dist.world == 1 and dist.rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, cfg, pb, m, x_gpu)
+
+    result = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": dist.world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generators, BASELINE.json shapes; DESIGN.md §Inputs)",
+        "config": {"workload": f"{args.config}: {cfg.name}", "n": pb.n, "nnz": pb.nnz, "k": cfg.k,
+                   "m": cfg.m, "s1": cfg.s1, "nu1": cfg.nu1, "nu2": cfg.nu2, "omega": cfg.omega,
+                   "delta": cfg.delta, "step": "one PCG solve to 1e-8 (device-resident b, x)",
+                   "l2": "inputs larger than L2 (%.2f GB streamed per iteration vs 126 MB L2)"
+                         % (bytes_iter / 1e9),
+                   "parallelism": f"replicas x{dist.world}"},
+        "iterations_per_solve": iters_per_solve,
+        "time_to_solution_ms": round(ms_local / args.steps, 3),
+        "ms_per_iteration": round(ms_local / iters, 4),
+        "setup": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in setup.items()},
+        "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "time_to_solution_ms": round(e2e_s * 1e3 / args.steps, 3)},
+        "roofline": roofline,
+        "kernels": {k: {kk: (round(vv, 2) if isinstance(vv, float) else vv) for kk, vv in v.items()}
+                    for k, v in kernels.items()},
+        "cpu_baseline": cpu,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if dist.rank == 0:
+        print(json.dumps(result), flush=True)
+
+
+def cpu_baseline(args, cfg, pb, m, x_gpu):
+    """The reference's pcg<TwoLevelPreconditioner> on 1 host core (the reference
+    solve is single-threaded) for a bounded number of iterations,
+    with the preconditioner seated from this run's basis and A_c."""
+    from oracle.oracle import Oracle, Reference, reference_available
+
+    basis, _, coarse = m._export()
+    a = (pb.n, pb.row_ptr, pb.col_idx, pb.values)
+    kind = "reference" if reference_available() else "port"
+    impl = Reference() if kind == "reference" else Oracle()
+    t = impl.twolevel_from_parts(a, basis, coarse, cfg.omega, cfg.nu1, cfg.nu2)
+    # size the sample to ~args.cpu_seconds from one probe iteration
+    probe = impl.pcg(a, pb.rhs, 2, t, 0.0, 1)
+    per_iter_ms = max(probe.solve_ms, 1e-3)
+    iters = int(max(1, min(args.cpu_max_iters, args.cpu_seconds * 1e3 / per_iter_ms)))
+    t0 = time.perf_counter()
+    res = impl.pcg(a, pb.rhs, 2, t, 0.0, iters)
+    wall = time.perf_counter() - t0
+    return {"value": round(res.iterations / wall, 4), "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"{res.iterations} iterations of the reference pcg<TwoLevelPreconditioner> "
+                      f"on the full {args.config} system (n={pb.n}), 1 thread, preconditioner "
+                      f"seated from this run's basis/A_c (constructor body skipped)",
+            "ms_per_iteration": round(wall * 1e3 / res.iterations, 2),
+            "host_cpu": _cpu_model(), "nproc": os.cpu_count()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+# ----------------------------------------------------------- reference arm --
+def run_reference(args, dist: Dist):
+    """The reference's own CPU solve on all host cores (rank 0 only)."""
+    if dist.rank != 0:
+        return
+    import scipy.sparse as sp
+
+    from oracle.oracle import Oracle, Reference, reference_available
+    from paper_2601_20174_b200 import problems
+
+    cfg = problems.CONFIGS[args.config]
+    pb = problems.generate(cfg)
+    a = (pb.n, pb.row_ptr, pb.col_idx, pb.values)
+    kind = "reference" if reference_available() else "port"
+    impl = Reference() if kind == "reference" else Oracle()
+    # an orthonormal n x k basis and its Galerkin operator (host LAPACK / scipy);
+    # the per-iteration cost of the solve does not depend on which basis
+    rng = np.random.default_rng(cfg.seed)
+    basis = np.linalg.qr(rng.standard_normal((pb.n, cfg.k)))[0]
+    A = sp.csr_matrix((pb.values, pb.col_idx.astype(np.int64), pb.row_ptr.astype(np.int64)),
+                      shape=(pb.n, pb.n))
+    coarse = basis.T @ (A @ basis)
+    coarse = 0.5 * (coarse + coarse.T)
+    t = impl.twolevel_from_parts(a, np.ascontiguousarray(basis), coarse, cfg.omega, cfg.nu1, cfg.nu2)
+    threads = int(args.ref_threads or os.cpu_count() or 1)
+    # each concurrent solve holds ~12 fp64 n-vectors; keep within half the free RAM
+    try:
+        free = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+        threads = max(1, min(threads, 64, int(0.5 * free / (12 * 8 * pb.n + 1))))
+    except (ValueError, OSError):
+        threads = max(1, min(threads, 64))
+    if kind == "reference":
+        probe_ms, _ = impl.pcg_parallel(a, pb.rhs, 2, t, 0.0, 1, threads)
+    else:
+        probe_ms = impl.pcg(a, pb.rhs, 2, t, 0.0, 1).solve_ms
+        threads = 1
+    per_step = int(max(1, min(args.cpu_max_iters, args.ref_step_seconds * 1e3 / max(probe_ms, 1e-3))))
+
+    def step():
+        if kind == "reference":
+            wall_ms, it = impl.pcg_parallel(a, pb.rhs, 2, t, 0.0, per_step, threads)
+            return wall_ms, it * threads
+        r = impl.pcg(a, pb.rhs, 2, t, 0.0, per_step)
+        return r.solve_ms, r.iterations
+
+    for _ in range(args.warmup):
+        step()
+    tot_ms, tot_it = 0.0, 0
+    for _ in range(args.steps):
+        w, it = step()
+        tot_ms += w
+        tot_it += it
+    value = tot_it / (tot_ms / 1e3)
+    sample = (f"{per_step} PCG iterations x {threads} concurrent single-threaded reference solves "
+              f"(pcg<TwoLevelPreconditioner>, two_level.hpp:141-191) on the full {args.config} "
+              f"system (n={pb.n}, k={cfg.k}) per step")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
+        "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(tot_ms / args.steps, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (same generators as our arm)",
+        "config": {"workload": f"{args.config}: {cfg.name}", "n": pb.n, "nnz": pb.nnz, "k": cfg.k,
+                   "m": cfg.m, "nu1": cfg.nu1, "nu2": cfg.nu2, "delta": cfg.delta,
+                   "step": "bounded sample of the reference CPU solve",
+                   "l2": "host run (no GPU L2)", "parallelism": f"{threads} host threads"},
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": sample, "host_cpu": _cpu_model(), "nproc": os.cpu_count()},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "ms_per_iteration_per_thread": round(tot_ms * threads / max(tot_it, 1), 2),
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--profile-iters", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-max-iters", type=int, default=200)
+    ap.add_argument("--ref-threads", type=int, default=0)
+    ap.add_argument("--ref-step-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    dist = Dist()
+    try:
+        if args.impl == "reference":
+            run_reference(args, dist)
+        else:
+            run_ours(args, dist)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

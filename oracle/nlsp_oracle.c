@@ -624,6 +624,41 @@ int orc_twolevel_create(uint64_t n, const uint64_t* rp, const uint64_t* ci, cons
     return ORC_OK;
 }
 
+/* The operator of an already-built preconditioner from its parts (orthonormal
+ * basis, symmetric A_c): smoother and Cholesky as in the constructor
+ * (two_level.hpp:25,52), the QR/Galerkin body skipped. Used to time the solve
+ * loop at sizes where the constructor's column-strided loops take minutes. */
+int orc_twolevel_from_parts(uint64_t n, const uint64_t* rp, const uint64_t* ci, const double* v,
+                            uint64_t k, const double* basis, const double* coarse, double omega,
+                            uint64_t nu1, uint64_t nu2, orc_twolevel** out) {
+    *out = NULL;
+    orc_twolevel* t = calloc(1, sizeof *t);
+    t->n = n;
+    t->k = k;
+    t->nu1 = nu1;
+    t->nu2 = nu2;
+    t->omega = omega;
+    t->dinv = malloc(sizeof(double) * (n ? n : 1));
+    int st = orc_inv_diag(n, rp, ci, v, omega, t->dinv);
+    if (st == ORC_OK && k == 0) st = fail(ORC_VALIDATION, "two-level: empty coarse space");
+    if (st != ORC_OK) {
+        orc_twolevel_destroy(t);
+        return st;
+    }
+    t->basis = malloc(sizeof(double) * n * k);
+    memcpy(t->basis, basis, sizeof(double) * n * k);
+    t->coarse = malloc(sizeof(double) * k * k);
+    memcpy(t->coarse, coarse, sizeof(double) * k * k);
+    t->l = malloc(sizeof(double) * k * k);
+    st = orc_cholesky(k, t->coarse, t->l);
+    if (st != ORC_OK) {
+        orc_twolevel_destroy(t);
+        return st;
+    }
+    *out = t;
+    return ORC_OK;
+}
+
 void orc_twolevel_export(const orc_twolevel* t, double* basis, double* chol, double* coarse) {
     if (basis) memcpy(basis, t->basis, sizeof(double) * t->n * t->k);
     if (chol) memcpy(chol, t->l, sizeof(double) * t->k * t->k);

@@ -70,6 +70,9 @@ int orc_twolevel_create(uint64_t n, const uint64_t* rp, const uint64_t* ci, cons
                         uint64_t k, const double* basis_any, double omega, uint64_t nu1,
                         uint64_t nu2, orc_twolevel** out);
 void orc_twolevel_destroy(orc_twolevel* t);
+int orc_twolevel_from_parts(uint64_t n, const uint64_t* rp, const uint64_t* ci, const double* v,
+                            uint64_t k, const double* basis, const double* coarse, double omega,
+                            uint64_t nu1, uint64_t nu2, orc_twolevel** out);
 /* basis_ (n x k), L (k x k), symmetrised Galerkin operator A_c (k x k) */
 void orc_twolevel_export(const orc_twolevel* t, double* basis, double* chol, double* coarse);
 int orc_twolevel_apply(const orc_twolevel* t, uint64_t n, const uint64_t* rp,

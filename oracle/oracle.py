@@ -117,6 +117,8 @@ class Oracle:
             "orc_cholesky_solve_factored": (None, [u64, Pdbl, Pdbl, Pdbl]),
             "orc_twolevel_create": (C.c_int, [u64, Pu64, Pu64, Pdbl, u64, Pdbl, dbl, u64, u64, C.POINTER(vp)]),
             "orc_twolevel_destroy": (None, [vp]),
+            "orc_twolevel_from_parts": (C.c_int, [u64, Pu64, Pu64, Pdbl, u64, Pdbl, Pdbl, dbl, u64, u64,
+                                                  C.POINTER(vp)]),
             "orc_twolevel_export": (None, [vp, Pdbl, Pdbl, Pdbl]),
             "orc_twolevel_apply": (C.c_int, [vp, u64, Pu64, Pu64, Pdbl, Pdbl, Pdbl]),
             "orc_pcg": (C.c_int, [u64, Pu64, Pu64, Pdbl, C.c_int, vp, Pdbl, dbl, u64, Pdbl, Pdbl, u64,
@@ -246,6 +248,16 @@ class Oracle:
                                                nu2, C.byref(h)))
         return _TwoLevel(self, h, n, k, csr)
 
+    def twolevel_from_parts(self, a, basis, coarse, omega, nu1, nu2):
+        csr = _csr(a)
+        n, rp, ci, v = csr
+        basis = np.ascontiguousarray(basis, np.float64)
+        coarse = np.ascontiguousarray(coarse, np.float64)
+        h = vp()
+        self._chk(self.lib.orc_twolevel_from_parts(n, _u(rp), _u(ci), _d(v), basis.shape[1], _d(basis),
+                                                   _d(coarse), omega, nu1, nu2, C.byref(h)))
+        return _TwoLevel(self, h, n, basis.shape[1], csr)
+
     def _export(self, t, basis, chol, coarse):
         self.lib.orc_twolevel_export(t.handle, _d(basis), _d(chol), _d(coarse))
 
@@ -318,6 +330,8 @@ class Reference:
             "ref_cholesky_solve": (C.c_int, [u64, Pdbl, Pdbl, Pdbl]),
             "ref_twolevel_create": (vp, [vp, u64, Pdbl, dbl, u64, u64, Pi32]),
             "ref_twolevel_destroy": (None, [vp]),
+            "ref_twolevel_from_parts": (vp, [vp, u64, Pdbl, Pdbl, dbl, u64, u64, Pi32]),
+            "ref_pcg_parallel": (C.c_int, [vp, C.c_int, vp, Pdbl, dbl, u64, C.c_int, Pdbl, Pu64]),
             "ref_twolevel_export": (None, [vp, Pdbl, Pdbl, Pdbl]),
             "ref_twolevel_galerkin": (None, [vp, vp, Pdbl]),
             "ref_twolevel_apply": (C.c_int, [vp, vp, Pdbl, Pdbl]),
@@ -485,6 +499,25 @@ class Reference:
         h = self.lib.ref_twolevel_create(self.handle(a), k, _d(basis), omega, nu1, nu2, C.byref(st))
         self._chk(st.value)
         return _TwoLevel(self, h, _csr(a)[0], k, a)
+
+    def twolevel_from_parts(self, a, basis, coarse, omega, nu1, nu2):
+        """Reference TwoLevelPreconditioner with basis_/coarse_/smoother_ seated
+        from given parts (the constructor body is bypassed; see ref_driver.cpp)."""
+        basis = np.ascontiguousarray(basis, np.float64)
+        coarse = np.ascontiguousarray(coarse, np.float64)
+        st = C.c_int(0)
+        h = self.lib.ref_twolevel_from_parts(self.handle(a), basis.shape[1], _d(basis), _d(coarse),
+                                             omega, nu1, nu2, C.byref(st))
+        self._chk(st.value)
+        return _TwoLevel(self, h, _csr(a)[0], basis.shape[1], a)
+
+    def pcg_parallel(self, a, b, kind, t, delta, max_iters, threads):
+        """`threads` concurrent reference pcg solves; returns (wall ms, iterations)."""
+        b = np.ascontiguousarray(b, np.float64)
+        ms, it = C.c_double(0.0), C.c_uint64(0)
+        self._chk(self.lib.ref_pcg_parallel(self.handle(a), kind, t.handle if t else None, _d(b), delta,
+                                            max_iters, threads, C.byref(ms), C.byref(it)))
+        return float(ms.value), int(it.value)
 
     def galerkin(self, t):
         out = np.empty((t.k, t.k))

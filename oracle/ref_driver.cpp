@@ -36,6 +36,7 @@
 #include <sstream>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -330,6 +331,65 @@ void* ref_twolevel_create(void* h, std::uint64_t k, const double* basis, double 
 }
 
 void ref_twolevel_destroy(void* t) { delete static_cast<RefTwoLevel*>(t); }
+
+// A TwoLevelPreconditioner whose members are set from given parts instead of
+// running the constructor body: basis_ = an orthonormal basis, coarse_ =
+// CholeskyFactor(A_c) (the reference's own factorisation, cholesky.hpp:15-37),
+// smoother_ = JacobiSmoother(a, omega). Used only to time the reference's own
+// apply/pcg (two_level.hpp:60-81,141-191) at full size, where the constructor's
+// column-strided QR + Galerkin loops alone take ~20 min.
+void* ref_twolevel_from_parts(void* h, std::uint64_t k, const double* basis, const double* coarse,
+                              double omega, std::uint64_t nu1, std::uint64_t nu2, int* status) {
+    RefTwoLevel* out = nullptr;
+    *status = guarded([&] {
+        auto* a = static_cast<SparseCsrMatrix*>(h);
+        // constructed on a 1x1 identity problem (trivially cheap), then re-seated
+        const auto tiny = SparseCsrMatrix::identity(1);
+        DenseMatrix one(1, 1, 1.0);
+        auto t = std::make_unique<RefTwoLevel>();
+        t->m = std::make_unique<TwoLevelPreconditioner>(tiny, one, omega, nu1, nu2);
+        t->m->basis_ = dense_from(a->dim(), k, basis);
+        t->m->coarse_ = std::make_unique<CholeskyFactor>(dense_from(k, k, coarse));
+        t->m->smoother_ = JacobiSmoother(*a, omega);
+        out = t.release();
+    });
+    return out;
+}
+
+// `threads` concurrent reference pcg solves of the same system (the reference
+// parallelises across instances only, pipeline.hpp:356 / parallel.hpp:26-55;
+// objects are safe for concurrent pcg). Returns wall ms and the
+// per-thread iteration count of thread 0.
+int ref_pcg_parallel(void* h, int kind, void* t, const double* b, double delta,
+                     std::uint64_t max_iters, int threads, double* wall_ms,
+                     std::uint64_t* iterations) {
+    return guarded([&] {
+        auto* a = static_cast<SparseCsrMatrix*>(h);
+        std::vector<double> bv(b, b + a->dim());
+        std::vector<std::uint64_t> its(threads, 0);
+        std::vector<std::string> errs(threads);
+        auto work = [&](int i) {
+            try {
+                PcgResult r;
+                if (kind == 0) r = pcg(*a, bv, IdentityPreconditioner{}, delta, max_iters);
+                else if (kind == 1) r = pcg(*a, bv, JacobiPreconditioner{}, delta, max_iters);
+                else r = pcg(*a, bv, *static_cast<RefTwoLevel*>(t)->m, delta, max_iters);
+                its[i] = r.report.iterations;
+            } catch (const std::exception& e) {
+                errs[i] = e.what();
+            }
+        };
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> th;
+        for (int i = 0; i < threads; ++i) th.emplace_back(work, i);
+        for (auto& x : th) x.join();
+        const auto t1 = std::chrono::steady_clock::now();
+        *wall_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        *iterations = its[0];
+        for (auto& e : errs)
+            if (!e.empty()) throw NumericError(e);
+    });
+}
 
 // basis_ (n x k), the Cholesky factor L (k x k) and A_c = L L^T (recomposed
 // from the reference's own factor, k x k)
