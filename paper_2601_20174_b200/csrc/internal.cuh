@@ -53,6 +53,9 @@ struct SolveArgs {
     const double* P;     // basis, n x k row-major, ld = k
     const double* L;     // Cholesky factor of A_c, k x k row-major
     int k;
+    int tile_nnz64;   // max nonzeros in any run of 64 / 128 consecutive rows
+    int tile_nnz128;  // (stage sizes of the TMA-staged kernels)
+    int tile_nnz256;
     double* x;
     double* r;
     double* q;

@@ -4,6 +4,7 @@
 // one PCG iteration, epilogue). Reference interface cited per entry point.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -72,6 +73,7 @@ struct nlsp_csr {
     double* diag;
     int diag_ok;  // all A_ii > 0
     int max_row;
+    int tile_nnz64, tile_nnz128, tile_nnz256;  // max nonzeros of any 64/128/256-row tile
 };
 
 struct nlsp_dense {
@@ -223,6 +225,9 @@ SolveArgs make_args(nlsp_ctx* c, const nlsp_csr* a, const nlsp_twolevel* m) {
     s.ci = a->ci;
     s.v = a->v;
     s.diag = a->diag;
+    s.tile_nnz64 = a->tile_nnz64;
+    s.tile_nnz128 = a->tile_nnz128;
+    s.tile_nnz256 = a->tile_nnz256;
     s.wd = m ? m->wd : nullptr;
     s.P = m ? m->basis : nullptr;
     s.L = m ? m->L : nullptr;
@@ -519,7 +524,19 @@ nlsp_status nlsp_csr_upload(nlsp_ctx* ctx, uint64_t n, uint64_t nnz, const uint6
         return cuda_fail(ctx, e, w);
     };
     cudaError_t e;
-    if ((e = dalloc(&a->rp, n + 1)) || (e = dalloc(&a->ci, nnz)) || (e = dalloc(&a->v, nnz)) ||
+    // TMA-staged tiles: max nonzeros per 64 / 128-row tile; arrays padded so the
+    // 16-B-rounded bulk copies of the last tile stay inside the allocations
+    a->tile_nnz64 = a->tile_nnz128 = a->tile_nnz256 = 0;
+    for (uint64_t r0 = 0; r0 < n; r0 += 64) {
+        auto span = [&](uint64_t len) {
+            const uint64_t r1 = r0 + len < n ? r0 + len : n;
+            return (int)(row_ptr[r1] - row_ptr[r0]);
+        };
+        a->tile_nnz64 = std::max(a->tile_nnz64, span(64));
+        if ((r0 & 127) == 0) a->tile_nnz128 = std::max(a->tile_nnz128, span(128));
+        if ((r0 & 255) == 0) a->tile_nnz256 = std::max(a->tile_nnz256, span(256));
+    }
+    if ((e = dalloc(&a->rp, n + 1 + 16)) || (e = dalloc(&a->ci, nnz + 16)) || (e = dalloc(&a->v, nnz + 16)) ||
         (e = dalloc(&a->diag, n)) || (e = dalloc(&rp64, n + 1)) || (e = dalloc(&ci64, nnz)))
         return fail(e, "csr_upload alloc");
     if ((e = cudaMemcpyAsync(rp64, row_ptr, (n + 1) * 8, cudaMemcpyHostToDevice, ctx->s)) ||

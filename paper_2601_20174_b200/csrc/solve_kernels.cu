@@ -21,6 +21,7 @@
 #include <utility>
 
 #include "internal.cuh"
+#include "tma_rows.cuh"
 
 namespace nlsp {
 
@@ -33,6 +34,14 @@ namespace nlsp {
 #endif
 #ifndef NLSP_BLOCKROWS
 #define NLSP_BLOCKROWS 0
+#endif
+// minimum resident CTAs per SM requested from ptxas (register cap) for the
+// basis-streaming (P) and the SpMV kernels
+#ifndef NLSP_MINB_P
+#define NLSP_MINB_P 1
+#endif
+#ifndef NLSP_MINB_S
+#define NLSP_MINB_S 1
 #endif
 constexpr int kU = NLSP_KU;
 constexpr int kUP = NLSP_KUP;
@@ -257,7 +266,7 @@ __global__ void k_init_ctl(PcgState* st) {
 // -------------------------------------------------------------- k_spmv_p --
 // p = z + beta p (written to the other ping-pong buffer), q = A p, p.q;
 // last CTA: p^T A p <= 0 -> NotSpdError (two_level.hpp:159-163), alpha = rz / pap
-__global__ void __launch_bounds__(kThreads) k_spmv_p(SolveArgs a) {
+__global__ void __launch_bounds__(kThreads, NLSP_MINB_S) k_spmv_p(SolveArgs a) {
     PcgState* st = a.st;
     if (st->done) return;
     const bool odd = st->it & 1;
@@ -367,7 +376,7 @@ __global__ void k_loop_ctl(PcgState* st, cudaGraphConditionalHandle h, int use_c
 // z_out = z_in + (w dinv)(r - A z_in) (smoothing.hpp:34-41, contracted), with
 // z_in given by the gather (implicit first sweep or a buffer); RZ: r.z_out
 template <class Gat, bool RZ>
-__global__ void __launch_bounds__(kThreads) k_sweep(SolveArgs a, Gat g, double* zout) {
+__global__ void __launch_bounds__(kThreads, NLSP_MINB_S) k_sweep(SolveArgs a, Gat g, double* zout) {
     PcgState* st = a.st;
     if (st->done) return;
     double s[1] = {0.0};
@@ -419,13 +428,13 @@ __device__ void coarse_solve_warp(const double* __restrict__ L, int k, double* y
 // res = r - A z_pre (two_level.hpp:63-67); c = P^T res (:69-72); the last CTA
 // sums the per-CTA c partials in a fixed order and solves A_c e = c (:73).
 // ZMODE 0: z_pre = 0 (nu1 = 0), 1: z_pre = w D^-1 r implicit (nu1 = 1), 2: buffer.
+template <int PPL, int NT>
+__device__ __forceinline__ void restrict_finish(double (&acc)[2 * PPL], const SolveArgs& a);
+
 template <int PPL, int ZMODE>
-__global__ void __launch_bounds__(kThreads) k_restrict(SolveArgs a, const double* zpre) {
+__global__ void __launch_bounds__(kThreads, NLSP_MINB_P) k_restrict(SolveArgs a, const double* zpre) {
     PcgState* st = a.st;
     if (st->done) return;
-    __shared__ double cs[kThreads / 32][2 * 8 * PPL];
-    __shared__ double red[kThreads];
-    __shared__ double ys[2 * 8 * PPL];
     const int ld = a.k + (a.k & 1);
     const int pairs = ld >> 1;
     double acc[2 * PPL];
@@ -460,6 +469,19 @@ __global__ void __launch_bounds__(kThreads) k_restrict(SolveArgs a, const double
             }
         }
     ROW_BATCH_END
+    restrict_finish<PPL, kThreads>(acc, a);
+}
+
+// Restriction epilogue shared by both restriction kernels: per-lane partials
+// -> CTA partial -> fixed-order grid sum in the last CTA -> coarse solve.
+template <int PPL, int NT>
+__device__ __forceinline__ void restrict_finish(double (&acc)[2 * PPL], const SolveArgs& a) {
+    PcgState* st = a.st;
+    __shared__ double cs[NT / 32][2 * 8 * PPL];
+    __shared__ double red[NT];
+    __shared__ double ys[2 * 8 * PPL];
+    const int ld = a.k + (a.k & 1);
+    const int pairs = ld >> 1;
     // groups of a warp -> lanes 0..7, warps -> shared, CTA partial -> global
 #pragma unroll
     for (int t = 0; t < 2 * PPL; ++t) {
@@ -621,6 +643,233 @@ __global__ void __launch_bounds__(kThreads) k_spmv(int n, const int* rp, const i
     ROW_BATCH_END
 }
 
+// ======================================================= TMA-staged rows ==
+__device__ __host__ __forceinline__ int tile_nnz_for(const SolveArgs& a, int TR) {
+    return TR <= 64 ? a.tile_nnz64 : (TR <= 128 ? a.tile_nnz128 : a.tile_nnz256);
+}
+
+// Row epilogues of the SpMV-family kernels (same arithmetic as the direct
+// kernels above). Each provides the gather, the per-row update (run by lane 0
+// of the row's group) and, with NV > 0, the last-CTA finish.
+struct OpSpmvP {
+    static constexpr int NV = 1;
+    static constexpr int TICKET = kTkSpmvP;
+    GPupd g;
+    double* pc;
+    double* q;
+    __device__ __forceinline__ void init(const SolveArgs& a) {
+        const bool odd = a.st->it & 1;
+        g = GPupd{a.z, odd ? a.p0 : a.p1, a.st->beta, a.st->first != 0};
+        pc = odd ? a.p1 : a.p0;
+        q = a.q;
+    }
+    __device__ __forceinline__ double operator()(int j) const { return g(j); }
+    __device__ __forceinline__ void row(int i, double y, double* s) const {
+        const double pi = g(i);
+        pc[i] = pi;
+        q[i] = y;
+        s[0] = fma(pi, y, s[0]);
+    }
+    __device__ __forceinline__ void finish(PcgState* st, const double* tot) const {
+        const double pap = tot[0];
+        st->pap = pap;
+        if (pap <= 0.0) {
+            st->error = kErrNotSpd;
+            st->done = 1;
+        } else {
+            st->alpha = st->rz / pap;
+        }
+    }
+};
+
+template <class Gat, bool RZ>
+struct OpSweep {
+    static constexpr int NV = RZ ? 1 : 0;
+    static constexpr int TICKET = kTkSweep;
+    Gat g;
+    const double* r;
+    const double* wd;
+    double* zout;
+    __device__ __forceinline__ double operator()(int j) const { return g(j); }
+    __device__ __forceinline__ void row(int i, double y, double* s) const {
+        const double ri = r[i];
+        const double zi = fma(wd[i], ri - y, g(i));
+        zout[i] = zi;
+        if (RZ) s[0] = fma(ri, zi, s[0]);
+    }
+    __device__ __forceinline__ void init(const SolveArgs&) {}
+    __device__ __forceinline__ void finish(PcgState* st, const double* tot) const {
+        st->rz_new = tot[0];
+    }
+};
+
+struct OpTrueRes {
+    static constexpr int NV = 1;
+    static constexpr int TICKET = kTkTrue;
+    const double* x;
+    const double* b;
+    __device__ __forceinline__ double operator()(int j) const { return x[j]; }
+    __device__ __forceinline__ void row(int i, double y, double* s) const {
+        const double d = b[i] - y;
+        s[0] = fma(d, d, s[0]);
+    }
+    __device__ __forceinline__ void init(const SolveArgs&) {}
+    __device__ __forceinline__ void finish(PcgState* st, const double* tot) const {
+        st->true_res = sqrt(tot[0]) / st->bnorm;
+    }
+};
+
+struct OpPlain {
+    static constexpr int NV = 0;
+    static constexpr int TICKET = kTkGeneric;
+    const double* x;
+    double* y;
+    __device__ __forceinline__ double operator()(int j) const { return x[j]; }
+    __device__ __forceinline__ void row(int i, double yy, double*) const { y[i] = yy; }
+    __device__ __forceinline__ void init(const SolveArgs&) {}
+    __device__ __forceinline__ void finish(PcgState*, const double*) const {}
+};
+
+// SKIP: 0 never, 1 when st->done (solve kernels), 2 when st->error (true residual)
+// G lanes per row (transposed mapping), U row steps per warp and tile:
+// TR = 8 warps * U * (32 / G) rows per staged tile.
+template <int G, int U, int S, int SKIP, class Op>
+__global__ void __launch_bounds__(kTmaThreads) k_spmv_tma(SolveArgs a, Op op) {
+    constexpr int R = 32 / G;
+    constexpr int TR = kConsumerWarps * U * R;
+    constexpr int CH = G == 1 ? 8 : (G == 2 ? 4 : 2);
+    static_assert(TR <= 256, "stage sizes are bounded by the 64/128/256-row nnz maxima");
+    PcgState* st = a.st;
+    if (SKIP == 1 && st->done) return;
+    if (SKIP == 2 && st->error) return;
+    op.init(a);
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem);
+    unsigned long long* empty = full + S;
+    unsigned char* stages = smem + 128;
+    const StageLayout L(TR, tile_nnz_for(a, TR), 0, false);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    const int ntiles = (a.n + TR - 1) / TR;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double s[Op::NV > 0 ? Op::NV : 1];
+    for (int j = 0; j < (Op::NV > 0 ? Op::NV : 1); ++j) s[j] = 0.0;
+    if (warp == kConsumerWarps) {
+        produce_tiles<S>(a.rp, a.ci, a.v, nullptr, 0, a.n, TR, stages, L, full, empty);
+    } else {
+        int i = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+            const int stg = i % S;
+            mbar_wait(&full[stg], (i / S) & 1);
+            const int r0 = tile * TR, rows = min(TR, a.n - r0);
+            int lr[U];
+            bool valid[U];
+            double y[U];
+            staged_rows_dot<G, U, CH>(stages + stg * L.bytes, L, rows, warp, lane, op, lr, valid, y);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stg]);
+            if (lane < R) {
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (valid[u]) op.row(r0 + lr[u], y[u], s);
+            }
+        }
+    }
+    if constexpr (Op::NV > 0) {
+        double v[Op::NV], tot[Op::NV];
+#pragma unroll
+        for (int j = 0; j < Op::NV; ++j) v[j] = s[j];
+        if (grid_reduce<Op::NV>(v, a.partials, &st->counter[Op::TICKET], tot) && threadIdx.x == 0)
+            op.finish(st, tot);
+    }
+}
+
+// res = r - A z_pre; c = P^T res with the tile's CSR slice AND its basis rows
+// staged by the producer warp (two_level.hpp:63-73). The SpMV of a 64-row tile
+// uses the transposed mapping (4 lanes per row, coalesced gathers), its
+// residuals go through shared memory to the basis pass (8 lanes per basis row,
+// 16-B reads of the staged rows).
+template <int PPL, int ZMODE, int S>
+__global__ void __launch_bounds__(kTmaThreads) k_restrict_tma(SolveArgs a, const double* zpre) {
+    constexpr int G = 4, R = 32 / G;
+    constexpr int TR = kConsumerWarps * R;  // 64
+    constexpr int UP = TR / kGroups;        // basis rows per 8-lane group
+    PcgState* st = a.st;
+    if (st->done) return;
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem);
+    unsigned long long* empty = full + S;
+    double* res_s = reinterpret_cast<double*>(smem + 64);  // [2][TR] residuals (after barriers)
+    unsigned char* stages = smem + 64 + 2 * TR * 8;
+    const int ld = a.k + (a.k & 1);
+    const int pairs = ld >> 1;
+    const StageLayout L(TR, a.tile_nnz64, ld, true);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    const int ntiles = (a.n + TR - 1) / TR;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double acc[2 * PPL];
+#pragma unroll
+    for (int t = 0; t < 2 * PPL; ++t) acc[t] = 0.0;
+    if (warp == kConsumerWarps) {
+        produce_tiles<S>(a.rp, a.ci, a.v, a.P, ld, a.n, TR, stages, L, full, empty);
+    } else {
+        const int grp = threadIdx.x >> 3, l = threadIdx.x & (kGroup - 1);
+        const GWdr gw{a.wd, a.r};
+        const GPlain gp{zpre};
+        int i = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+            const int stg = i % S;
+            const unsigned char* base = stages + stg * L.bytes;
+            const int r0 = tile * TR, rows = min(TR, a.n - r0);
+            double* rs = res_s + (i & 1) * TR;
+            // residual of row r0 + lr: r - A z_pre (own r read before the wait)
+            const int lr0 = warp * R + (lane % R);
+            const double rown = lr0 < rows ? a.r[r0 + lr0] : 0.0;
+            mbar_wait(&full[stg], (i / S) & 1);
+            int lr[1];
+            bool valid[1];
+            double y[1] = {0.0};
+            if (ZMODE == 1) staged_rows_dot<G, 1, 2>(base, L, rows, warp, lane, gw, lr, valid, y);
+            if (ZMODE == 2) staged_rows_dot<G, 1, 2>(base, L, rows, warp, lane, gp, lr, valid, y);
+            if (lane < R) rs[lr0] = lr0 < rows ? rown - y[0] : 0.0;
+            asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+            const double* ps = reinterpret_cast<const double*>(base + L.p_off);
+#pragma unroll
+            for (int u = 0; u < UP; ++u) {
+                const int lrp = grp + kGroups * u;
+                const bool ok = lrp < rows;
+                const double res = ok ? rs[lrp] : 0.0;
+                const double* prow = ps + lrp * ld;
+#pragma unroll
+                for (int t = 0; t < PPL; ++t) {
+                    const int pi = l + kGroup * t;
+                    if (ok && pi < pairs) {
+                        const double2 pv = *reinterpret_cast<const double2*>(prow + 2 * pi);
+                        acc[2 * t] = fma(pv.x, res, acc[2 * t]);
+                        acc[2 * t + 1] = fma(pv.y, res, acc[2 * t + 1]);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stg]);
+        }
+    }
+    restrict_finish<PPL, kTmaThreads>(acc, a);
+}
+
 // ======================================================== host launchers ==
 
 namespace {
@@ -651,6 +900,41 @@ template <int U, class... KArgs, class... Args>
 void launch_rows(const LaunchCtx& c, void (*f)(KArgs...), long long n, Args&&... args) {
     const int g = occ_grid(c, reinterpret_cast<const void*>(f), n, (kThreads / 32) * kRowsPerWarp * U);
     f<<<g, kThreads, 0, c.s>>>(std::forward<Args>(args)...);
+}
+// TMA-staged kernels: one CTA = 8 consumer warps + 1 producer warp, dynamic
+// shared memory for the stage ring, grid = min(tiles, resident CTAs).
+template <class... KArgs, class... Args>
+void launch_tma(const LaunchCtx& c, void (*f)(KArgs...), long long ntiles, size_t smem,
+                Args&&... args) {
+    static std::mutex mu;
+    static std::unordered_map<const void*, size_t> attr;
+    static std::unordered_map<unsigned long long, int> occ;
+    const void* fp = reinterpret_cast<const void*>(f);
+    int nb = 1;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        size_t& cur = attr[fp];
+        if (smem > cur) {
+            cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cur = smem;
+        }
+        const unsigned long long key = reinterpret_cast<unsigned long long>(fp) * 1315423911ull ^ smem;
+        auto it = occ.find(key);
+        if (it == occ.end()) {
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kTmaThreads, smem) != cudaSuccess ||
+                nb < 1)
+                nb = 1;
+            cudaGetLastError();
+            occ[key] = nb;
+        } else {
+            nb = it->second;
+        }
+    }
+    long long g = (long long)c.num_sms * nb;
+    if (g > kMaxGrid) g = kMaxGrid;
+    if (g > ntiles) g = ntiles;
+    if (g < 1) g = 1;
+    f<<<(int)g, kTmaThreads, smem, c.s>>>(std::forward<Args>(args)...);
 }
 // element kernels: units = elements (2 per thread)
 template <class... KArgs, class... Args>
@@ -684,8 +968,44 @@ void launch_init_ctl(const LaunchCtx& c, PcgState* st) {
     count(c);
 }
 
+#ifndef NLSP_TMA
+#define NLSP_TMA 1
+#endif
+#ifndef NLSP_SPMV_STAGES
+#define NLSP_SPMV_STAGES 3
+#endif
+#ifndef NLSP_RESTRICT_STAGES
+#define NLSP_RESTRICT_STAGES 2
+#endif
+#ifndef NLSP_SPMV_G
+#define NLSP_SPMV_G 1
+#endif
+#ifndef NLSP_SPMV_U
+#define NLSP_SPMV_U 1
+#endif
+constexpr int kSpmvTR = kConsumerWarps * NLSP_SPMV_U * (32 / NLSP_SPMV_G);
+constexpr int kRestrictTR = kConsumerWarps * 8;
+
+size_t spmv_stage_smem(const SolveArgs& a) {
+    return 128 + (size_t)NLSP_SPMV_STAGES * StageLayout(kSpmvTR, tile_nnz_for(a, kSpmvTR), 0, false).bytes;
+}
+size_t restrict_stage_smem(const SolveArgs& a) {
+    const int ld = a.k + (a.k & 1);
+    return 64 + 2 * kRestrictTR * 8 +
+           (size_t)NLSP_RESTRICT_STAGES * StageLayout(kRestrictTR, a.tile_nnz64, ld, true).bytes;
+}
+long long spmv_tiles(const SolveArgs& a) { return (a.n + kSpmvTR - 1) / kSpmvTR; }
+long long restrict_tiles(const SolveArgs& a) { return (a.n + kRestrictTR - 1) / kRestrictTR; }
+
+template <int SKIP, class Op>
+void launch_spmv_op(const LaunchCtx& c, const SolveArgs& a, const Op& op) {
+    launch_tma(c, k_spmv_tma<NLSP_SPMV_G, NLSP_SPMV_U, NLSP_SPMV_STAGES, SKIP, Op>, spmv_tiles(a),
+               spmv_stage_smem(a), a, op);
+}
+
 void launch_spmv_p(const LaunchCtx& c, const SolveArgs& a) {
-    launch_rows<kU>(c, k_spmv_p, a.n, a);
+    if (NLSP_TMA) launch_spmv_op<1>(c, a, OpSpmvP{});
+    else launch_rows<kU>(c, k_spmv_p, a.n, a);
     count(c);
 }
 
@@ -703,7 +1023,8 @@ void launch_loop_ctl(const LaunchCtx& c, PcgState* st, cudaGraphConditionalHandl
 }
 
 void launch_true_res(const LaunchCtx& c, const SolveArgs& a) {
-    launch_rows<kU>(c, k_true_res, a.n, a);
+    if (NLSP_TMA) launch_spmv_op<2>(c, a, OpTrueRes{a.x, a.b});
+    else launch_rows<kU>(c, k_true_res, a.n, a);
     count(c);
 }
 
@@ -715,6 +1036,15 @@ void launch_spmv(const LaunchCtx& c, int n, const int* rp, const int* ci, const 
 
 template <int PPL>
 static void restrict_ppl(const LaunchCtx& c, const SolveArgs& a, int zmode, const double* zpre) {
+    if (NLSP_TMA) {
+        const long long nt = restrict_tiles(a);
+        const size_t sm = restrict_stage_smem(a);
+        constexpr int S = NLSP_RESTRICT_STAGES;
+        if (zmode == 0) launch_tma(c, k_restrict_tma<PPL, 0, S>, nt, sm, a, zpre);
+        else if (zmode == 1) launch_tma(c, k_restrict_tma<PPL, 1, S>, nt, sm, a, zpre);
+        else launch_tma(c, k_restrict_tma<PPL, 2, S>, nt, sm, a, zpre);
+        return;
+    }
     if (zmode == 0) launch_rows<kUP>(c, k_restrict<PPL, 0>, a.n, a, zpre);
     else if (zmode == 1) launch_rows<kUP>(c, k_restrict<PPL, 1>, a.n, a, zpre);
     else launch_rows<kUP>(c, k_restrict<PPL, 2>, a.n, a, zpre);
@@ -769,6 +1099,19 @@ void launch_prolong(const LaunchCtx& c, const SolveArgs& a, int zmode, bool rz, 
 // sweep with z_in = implicit w D^-1 r (first pre-sweep) or a buffer
 void launch_sweep(const LaunchCtx& c, const SolveArgs& a, bool implicit_in, const double* zin,
                   double* zout, bool rz) {
+    if (NLSP_TMA) {
+        if (implicit_in) {
+            const GWdr gw{a.wd, a.r};
+            if (rz) launch_spmv_op<1>(c, a, OpSweep<GWdr, true>{gw, a.r, a.wd, zout});
+            else launch_spmv_op<1>(c, a, OpSweep<GWdr, false>{gw, a.r, a.wd, zout});
+        } else {
+            const GPlain gp{zin};
+            if (rz) launch_spmv_op<1>(c, a, OpSweep<GPlain, true>{gp, a.r, a.wd, zout});
+            else launch_spmv_op<1>(c, a, OpSweep<GPlain, false>{gp, a.r, a.wd, zout});
+        }
+        count(c);
+        return;
+    }
     if (implicit_in) {
         const GWdr gw{a.wd, a.r};
         if (rz) launch_rows<kU>(c, k_sweep<GWdr, true>, a.n, a, gw, zout);

@@ -5,9 +5,13 @@ set -u
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
 CFG=${CFG:-C4}
+if [ "${BENCH:-1}" = "1" ]; then
 timeout 600 python bench.py --config $CFG > gpurun_out/bench_$CFG.json 2> gpurun_out/bench_$CFG.err; echo "bench exit=$?"
 timeout 600 python bench.py --config $CFG --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_$CFG.json 2> gpurun_out/bench_ref_$CFG.err; echo "ref exit=$?"
-SHORT="python bench.py --config $CFG --steps 1 --warmup 3 --no-cpu-baseline --profile-iters 1"
+fi
+# ncu cannot profile kernel nodes of graphs with conditional nodes: the
+# profiled command runs the same kernels stream-ordered (NLSP_LOOP=host)
+SHORT="env NLSP_LOOP=host python bench.py --config $CFG --steps 1 --warmup 3 --no-cpu-baseline --profile-iters 1"
 if [ "${NCU:-1}" = "1" ]; then
   timeout 300 $SHORT > gpurun_out/short_plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches_$CFG.csv $SHORT > gpurun_out/ncu_list.log 2>&1; echo "ncu list exit=$?"
