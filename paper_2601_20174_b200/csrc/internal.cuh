@@ -31,7 +31,7 @@ enum DevError : int {
 // Device-resident PCG scalars (two_level.hpp:141-191 locals).
 struct PcgState {
     double rz, rz_new, pap, alpha, beta, rr, bnorm, delta, true_res, last_rel;
-    long long it, max_it, iterations;
+    long long it, max_it, iterations, body_runs;
     int done, converged, error, first;
     unsigned int counter[16];  // last-CTA tickets, one slot per kernel kind
 };
@@ -52,6 +52,8 @@ struct SolveArgs {
     const double* diag;  // A_ii                   (Jacobi preconditioner)
     const double* P;     // basis, n x k row-major, ld = k
     const double* L;     // Cholesky factor of A_c, k x k row-major
+    const double* W1;    // (I - w D^-1 A)^nu1 P, n x ld (restriction basis)
+    const double* W2;    // (I - w D^-1 A)^nu2 P, n x ld (prolongation basis; may alias W1)
     int k;
     int tile_nnz64;   // max nonzeros in any run of 64 / 128 consecutive rows
     int tile_nnz128;  // (stage sizes of the TMA-staged kernels)

@@ -33,6 +33,9 @@ void launch_restrict(const LaunchCtx&, const SolveArgs&, int, const double*);
 void launch_prolong(const LaunchCtx&, const SolveArgs&, int, bool, const double*, double*);
 void launch_twolevel_apply(const LaunchCtx&, const SolveArgs&, unsigned long long,
                            unsigned long long);
+void launch_update_restrict(const LaunchCtx&, const SolveArgs&, bool);
+void launch_folded_tail(const LaunchCtx&, const SolveArgs&, unsigned long long, unsigned long long);
+void launch_folded_apply(const LaunchCtx&, const SolveArgs&, unsigned long long, unsigned long long);
 int ppl_for(int k);
 // setup_kernels.cu
 void launch_csr_import(const LaunchCtx&, int, long long, const unsigned long long*,
@@ -93,6 +96,9 @@ struct nlsp_twolevel {
     double* L;       // k x k
     double* coarse;  // k x k
     double* wd;      // n
+    double* W1;      // (I - w D^-1 A)^nu1 P, n x ld (folded cycle)
+    double* W2;      // (I - w D^-1 A)^nu2 P, n x ld (aliases W1 when nu1 == nu2)
+    bool folded;     // folded cycle (default) or the literal schedule (NLSP_CYCLE=literal)
 };
 
 struct GraphKey {
@@ -126,6 +132,7 @@ struct nlsp_ctx {
     cudaGraphExec_t gexec = nullptr;
     GraphKey gkey;
     bool use_graph = true;
+    unsigned long long gk_pro = 0, gk_body = 0, gk_epi = 0;  // kernels per graph part
 };
 
 // ------------------------------------------------------------------ helpers --
@@ -200,7 +207,7 @@ nlsp_status ensure_ws(nlsp_ctx* ctx, long long n, long long hist) {
         free_ws(ctx);
         for (double** p : {&ctx->x, &ctx->r, &ctx->q, &ctx->z, &ctx->p0, &ctx->p1, &ctx->zt0,
                            &ctx->zt1, &ctx->b})
-            CU(dalloc(p, (size_t)n));
+            CU(dalloc(p, (size_t)n + 16));  // padded for 16-B bulk copies of tile slices
         CU(dalloc(&ctx->e, (size_t)kMaxCoarse + 2));
         CU(dalloc(&ctx->partials, (size_t)kMaxGrid * 256));
         ctx->ws_n = n;
@@ -231,6 +238,8 @@ SolveArgs make_args(nlsp_ctx* c, const nlsp_csr* a, const nlsp_twolevel* m) {
     s.wd = m ? m->wd : nullptr;
     s.P = m ? m->basis : nullptr;
     s.L = m ? m->L : nullptr;
+    s.W1 = m ? m->W1 : nullptr;
+    s.W2 = m ? m->W2 : nullptr;
     s.k = m ? m->k : 0;
     s.x = c->x;
     s.r = c->r;
@@ -252,8 +261,13 @@ SolveArgs make_args(nlsp_ctx* c, const nlsp_csr* a, const nlsp_twolevel* m) {
 void enqueue_iteration(const LaunchCtx& lc, const SolveArgs& a, int mode, const nlsp_twolevel* m,
                        cudaGraphConditionalHandle h, int use_cond) {
     launch_spmv_p(lc, a);
-    launch_update(lc, a, mode);
-    if (mode == 0) launch_twolevel_apply(lc, a, m->nu1, m->nu2);
+    if (mode == 0 && m->folded) {
+        launch_update_restrict(lc, a, true);  // x, r, ||r||, c = W1^T r, e
+        launch_folded_tail(lc, a, m->nu1, m->nu2);
+    } else {
+        launch_update(lc, a, mode);
+        if (mode == 0) launch_twolevel_apply(lc, a, m->nu1, m->nu2);
+    }
     launch_loop_ctl(lc, a.st, h, use_cond);
 }
 
@@ -262,7 +276,8 @@ void enqueue_prologue(const LaunchCtx& lc, const SolveArgs& a, int mode, const n
                       const double* params_dev) {
     (void)params_dev;
     launch_bnorm(lc, a);
-    if (mode == 0) launch_twolevel_apply(lc, a, m->nu1, m->nu2);
+    if (mode == 0 && m->folded) launch_folded_apply(lc, a, m->nu1, m->nu2);
+    else if (mode == 0) launch_twolevel_apply(lc, a, m->nu1, m->nu2);
     else launch_init_simple(lc, a, mode == 2 ? 1 : 0);
     launch_init_ctl(lc, a.st);
 }
@@ -276,8 +291,8 @@ nlsp_status build_graph(nlsp_ctx* ctx, const SolveArgs& a, int mode, const nlsp_
     }
     cudaGraph_t g = nullptr;
     LaunchCtx lc = ctx->lc;
-    unsigned long long dummy = 0;
-    lc.launches = &dummy;
+    ctx->gk_pro = ctx->gk_body = ctx->gk_epi = 0;
+    lc.launches = &ctx->gk_pro;
     CU(cudaStreamBeginCapture(ctx->s, cudaStreamCaptureModeThreadLocal));
     enqueue_prologue(lc, a, mode, m, nullptr);
     cudaStreamCaptureStatus cs;
@@ -306,9 +321,11 @@ nlsp_status build_graph(nlsp_ctx* ctx, const SolveArgs& a, int mode, const nlsp_
     if (e == cudaSuccess) {
         LaunchCtx lb = lc;
         lb.s = ctx->s_body;
+        lb.launches = &ctx->gk_body;
         enqueue_iteration(lb, a, mode, m, h, 1);
         e = cudaStreamEndCapture(ctx->s_body, &body);
     }
+    lc.launches = &ctx->gk_epi;
     if (e == cudaSuccess) launch_true_res(lc, a);
     cudaError_t e2 = cudaStreamEndCapture(ctx->s, &g);
     if (e != cudaSuccess) {
@@ -322,23 +339,6 @@ nlsp_status build_graph(nlsp_ctx* ctx, const SolveArgs& a, int mode, const nlsp_
     return NLSP_OK;
 }
 
-// number of kernels one iteration / the prologue launch (for the report)
-unsigned long long iteration_kernels(int mode, const nlsp_twolevel* m) {
-    unsigned long long c = 3;  // spmv_p, update, loop_ctl
-    if (mode == 0) {
-        const unsigned long long pre = m->nu1 >= 2 ? m->nu1 - 1 : 0;
-        c += pre + 1 + 1 + m->nu2;  // sweeps, restrict, prolong, post sweeps
-    }
-    return c;
-}
-
-unsigned long long prologue_kernels(int mode, const nlsp_twolevel* m) {
-    unsigned long long c = 2 + 1;  // bnorm, init_ctl, (state_init outside)
-    if (mode == 0) c += iteration_kernels(0, m) - 3;
-    else c += 1;
-    return c;
-}
-
 // Runs the solve on ctx->b -> ctx->x. Caller has ensured the workspace.
 nlsp_status run_pcg(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twolevel* m,
                     double delta, unsigned long long max_iters, nlsp_solve_report* rep,
@@ -347,7 +347,6 @@ nlsp_status run_pcg(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twole
     const SolveArgs args = make_args(ctx, a, m);
     launch_state_init(ctx->lc, ctx->st, delta, (long long)max_iters);
     CHECK_LAUNCH();
-    CU(cudaEventRecord(ctx->ev0, ctx->s));
     unsigned long long klaunch = 1;
     bool graph_ok = false;
     if (ctx->use_graph) {
@@ -361,6 +360,10 @@ nlsp_status run_pcg(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twole
                 ctx->gkey = GraphKey{};
             }
         }
+    }
+    // solve_ms starts after the (cached) graph build
+    CU(cudaEventRecord(ctx->ev0, ctx->s));
+    if (ctx->use_graph) {
         if (ctx->gexec) {
             CU(cudaGraphLaunch(ctx->gexec, ctx->s));
             graph_ok = true;
@@ -388,8 +391,9 @@ nlsp_status run_pcg(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twole
     CU(cudaStreamSynchronize(ctx->s));
     const PcgState& st = *ctx->st_host;
     if (graph_ok) {
-        const unsigned long long its = st.it + (st.done && st.it < (long long)max_iters ? 1 : 0);
-        klaunch += prologue_kernels(mode, m) + iteration_kernels(mode, m) * (its ? its : 1) + 1;
+        // kernels counted while capturing each graph part; the WHILE body ran
+        // st.body_runs times (k_loop_ctl counts itself)
+        klaunch += ctx->gk_pro + ctx->gk_body * (unsigned long long)st.body_runs + ctx->gk_epi;
         ctx->launches += klaunch;
     }
     float ms = 0.f;
@@ -907,6 +911,10 @@ nlsp_status nlsp_twolevel_build(nlsp_ctx* ctx, const nlsp_csr* a, const nlsp_den
     m->nu1 = nu1;
     m->nu2 = nu2;
     m->omega = omega;
+    {
+        const char* cyc = std::getenv("NLSP_CYCLE");
+        m->folded = !(cyc && std::strcmp(cyc, "literal") == 0);
+    }
     const size_t kk = (size_t)k * k;
     const int g = gram_grid(ctx->lc, n);
     double *part = nullptr, *G = nullptr, *U = nullptr, *Q1 = nullptr, *Q = nullptr, *Y = nullptr;
@@ -947,6 +955,31 @@ nlsp_status nlsp_twolevel_build(nlsp_ctx* ctx, const nlsp_csr* a, const nlsp_den
                               cudaMemcpyDeviceToDevice, ctx->s);
     if (!e && m->ld != k)
         e = cudaMemset2DAsync(m->basis + k, (size_t)m->ld * 8, 0, 8, n, ctx->s);
+    // folded cycle bases W = (I - w D^-1 A)^nu P: nu homogeneous block sweeps
+    // of the orthonormal basis (smoothing.hpp:50-60 applied to its k columns)
+    auto fold = [&](unsigned long long nu, double** out) -> cudaError_t {
+        cudaError_t err = dalloc(out, (size_t)n * m->ld);
+        if (err) return err;
+        double* cur = Q;
+        double* other = Y;  // Y and Q1 are free scratch (n x k) at this point
+        for (unsigned long long s = 0; s < nu; ++s) {
+            double* dst = (cur == Y) ? Q1 : Y;
+            launch_block_op(ctx->lc, 0, (int)n, a->rp, a->ci, a->v, m->wd, k, cur, dst);
+            cur = dst;
+        }
+        (void)other;
+        err = cudaMemcpy2DAsync(*out, (size_t)m->ld * 8, cur, (size_t)k * 8, (size_t)k * 8, n,
+                                cudaMemcpyDeviceToDevice, ctx->s);
+        if (!err && m->ld != k) err = cudaMemset2DAsync(*out + k, (size_t)m->ld * 8, 0, 8, n, ctx->s);
+        return err;
+    };
+    if (!e && m->folded) {
+        e = fold(nu1, &m->W1);
+        if (!e) {
+            if (nu2 == nu1) m->W2 = m->W1;
+            else e = fold(nu2, &m->W2);
+        }
+    }
     if (!e) e = cudaMemcpyAsync(ctx->flags_host, ctx->flags, 16 * sizeof(int), cudaMemcpyDeviceToHost, ctx->s);
     if (!e) e = cudaStreamSynchronize(ctx->s);
     if (e) return fail_cuda(e, "two-level build");
@@ -971,7 +1004,8 @@ nlsp_status nlsp_twolevel_build(nlsp_ctx* ctx, const nlsp_csr* a, const nlsp_den
 void nlsp_twolevel_destroy(nlsp_twolevel* m) {
     if (!m) return;
     cudaSetDevice(m->device);
-    for (double* p : {m->basis, m->L, m->coarse, m->wd}) dfree(p);
+    if (m->W2 && m->W2 != m->W1) dfree(m->W2);
+    for (double* p : {m->basis, m->L, m->coarse, m->wd, m->W1}) dfree(p);
     delete m;
 }
 
@@ -1007,7 +1041,8 @@ nlsp_status nlsp_twolevel_apply(nlsp_ctx* ctx, const nlsp_twolevel* m, const nls
     CU(cudaMemcpyAsync(ctx->r, r, bytes, cudaMemcpyHostToDevice, ctx->s));
     CU(cudaMemsetAsync(ctx->st, 0, sizeof(PcgState), ctx->s));
     const SolveArgs args = make_args(ctx, a, m);
-    launch_twolevel_apply(ctx->lc, args, m->nu1, m->nu2);
+    if (m->folded) launch_folded_apply(ctx->lc, args, m->nu1, m->nu2);
+    else launch_twolevel_apply(ctx->lc, args, m->nu1, m->nu2);
     CHECK_LAUNCH();
     CU(cudaMemcpyAsync(z, ctx->z, bytes, cudaMemcpyDeviceToHost, ctx->s));
     CU(cudaStreamSynchronize(ctx->s));
@@ -1091,15 +1126,18 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
     };
     const double n = a->n, nnz = (double)a->nnz, k = m ? m->k : 0;
     const double csr = 12.0 * nnz + 4.0 * (n + 1);
+    // algorithmic bytes per launch
     std::vector<Acc> acc = {
-        {"spmv_p", csr + 32.0 * n},          // reads z, p; writes p, q
+        {"spmv_p", csr + 32.0 * n},                  // reads z, p; writes p, q
         {"update", (mode == 0 ? 48.0 : (mode == 1 ? 56.0 : 64.0)) * n},
-        {"restrict", csr + 8.0 * n * k + 16.0 * n},  // P, r, w (implicit z1)
-        {"prolong", 8.0 * n * k + 24.0 * n},         // P, r, w; writes z2
+        {"restrict", csr + 8.0 * n * k + 16.0 * n},  // literal: P, r, w (implicit z1)
+        {"prolong", 8.0 * n * k + 24.0 * n},         // literal: P, r, w; writes z2
         {"post_sweep", csr + 32.0 * n},              // z2, r, w; writes z
+        {"update_restrict", 8.0 * n * k + 48.0 * n}, // folded: W1, x, p, q, r; writes x, r
+        {"smooth", csr + 32.0 * n},                  // folded: intermediate sweeps
         {"loop_ctl", 0.0},
     };
-    std::vector<cudaEvent_t> evs(2 * 8);
+    std::vector<cudaEvent_t> evs(2);
     for (auto& e : evs) cudaEventCreate(&e);
     auto timed = [&](int slot, auto&& fn) {
         cudaEventRecord(evs[0], ctx->s);
@@ -1111,20 +1149,40 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
         acc[slot].ms += t;
         acc[slot].launches++;
     };
-    const bool simple_apply = mode == 0 && m->nu1 == 1 && m->nu2 == 1;
+    const bool folded = mode == 0 && m->folded;
+    const bool simple_apply = mode == 0 && !folded && m->nu1 == 1 && m->nu2 == 1;
     for (uint64_t it = 0; it < iters; ++it) {
         timed(0, [&] { launch_spmv_p(ctx->lc, args); });
-        timed(1, [&] { launch_update(ctx->lc, args, mode); });
-        if (mode == 0) {
-            if (simple_apply) {
-                timed(2, [&] { launch_restrict(ctx->lc, args, 1, nullptr); });
-                timed(3, [&] { launch_prolong(ctx->lc, args, 1, false, nullptr, ctx->zt0); });
-                timed(4, [&] { launch_sweep(ctx->lc, args, false, ctx->zt0, ctx->z, true); });
+        if (folded) {
+            timed(5, [&] { launch_update_restrict(ctx->lc, args, true); });
+            // launch_folded_tail, each launch timed on its own
+            const unsigned long long T = m->nu1 + m->nu2;
+            SolveArgs b = args;
+            b.P = m->W2;
+            if (T <= 1) {
+                timed(3, [&] { launch_prolong(ctx->lc, b, T == 0 ? 0 : 1, true, nullptr, ctx->z); });
             } else {
-                timed(2, [&] { launch_twolevel_apply(ctx->lc, args, m->nu1, m->nu2); });
+                double* cur = nullptr;
+                for (unsigned long long j = 2; j <= T; ++j) {
+                    double* nxt = (cur == ctx->zt0) ? ctx->zt1 : ctx->zt0;
+                    timed(6, [&] { launch_sweep(ctx->lc, args, cur == nullptr, cur, nxt, false); });
+                    cur = nxt;
+                }
+                timed(3, [&] { launch_prolong(ctx->lc, b, 2, true, cur, ctx->z); });
+            }
+        } else {
+            timed(1, [&] { launch_update(ctx->lc, args, mode); });
+            if (mode == 0) {
+                if (simple_apply) {
+                    timed(2, [&] { launch_restrict(ctx->lc, args, 1, nullptr); });
+                    timed(3, [&] { launch_prolong(ctx->lc, args, 1, false, nullptr, ctx->zt0); });
+                    timed(4, [&] { launch_sweep(ctx->lc, args, false, ctx->zt0, ctx->z, true); });
+                } else {
+                    timed(2, [&] { launch_twolevel_apply(ctx->lc, args, m->nu1, m->nu2); });
+                }
             }
         }
-        timed(5, [&] { launch_loop_ctl(ctx->lc, ctx->st, cudaGraphConditionalHandle{}, 0); });
+        timed(8, [&] { launch_loop_ctl(ctx->lc, ctx->st, cudaGraphConditionalHandle{}, 0); });
     }
     for (auto& e : evs) cudaEventDestroy(e);
     cudaStreamSynchronize(ctx->s);

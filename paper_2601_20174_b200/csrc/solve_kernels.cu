@@ -211,6 +211,7 @@ __global__ void k_state_init(PcgState* st, double delta, long long max_it) {
     st->it = 0;
     st->max_it = max_it;
     st->iterations = 0;
+    st->body_runs = 0;
     st->done = 0;
     st->converged = 0;
     st->error = 0;
@@ -362,6 +363,7 @@ __global__ void __launch_bounds__(kThreads) k_update(SolveArgs a) {
 
 // beta = rz' / rz, p-update bookkeeping, iteration advance, graph WHILE control
 __global__ void k_loop_ctl(PcgState* st, cudaGraphConditionalHandle h, int use_cond) {
+    st->body_runs += 1;
     if (!st->done) {
         st->beta = st->rz_new / st->rz;
         st->rz = st->rz_new;
@@ -428,8 +430,8 @@ __device__ void coarse_solve_warp(const double* __restrict__ L, int k, double* y
 // res = r - A z_pre (two_level.hpp:63-67); c = P^T res (:69-72); the last CTA
 // sums the per-CTA c partials in a fixed order and solves A_c e = c (:73).
 // ZMODE 0: z_pre = 0 (nu1 = 0), 1: z_pre = w D^-1 r implicit (nu1 = 1), 2: buffer.
-template <int PPL, int NT>
-__device__ __forceinline__ void restrict_finish(double (&acc)[2 * PPL], const SolveArgs& a);
+template <int PPL, int NT, bool RR>
+__device__ __forceinline__ void restrict_finish(double (&acc)[2 * PPL], double rr, const SolveArgs& a);
 
 template <int PPL, int ZMODE>
 __global__ void __launch_bounds__(kThreads, NLSP_MINB_P) k_restrict(SolveArgs a, const double* zpre) {
@@ -469,25 +471,30 @@ __global__ void __launch_bounds__(kThreads, NLSP_MINB_P) k_restrict(SolveArgs a,
             }
         }
     ROW_BATCH_END
-    restrict_finish<PPL, kThreads>(acc, a);
+    restrict_finish<PPL, kThreads, false>(acc, 0.0, a);
 }
 
-// Restriction epilogue shared by both restriction kernels: per-lane partials
-// -> CTA partial -> fixed-order grid sum in the last CTA -> coarse solve.
-template <int PPL, int NT>
-__device__ __forceinline__ void restrict_finish(double (&acc)[2 * PPL], const SolveArgs& a) {
+// Restriction epilogue shared by the restriction kernels: per-lane partials
+// -> CTA partial -> fixed-order grid sum in the last CTA -> coarse solve. With
+// RR the CTA also carries ||r||^2 (fused update): the last CTA writes the
+// history entry and runs the convergence test (two_level.hpp:168-176) first.
+template <int PPL, int NT, bool RR>
+__device__ __forceinline__ void restrict_finish(double (&acc)[2 * PPL], double rr, const SolveArgs& a) {
     PcgState* st = a.st;
-    __shared__ double cs[NT / 32][2 * 8 * PPL];
-    __shared__ double red[NT];
-    __shared__ double ys[2 * 8 * PPL];
+    constexpr int CMAX = 2 * 8 * PPL + 1;
+    __shared__ double cs[NT / 32][CMAX];
+    __shared__ double red[NT + CMAX];
+    __shared__ double ys[CMAX];
     const int ld = a.k + (a.k & 1);
     const int pairs = ld >> 1;
+    const int wc = ld + (RR ? 1 : 0);  // partial columns
     // groups of a warp -> lanes 0..7, warps -> shared, CTA partial -> global
 #pragma unroll
     for (int t = 0; t < 2 * PPL; ++t) {
         acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], 8);
         acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], 16);
     }
+    if (RR) rr = warp_sum(rr);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if (lane < kGroup) {
 #pragma unroll
@@ -499,11 +506,12 @@ __device__ __forceinline__ void restrict_finish(double (&acc)[2 * PPL], const So
             }
         }
     }
+    if (RR && lane == 0) cs[warp][ld] = rr;
     __syncthreads();
-    for (int c = threadIdx.x; c < ld; c += blockDim.x) {
+    for (int c = threadIdx.x; c < wc; c += blockDim.x) {
         double t = 0.0;
         for (int w = 0; w < nw; ++w) t += cs[w][c];
-        a.partials[(long long)blockIdx.x * ld + c] = t;
+        a.partials[(long long)blockIdx.x * wc + c] = t;
     }
     __shared__ int is_last;
     __syncthreads();
@@ -516,20 +524,31 @@ __device__ __forceinline__ void restrict_finish(double (&acc)[2 * PPL], const So
     if (!is_last) return;
     __threadfence();
     // fixed-order grid sum: S slices of CTAs per column, then slices in order
-    const int S = blockDim.x / ld;  // ld <= 256 enforced on the host
-    const int c = threadIdx.x % ld, sl = threadIdx.x / ld;
-    if (sl < S) {
+    const int S = max(1, (int)blockDim.x / wc);
+    for (int idx = threadIdx.x; idx < S * wc; idx += blockDim.x) {
+        const int c = idx % wc, sl = idx / wc;
         double t = 0.0;
-        for (int b = sl; b < gridDim.x; b += S) t += __ldcg(a.partials + (long long)b * ld + c);
-        red[threadIdx.x] = t;
+        for (int b = sl; b < gridDim.x; b += S) t += __ldcg(a.partials + (long long)b * wc + c);
+        red[idx] = t;
     }
     __syncthreads();
-    if (threadIdx.x < ld) {
+    for (int c = threadIdx.x; c < wc; c += blockDim.x) {
         double t = 0.0;
-        for (int q = 0; q < S; ++q) t += red[q * ld + threadIdx.x];
-        ys[threadIdx.x] = t;
+        for (int q = 0; q < S; ++q) t += red[q * wc + c];
+        ys[c] = t;
     }
     __syncthreads();
+    if (RR && threadIdx.x == 0) {
+        const double rel = sqrt(ys[ld]) / st->bnorm;
+        st->rr = ys[ld];
+        st->last_rel = rel;
+        a.hist[st->it] = rel;
+        st->iterations = st->it + 1;
+        if (rel < st->delta) {
+            st->converged = 1;
+            st->done = 1;
+        }
+    }
     if (warp == 0) {
         coarse_solve_warp(a.L, a.k, ys, a.e);
         if (lane == 0) {
@@ -867,7 +886,195 @@ __global__ void __launch_bounds__(kTmaThreads) k_restrict_tma(SolveArgs a, const
             if (lane == 0) mbar_arrive(&empty[stg]);
         }
     }
-    restrict_finish<PPL, kTmaThreads>(acc, a);
+    restrict_finish<PPL, kTmaThreads, false>(acc, 0.0, a);
+}
+
+// ================================================ folded two-level cycle ==
+// The cycle of two_level.hpp:60-81 is linear in r. With G = I - w D^-1 A
+// (one homogeneous Jacobi sweep) and S_t(r) = sum_{i<t} G^i w D^-1 r (t sweeps
+// from zero):
+//   restriction  P^T (r - A S_nu1(r)) = (G^nu1 P)^T r = W1^T r      (A = A^T)
+//   result       z = S_{nu1+nu2}(r) + (G^nu2 P) e = S_{nu1+nu2}(r) + W2 e
+// W1, W2 are formed once at build time (nu homogeneous block sweeps of the
+// orthonormal basis). Same operator as the reference's cycle; per iteration one
+// CSR pass fewer than the literal schedule, and the restriction fuses with the
+// x/r update. Rounding differs from the literal order at the 1e-16 level.
+
+// x += alpha p, r -= alpha q, ||r||^2 (two_level.hpp:164-170) fused with
+// c = W1^T r_new; last CTA: history + convergence test, then L L^T e = c.
+// UPDATE = false: c = W1^T r only (preconditioner apply / PCG prologue).
+// CTA tiles of 64 rows: every 8-lane group first issues its two W1 rows
+// (16-B streaming loads), then threads 0..63 update x, r with coalesced loads
+// and hand r_new over through shared memory (double-buffered by tile parity).
+template <int PPL, bool UPDATE>
+__global__ void __launch_bounds__(kThreads) k_update_restrict(SolveArgs a) {
+    constexpr int TR = 64;
+    constexpr int UP = TR / (kThreads / kGroup);  // W1 rows per group: 2
+    PcgState* st = a.st;
+    if (st->done) return;
+    __shared__ double rn_s[2][TR];
+    const int ld = a.k + (a.k & 1);
+    const int pairs = ld >> 1;
+    const double alpha = UPDATE ? st->alpha : 0.0;
+    const double* p = (st->it & 1) ? a.p1 : a.p0;
+    const int grp = threadIdx.x >> 3, l = threadIdx.x & (kGroup - 1);
+    double acc[2 * PPL];
+#pragma unroll
+    for (int t = 0; t < 2 * PPL; ++t) acc[t] = 0.0;
+    double rr = 0.0;
+    const int ntiles = (a.n + TR - 1) / TR;
+    int par = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, par ^= 1) {
+        const int r0 = tile * TR, rows = min(TR, a.n - r0);
+        double2 wv[UP][PPL];
+#pragma unroll
+        for (int u = 0; u < UP; ++u) {
+            const int lr = grp + (kThreads / kGroup) * u;
+            const double* wrow = a.W1 + (long long)(r0 + lr) * ld;
+#pragma unroll
+            for (int t = 0; t < PPL; ++t) {
+                const int pi = l + kGroup * t;
+                wv[u][t] = (lr < rows && pi < pairs) ? ld_stream2(wrow + 2 * pi) : make_double2(0.0, 0.0);
+            }
+        }
+        if (threadIdx.x < TR) {
+            const int lr = threadIdx.x;
+            double rnew = 0.0;
+            if (lr < rows) {
+                const int i = r0 + lr;
+                if (UPDATE) {
+                    rnew = fma(-alpha, a.q[i], a.r[i]);
+                    a.x[i] = fma(alpha, p[i], a.x[i]);
+                    a.r[i] = rnew;
+                    rr = fma(rnew, rnew, rr);
+                } else {
+                    rnew = a.r[i];
+                }
+            }
+            rn_s[par][lr] = rnew;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < UP; ++u) {
+            const double rv = rn_s[par][grp + (kThreads / kGroup) * u];
+#pragma unroll
+            for (int t = 0; t < PPL; ++t) {
+                acc[2 * t] = fma(wv[u][t].x, rv, acc[2 * t]);
+                acc[2 * t + 1] = fma(wv[u][t].y, rv, acc[2 * t + 1]);
+            }
+        }
+    }
+    restrict_finish<PPL, kThreads, UPDATE>(acc, rr, a);
+}
+
+// The same fused update + restriction with everything staged by the producer
+// warp: per 64-row tile the W1 rows and the x, p, q, r slices (contiguous, one
+// bulk copy each). Consumers: 64 threads update x, r for the tile's rows
+// (coalesced stores, r_new to shared memory), then all 8 warps accumulate
+// c += r_new W1 with 8 lanes per row.
+template <int PPL, bool UPDATE, int S>
+__global__ void __launch_bounds__(kTmaThreads) k_update_restrict_tma(SolveArgs a) {
+    constexpr int TR = 64;
+    constexpr int UP = TR / kGroups;
+    PcgState* st = a.st;
+    if (st->done) return;
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem);
+    unsigned long long* empty = full + S;
+    double* rn_s = reinterpret_cast<double*>(smem + 64);  // [2][TR]
+    unsigned char* stages = smem + 64 + 2 * TR * 8;
+    const int ld = a.k + (a.k & 1);
+    const int pairs = ld >> 1;
+    constexpr int NV = UPDATE ? 4 : 1;  // staged vectors: r (+ x, p, q)
+    const unsigned vbytes = TR * 8;
+    const unsigned stage_bytes = NV * vbytes + round16(TR * ld * 8);
+    const double alpha = UPDATE ? st->alpha : 0.0;
+    const double* p = (st->it & 1) ? a.p1 : a.p0;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    const int ntiles = (a.n + TR - 1) / TR;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double acc[2 * PPL];
+#pragma unroll
+    for (int t = 0; t < 2 * PPL; ++t) acc[t] = 0.0;
+    double rr = 0.0;
+    if (warp == kConsumerWarps) {
+        if (lane == 0) {
+            int i = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+                const int stg = i % S;
+                if (i >= S) mbar_wait(&empty[stg], ((i / S) - 1) & 1);
+                unsigned char* base = stages + stg * stage_bytes;
+                const int r0 = tile * TR, rows = min(TR, a.n - r0);
+                const unsigned vb = round16(rows * 8);  // vectors are padded by 16 doubles
+                const unsigned wb = rows * ld * 8;
+                mbar_arrive_tx(&full[stg], NV * vb + wb);
+                bulk_g2s(base, a.r + r0, vb, &full[stg]);
+                if (UPDATE) {
+                    bulk_g2s(base + vbytes, a.x + r0, vb, &full[stg]);
+                    bulk_g2s(base + 2 * vbytes, p + r0, vb, &full[stg]);
+                    bulk_g2s(base + 3 * vbytes, a.q + r0, vb, &full[stg]);
+                }
+                bulk_g2s(base + NV * vbytes, a.W1 + (long long)r0 * ld, wb, &full[stg]);
+            }
+        }
+    } else {
+        const int grp = threadIdx.x >> 3, l = threadIdx.x & (kGroup - 1);
+        int i = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+            const int stg = i % S;
+            const unsigned char* base = stages + stg * stage_bytes;
+            const int r0 = tile * TR, rows = min(TR, a.n - r0);
+            double* rn = rn_s + (i & 1) * TR;
+            mbar_wait(&full[stg], (i / S) & 1);
+            const double* rs = reinterpret_cast<const double*>(base);
+            if (threadIdx.x < TR) {
+                const int lr = threadIdx.x;
+                double rnew = 0.0;
+                if (lr < rows) {
+                    if (UPDATE) {
+                        const double* xs = rs + TR;
+                        const double* pps = rs + 2 * TR;
+                        const double* qs = rs + 3 * TR;
+                        rnew = fma(-alpha, qs[lr], rs[lr]);
+                        a.x[r0 + lr] = fma(alpha, pps[lr], xs[lr]);
+                        a.r[r0 + lr] = rnew;
+                        rr = fma(rnew, rnew, rr);
+                    } else {
+                        rnew = rs[lr];
+                    }
+                }
+                rn[lr] = rnew;
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+            const double* ws = rs + NV * TR;
+#pragma unroll
+            for (int u = 0; u < UP; ++u) {
+                const int lrp = grp + kGroups * u;
+                if (lrp >= rows) continue;
+                const double res = rn[lrp];
+                const double* wrow = ws + lrp * ld;
+#pragma unroll
+                for (int t = 0; t < PPL; ++t) {
+                    const int pi = l + kGroup * t;
+                    if (pi < pairs) {
+                        const double2 wv = *reinterpret_cast<const double2*>(wrow + 2 * pi);
+                        acc[2 * t] = fma(wv.x, res, acc[2 * t]);
+                        acc[2 * t + 1] = fma(wv.y, res, acc[2 * t + 1]);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stg]);
+        }
+    }
+    restrict_finish<PPL, kTmaThreads, UPDATE>(acc, rr, a);
 }
 
 // ======================================================== host launchers ==
@@ -1156,6 +1363,66 @@ void launch_twolevel_apply(const LaunchCtx& c, const SolveArgs& a, unsigned long
         launch_sweep(c, a, false, cur, out, s == nu2);
         cur = out;
     }
+}
+
+// ------------------------------------------------------- folded cycle host --
+#ifndef NLSP_UR_STAGES
+#define NLSP_UR_STAGES 4
+#endif
+#ifndef NLSP_UR_TMA
+#define NLSP_UR_TMA 1
+#endif
+template <int PPL>
+static void update_restrict_ppl(const LaunchCtx& c, const SolveArgs& a, bool update) {
+    if (NLSP_UR_TMA) {
+        constexpr int S = NLSP_UR_STAGES;
+        const int ld = a.k + (a.k & 1);
+        const long long nt = (a.n + 63) / 64;
+        const size_t stage = (size_t)(update ? 4 : 1) * 64 * 8 + round16(64 * ld * 8);
+        const size_t sm = 64 + 2 * 64 * 8 + S * stage;
+        if (update) launch_tma(c, k_update_restrict_tma<PPL, true, S>, nt, sm, a);
+        else launch_tma(c, k_update_restrict_tma<PPL, false, S>, nt, sm, a);
+        return;
+    }
+    if (update) launch_rows<kUP>(c, k_update_restrict<PPL, true>, a.n, a);
+    else launch_rows<kUP>(c, k_update_restrict<PPL, false>, a.n, a);
+}
+
+// update = true: x/r update + ||r|| + convergence + c = W1^T r + coarse solve;
+// update = false: c = W1^T r + coarse solve
+void launch_update_restrict(const LaunchCtx& c, const SolveArgs& a, bool update) {
+#define CALL(P) update_restrict_ppl<P>(c, a, update)
+    NLSP_PPL_SWITCH(ppl_for(a.k), CALL)
+#undef CALL
+    count(c);
+}
+
+// The smoothing + prolongation half of the folded cycle, after the restriction
+// (e is in a.e): z = S_{nu1+nu2}(r) + W2 e, r.z -> st->rz_new.
+void launch_folded_tail(const LaunchCtx& c, const SolveArgs& a, unsigned long long nu1,
+                        unsigned long long nu2) {
+    const unsigned long long T = nu1 + nu2;
+    SolveArgs b = a;
+    b.P = a.W2;
+    if (T <= 1) {  // z = (T ? w D^-1 r : 0) + W2 e
+        launch_prolong(c, b, T == 0 ? 0 : 1, true, nullptr, a.z);
+        return;
+    }
+    // s_j = s_{j-1} + w D^-1 (r - A s_{j-1}), s_1 = w D^-1 r implicit; then
+    // z = s_T + W2 e streamed with the prolongation kernel (r.z fused)
+    double* cur = nullptr;
+    for (unsigned long long j = 2; j <= T; ++j) {
+        double* nxt = (cur == a.zt0) ? a.zt1 : a.zt0;
+        launch_sweep(c, a, cur == nullptr, cur, nxt, false);
+        cur = nxt;
+    }
+    launch_prolong(c, b, 2, true, cur, a.z);
+}
+
+void launch_folded_apply(const LaunchCtx& c, const SolveArgs& a, unsigned long long nu1,
+                         unsigned long long nu2) {
+    launch_update_restrict(c, a, false);
+    launch_folded_tail(c, a, nu1, nu2);
 }
 
 }  // namespace nlsp
