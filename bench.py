@@ -144,13 +144,27 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- byte model --
-def byte_model(n, nnz, k, nu1, nu2):
-    """Algorithmic HBM bytes per PCG iteration:
-    A streamed once per SpMV pass (first pre-sweep from 0 is free), P twice,
-    V*n fp64 vector bytes for the fused schedule."""
+def byte_model_literal(n, nnz, k, nu1, nu2):
+    """SURVEY §8d's model of the literal schedule: A streamed once per SpMV pass
+    (first pre-sweep from 0 is free), P twice, V*n fp64 vector bytes."""
     csr = 12.0 * nnz + 4.0 * (n + 1)
     v = 160 + 32 * (nu1 - 1) + 32 * (nu2 - 1)
     return (1 + nu1 + nu2) * csr + 16.0 * n * k + v * n
+
+
+def byte_model(n, nnz, k, nu1, nu2):
+    """Algorithmic HBM bytes per PCG iteration of the schedule this library runs
+    (folded cycle): spmv_p (CSR + 32n), update+restriction through
+    W1 (8nk + 48n), nu1+nu2-1 smoothing sweeps (CSR + 24n for the first, CSR + 32n
+    after), prolongation through W2 with r.z (8nk + 24n)."""
+    csr = 12.0 * nnz + 4.0 * (n + 1)
+    ld = k + (k & 1)
+    t = nu1 + nu2
+    sweeps = 0.0
+    if t >= 2:
+        sweeps = (csr + 24.0 * n) + (t - 2) * (csr + 32.0 * n)
+    pro = 8.0 * n * ld + (24.0 if t >= 1 else 16.0) * n
+    return (csr + 32.0 * n) + (8.0 * n * ld + 48.0 * n) + sweeps + pro
 
 
 def measured_peaks():
@@ -298,7 +312,11 @@ def run_ours(args, dist: Dist):
                 "traffic": traffic, "peak_source": peak_kind,
                 "bytes_per_launch": dk["bytes_per_launch"], "avg_launch_us": round(dk["avg_us"], 2),
                 "iteration": {"bytes_per_iter": bytes_iter, "achieved": round(iter_gbs, 1),
-                              "frac": round(iter_gbs / peak, 4)}}
+                              "frac": round(iter_gbs / peak, 4),
+                              "literal_schedule_bytes_per_iter": byte_model_literal(
+                                  pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2),
+                              "literal_equivalent_gbs": round(byte_model_literal(
+                                  pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2) * iters / (ms_local / 1e3) / 1e9, 1)}}
 
     # ---- CPU baseline: the reference's own pcg, 1 core, bounded sample ----
     cpu = None

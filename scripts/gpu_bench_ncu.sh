@@ -15,5 +15,7 @@ SHORT="env NLSP_LOOP=host python bench.py --config $CFG --steps 1 --warmup 3 --n
 if [ "${NCU:-1}" = "1" ]; then
   timeout 300 $SHORT > gpurun_out/short_plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches_$CFG.csv $SHORT > gpurun_out/ncu_list.log 2>&1; echo "ncu list exit=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KERNEL:-k_restrict} -s ${SKIP:-20} -c 1 -o gpurun_out/prof_${CFG}_${KERNEL:-k_restrict} -f $SHORT > gpurun_out/ncu_full.log 2>&1; echo "ncu full exit=$?"
+  for K in ${KERNELS:-k_update_restrict k_prolong}; do
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s ${SKIP:-20} -c 1 -o gpurun_out/prof_${CFG}_$K -f $SHORT > gpurun_out/ncu_full_$K.log 2>&1; echo "ncu full $K exit=$?"
+  done
 fi
