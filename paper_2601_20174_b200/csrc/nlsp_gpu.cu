@@ -1126,7 +1126,8 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
     };
     const double n = a->n, nnz = (double)a->nnz, k = m ? m->k : 0;
     const double csr = 12.0 * nnz + 4.0 * (n + 1);
-    // algorithmic bytes per launch
+    // algorithmic bytes per launch; slots by name below
+    enum { kSpmvP = 0, kUpd, kRes, kPro, kPost, kUR, kSmooth, kCtl, kSlots };
     std::vector<Acc> acc = {
         {"spmv_p", csr + 32.0 * n},                  // reads z, p; writes p, q
         {"update", (mode == 0 ? 48.0 : (mode == 1 ? 56.0 : 64.0)) * n},
@@ -1137,6 +1138,7 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
         {"smooth", csr + 32.0 * n},                  // folded: intermediate sweeps
         {"loop_ctl", 0.0},
     };
+    if ((int)acc.size() != kSlots) return -1;
     std::vector<cudaEvent_t> evs(2);
     for (auto& e : evs) cudaEventCreate(&e);
     auto timed = [&](int slot, auto&& fn) {
@@ -1152,37 +1154,37 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
     const bool folded = mode == 0 && m->folded;
     const bool simple_apply = mode == 0 && !folded && m->nu1 == 1 && m->nu2 == 1;
     for (uint64_t it = 0; it < iters; ++it) {
-        timed(0, [&] { launch_spmv_p(ctx->lc, args); });
+        timed(kSpmvP, [&] { launch_spmv_p(ctx->lc, args); });
         if (folded) {
-            timed(5, [&] { launch_update_restrict(ctx->lc, args, true); });
+            timed(kUR, [&] { launch_update_restrict(ctx->lc, args, true); });
             // launch_folded_tail, each launch timed on its own
             const unsigned long long T = m->nu1 + m->nu2;
             SolveArgs b = args;
             b.P = m->W2;
             if (T <= 1) {
-                timed(3, [&] { launch_prolong(ctx->lc, b, T == 0 ? 0 : 1, true, nullptr, ctx->z); });
+                timed(kPro, [&] { launch_prolong(ctx->lc, b, T == 0 ? 0 : 1, true, nullptr, ctx->z); });
             } else {
                 double* cur = nullptr;
                 for (unsigned long long j = 2; j <= T; ++j) {
                     double* nxt = (cur == ctx->zt0) ? ctx->zt1 : ctx->zt0;
-                    timed(6, [&] { launch_sweep(ctx->lc, args, cur == nullptr, cur, nxt, false); });
+                    timed(kSmooth, [&] { launch_sweep(ctx->lc, args, cur == nullptr, cur, nxt, false); });
                     cur = nxt;
                 }
-                timed(3, [&] { launch_prolong(ctx->lc, b, 2, true, cur, ctx->z); });
+                timed(kPro, [&] { launch_prolong(ctx->lc, b, 2, true, cur, ctx->z); });
             }
         } else {
-            timed(1, [&] { launch_update(ctx->lc, args, mode); });
+            timed(kUpd, [&] { launch_update(ctx->lc, args, mode); });
             if (mode == 0) {
                 if (simple_apply) {
-                    timed(2, [&] { launch_restrict(ctx->lc, args, 1, nullptr); });
-                    timed(3, [&] { launch_prolong(ctx->lc, args, 1, false, nullptr, ctx->zt0); });
-                    timed(4, [&] { launch_sweep(ctx->lc, args, false, ctx->zt0, ctx->z, true); });
+                    timed(kRes, [&] { launch_restrict(ctx->lc, args, 1, nullptr); });
+                    timed(kPro, [&] { launch_prolong(ctx->lc, args, 1, false, nullptr, ctx->zt0); });
+                    timed(kPost, [&] { launch_sweep(ctx->lc, args, false, ctx->zt0, ctx->z, true); });
                 } else {
-                    timed(2, [&] { launch_twolevel_apply(ctx->lc, args, m->nu1, m->nu2); });
+                    timed(kRes, [&] { launch_twolevel_apply(ctx->lc, args, m->nu1, m->nu2); });
                 }
             }
         }
-        timed(8, [&] { launch_loop_ctl(ctx->lc, ctx->st, cudaGraphConditionalHandle{}, 0); });
+        timed(kCtl, [&] { launch_loop_ctl(ctx->lc, ctx->st, cudaGraphConditionalHandle{}, 0); });
     }
     for (auto& e : evs) cudaEventDestroy(e);
     cudaStreamSynchronize(ctx->s);
