@@ -206,28 +206,37 @@ def run_ours(args, dist: Dist):
     dcsr = a.device(ctx)
     mask = pb.mask if pb.mask.any() else None
 
-    # setup: S^(0) (host, reference RNG) + upload, then device sweeps / SVD / build
+    # setup: S^(0) (host, reference RNG) + upload, then device sweeps / SVD /
+    # build. Run twice; the second run is timed (the first also pays the lazy
+    # loading of every kernel's module).
     t0 = time.perf_counter()
     s0 = problems.smoothed_s0(cfg.s0_seed, pb.n, cfg.m, mask)
-    s = nlsp.DeviceDense.upload(s0, ctx)
-    del s0
     s0_s = time.perf_counter() - t0
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
-    ctx.synchronize()
-    ev[0].record(stream)
-    nlsp.smooth_vectors(a, s, cfg.s1, cfg.omega)
-    ev[1].record(stream)
-    p, sigma, sweeps = nlsp.svd_basis(s, cfg.k, ctx)
-    ev[2].record(stream)
-    m = nlsp.TwoLevelPreconditioner(a, p, cfg.omega, cfg.nu1, cfg.nu2)
-    ev[3].record(stream)
-    ctx.synchronize()
-    setup = {"smooth_ms": ev[0].elapsed_time(ev[1]), "svd_basis_ms": ev[1].elapsed_time(ev[2]),
-             "twolevel_build_ms": ev[2].elapsed_time(ev[3]), "s0_host_gen_upload_ms": s0_s * 1e3,
-             "input_gen_s": gen_s, "eigh_sweeps": sweeps}
+
+    def setup_once():
+        t1 = time.perf_counter()
+        s = nlsp.DeviceDense.upload(s0, ctx)
+        up_s = time.perf_counter() - t1
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ctx.synchronize()
+        ev[0].record(stream)
+        nlsp.smooth_vectors(a, s, cfg.s1, cfg.omega)
+        ev[1].record(stream)
+        p, sigma, sweeps = nlsp.svd_basis(s, cfg.k, ctx)
+        ev[2].record(stream)
+        m = nlsp.TwoLevelPreconditioner(a, p, cfg.omega, cfg.nu1, cfg.nu2)
+        ev[3].record(stream)
+        ctx.synchronize()
+        return m, {"smooth_ms": ev[0].elapsed_time(ev[1]), "svd_basis_ms": ev[1].elapsed_time(ev[2]),
+                   "twolevel_build_ms": ev[2].elapsed_time(ev[3]),
+                   "s0_host_gen_ms": s0_s * 1e3, "s0_upload_ms": up_s * 1e3,
+                   "input_gen_s": gen_s, "eigh_sweeps": sweeps}
+
+    setup_once()
+    m, setup = setup_once()
     setup["total_ms"] = setup["smooth_ms"] + setup["svd_basis_ms"] + setup["twolevel_build_ms"]
-    del s
+    del s0
 
     bd = nlsp.DeviceDense.upload(pb.rhs.reshape(-1, 1), ctx)
     xd = nlsp.DeviceDense.upload(np.zeros((pb.n, 1)), ctx)

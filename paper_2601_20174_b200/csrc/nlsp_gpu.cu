@@ -1135,7 +1135,7 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
         {"prolong", 8.0 * n * k + 24.0 * n},         // literal: P, r, w; writes z2
         {"post_sweep", csr + 32.0 * n},              // z2, r, w; writes z
         {"update_restrict", 8.0 * n * k + 48.0 * n}, // folded: W1, x, p, q, r; writes x, r
-        {"smooth", csr + 32.0 * n},                  // folded: intermediate sweeps
+        {"smooth", csr + ((m && m->nu1 + m->nu2 == 2) ? 24.0 : 32.0) * n},  // folded sweeps
         {"loop_ctl", 0.0},
     };
     if ((int)acc.size() != kSlots) return -1;
