@@ -58,6 +58,7 @@ struct SolveArgs {
     int tile_nnz64;   // max nonzeros in any run of 64 / 128 consecutive rows
     int tile_nnz128;  // (stage sizes of the TMA-staged kernels)
     int tile_nnz256;
+    int max_row;      // longest CSR row
     double* x;
     double* r;
     double* q;

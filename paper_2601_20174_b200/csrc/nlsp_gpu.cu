@@ -26,15 +26,18 @@ void launch_spmv_p(const LaunchCtx&, const SolveArgs&);
 void launch_update(const LaunchCtx&, const SolveArgs&, int);
 void launch_loop_ctl(const LaunchCtx&, PcgState*, cudaGraphConditionalHandle, int);
 void launch_true_res(const LaunchCtx&, const SolveArgs&);
+void launch_spmv_args(const LaunchCtx&, const SolveArgs&, const double*, double*);
 void launch_spmv(const LaunchCtx&, int, const int*, const int*, const double*, const double*,
                  double*);
 void launch_sweep(const LaunchCtx&, const SolveArgs&, bool, const double*, double*, bool);
 void launch_restrict(const LaunchCtx&, const SolveArgs&, int, const double*);
-void launch_prolong(const LaunchCtx&, const SolveArgs&, int, bool, const double*, double*);
+void launch_prolong(const LaunchCtx&, const SolveArgs&, int, bool, const double*, double*,
+                    cudaGraphConditionalHandle, int);
 void launch_twolevel_apply(const LaunchCtx&, const SolveArgs&, unsigned long long,
                            unsigned long long);
 void launch_update_restrict(const LaunchCtx&, const SolveArgs&, bool);
-void launch_folded_tail(const LaunchCtx&, const SolveArgs&, unsigned long long, unsigned long long);
+void launch_folded_tail(const LaunchCtx&, const SolveArgs&, unsigned long long, unsigned long long,
+                        cudaGraphConditionalHandle, int);
 void launch_folded_apply(const LaunchCtx&, const SolveArgs&, unsigned long long, unsigned long long);
 int ppl_for(int k);
 // setup_kernels.cu
@@ -235,6 +238,7 @@ SolveArgs make_args(nlsp_ctx* c, const nlsp_csr* a, const nlsp_twolevel* m) {
     s.tile_nnz64 = a->tile_nnz64;
     s.tile_nnz128 = a->tile_nnz128;
     s.tile_nnz256 = a->tile_nnz256;
+    s.max_row = a->max_row;
     s.wd = m ? m->wd : nullptr;
     s.P = m ? m->basis : nullptr;
     s.L = m ? m->L : nullptr;
@@ -263,11 +267,12 @@ void enqueue_iteration(const LaunchCtx& lc, const SolveArgs& a, int mode, const 
     launch_spmv_p(lc, a);
     if (mode == 0 && m->folded) {
         launch_update_restrict(lc, a, true);  // x, r, ||r||, c = W1^T r, e
-        launch_folded_tail(lc, a, m->nu1, m->nu2);
-    } else {
-        launch_update(lc, a, mode);
-        if (mode == 0) launch_twolevel_apply(lc, a, m->nu1, m->nu2);
+        // the prolongation ends the iteration and runs the loop control too
+        launch_folded_tail(lc, a, m->nu1, m->nu2, h, use_cond ? 2 : 1);
+        return;
     }
+    launch_update(lc, a, mode);
+    if (mode == 0) launch_twolevel_apply(lc, a, m->nu1, m->nu2);
     launch_loop_ctl(lc, a.st, h, use_cond);
 }
 
@@ -609,7 +614,7 @@ nlsp_status nlsp_spmv_device(nlsp_ctx* ctx, const nlsp_csr* a, const double* x, 
     nlsp_status b = bind(ctx);
     if (b) return b;
     if (!a) return set_err(ctx, NLSP_E_VALIDATION, "spmv: null matrix");
-    if (a->n) launch_spmv(ctx->lc, a->n, a->rp, a->ci, a->v, x, y);
+    if (a->n) launch_spmv_args(ctx->lc, make_args(ctx, a, nullptr), x, y);
     CHECK_LAUNCH();
     CU(cudaStreamSynchronize(ctx->s));
     return NLSP_OK;
@@ -623,7 +628,7 @@ nlsp_status nlsp_spmv(nlsp_ctx* ctx, const nlsp_csr* a, const double* x, double*
     if (b) return b;
     const size_t bytes = (size_t)a->n * 8;
     CU(cudaMemcpyAsync(ctx->zt0, x, bytes, cudaMemcpyHostToDevice, ctx->s));
-    if (a->n) launch_spmv(ctx->lc, a->n, a->rp, a->ci, a->v, ctx->zt0, ctx->zt1);
+    if (a->n) launch_spmv_args(ctx->lc, make_args(ctx, a, nullptr), ctx->zt0, ctx->zt1);
     CHECK_LAUNCH();
     CU(cudaMemcpyAsync(y, ctx->zt1, bytes, cudaMemcpyDeviceToHost, ctx->s));
     CU(cudaStreamSynchronize(ctx->s));
@@ -1162,7 +1167,7 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
             SolveArgs b = args;
             b.P = m->W2;
             if (T <= 1) {
-                timed(kPro, [&] { launch_prolong(ctx->lc, b, T == 0 ? 0 : 1, true, nullptr, ctx->z); });
+                timed(kPro, [&] { launch_prolong(ctx->lc, b, T == 0 ? 0 : 1, true, nullptr, ctx->z, 0, 1); });
             } else {
                 double* cur = nullptr;
                 for (unsigned long long j = 2; j <= T; ++j) {
@@ -1170,21 +1175,21 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
                     timed(kSmooth, [&] { launch_sweep(ctx->lc, args, cur == nullptr, cur, nxt, false); });
                     cur = nxt;
                 }
-                timed(kPro, [&] { launch_prolong(ctx->lc, b, 2, true, cur, ctx->z); });
+                timed(kPro, [&] { launch_prolong(ctx->lc, b, 2, true, cur, ctx->z, 0, 1); });
             }
         } else {
             timed(kUpd, [&] { launch_update(ctx->lc, args, mode); });
             if (mode == 0) {
                 if (simple_apply) {
                     timed(kRes, [&] { launch_restrict(ctx->lc, args, 1, nullptr); });
-                    timed(kPro, [&] { launch_prolong(ctx->lc, args, 1, false, nullptr, ctx->zt0); });
+                    timed(kPro, [&] { launch_prolong(ctx->lc, args, 1, false, nullptr, ctx->zt0, 0, 0); });
                     timed(kPost, [&] { launch_sweep(ctx->lc, args, false, ctx->zt0, ctx->z, true); });
                 } else {
                     timed(kRes, [&] { launch_twolevel_apply(ctx->lc, args, m->nu1, m->nu2); });
                 }
             }
         }
-        timed(kCtl, [&] { launch_loop_ctl(ctx->lc, ctx->st, cudaGraphConditionalHandle{}, 0); });
+        if (!folded) timed(kCtl, [&] { launch_loop_ctl(ctx->lc, ctx->st, cudaGraphConditionalHandle{}, 0); });
     }
     for (auto& e : evs) cudaEventDestroy(e);
     cudaStreamSynchronize(ctx->s);

@@ -362,7 +362,8 @@ __global__ void __launch_bounds__(kThreads) k_update(SolveArgs a) {
 }
 
 // beta = rz' / rz, p-update bookkeeping, iteration advance, graph WHILE control
-__global__ void k_loop_ctl(PcgState* st, cudaGraphConditionalHandle h, int use_cond) {
+__device__ __forceinline__ void loop_ctl_body(PcgState* st, cudaGraphConditionalHandle h,
+                                              int use_cond) {
     st->body_runs += 1;
     if (!st->done) {
         st->beta = st->rz_new / st->rz;
@@ -372,6 +373,10 @@ __global__ void k_loop_ctl(PcgState* st, cudaGraphConditionalHandle h, int use_c
         if (st->it >= st->max_it) st->done = 1;
     }
     if (use_cond && st->done) cudaGraphSetConditional(h, 0);
+}
+
+__global__ void k_loop_ctl(PcgState* st, cudaGraphConditionalHandle h, int use_cond) {
+    loop_ctl_body(st, h, use_cond);
 }
 
 // --------------------------------------------------------------- k_sweep --
@@ -562,9 +567,15 @@ __device__ __forceinline__ void restrict_finish(double (&acc)[2 * PPL], double r
 // z = z_pre + P e (two_level.hpp:74-78); RZ: r.z when no post-sweep follows
 template <int PPL, int ZMODE, bool RZ>
 __global__ void __launch_bounds__(kThreads) k_prolong(SolveArgs a, const double* zpre,
-                                                      double* zout) {
+                                                      double* zout, cudaGraphConditionalHandle h,
+                                                      int ctl) {
+    // ctl > 0: this is the last kernel of an iteration and also does the loop
+    // control of k_loop_ctl (ctl == 2: inside the graph WHILE body)
     PcgState* st = a.st;
-    if (st->done) return;
+    if (st->done) {
+        if (ctl && blockIdx.x == 0 && threadIdx.x == 0) loop_ctl_body(st, h, ctl == 2);
+        return;
+    }
     const int ld = a.k + (a.k & 1);
     const int pairs = ld >> 1;
     double ev[2 * PPL];
@@ -617,8 +628,10 @@ __global__ void __launch_bounds__(kThreads) k_prolong(SolveArgs a, const double*
     ROW_BATCH_END
     if (RZ) {
         double tot[1];
-        if (grid_reduce<1>(s, a.partials, &st->counter[kTkProlong], tot) && threadIdx.x == 0)
+        if (grid_reduce<1>(s, a.partials, &st->counter[kTkProlong], tot) && threadIdx.x == 0) {
             st->rz_new = tot[0];
+            if (ctl) loop_ctl_body(st, h, ctl == 2);
+        }
     }
 }
 
@@ -752,11 +765,11 @@ struct OpPlain {
 // SKIP: 0 never, 1 when st->done (solve kernels), 2 when st->error (true residual)
 // G lanes per row (transposed mapping), U row steps per warp and tile:
 // TR = 8 warps * U * (32 / G) rows per staged tile.
-template <int G, int U, int S, int SKIP, class Op>
+template <int G, int U, int S, int SKIP, int CHW, class Op>
 __global__ void __launch_bounds__(kTmaThreads) k_spmv_tma(SolveArgs a, Op op) {
     constexpr int R = 32 / G;
     constexpr int TR = kConsumerWarps * U * R;
-    constexpr int CH = G == 1 ? 8 : (G == 2 ? 4 : 2);
+    constexpr int CH = CHW;  // nonzeros per lane per pass (G * CH per row)
     static_assert(TR <= 256, "stage sizes are bounded by the 64/128/256-row nnz maxima");
     PcgState* st = a.st;
     if (SKIP == 1 && st->done) return;
@@ -1206,8 +1219,14 @@ long long restrict_tiles(const SolveArgs& a) { return (a.n + kRestrictTR - 1) / 
 
 template <int SKIP, class Op>
 void launch_spmv_op(const LaunchCtx& c, const SolveArgs& a, const Op& op) {
-    launch_tma(c, k_spmv_tma<NLSP_SPMV_G, NLSP_SPMV_U, NLSP_SPMV_STAGES, SKIP, Op>, spmv_tiles(a),
-               spmv_stage_smem(a), a, op);
+    // one pass over a row covers G * CH nonzeros: size CH from the longest row
+    constexpr int G = NLSP_SPMV_G, U = NLSP_SPMV_U, S = NLSP_SPMV_STAGES;
+    const int need = (a.max_row + G - 1) / G;
+    const long long nt = spmv_tiles(a);
+    const size_t sm = spmv_stage_smem(a);
+    if (need <= 8) launch_tma(c, k_spmv_tma<G, U, S, SKIP, 8, Op>, nt, sm, a, op);
+    else if (need <= 12) launch_tma(c, k_spmv_tma<G, U, S, SKIP, 12, Op>, nt, sm, a, op);
+    else launch_tma(c, k_spmv_tma<G, U, S, SKIP, 16, Op>, nt, sm, a, op);
 }
 
 void launch_spmv_p(const LaunchCtx& c, const SolveArgs& a) {
@@ -1241,6 +1260,12 @@ void launch_spmv(const LaunchCtx& c, int n, const int* rp, const int* ci, const 
     count(c);
 }
 
+// y = A x through the TMA-staged engine (the product path of nlsp_spmv)
+void launch_spmv_args(const LaunchCtx& c, const SolveArgs& a, const double* x, double* y) {
+    launch_spmv_op<0>(c, a, OpPlain{x, y});
+    count(c);
+}
+
 template <int PPL>
 static void restrict_ppl(const LaunchCtx& c, const SolveArgs& a, int zmode, const double* zpre) {
     if (NLSP_TMA) {
@@ -1259,8 +1284,8 @@ static void restrict_ppl(const LaunchCtx& c, const SolveArgs& a, int zmode, cons
 
 template <int PPL>
 static void prolong_ppl(const LaunchCtx& c, const SolveArgs& a, int zmode, bool rz,
-                        const double* zpre, double* zout) {
-#define NLSP_PRO(Z, R) launch_rows<kUP>(c, k_prolong<PPL, Z, R>, a.n, a, zpre, zout)
+                        const double* zpre, double* zout, cudaGraphConditionalHandle h, int ctl) {
+#define NLSP_PRO(Z, R) launch_rows<kUP>(c, k_prolong<PPL, Z, R>, a.n, a, zpre, zout, h, ctl)
     if (zmode == 0) { if (rz) NLSP_PRO(0, true); else NLSP_PRO(0, false); }
     else if (zmode == 1) { if (rz) NLSP_PRO(1, true); else NLSP_PRO(1, false); }
     else { if (rz) NLSP_PRO(2, true); else NLSP_PRO(2, false); }
@@ -1295,9 +1320,10 @@ void launch_restrict(const LaunchCtx& c, const SolveArgs& a, int zmode, const do
     count(c);
 }
 
+// ctl: 0 plain, 1 / 2 also the loop control of k_loop_ctl (2: graph WHILE body)
 void launch_prolong(const LaunchCtx& c, const SolveArgs& a, int zmode, bool rz, const double* zpre,
-                    double* zout) {
-#define CALL(P) prolong_ppl<P>(c, a, zmode, rz, zpre, zout)
+                    double* zout, cudaGraphConditionalHandle h = 0, int ctl = 0) {
+#define CALL(P) prolong_ppl<P>(c, a, zmode, rz, zpre, zout, h, ctl)
     NLSP_PPL_SWITCH(ppl_for(a.k), CALL)
 #undef CALL
     count(c);
@@ -1399,13 +1425,14 @@ void launch_update_restrict(const LaunchCtx& c, const SolveArgs& a, bool update)
 
 // The smoothing + prolongation half of the folded cycle, after the restriction
 // (e is in a.e): z = S_{nu1+nu2}(r) + W2 e, r.z -> st->rz_new.
+// ctl > 0: the prolongation also runs the loop control (no k_loop_ctl launch)
 void launch_folded_tail(const LaunchCtx& c, const SolveArgs& a, unsigned long long nu1,
-                        unsigned long long nu2) {
+                        unsigned long long nu2, cudaGraphConditionalHandle h, int ctl) {
     const unsigned long long T = nu1 + nu2;
     SolveArgs b = a;
     b.P = a.W2;
     if (T <= 1) {  // z = (T ? w D^-1 r : 0) + W2 e
-        launch_prolong(c, b, T == 0 ? 0 : 1, true, nullptr, a.z);
+        launch_prolong(c, b, T == 0 ? 0 : 1, true, nullptr, a.z, h, ctl);
         return;
     }
     // s_j = s_{j-1} + w D^-1 (r - A s_{j-1}), s_1 = w D^-1 r implicit; then
@@ -1416,13 +1443,13 @@ void launch_folded_tail(const LaunchCtx& c, const SolveArgs& a, unsigned long lo
         launch_sweep(c, a, cur == nullptr, cur, nxt, false);
         cur = nxt;
     }
-    launch_prolong(c, b, 2, true, cur, a.z);
+    launch_prolong(c, b, 2, true, cur, a.z, h, ctl);
 }
 
 void launch_folded_apply(const LaunchCtx& c, const SolveArgs& a, unsigned long long nu1,
                          unsigned long long nu2) {
     launch_update_restrict(c, a, false);
-    launch_folded_tail(c, a, nu1, nu2);
+    launch_folded_tail(c, a, nu1, nu2, 0, 0);
 }
 
 }  // namespace nlsp

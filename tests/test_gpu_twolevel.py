@@ -5,6 +5,8 @@ and compares every configuration family with the reference's own outputs
 ||x - x_ref|| / ||x_ref|| <= 1e-9, P and A_c to 1e-10."""
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 
@@ -250,3 +252,39 @@ def test_odd_coarse_dimension_and_repeat_solves_are_deterministic(nlsp):
     r2 = nlsp.pcg(a, d["rhs"], m, 1e-8, 10 * a.dim())
     assert r1.report.converged and np.array_equal(r1.solution, r2.solution)
     assert np.array_equal(r1.report.residual_history, r2.report.residual_history)
+
+
+_LOOP_SCRIPT = r"""
+import sys, json, numpy as np
+sys.path.insert(0, {root!r})
+from paper_2601_20174_b200 import nlsp
+d = np.load({path!r})
+a = nlsp.SparseCsrMatrix(int(d["n"]), d["row_ptr"], d["col_idx"], d["values"])
+m = nlsp.TwoLevelPreconditioner(a, d["P"], float(d["omega"]), int(d["nu1"]), int(d["nu2"]))
+r = nlsp.pcg(a, d["rhs"], m, float(d["delta"]), 10 * a.dim())
+np.save({out!r}, r.solution)
+print(json.dumps({{"iterations": r.report.iterations, "launches": r.report.kernel_launches}}))
+"""
+
+
+@pytest.mark.parametrize("cycle", ["folded", "literal"])
+def test_graph_and_stream_loops_agree(tmp_path, cycle):
+    """The CUDA-graph WHILE loop and the stream-ordered loop (NLSP_LOOP=host, used
+    under ncu) run the same kernels: identical iterations and bitwise x, for the
+    folded and the literal cycle."""
+    import json
+    import subprocess
+    import sys
+    from conftest import GOLDEN, ROOT
+    res = {}
+    for loop in ["graph", "host"]:
+        out = str(tmp_path / f"x_{loop}.npy")
+        code = _LOOP_SCRIPT.format(root=ROOT, path=f"{GOLDEN}/scaled_C3.npz", out=out)
+        env = dict(os.environ, NLSP_LOOP=loop, NLSP_CYCLE=cycle)
+        p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                           timeout=300)
+        assert p.returncode == 0, p.stderr[-2000:]
+        res[loop] = (json.loads(p.stdout.strip().splitlines()[-1]), np.load(out))
+    assert res["graph"][0]["iterations"] == res["host"][0]["iterations"]
+    assert np.array_equal(res["graph"][1], res["host"][1])
+    assert res["graph"][0]["launches"] > 0
