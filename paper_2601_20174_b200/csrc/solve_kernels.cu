@@ -1229,8 +1229,14 @@ void launch_spmv_op(const LaunchCtx& c, const SolveArgs& a, const Op& op) {
     else launch_tma(c, k_spmv_tma<G, U, S, SKIP, 16, Op>, nt, sm, a, op);
 }
 
+// Staged tiles must fit in shared memory (227 KB per CTA); matrices with very
+// long rows (a tile's nonzeros beyond the budget) take the direct-load kernels.
+constexpr size_t kStageBudget = 200 * 1024;
+bool spmv_tma_ok(const SolveArgs& a) { return NLSP_TMA && spmv_stage_smem(a) <= kStageBudget; }
+bool restrict_tma_ok(const SolveArgs& a) { return NLSP_TMA && restrict_stage_smem(a) <= kStageBudget; }
+
 void launch_spmv_p(const LaunchCtx& c, const SolveArgs& a) {
-    if (NLSP_TMA) launch_spmv_op<1>(c, a, OpSpmvP{});
+    if (spmv_tma_ok(a)) launch_spmv_op<1>(c, a, OpSpmvP{});
     else launch_rows<kU>(c, k_spmv_p, a.n, a);
     count(c);
 }
@@ -1249,7 +1255,7 @@ void launch_loop_ctl(const LaunchCtx& c, PcgState* st, cudaGraphConditionalHandl
 }
 
 void launch_true_res(const LaunchCtx& c, const SolveArgs& a) {
-    if (NLSP_TMA) launch_spmv_op<2>(c, a, OpTrueRes{a.x, a.b});
+    if (spmv_tma_ok(a)) launch_spmv_op<2>(c, a, OpTrueRes{a.x, a.b});
     else launch_rows<kU>(c, k_true_res, a.n, a);
     count(c);
 }
@@ -1262,13 +1268,14 @@ void launch_spmv(const LaunchCtx& c, int n, const int* rp, const int* ci, const 
 
 // y = A x through the TMA-staged engine (the product path of nlsp_spmv)
 void launch_spmv_args(const LaunchCtx& c, const SolveArgs& a, const double* x, double* y) {
-    launch_spmv_op<0>(c, a, OpPlain{x, y});
+    if (spmv_tma_ok(a)) launch_spmv_op<0>(c, a, OpPlain{x, y});
+    else launch_rows<kU>(c, k_spmv, a.n, a.n, a.rp, a.ci, a.v, x, y);
     count(c);
 }
 
 template <int PPL>
 static void restrict_ppl(const LaunchCtx& c, const SolveArgs& a, int zmode, const double* zpre) {
-    if (NLSP_TMA) {
+    if (restrict_tma_ok(a)) {
         const long long nt = restrict_tiles(a);
         const size_t sm = restrict_stage_smem(a);
         constexpr int S = NLSP_RESTRICT_STAGES;
@@ -1332,7 +1339,7 @@ void launch_prolong(const LaunchCtx& c, const SolveArgs& a, int zmode, bool rz, 
 // sweep with z_in = implicit w D^-1 r (first pre-sweep) or a buffer
 void launch_sweep(const LaunchCtx& c, const SolveArgs& a, bool implicit_in, const double* zin,
                   double* zout, bool rz) {
-    if (NLSP_TMA) {
+    if (spmv_tma_ok(a)) {
         if (implicit_in) {
             const GWdr gw{a.wd, a.r};
             if (rz) launch_spmv_op<1>(c, a, OpSweep<GWdr, true>{gw, a.r, a.wd, zout});
@@ -1400,14 +1407,20 @@ void launch_twolevel_apply(const LaunchCtx& c, const SolveArgs& a, unsigned long
 #endif
 template <int PPL>
 static void update_restrict_ppl(const LaunchCtx& c, const SolveArgs& a, bool update) {
-    if (NLSP_UR_TMA) {
+    const int ld = a.k + (a.k & 1);
+    const size_t stage = (size_t)(update ? 4 : 1) * 64 * 8 + round16(64 * ld * 8);
+    const long long nt = (a.n + 63) / 64;
+    if (NLSP_UR_TMA && 64 + 2 * 64 * 8 + NLSP_UR_STAGES * stage <= kStageBudget) {
         constexpr int S = NLSP_UR_STAGES;
-        const int ld = a.k + (a.k & 1);
-        const long long nt = (a.n + 63) / 64;
-        const size_t stage = (size_t)(update ? 4 : 1) * 64 * 8 + round16(64 * ld * 8);
         const size_t sm = 64 + 2 * 64 * 8 + S * stage;
         if (update) launch_tma(c, k_update_restrict_tma<PPL, true, S>, nt, sm, a);
         else launch_tma(c, k_update_restrict_tma<PPL, false, S>, nt, sm, a);
+        return;
+    }
+    if (NLSP_UR_TMA && 64 + 2 * 64 * 8 + 2 * stage <= kStageBudget) {  // large k: 2 stages
+        const size_t sm = 64 + 2 * 64 * 8 + 2 * stage;
+        if (update) launch_tma(c, k_update_restrict_tma<PPL, true, 2>, nt, sm, a);
+        else launch_tma(c, k_update_restrict_tma<PPL, false, 2>, nt, sm, a);
         return;
     }
     if (update) launch_rows<kUP>(c, k_update_restrict<PPL, true>, a.n, a);

@@ -288,3 +288,54 @@ def test_graph_and_stream_loops_agree(tmp_path, cycle):
     assert res["graph"][0]["iterations"] == res["host"][0]["iterations"]
     assert np.array_equal(res["graph"][1], res["host"][1])
     assert res["graph"][0]["launches"] > 0
+
+
+@pytest.mark.parametrize("k", [65, 128, 200])
+def test_large_coarse_dimension(nlsp, oracle, k):
+    """k beyond the configs' 64 (the reference has no limit): wider basis rows,
+    2-stage or direct-load fallbacks of the staged kernels."""
+    d = golden("scaled_C4")
+    a = csr_from_golden(d)
+    ao = (a.dim(), a.row_ptr(), a.col_idx(), a.values())
+    basis = np.linalg.qr(np.random.default_rng(k).standard_normal((a.dim(), k)))[0]
+    m = nlsp.TwoLevelPreconditioner(a, basis, 2 / 3, 1, 1)
+    t = oracle.twolevel(ao, basis, 2 / 3, 1, 1)
+    r = np.random.default_rng(1).standard_normal(a.dim())
+    z, zo = m.apply(a, r), t.apply(r)
+    assert np.linalg.norm(z - zo) <= 1e-11 * np.linalg.norm(zo)
+    res = nlsp.pcg(a, d["rhs"], m, 1e-8, 10 * a.dim())
+    ro = oracle.pcg(ao, d["rhs"], 2, t, 1e-8, 10 * a.dim())
+    assert abs(res.report.iterations - ro.iterations) <= 2
+    assert np.linalg.norm(res.solution - ro.x) <= 1e-9 * np.linalg.norm(ro.x)
+
+
+def test_long_rows_fall_back_from_staged_tiles(nlsp, oracle):
+    """An SPD matrix with a few dense rows/columns: staged tiles would exceed
+    shared memory, the direct-load kernels take over; results unchanged."""
+    rng = np.random.default_rng(21)
+    n = 3000
+    dense = np.zeros((n, n))
+    for i in range(n):
+        for dj in (-1, 1):
+            if 0 <= i + dj < n:
+                dense[i, i + dj] = -1.0
+    hub = [5, 1700]
+    for h in hub:
+        cols = rng.choice(n, size=2500, replace=False)
+        vals = 0.01 * rng.standard_normal(2500)
+        dense[h, cols] += vals
+        dense[cols, h] += vals
+    dense += np.diag(np.abs(dense).sum(axis=1) + 1.0)
+    ii, jj = np.nonzero(dense)
+    a = nlsp.SparseCsrMatrix.from_coo(n, ii, jj, dense[ii, jj])
+    ao = (n, a.row_ptr(), a.col_idx(), a.values())
+    x = rng.standard_normal(n)
+    assert np.abs(nlsp.spmv(a, x) - dense @ x).max() <= 1e-12 * np.abs(dense @ x).max()
+    basis = np.linalg.qr(rng.standard_normal((n, 6)))[0]
+    m = nlsp.TwoLevelPreconditioner(a, basis, 2 / 3, 1, 1)
+    t = oracle.twolevel(ao, basis, 2 / 3, 1, 1)
+    b = rng.standard_normal(n)
+    res = nlsp.pcg(a, b, m, 1e-10, 10 * n)
+    ro = oracle.pcg(ao, b, 2, t, 1e-10, 10 * n)
+    assert abs(res.report.iterations - ro.iterations) <= 2
+    assert np.linalg.norm(res.solution - ro.x) <= 1e-9 * np.linalg.norm(ro.x)
