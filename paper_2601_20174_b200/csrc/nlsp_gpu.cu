@@ -816,6 +816,7 @@ nlsp_status nlsp_svd_basis(nlsp_ctx* ctx, const nlsp_dense* s, uint64_t k, nlsp_
     if ((long long)m > n) return set_err(ctx, NLSP_E_VALIDATION, "svd_basis: requires rows >= cols");
     if (k > (uint64_t)m) return set_err(ctx, NLSP_E_VALIDATION, "first_cols: k exceeds column count");
     if (m > 1024) return set_err(ctx, NLSP_E_VALIDATION, "svd_basis: at most 1024 columns");
+    if (k > 256) return set_err(ctx, NLSP_E_VALIDATION, "svd_basis: at most 256 basis columns");
     if (k == 0) {
         nlsp_dense* d = nullptr;
         st = dense_alloc(ctx, n, 0, &d);

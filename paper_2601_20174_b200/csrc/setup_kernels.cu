@@ -116,8 +116,8 @@ __global__ void __launch_bounds__(256) k_block_sweep(int n, const int* __restric
 // 16 x 16 grid; thread (ti, tj) owns a TI x TJ block of C. Row tiles of X and Y
 // are staged in shared memory; each CTA writes its partial C.
 template <int TI>
-__global__ void __launch_bounds__(256) k_gram_partial(long long rows, int ca, int cb,
-                                                      const double* __restrict__ X,
+__global__ void __launch_bounds__(256) k_gram_partial(long long rows, int ca, int cb, int lda,
+                                                      int ldb, const double* __restrict__ X,
                                                       const double* __restrict__ Y,
                                                       double* __restrict__ part) {
     constexpr int RB = 16;
@@ -137,8 +137,8 @@ __global__ void __launch_bounds__(256) k_gram_partial(long long rows, int ca, in
         for (int idx = threadIdx.x; idx < RB * W; idx += blockDim.x) {
             const int rr = idx / W, cc = idx % W;
             const long long row = r0 + rr;
-            xs[idx] = (row < rows && cc < ca) ? X[row * ca + cc] : 0.0;
-            ys[idx] = (row < rows && cc < cb) ? Y[row * cb + cc] : 0.0;
+            xs[idx] = (row < rows && cc < ca) ? X[row * lda + cc] : 0.0;
+            ys[idx] = (row < rows && cc < cb) ? Y[row * ldb + cc] : 0.0;
         }
         __syncthreads();
 #pragma unroll 4
@@ -165,13 +165,14 @@ __global__ void __launch_bounds__(256) k_gram_partial(long long rows, int ca, in
         }
 }
 
-// fixed-order sum of the CTA partials
-__global__ void k_gram_reduce(int nparts, int count, const double* part, double* c) {
+// fixed-order sum of the CTA partials of a ca x cb block into C (row stride ldc)
+__global__ void k_gram_reduce(int nparts, int ca, int cb, const double* part, double* c, int ldc) {
+    const int count = ca * cb;
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < count;
          idx += gridDim.x * blockDim.x) {
         double s = 0.0;
         for (int p = 0; p < nparts; ++p) s += part[(long long)p * count + idx];
-        c[idx] = s;
+        c[(idx / cb) * ldc + idx % cb] = s;
     }
 }
 
@@ -653,30 +654,37 @@ int gram_grid(const LaunchCtx& c, long long rows) {
     return static_cast<int>(g);
 }
 
+// C (ca x cb) = X^T Y in register tiles of at most 128 x 128 columns; part must
+// hold gram_grid(rows) * min(ca,128) * min(cb,128) doubles
 void launch_gram(const LaunchCtx& c, long long rows, int ca, int cb, const double* X,
                  const double* Y, double* part, double* C) {
     const int g = gram_grid(c, rows);
-    const int w = ca > cb ? ca : cb;
-    const int ti = (w + 15) / 16;
-#define NLSP_G(T)                                                                       \
-    do {                                                                                \
-        const size_t smem = 2 * 16 * 16 * (T) * sizeof(double);                         \
-        k_gram_partial<T><<<g, 256, smem, c.s>>>(rows, ca, cb, X, Y, part);             \
+    for (int i0 = 0; i0 < ca; i0 += 128)
+        for (int j0 = 0; j0 < cb; j0 += 128) {
+            const int bi = ca - i0 < 128 ? ca - i0 : 128, bj = cb - j0 < 128 ? cb - j0 : 128;
+            const int w = bi > bj ? bi : bj;
+            const int ti = (w + 15) / 16;
+#define NLSP_G(T)                                                                              \
+    do {                                                                                       \
+        const size_t smem = 2 * 16 * 16 * (T) * sizeof(double);                                \
+        k_gram_partial<T><<<g, 256, smem, c.s>>>(rows, bi, bj, ca, cb, X + i0, Y + j0, part);  \
     } while (0)
-    switch (ti) {
-        case 1: NLSP_G(1); break;
-        case 2: NLSP_G(2); break;
-        case 3: NLSP_G(3); break;
-        case 4: NLSP_G(4); break;
-        case 5: NLSP_G(5); break;
-        case 6: NLSP_G(6); break;
-        case 7: NLSP_G(7); break;
-        default: NLSP_G(8); break;
-    }
+            switch (ti) {
+                case 1: NLSP_G(1); break;
+                case 2: NLSP_G(2); break;
+                case 3: NLSP_G(3); break;
+                case 4: NLSP_G(4); break;
+                case 5: NLSP_G(5); break;
+                case 6: NLSP_G(6); break;
+                case 7: NLSP_G(7); break;
+                default: NLSP_G(8); break;
+            }
 #undef NLSP_G
-    count(c);
-    k_gram_reduce<<<grid_for(c, (long long)ca * cb, 256), 256, 0, c.s>>>(g, ca * cb, part, C);
-    count(c);
+            count(c);
+            k_gram_reduce<<<grid_for(c, (long long)bi * bj, 256), 256, 0, c.s>>>(g, bi, bj, part,
+                                                                                  C + (long long)i0 * cb + j0, cb);
+            count(c);
+        }
 }
 
 void launch_eigh(const LaunchCtx& c, int m, const double* g, double* evals, double* evecs,

@@ -209,3 +209,17 @@ def test_svd_basis_matches_reference(nlsp, name):
     # only by the gap after column k
     sin_max = np.linalg.norm(d["P"] - pg @ (pg.T @ d["P"]), 2)
     assert sin_max <= max(1e-10, 1e-13 * lam[0] / (lam[k - 1] - lam[k]))
+
+
+@pytest.mark.parametrize("m,k", [(200, 20), (256, 130)])
+def test_svd_basis_wide_gram_blocks(nlsp, oracle, m, k):
+    """m > 128: the Gram is tiled over 128-column blocks and the eigensolver
+    works out of global scratch."""
+    rng = np.random.default_rng(m)
+    # a spread spectrum so every column is well separated
+    s = rng.standard_normal((3000, m)) * np.geomspace(1.0, 1e-2, m)
+    p, sig, sweeps = nlsp.svd_basis(s, k)
+    u, sig_o, _, _ = oracle.svd(s)
+    assert np.abs(sig - sig_o).max() <= 1e-11 * sig_o[0]
+    errs, _ = col_match(p.numpy(), u[:, :k])
+    assert errs.max() <= 1e-9
