@@ -74,6 +74,24 @@ struct SolveArgs {
     double* e;           // coarse correction, k
 };
 
+// The single-cluster solver (cluster_solve.cu): one CTA per row block.
+struct ClusterArgs {
+    int n, k, ld, rows;  // rows per CTA
+    int nu1, nu2;
+    int max_nnz;         // max nonzeros of any CTA's row block
+    const int* rp;
+    const int* ci;
+    const double* v;
+    const double* wd;
+    const double* W1;
+    const double* W2;    // may equal W1
+    const double* L;
+    const double* b;
+    double* x;           // out
+    double* hist;
+    PcgState* st;
+};
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

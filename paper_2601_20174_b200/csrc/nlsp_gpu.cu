@@ -40,6 +40,10 @@ void launch_folded_tail(const LaunchCtx&, const SolveArgs&, unsigned long long, 
                         cudaGraphConditionalHandle, int);
 void launch_folded_apply(const LaunchCtx&, const SolveArgs&, unsigned long long, unsigned long long);
 int ppl_for(int k);
+// cluster_solve.cu
+int cluster_plan(int n, int k, const int* rp_host, bool two_w, int* rows_out, int* max_nnz_out,
+                 size_t* smem_out);
+cudaError_t launch_cluster_pcg(cudaStream_t s, const ClusterArgs& a, int ncta, size_t smem);
 // setup_kernels.cu
 void launch_csr_import(const LaunchCtx&, int, long long, const unsigned long long*,
                        const unsigned long long*, const double*, int*, int*, double*, int*, int*);
@@ -80,6 +84,7 @@ struct nlsp_csr {
     int diag_ok;  // all A_ii > 0
     int max_row;
     int tile_nnz64, tile_nnz128, tile_nnz256;  // max nonzeros of any 64/128/256-row tile
+    std::vector<int> rp_host;  // row_ptr kept on the host for small systems (cluster plan)
 };
 
 struct nlsp_dense {
@@ -135,6 +140,7 @@ struct nlsp_ctx {
     cudaGraphExec_t gexec = nullptr;
     GraphKey gkey;
     bool use_graph = true;
+    bool use_cluster = true;  // single-cluster solver for small systems
     unsigned long long gk_pro = 0, gk_body = 0, gk_epi = 0;  // kernels per graph part
 };
 
@@ -354,7 +360,27 @@ nlsp_status run_pcg(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twole
     CHECK_LAUNCH();
     unsigned long long klaunch = 1;
     bool graph_ok = false;
-    if (ctx->use_graph) {
+    // small systems: the whole solve in one launch of one thread-block cluster
+    bool cluster_ok = false;
+    int c_rows = 0, c_nnz = 0, c_ncta = 0;
+    size_t c_smem = 0;
+    if (mode == 0 && m->folded && ctx->use_cluster && !a->rp_host.empty())
+        c_ncta = cluster_plan(a->n, m->k, a->rp_host.data(), m->W2 != m->W1, &c_rows, &c_nnz, &c_smem);
+    if (c_ncta) {
+        ClusterArgs ca{a->n, m->k, m->ld, c_rows, (int)m->nu1, (int)m->nu2, c_nnz, a->rp, a->ci, a->v,
+                       m->wd, m->W1, m->W2, m->L, ctx->b, ctx->x, ctx->hist, ctx->st};
+        CU(cudaEventRecord(ctx->ev0, ctx->s));
+        const cudaError_t ce = launch_cluster_pcg(ctx->s, ca, c_ncta, c_smem);
+        if (ce == cudaSuccess) {
+            cluster_ok = true;
+            klaunch += 1;
+            ctx->launches += klaunch;
+        } else {
+            cudaGetLastError();
+            ctx->use_cluster = false;  // not schedulable here: multi-kernel path
+        }
+    }
+    if (!cluster_ok && ctx->use_graph) {
         GraphKey key{a->id, m ? m->id : 0, kind, ctx->ws_gen};
         if (!ctx->gexec || !(ctx->gkey == key)) {
             if (build_graph(ctx, args, mode, m) == NLSP_OK) {
@@ -367,14 +393,14 @@ nlsp_status run_pcg(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twole
         }
     }
     // solve_ms starts after the (cached) graph build
-    CU(cudaEventRecord(ctx->ev0, ctx->s));
-    if (ctx->use_graph) {
+    if (!cluster_ok) CU(cudaEventRecord(ctx->ev0, ctx->s));
+    if (!cluster_ok && ctx->use_graph) {
         if (ctx->gexec) {
             CU(cudaGraphLaunch(ctx->gexec, ctx->s));
             graph_ok = true;
         }
     }
-    if (!graph_ok) {
+    if (!graph_ok && !cluster_ok) {
         // stream-ordered loop: chunks of iterations, converged kernels exit early
         enqueue_prologue(ctx->lc, args, mode, m, nullptr);
         CHECK_LAUNCH();
@@ -473,6 +499,8 @@ nlsp_status nlsp_ctx_create(int device, nlsp_ctx** out) {
     ctx->lc.launches = &ctx->launches;
     const char* loop = std::getenv("NLSP_LOOP");
     ctx->use_graph = !(loop && std::strcmp(loop, "host") == 0);
+    const char* clu = std::getenv("NLSP_CLUSTER");
+    ctx->use_cluster = !(clu && std::strcmp(clu, "0") == 0);
     *out = ctx;
     return NLSP_OK;
 }
@@ -576,6 +604,7 @@ nlsp_status nlsp_csr_upload(nlsp_ctx* ctx, uint64_t n, uint64_t nnz, const uint6
                                   : "csr_upload: columns must be sorted without duplicates");
     }
     a->max_row = ctx->flags_host[1];
+    if (n <= 65536) a->rp_host.assign(row_ptr, row_ptr + n + 1);
     // diag_ok: any A_ii <= 0 ?
     {
         int* f = ctx->flags + 2;

@@ -1,0 +1,67 @@
+"""The three execution paths of nlsp_pcg run the same arithmetic: the
+single-cluster solver (small systems, one launch), the multi-kernel CUDA-graph
+WHILE loop, and the stream-ordered loop (NLSP_LOOP=host, used under ncu) — for
+the folded and the literal cycle. Each is checked against the reference's
+golden outputs; the paths agree with each other to rounding."""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, ROOT, golden
+
+pytestmark = pytest.mark.gpu
+
+SCRIPT = r"""
+import sys, json, numpy as np
+sys.path.insert(0, {root!r})
+from paper_2601_20174_b200 import nlsp
+d = np.load({path!r})
+a = nlsp.SparseCsrMatrix(int(d["n"]), d["row_ptr"], d["col_idx"], d["values"])
+m = nlsp.TwoLevelPreconditioner(a, d["P"], float(d["omega"]), int(d["nu1"]), int(d["nu2"]))
+r = nlsp.pcg(a, d["rhs"], m, float(d["delta"]), 10 * a.dim())
+r2 = nlsp.pcg(a, d["rhs"], m, float(d["delta"]), 10 * a.dim())
+np.save({out!r}, r.solution)
+print(json.dumps({{"iterations": r.report.iterations, "launches": r.report.kernel_launches,
+                   "true": r.report.true_relative_residual, "hist_len": len(r.report.residual_history),
+                   "repeat_equal": bool(np.array_equal(r.solution, r2.solution)),
+                   "last": float(r.report.residual_history[-1])}}))
+"""
+
+PATHS = {
+    "cluster": {"NLSP_CLUSTER": "1"},
+    "graph": {"NLSP_CLUSTER": "0"},
+    "host": {"NLSP_CLUSTER": "0", "NLSP_LOOP": "host"},
+    "literal": {"NLSP_CLUSTER": "0", "NLSP_CYCLE": "literal"},
+}
+
+
+def run(tmp_path, name, env_extra):
+    out = str(tmp_path / f"x_{name}.npy")
+    code = SCRIPT.format(root=ROOT, path=os.path.join(GOLDEN, name.split(":")[0] + ".npz"), out=out)
+    env = dict(os.environ, **env_extra)
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+    assert p.returncode == 0, p.stderr[-3000:]
+    return json.loads(p.stdout.strip().splitlines()[-1]), np.load(out)
+
+
+@pytest.mark.parametrize("case", ["c1_default", "scaled_C2", "scaled_C3", "scaled_C4", "scaled_C5"])
+def test_execution_paths_match_reference(tmp_path, case):
+    d = golden(case)
+    res = {p: run(tmp_path, f"{case}:{p}", env) for p, env in PATHS.items()}
+    for p, (info, x) in res.items():
+        assert abs(info["iterations"] - int(d["iterations"])) <= 2, p
+        assert info["hist_len"] == info["iterations"] and info["last"] < float(d["delta"]), p
+        assert info["true"] < 10 * float(d["delta"]), p
+        assert info["repeat_equal"], p
+        assert np.linalg.norm(x - d["x"]) <= 1e-9 * np.linalg.norm(d["x"]), p
+    # the cluster solver is one launch; the stream loop and the graph loop are
+    # bitwise the same kernels
+    assert res["cluster"][0]["launches"] == 2  # state init + the cluster kernel
+    assert res["graph"][0]["iterations"] == res["host"][0]["iterations"]
+    assert np.array_equal(res["graph"][1], res["host"][1])
