@@ -5,15 +5,23 @@
 // setting) are launch- and latency-bound on the multi-kernel path: each PCG
 // iteration is 4 dependent grid-wide kernels of a few microseconds. Here a
 // cluster of up to 16 CTAs keeps the system on chip for the entire solve:
-// CTA q owns rows [q R, q R + R) and holds their CSR slice, their rows of the
-// folded bases W1 / W2 (two_level cycle), omega D^-1, b and every
-// PCG vector in shared memory. Gathers x[col] of other CTAs' rows are
-// distributed-shared-memory (DSMEM) loads; every dot product / the restriction
-// is a cluster all-reduce (each CTA pushes its partial into every CTA's slot,
-// one cluster barrier, each CTA sums the slots in rank order — deterministic and
-// identical in every CTA); the k x k Cholesky solve runs redundantly in every
-// CTA. Arithmetic is that of the multi-kernel folded path; only reduction order
-// differs.
+// CTA q owns rows [q R, q R + R) and holds, in shared memory, their matrix rows
+// as a column-major ELL slice, their rows of the folded bases W1 / W2
+// (two_level cycle) column-major, omega D^-1, b and every PCG
+// vector. Each ELL entry stores the shared::cluster ADDRESS of its column's
+// slot (owner CTA, local row) instead of the column index, so a gather x[col]
+// of any vector is one `ld.shared::cluster` at (entry + the vector's offset) —
+// local or remote (DSMEM) alike, no division, no branch. Every dot product /
+// the restriction is a cluster all-reduce (each CTA pushes its partial into
+// every CTA's slot, one cluster barrier, each CTA sums the slots in rank order
+// — deterministic and identical in every CTA). Three cluster barriers per PCG
+// iteration for nu1 + nu2 = 2: (p.Ap), (||r||^2 with W1^T r fused), (r.z).
+//
+// Arithmetic is that of the folded multi-kernel path (same per-row summation
+// order of A x, same sweeps) except: reduction order, and the k x k coarse
+// solve, which for k <= 32 applies the explicit inverse (L L^T)^-1 (formed once
+// per solve from the Cholesky factor, column-wise triangular inversion) as one
+// k x k mat-vec instead of 2k dependent substitution steps.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -24,22 +32,23 @@ namespace cg = cooperative_groups;
 
 namespace nlsp {
 
-constexpr int kClusterThreads = 256;
+constexpr int kClusterThreads = 512;
+constexpr int kClusterWarps = kClusterThreads / 32;
 constexpr int kMaxClusterCtas = 16;
+constexpr int kInvMax = 32;  // explicit coarse inverse up to this k
 
 // shared-memory layout (identical in every CTA of the cluster)
 struct ClusterLayout {
-    unsigned rp, ci, v, wd, b, x, r, p0, p1, q, z, s0, s1, w1, w2, red, e, Lm, wpart, bytes;
-    __host__ __device__ ClusterLayout(int R, int max_nnz, int ld, int k, bool two_w, int ncta) {
+    unsigned ea, ev_, wd, b, x, r, p0, p1, q, z, s0, s1, w1, w2, red, e, tot, wsum, Lm, Li, Ai, bytes;
+    __host__ __device__ ClusterLayout(int R, int W, int ld, int k, bool two_w, int ncta) {
         unsigned o = 0;
         auto take = [&](unsigned bytes) {
             const unsigned at = o;
             o += (bytes + 15u) & ~15u;
             return at;
         };
-        rp = take((R + 1) * 4);
-        ci = take(max_nnz * 4);
-        v = take(max_nnz * 8);
+        ev_ = take(W * R * 8);  // ELL values [W][R]
+        ea = take(W * R * 4);   // ELL shared::cluster addresses [W][R]
         wd = take(R * 8);
         b = take(R * 8);
         x = take(R * 8);
@@ -50,83 +59,98 @@ struct ClusterLayout {
         z = take(R * 8);
         s0 = take(R * 8);
         s1 = take(R * 8);
-        w1 = take(R * ld * 8);
+        w1 = take(R * ld * 8);  // [ld][R]
         w2 = two_w ? take(R * ld * 8) : w1;
         red = take(2 * ncta * (ld + 4) * 8);  // double-buffered all-reduce slots
         e = take((ld + 4) * 8);
+        tot = take((ld + 4) * 8);
+        wsum = take(kClusterWarps * (ld + 4) * 8);
         Lm = take(k * k * 8);
-        wpart = take((kClusterThreads / 32) * (ld + 4) * 8);  // per-warp restriction partials
+        Li = k <= kInvMax ? take(k * k * 8) : Lm;
+        Ai = k <= kInvMax ? take(k * k * 8) : Lm;
         bytes = o;
     }
 };
 
 namespace {
 
-__device__ __forceinline__ double block_sum_t(double v, double* scratch) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    v = warp_sum(v);
-    __syncthreads();
-    if (lane == 0) scratch[warp] = v;
-    __syncthreads();
-    double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += scratch[w];
-    return t;
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ unsigned mapa_u32(unsigned a, unsigned rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+// volatile keeps these in program order relative to the cluster barriers;
+// independent loads still overlap in flight
+__device__ __forceinline__ double ld_dsm(unsigned a) {
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void st_dsm(unsigned a, double v) {
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
 }
 
-}  // namespace
-
-// y = A x for own rows, x gathered from whichever CTA owns the column; x is the
-// value array at local offset `xo` in every CTA; `fx` transforms (used for the
-// implicit first sweep s = w D^-1 r and the p = z + beta p gather).
-template <class Fx>
-__device__ __forceinline__ double cluster_row_dot(cg::cluster_group& cl, const int* rps,
-                                                  const int* cis, const double* vs, int lr, int R,
-                                                  const Fx& fx) {
+// sum_s v[s][i] * f(gather(s, i)) over the ELL row, in CSR order (padding
+// entries carry value 0 and point at a valid local slot)
+template <int NG, class F>
+__device__ __forceinline__ double ell_row(const unsigned* ea, const double* ev, int W, int R, int i,
+                                          unsigned off0, unsigned off1, const F& f) {
     double s = 0.0;
-    for (int kk = rps[lr]; kk < rps[lr + 1]; ++kk) {
-        const int col = cis[kk];
-        s = fma(vs[kk], fx(col / R, col % R), s);
+#pragma unroll 4
+    for (int t = 0; t < W; ++t) {
+        const unsigned a = ea[t * R + i];
+        const double g0 = ld_dsm(a + off0);
+        const double g1 = NG == 2 ? ld_dsm(a + off1) : 0.0;
+        s = fma(ev[t * R + i], f(g0, g1), s);
     }
     return s;
 }
 
-__global__ void __launch_bounds__(kClusterThreads) k_cluster_pcg(ClusterArgs a) {
+}  // namespace
+
+__global__ void __launch_bounds__(kClusterThreads, 1) k_cluster_pcg(ClusterArgs a) {
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ __align__(16) unsigned char sm[];
-    __shared__ double scratch[32];
+    __shared__ double wsc[kClusterWarps];
     const int ncta = (int)cl.num_blocks();
     const int q = (int)cl.block_rank();
-    const int R = a.rows, ld = a.ld, k = a.k;
+    const int R = a.rows, ld = a.ld, k = a.k, W = a.width;
     const int row0 = q * R;
     const int nr = max(0, min(R, a.n - row0));
-    const ClusterLayout Lo(R, a.max_nnz, ld, k, a.W2 != a.W1, ncta);
-    int* rps = reinterpret_cast<int*>(sm + Lo.rp);
-    int* cis = reinterpret_cast<int*>(sm + Lo.ci);
-    double* vs = reinterpret_cast<double*>(sm + Lo.v);
-    double* wd = reinterpret_cast<double*>(sm + Lo.wd);
-    double* bv = reinterpret_cast<double*>(sm + Lo.b);
-    double* xv = reinterpret_cast<double*>(sm + Lo.x);
-    double* rv = reinterpret_cast<double*>(sm + Lo.r);
-    double* pv[2] = {reinterpret_cast<double*>(sm + Lo.p0), reinterpret_cast<double*>(sm + Lo.p1)};
-    double* qv = reinterpret_cast<double*>(sm + Lo.q);
-    double* zv = reinterpret_cast<double*>(sm + Lo.z);
-    double* sv[2] = {reinterpret_cast<double*>(sm + Lo.s0), reinterpret_cast<double*>(sm + Lo.s1)};
-    double* w1 = reinterpret_cast<double*>(sm + Lo.w1);
-    double* w2 = reinterpret_cast<double*>(sm + Lo.w2);
-    double* red = reinterpret_cast<double*>(sm + Lo.red);
-    double* ev = reinterpret_cast<double*>(sm + Lo.e);
-    double* Lm = reinterpret_cast<double*>(sm + Lo.Lm);
-    double* wpart = reinterpret_cast<double*>(sm + Lo.wpart);
-    const int tid = threadIdx.x, nt = blockDim.x;
+    const ClusterLayout Lo(R, W, ld, k, a.W2 != a.W1, ncta);
+    const unsigned base = smem_u32(sm);
+    auto D = [&](unsigned off) { return reinterpret_cast<double*>(sm + off); };
+    unsigned* ea = reinterpret_cast<unsigned*>(sm + Lo.ea);
+    double* ev = D(Lo.ev_);
+    double *wd = D(Lo.wd), *bv = D(Lo.b), *xv = D(Lo.x), *rv = D(Lo.r), *qv = D(Lo.q), *zv = D(Lo.z);
+    double* pv[2] = {D(Lo.p0), D(Lo.p1)};
+    double* sv[2] = {D(Lo.s0), D(Lo.s1)};
+    double *w1 = D(Lo.w1), *w2 = D(Lo.w2), *red = D(Lo.red), *ec = D(Lo.e), *tot = D(Lo.tot);
+    double *wsum = D(Lo.wsum), *Lm = D(Lo.Lm), *Li = D(Lo.Li), *Ai = D(Lo.Ai);
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    const int nw = nt >> 5;
     PcgState* st = a.st;
 
     // ---- load the CTA's slice of the system into shared memory
-    const int base = nr ? a.rp[row0] : 0;
-    for (int i = tid; i <= nr; i += nt) rps[i] = (nr ? a.rp[row0 + i] : 0) - base;
-    const int nnz_loc = nr ? a.rp[row0 + nr] - base : 0;
-    for (int i = tid; i < nnz_loc; i += nt) {
-        cis[i] = a.ci[base + i];
-        vs[i] = a.v[base + i];
+    const unsigned pad = mapa_u32(base, (unsigned)q);  // a valid local slot
+    for (int idx = tid; idx < W * R; idx += nt) {
+        const int t = idx / R, i = idx - t * R;
+        unsigned ad = pad;
+        double v = 0.0;
+        if (i < nr) {
+            const int k0 = a.rp[row0 + i], k1 = a.rp[row0 + i + 1];
+            if (k0 + t < k1) {
+                const int col = a.ci[k0 + t];
+                const int o = col / R;
+                ad = mapa_u32(base, (unsigned)o) + (unsigned)(col - o * R) * 8u;
+                v = a.v[k0 + t];
+            }
+        }
+        ea[idx] = ad;
+        ev[idx] = v;
     }
     for (int i = tid; i < R; i += nt) {
         const bool own = i < nr;
@@ -136,90 +160,130 @@ __global__ void __launch_bounds__(kClusterThreads) k_cluster_pcg(ClusterArgs a) 
         rv[i] = bv[i];
         pv[0][i] = pv[1][i] = qv[i] = zv[i] = sv[0][i] = sv[1][i] = 0.0;
     }
-    for (int i = tid; i < nr * ld; i += nt) {
-        w1[i] = a.W1[(long long)row0 * ld + i];
-        if (a.W2 != a.W1) w2[i] = a.W2[(long long)row0 * ld + i];
+    for (int idx = tid; idx < R * ld; idx += nt) {
+        const int i = idx / ld, j = idx - i * ld;
+        const bool own = i < nr;
+        w1[j * R + i] = own ? a.W1[(long long)(row0 + i) * ld + j] : 0.0;
+        if (a.W2 != a.W1) w2[j * R + i] = own ? a.W2[(long long)(row0 + i) * ld + j] : 0.0;
     }
     for (int i = tid; i < k * k; i += nt) Lm[i] = a.L[i];
+    const bool inv = k <= kInvMax;
+    if (inv) {
+        // L^-1 column by column (forward substitution), then (L L^T)^-1 = L^-T L^-1
+        __syncthreads();
+        if (tid < k) {
+            const int j = tid;
+            for (int i = 0; i < k; ++i) {
+                if (i < j) {
+                    Li[i * k + j] = 0.0;
+                    continue;
+                }
+                double s = i == j ? 1.0 : 0.0;
+                for (int m = j; m < i; ++m) s = fma(-Lm[i * k + m], Li[m * k + j], s);
+                Li[i * k + j] = s / Lm[i * k + i];
+            }
+        }
+        __syncthreads();
+        for (int idx = tid; idx < k * k; idx += nt) {
+            const int i = idx / k, j = idx - i * k;
+            double s = 0.0;
+            for (int m = max(i, j); m < k; ++m) s = fma(Li[m * k + i], Li[m * k + j], s);
+            Ai[idx] = s;
+        }
+    }
+    const int stride = ld + 4;
     int rbuf = 0;
-    // all-reduce of `cnt` doubles from `part` (shared, this CTA's partial) into
-    // `out` (shared, every CTA): push to every CTA's slot q, one barrier, sum
-    // the slots in rank order
-    auto allreduce = [&](const double* part, int cnt, double* out) {
-        const int stride = ld + 4;
+    cl.sync();  // every CTA's slice is resident before any DSMEM access
+
+    // scalar all-reduce of a per-thread value; every thread gets the sum
+    auto reduce_scalar = [&](double v) -> double {
+        v = warp_sum(v);
+        if (lane == 0) wsc[warp] = v;
+        __syncthreads();
         double* slot0 = red + (size_t)rbuf * ncta * stride;
-        for (int idx = tid; idx < ncta * cnt; idx += nt) {
-            const int dst = idx / cnt, j = idx % cnt;
-            double* remote = cl.map_shared_rank(slot0, dst);
-            remote[q * stride + j] = part[j];
+        if (tid < ncta) {
+            double t = 0.0;
+            for (int w = 0; w < nw; ++w) t += wsc[w];
+            st_dsm(mapa_u32(smem_u32(slot0 + q * stride), (unsigned)tid), t);
         }
         cl.sync();
-        for (int j = tid; j < cnt; j += nt) {
-            double t = 0.0;
-            for (int c = 0; c < ncta; ++c) t += slot0[c * stride + j];
-            out[j] = t;
-        }
-        __syncthreads();
+        double t = 0.0;
+        for (int c = 0; c < ncta; ++c) t += slot0[c * stride];
         rbuf ^= 1;
-    };
-    __shared__ double part[264];
-    __shared__ double tot[264];
-    cl.sync();  // every CTA's slice is resident before any DSMEM gather
-
-    // remote readers
-    auto remote_val = [&](double* local_arr, int owner, int li) -> double {
-        return owner == q ? local_arr[li] : cl.map_shared_rank(local_arr, owner)[li];
-    };
-    // scalar all-reduce of a per-thread value
-    auto sum_scalar = [&](double v) -> double {
-        const double t = block_sum_t(v, scratch);
-        if (tid == 0) part[0] = t;
-        __syncthreads();
-        allreduce(part, 1, tot);
-        return tot[0];
+        return t;
     };
 
-    // restriction c = W1^T r (own rows), all-reduce, coarse solve L L^T e = c
-    auto restrict_solve = [&]() {
-        // lane j of warp w accumulates column j over rows w, w+8, ...; warps
-        // combine in a fixed order
-        const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-        for (int j = lane; j < ld; j += 32) {
-            double accj = 0.0;
-            for (int i = warp; i < nr; i += nw) accj = fma(w1[i * ld + j], rv[i], accj);
-            wpart[warp * (ld + 4) + j] = accj;
+    // ||r||^2 and c = W1^T r (own rows) in one all-reduce, then the coarse
+    // solve e = (L L^T)^-1 c into ec (two_level.hpp:98-115); returns ||r||^2
+    auto restrict_solve = [&](double rr) -> double {
+        const int cnt = ld + 1;
+        for (int j0 = 0; j0 < ld; j0 += 8) {
+            double acc[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+            for (int i = tid; i < nr; i += nt) {
+                const double ri = rv[i];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (j0 + u < ld) acc[u] = fma(w1[(j0 + u) * R + i], ri, acc[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const double t = warp_sum(acc[u]);
+                if (lane == 0 && j0 + u < ld) wsum[warp * stride + j0 + u] = t;
+            }
         }
+        rr = warp_sum(rr);
+        if (lane == 0) wsum[warp * stride + ld] = rr;
         __syncthreads();
-        for (int j = tid; j < ld; j += nt) {
+        double* slot0 = red + (size_t)rbuf * ncta * stride;
+        if (tid < cnt) {
             double t = 0.0;
-            for (int w = 0; w < nw; ++w) t += wpart[w * (ld + 4) + j];
-            part[j] = t;
+            for (int w = 0; w < nw; ++w) t += wsum[w * stride + tid];
+            const unsigned my = smem_u32(slot0 + q * stride + tid);
+            for (int dst = 0; dst < ncta; ++dst) st_dsm(mapa_u32(my, (unsigned)dst), t);
         }
+        cl.sync();
+        if (tid < cnt) {
+            double t = 0.0;
+            for (int c = 0; c < ncta; ++c) t += slot0[c * stride + tid];
+            tot[tid] = t;
+        }
+        rbuf ^= 1;
         __syncthreads();
-        allreduce(part, ld, tot);
-        // L y = c, L^T e = y (cholesky.hpp:41-57) by warp 0, column-oriented
-        if (tid < 32) {
-            for (int i = tid; i < k; i += 32) ev[i] = tot[i];
+        if (inv) {
+            if (tid < k) {
+                double s = 0.0;
+                for (int j = 0; j < k; ++j) s = fma(Ai[tid * k + j], tot[j], s);
+                ec[tid] = s;
+            }
+        } else if (tid < 32) {
+            // L y = c, L^T e = y (cholesky.hpp:41-57) by warp 0
+            for (int i = tid; i < k; i += 32) ec[i] = tot[i];
             for (int j = 0; j < k; ++j) {
                 __syncwarp();
-                const double yj = ev[j] / Lm[j * k + j];
+                const double yj = ec[j] / Lm[j * k + j];
                 __syncwarp();
-                if (tid == 0) ev[j] = yj;
-                for (int i = j + 1 + tid; i < k; i += 32) ev[i] = fma(-Lm[i * k + j], yj, ev[i]);
+                if (tid == 0) ec[j] = yj;
+                for (int i = j + 1 + tid; i < k; i += 32) ec[i] = fma(-Lm[i * k + j], yj, ec[i]);
             }
             for (int j = k - 1; j >= 0; --j) {
                 __syncwarp();
-                const double xj = ev[j] / Lm[j * k + j];
+                const double xj = ec[j] / Lm[j * k + j];
                 __syncwarp();
-                if (tid == 0) ev[j] = xj;
-                for (int i = tid; i < j; i += 32) ev[i] = fma(-Lm[j * k + i], xj, ev[i]);
+                if (tid == 0) ec[j] = xj;
+                for (int i = tid; i < j; i += 32) ec[i] = fma(-Lm[j * k + i], xj, ec[i]);
             }
-            if (tid == 0 && (k & 1)) ev[k] = 0.0;
         }
+        if (tid == 0 && (k & 1)) ec[k] = 0.0;
+        const double rr_tot = tot[ld];
         __syncthreads();
+        return rr_tot;
     };
 
-    // z = S_T(r) + W2 e (folded cycle tail); returns r.z (all-reduced)
+    // z = S_T(r) + W2 e (folded cycle tail); returns r.z (all-reduced). The
+    // sweep outputs are published by a barrier only when another sweep gathers
+    // them; z itself by the r.z all-reduce.
     auto tail = [&]() -> double {
         const int T = a.nu1 + a.nu2;
         double* cur = nullptr;  // s_1 = w D^-1 r implicit
@@ -229,45 +293,43 @@ __global__ void __launch_bounds__(kClusterThreads) k_cluster_pcg(ClusterArgs a) 
             for (int i = tid; i < nr; i += nt) {
                 double y;
                 if (cur == nullptr)
-                    y = cluster_row_dot(cl, rps, cis, vs, i, R, [&](int o, int li) {
-                        return remote_val(wd, o, li) * remote_val(rv, o, li);
-                    });
+                    y = ell_row<2>(ea, ev, W, R, i, Lo.wd, Lo.r,
+                                   [](double g0, double g1) { return g0 * g1; });
                 else
-                    y = cluster_row_dot(cl, rps, cis, vs, i, R,
-                                        [&](int o, int li) { return remote_val(cur, o, li); });
+                    y = ell_row<1>(ea, ev, W, R, i, (unsigned)((unsigned char*)cur - sm), 0u,
+                                   [](double g0, double) { return g0; });
                 const double si = cur == nullptr ? wd[i] * rv[i] : cur[i];
                 nxt[i] = fma(wd[i], rv[i] - y, si);
             }
-            cl.sync();  // the next sweep gathers this one's output
+            if (j < T) cl.sync();  // the next sweep gathers this one's output
             cur = nxt;
             cb ^= 1;
         }
         double rz = 0.0;
         for (int i = tid; i < nr; i += nt) {
             double s = 0.0;
-            for (int j = 0; j < ld; ++j) s = fma(w2[i * ld + j], ev[j], s);
+            for (int j = 0; j < ld; ++j) s = fma(w2[j * R + i], ec[j], s);
             const double zp = T == 0 ? 0.0 : (cur == nullptr ? wd[i] * rv[i] : cur[i]);
             const double zi = zp + s;
             zv[i] = zi;
             rz = fma(rv[i], zi, rz);
         }
-        return sum_scalar(rz);
+        return reduce_scalar(rz);
     };
 
-    // ---- prologue: ||b||, z = M b, rz (two_level.hpp:143-156)
+    // ---- prologue: ||b|| (fused with W1^T b), z = M b, rz (two_level.hpp:143-156)
     double bb = 0.0;
     for (int i = tid; i < nr; i += nt) bb = fma(bv[i], bv[i], bb);
-    const double bnorm = sqrt(sum_scalar(bb));
+    const double bnorm = sqrt(restrict_solve(bb));
     if (bnorm == 0.0) {
         if (q == 0 && tid == 0) {
             st->error = kErrValidation;
             st->done = 1;
         }
+        cl.sync();
         return;
     }
-    restrict_solve();
     double rz = tail();
-    cl.sync();  // z complete everywhere before p = z is gathered
     const long long max_it = st->max_it;
     const double delta = st->delta;
     double beta = 0.0;
@@ -276,26 +338,31 @@ __global__ void __launch_bounds__(kClusterThreads) k_cluster_pcg(ClusterArgs a) 
     for (; it < max_it; ++it) {
         double* pc = pv[it & 1];
         double* pp = pv[(it + 1) & 1];
-        const bool first = it == 0;
         // p = z + beta p (gathered on the fly), q = A p, p.q (:159-163)
         double pap_part = 0.0;
         for (int i = tid; i < nr; i += nt) {
-            const double y = cluster_row_dot(cl, rps, cis, vs, i, R, [&](int o, int li) {
-                const double zz = remote_val(zv, o, li);
-                return first ? zz : fma(beta, remote_val(pp, o, li), zz);
-            });
-            const double pi = first ? zv[i] : fma(beta, pp[i], zv[i]);
+            double y, pi;
+            if (it == 0) {
+                y = ell_row<1>(ea, ev, W, R, i, Lo.z, 0u, [](double g0, double) { return g0; });
+                pi = zv[i];
+            } else {
+                const unsigned opp = (unsigned)((unsigned char*)pp - sm);
+                y = ell_row<2>(ea, ev, W, R, i, Lo.z, opp,
+                               [beta](double g0, double g1) { return fma(beta, g1, g0); });
+                pi = fma(beta, pp[i], zv[i]);
+            }
             pc[i] = pi;
             qv[i] = y;
             pap_part = fma(pi, y, pap_part);
         }
-        const double pap = sum_scalar(pap_part);
+        const double pap = reduce_scalar(pap_part);
         if (pap <= 0.0) {
             err = kErrNotSpd;
             break;
         }
         const double alpha = rz / pap;
-        // x += alpha p, r -= alpha q, ||r|| (:164-176)
+        // x += alpha p, r -= alpha q, ||r|| (:164-176) fused with W1^T r and
+        // the coarse solve of the next preconditioner application
         double rr = 0.0;
         for (int i = tid; i < nr; i += nt) {
             xv[i] = fma(alpha, pc[i], xv[i]);
@@ -303,7 +370,7 @@ __global__ void __launch_bounds__(kClusterThreads) k_cluster_pcg(ClusterArgs a) 
             rv[i] = ri;
             rr = fma(ri, ri, rr);
         }
-        const double rel = sqrt(sum_scalar(rr)) / bnorm;
+        const double rel = sqrt(restrict_solve(rr)) / bnorm;
         if (q == 0 && tid == 0) a.hist[it] = rel;
         if (rel < delta) {
             converged = 1;
@@ -311,25 +378,22 @@ __global__ void __launch_bounds__(kClusterThreads) k_cluster_pcg(ClusterArgs a) 
             break;
         }
         // z = M r (folded cycle), beta = rz' / rz (:177-182)
-        restrict_solve();
         const double rz_new = tail();
         beta = rz_new / rz;
         rz = rz_new;
-        cl.sync();  // z and p complete everywhere before the next gathers
     }
     // true residual ||b - A x|| / ||b|| (:185-189)
     cl.sync();
     double tr = 0.0;
     for (int i = tid; i < nr; i += nt) {
-        const double y = cluster_row_dot(cl, rps, cis, vs, i, R,
-                                         [&](int o, int li) { return remote_val(xv, o, li); });
+        const double y = ell_row<1>(ea, ev, W, R, i, Lo.x, 0u, [](double g0, double) { return g0; });
         const double d = bv[i] - y;
         tr = fma(d, d, tr);
     }
-    const double true_res = sqrt(sum_scalar(tr)) / bnorm;
+    const double true_res = sqrt(reduce_scalar(tr)) / bnorm;
     for (int i = tid; i < nr; i += nt) a.x[row0 + i] = xv[i];
     if (q == 0 && tid == 0) {
-        st->iterations = err ? it : it;
+        st->iterations = it;
         st->converged = converged;
         st->error = err;
         st->done = 1;
@@ -341,28 +405,29 @@ __global__ void __launch_bounds__(kClusterThreads) k_cluster_pcg(ClusterArgs a) 
     cl.sync();  // no CTA exits while others may still read its shared memory
 }
 
-// Cluster size and rows per CTA for an n x n system (row_ptr on the host), or 0
-// when its slices do not fit in shared memory.
-int cluster_plan(int n, int k, const int* rp_host, bool two_w, int* rows_out, int* max_nnz_out,
-                 size_t* smem_out) {
+// Cluster size and rows per CTA for an n x n system with rows of at most
+// `width` nonzeros, or 0 when the slices do not fit in shared memory. Prefers
+// the smallest cluster whose CTAs hold at most one row per thread.
+int cluster_plan(int n, int k, int width, bool two_w, int* rows_out, size_t* smem_out) {
     const int ld = k + (k & 1);
-    if (k > 256) return 0;
-    for (int ncta = 2; ncta <= kMaxClusterCtas; ncta *= 2) {
+    if (k > 256 || n < 1) return 0;
+    int best = 0;
+    for (int ncta = 1; ncta <= kMaxClusterCtas; ncta *= 2) {
         const int R = (n + ncta - 1) / ncta;
-        int mx = 0;
-        for (int q = 0; q < ncta; ++q) {
-            const int r0 = q * R, r1 = std::min(n, r0 + R);
-            if (r0 < r1) mx = std::max(mx, rp_host[r1] - rp_host[r0]);
-        }
-        const ClusterLayout Lo(R, mx, ld, k, two_w, ncta);
-        if (Lo.bytes <= 200 * 1024) {
+        const ClusterLayout Lo(R, std::max(width, 1), ld, k, two_w, ncta);
+        if (Lo.bytes > 200 * 1024) continue;
+        if (!best) {
+            best = ncta;
             *rows_out = R;
-            *max_nnz_out = mx;
+            *smem_out = Lo.bytes;
+        }
+        if (R <= kClusterThreads) {
+            *rows_out = R;
             *smem_out = Lo.bytes;
             return ncta;
         }
     }
-    return 0;
+    return best;
 }
 
 cudaError_t launch_cluster_pcg(cudaStream_t s, const ClusterArgs& a, int ncta, size_t smem) {

@@ -78,7 +78,7 @@ struct SolveArgs {
 struct ClusterArgs {
     int n, k, ld, rows;  // rows per CTA
     int nu1, nu2;
-    int max_nnz;         // max nonzeros of any CTA's row block
+    int width;           // ELL width = longest row
     const int* rp;
     const int* ci;
     const double* v;

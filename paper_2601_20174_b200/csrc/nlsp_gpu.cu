@@ -41,7 +41,7 @@ void launch_folded_tail(const LaunchCtx&, const SolveArgs&, unsigned long long, 
 void launch_folded_apply(const LaunchCtx&, const SolveArgs&, unsigned long long, unsigned long long);
 int ppl_for(int k);
 // cluster_solve.cu
-int cluster_plan(int n, int k, const int* rp_host, bool two_w, int* rows_out, int* max_nnz_out,
+int cluster_plan(int n, int k, int width, bool two_w, int* rows_out,
                  size_t* smem_out);
 cudaError_t launch_cluster_pcg(cudaStream_t s, const ClusterArgs& a, int ncta, size_t smem);
 // setup_kernels.cu
@@ -362,12 +362,12 @@ nlsp_status run_pcg(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twole
     bool graph_ok = false;
     // small systems: the whole solve in one launch of one thread-block cluster
     bool cluster_ok = false;
-    int c_rows = 0, c_nnz = 0, c_ncta = 0;
+    int c_rows = 0, c_ncta = 0;
     size_t c_smem = 0;
     if (mode == 0 && m->folded && ctx->use_cluster && !a->rp_host.empty())
-        c_ncta = cluster_plan(a->n, m->k, a->rp_host.data(), m->W2 != m->W1, &c_rows, &c_nnz, &c_smem);
+        c_ncta = cluster_plan(a->n, m->k, a->max_row, m->W2 != m->W1, &c_rows, &c_smem);
     if (c_ncta) {
-        ClusterArgs ca{a->n, m->k, m->ld, c_rows, (int)m->nu1, (int)m->nu2, c_nnz, a->rp, a->ci, a->v,
+        ClusterArgs ca{a->n, m->k, m->ld, c_rows, (int)m->nu1, (int)m->nu2, a->max_row, a->rp, a->ci, a->v,
                        m->wd, m->W1, m->W2, m->L, ctx->b, ctx->x, ctx->hist, ctx->st};
         CU(cudaEventRecord(ctx->ev0, ctx->s));
         const cudaError_t ce = launch_cluster_pcg(ctx->s, ca, c_ncta, c_smem);
