@@ -18,10 +18,9 @@
 // iteration for nu1 + nu2 = 2: (p.Ap), (||r||^2 with W1^T r fused), (r.z).
 //
 // Arithmetic is that of the folded multi-kernel path (same per-row summation
-// order of A x, same sweeps) except: reduction order, and the k x k coarse
-// solve, which for k <= 32 applies the explicit inverse (L L^T)^-1 (formed once
-// per solve from the Cholesky factor, column-wise triangular inversion) as one
-// k x k mat-vec instead of 2k dependent substitution steps.
+// order of A x, same sweeps, the same coarse solve: A_c^-1 c as one k x k
+// mat-vec, or the triangular substitutions with NLSP_COARSE=chol); only the
+// reduction order differs.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -35,11 +34,11 @@ namespace nlsp {
 constexpr int kClusterThreads = 512;
 constexpr int kClusterWarps = kClusterThreads / 32;
 constexpr int kMaxClusterCtas = 16;
-constexpr int kInvMax = 32;  // explicit coarse inverse up to this k
+constexpr int kInvMax = 64;  // coarse inverse held in shared memory up to this k
 
 // shared-memory layout (identical in every CTA of the cluster)
 struct ClusterLayout {
-    unsigned ea, ev_, wd, b, x, r, p0, p1, q, z, s0, s1, w1, w2, red, e, tot, wsum, Lm, Li, Ai, bytes;
+    unsigned ea, ev_, wd, b, x, r, p0, p1, q, z, s0, s1, w1, w2, red, e, tot, wsum, Lm, Ai, bytes;
     __host__ __device__ ClusterLayout(int R, int W, int ld, int k, bool two_w, int ncta) {
         unsigned o = 0;
         auto take = [&](unsigned bytes) {
@@ -65,9 +64,8 @@ struct ClusterLayout {
         e = take((ld + 4) * 8);
         tot = take((ld + 4) * 8);
         wsum = take(kClusterWarps * (ld + 4) * 8);
-        Lm = take(k * k * 8);
-        Li = k <= kInvMax ? take(k * k * 8) : Lm;
-        Ai = k <= kInvMax ? take(k * k * 8) : Lm;
+        Lm = take(k * k * 8);  // L, or A_c^-1 for k <= kInvMax
+        Ai = Lm;
         bytes = o;
     }
 };
@@ -129,7 +127,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster_pcg(ClusterArgs 
     double* pv[2] = {D(Lo.p0), D(Lo.p1)};
     double* sv[2] = {D(Lo.s0), D(Lo.s1)};
     double *w1 = D(Lo.w1), *w2 = D(Lo.w2), *red = D(Lo.red), *ec = D(Lo.e), *tot = D(Lo.tot);
-    double *wsum = D(Lo.wsum), *Lm = D(Lo.Lm), *Li = D(Lo.Li), *Ai = D(Lo.Ai);
+    double *wsum = D(Lo.wsum), *Lm = D(Lo.Lm), *Ai = D(Lo.Ai);
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
     const int nw = nt >> 5;
     PcgState* st = a.st;
@@ -166,30 +164,10 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster_pcg(ClusterArgs 
         w1[j * R + i] = own ? a.W1[(long long)(row0 + i) * ld + j] : 0.0;
         if (a.W2 != a.W1) w2[j * R + i] = own ? a.W2[(long long)(row0 + i) * ld + j] : 0.0;
     }
-    for (int i = tid; i < k * k; i += nt) Lm[i] = a.L[i];
-    const bool inv = k <= kInvMax;
-    if (inv) {
-        // L^-1 column by column (forward substitution), then (L L^T)^-1 = L^-T L^-1
-        __syncthreads();
-        if (tid < k) {
-            const int j = tid;
-            for (int i = 0; i < k; ++i) {
-                if (i < j) {
-                    Li[i * k + j] = 0.0;
-                    continue;
-                }
-                double s = i == j ? 1.0 : 0.0;
-                for (int m = j; m < i; ++m) s = fma(-Lm[i * k + m], Li[m * k + j], s);
-                Li[i * k + j] = s / Lm[i * k + i];
-            }
-        }
-        __syncthreads();
-        for (int idx = tid; idx < k * k; idx += nt) {
-            const int i = idx / k, j = idx - i * k;
-            double s = 0.0;
-            for (int m = max(i, j); m < k; ++m) s = fma(Li[m * k + i], Li[m * k + j], s);
-            Ai[idx] = s;
-        }
+    const bool inv = a.Ainv != nullptr && k <= kInvMax;
+    for (int i = tid; i < k * k; i += nt) {
+        if (inv) Ai[i] = a.Ainv[i];
+        else Lm[i] = a.L[i];
     }
     const int stride = ld + 4;
     int rbuf = 0;

@@ -52,6 +52,7 @@ struct SolveArgs {
     const double* diag;  // A_ii                   (Jacobi preconditioner)
     const double* P;     // basis, n x k row-major, ld = k
     const double* L;     // Cholesky factor of A_c, k x k row-major
+    const double* Ainv;  // A_c^-1 = L^-T L^-1 (k x k), or null: triangular solves
     const double* W1;    // (I - w D^-1 A)^nu1 P, n x ld (restriction basis)
     const double* W2;    // (I - w D^-1 A)^nu2 P, n x ld (prolongation basis; may alias W1)
     int k;
@@ -86,6 +87,7 @@ struct ClusterArgs {
     const double* W1;
     const double* W2;    // may equal W1
     const double* L;
+    const double* Ainv;  // A_c^-1 or null
     const double* b;
     double* x;           // out
     double* hist;

@@ -60,6 +60,7 @@ void launch_dense_mm(const LaunchCtx&, long long, int, int, const double*, const
 void launch_colsign(const LaunchCtx&, long long, int, double*, double*, long long*, double*,
                     double*);
 void launch_chol(const LaunchCtx&, int, const double*, double*, double, int*);
+void launch_coarse_inverse(const LaunchCtx&, int, const double*, double*);
 void launch_tri_inv_t(const LaunchCtx&, int, const double*, double*);
 void launch_symmetrize(const LaunchCtx&, int, double*);
 void launch_sigma(const LaunchCtx&, int, int, const double*, const double*, double*, double*,
@@ -102,6 +103,7 @@ struct nlsp_twolevel {
     double omega;
     double* basis;   // n x ld
     double* L;       // k x k
+    double* Ainv;    // A_c^-1 = L^-T L^-1, k x k (coarse solve as one mat-vec)
     double* coarse;  // k x k
     double* wd;      // n
     double* W1;      // (I - w D^-1 A)^nu1 P, n x ld (folded cycle)
@@ -141,6 +143,7 @@ struct nlsp_ctx {
     GraphKey gkey;
     bool use_graph = true;
     bool use_cluster = true;  // single-cluster solver for small systems
+    bool coarse_inverse = true;  // coarse solve through A_c^-1 (NLSP_COARSE=chol: substitutions)
     unsigned long long gk_pro = 0, gk_body = 0, gk_epi = 0;  // kernels per graph part
 };
 
@@ -248,6 +251,7 @@ SolveArgs make_args(nlsp_ctx* c, const nlsp_csr* a, const nlsp_twolevel* m) {
     s.wd = m ? m->wd : nullptr;
     s.P = m ? m->basis : nullptr;
     s.L = m ? m->L : nullptr;
+    s.Ainv = (m && c->coarse_inverse) ? m->Ainv : nullptr;
     s.W1 = m ? m->W1 : nullptr;
     s.W2 = m ? m->W2 : nullptr;
     s.k = m ? m->k : 0;
@@ -368,7 +372,7 @@ nlsp_status run_pcg(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twole
         c_ncta = cluster_plan(a->n, m->k, a->max_row, m->W2 != m->W1, &c_rows, &c_smem);
     if (c_ncta) {
         ClusterArgs ca{a->n, m->k, m->ld, c_rows, (int)m->nu1, (int)m->nu2, a->max_row, a->rp, a->ci, a->v,
-                       m->wd, m->W1, m->W2, m->L, ctx->b, ctx->x, ctx->hist, ctx->st};
+                       m->wd, m->W1, m->W2, m->L, args.Ainv, ctx->b, ctx->x, ctx->hist, ctx->st};
         CU(cudaEventRecord(ctx->ev0, ctx->s));
         const cudaError_t ce = launch_cluster_pcg(ctx->s, ca, c_ncta, c_smem);
         if (ce == cudaSuccess) {
@@ -501,6 +505,8 @@ nlsp_status nlsp_ctx_create(int device, nlsp_ctx** out) {
     ctx->use_graph = !(loop && std::strcmp(loop, "host") == 0);
     const char* clu = std::getenv("NLSP_CLUSTER");
     ctx->use_cluster = !(clu && std::strcmp(clu, "0") == 0);
+    const char* co = std::getenv("NLSP_COARSE");
+    ctx->coarse_inverse = !(co && std::strcmp(co, "chol") == 0);
     *out = ctx;
     return NLSP_OK;
 }
@@ -963,7 +969,7 @@ nlsp_status nlsp_twolevel_build(nlsp_ctx* ctx, const nlsp_csr* a, const nlsp_den
     };
     cudaError_t e;
     if ((e = dalloc(&m->basis, (size_t)n * m->ld)) || (e = dalloc(&m->L, kk)) ||
-        (e = dalloc(&m->coarse, kk)) || (e = dalloc(&m->wd, n)) || (e = dalloc(&part, (size_t)g * kk)) ||
+        (e = dalloc(&m->Ainv, kk)) || (e = dalloc(&m->coarse, kk)) || (e = dalloc(&m->wd, n)) || (e = dalloc(&part, (size_t)g * kk)) ||
         (e = dalloc(&G, kk)) || (e = dalloc(&U, kk)) || (e = dalloc(&Q1, (size_t)n * k)) ||
         (e = dalloc(&Q, (size_t)n * k)) || (e = dalloc(&Y, (size_t)n * k)))
         return fail_cuda(e, "two-level alloc");
@@ -984,6 +990,8 @@ nlsp_status nlsp_twolevel_build(nlsp_ctx* ctx, const nlsp_csr* a, const nlsp_den
     launch_gram(ctx->lc, n, k, k, Q, Y, part, m->coarse);
     launch_symmetrize(ctx->lc, k, m->coarse);
     launch_chol(ctx->lc, k, m->coarse, m->L, 0.0, ctx->flags + 10);
+    launch_tri_inv_t(ctx->lc, k, m->L, U);
+    launch_coarse_inverse(ctx->lc, k, U, m->Ainv);
     // basis with an even leading dimension (zero pad column for odd k)
     if (!(e = cudaGetLastError()))
         e = cudaMemcpy2DAsync(m->basis, (size_t)m->ld * 8, Q, (size_t)k * 8, (size_t)k * 8, n,
@@ -1040,7 +1048,7 @@ void nlsp_twolevel_destroy(nlsp_twolevel* m) {
     if (!m) return;
     cudaSetDevice(m->device);
     if (m->W2 && m->W2 != m->W1) dfree(m->W2);
-    for (double* p : {m->basis, m->L, m->coarse, m->wd, m->W1}) dfree(p);
+    for (double* p : {m->basis, m->L, m->Ainv, m->coarse, m->wd, m->W1}) dfree(p);
     delete m;
 }
 

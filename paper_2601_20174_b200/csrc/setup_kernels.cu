@@ -563,6 +563,17 @@ __global__ void k_tri_inv_lower_t(int k, const double* __restrict__ L, double* _
     }
 }
 
+// A_c^-1 = L^-T L^-1 from U = (L^-1)^T: (A_c^-1)_ab = sum_{m >= max(a,b)} U_am U_bm
+// (the coarse solve of the two-level cycle becomes one k x k mat-vec)
+__global__ void k_coarse_inverse(int k, const double* __restrict__ U, double* __restrict__ Ainv) {
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < k * k; idx += gridDim.x * blockDim.x) {
+        const int a = idx / k, b = idx % k;
+        double s = 0.0;
+        for (int m = max(a, b); m < k; ++m) s = fma(U[a * k + m], U[b * k + m], s);
+        Ainv[idx] = s;
+    }
+}
+
 // c_ij = c_ji = (c_ij + c_ji) / 2 (two_level.hpp:46-51)
 __global__ void k_symmetrize(int k, double* C) {
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < k * k;
@@ -745,6 +756,11 @@ void launch_chol(const LaunchCtx& c, int k, const double* A, double* L, double r
 
 void launch_tri_inv_t(const LaunchCtx& c, int k, const double* L, double* U) {
     k_tri_inv_lower_t<<<(k + 127) / 128, 128, 0, c.s>>>(k, L, U);
+    count(c);
+}
+
+void launch_coarse_inverse(const LaunchCtx& c, int k, const double* U, double* Ainv) {
+    k_coarse_inverse<<<(k * k + 255) / 256, 256, 0, c.s>>>(k, U, Ainv);
     count(c);
 }
 

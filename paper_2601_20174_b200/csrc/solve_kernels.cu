@@ -431,6 +431,23 @@ __device__ void coarse_solve_warp(const double* __restrict__ L, int k, double* y
     for (int i = lane; i < k; i += 32) e[i] = ys[i];
 }
 
+// e = A_c^-1 c with the whole CTA: 4 lanes per output row, each a strided
+// quarter of the dot, combined by shuffles. The k^2 loads of A_c^-1 (L2
+// resident) are all in flight at once, where the substitutions above are 2k
+// dependent steps of L2 latency each.
+__device__ void coarse_apply_inverse(const double* __restrict__ Ainv, int k, const double* ys,
+                                     double* e) {
+    for (int i0 = 0; i0 < k; i0 += (int)(blockDim.x >> 2)) {
+        const int i = i0 + (int)(threadIdx.x >> 2), sub = threadIdx.x & 3;
+        double s = 0.0;
+        if (i < k)
+            for (int j = sub; j < k; j += 4) s = fma(__ldg(Ainv + (long long)i * k + j), ys[j], s);
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        if (i < k && sub == 0) e[i] = s;
+    }
+}
+
 // ------------------------------------------------------------ k_restrict --
 // res = r - A z_pre (two_level.hpp:63-67); c = P^T res (:69-72); the last CTA
 // sums the per-CTA c partials in a fixed order and solves A_c e = c (:73).
@@ -530,10 +547,21 @@ __device__ __forceinline__ void restrict_finish(double (&acc)[2 * PPL], double r
     __threadfence();
     // fixed-order grid sum: S slices of CTAs per column, then slices in order
     const int S = max(1, (int)blockDim.x / wc);
+    // (loads batched 8 deep so a slice costs ceil(G / 8S) L2 round trips, not
+    // G / S; the sum order is unchanged)
     for (int idx = threadIdx.x; idx < S * wc; idx += blockDim.x) {
         const int c = idx % wc, sl = idx / wc;
         double t = 0.0;
-        for (int b = sl; b < gridDim.x; b += S) t += __ldcg(a.partials + (long long)b * wc + c);
+        for (int b = sl; b < (int)gridDim.x; b += 8 * S) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int bb = b + u * S;
+                v[u] = bb < (int)gridDim.x ? __ldcg(a.partials + (long long)bb * wc + c) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) t += v[u];
+        }
         red[idx] = t;
     }
     __syncthreads();
@@ -554,7 +582,13 @@ __device__ __forceinline__ void restrict_finish(double (&acc)[2 * PPL], double r
             st->done = 1;
         }
     }
-    if (warp == 0) {
+    if (a.Ainv) {
+        coarse_apply_inverse(a.Ainv, a.k, ys, a.e);
+        if (threadIdx.x == 0) {
+            if (a.k & 1) a.e[a.k] = 0.0;  // padded column
+            st->counter[kTkRestrict] = 0u;
+        }
+    } else if (warp == 0) {
         coarse_solve_warp(a.L, a.k, ys, a.e);
         if (lane == 0) {
             if (a.k & 1) a.e[a.k] = 0.0;  // padded column

@@ -1,7 +1,8 @@
 """The three execution paths of nlsp_pcg run the same arithmetic: the
 single-cluster solver (small systems, one launch), the multi-kernel CUDA-graph
 WHILE loop, and the stream-ordered loop (NLSP_LOOP=host, used under ncu) — for
-the folded and the literal cycle. Each is checked against the reference's
+the folded and the literal cycle, with the coarse solve as the A_c^-1 mat-vec
+or as the reference's two triangular substitutions. Each is checked against the reference's
 golden outputs; the paths agree with each other to rounding."""
 from __future__ import annotations
 
@@ -38,6 +39,9 @@ PATHS = {
     "graph": {"NLSP_CLUSTER": "0"},
     "host": {"NLSP_CLUSTER": "0", "NLSP_LOOP": "host"},
     "literal": {"NLSP_CLUSTER": "0", "NLSP_CYCLE": "literal"},
+    # coarse solve by the reference's triangular substitutions instead of A_c^-1
+    "chol": {"NLSP_CLUSTER": "0", "NLSP_COARSE": "chol"},
+    "cluster_chol": {"NLSP_CLUSTER": "1", "NLSP_COARSE": "chol"},
 }
 
 
