@@ -75,6 +75,8 @@ struct SolveArgs {
     double* e;           // coarse correction, k
 };
 
+constexpr int kColsignPerSm = 8;  // CTAs per SM of the column-sign scan
+
 // The single-cluster solver (cluster_solve.cu): one CTA per row block.
 struct ClusterArgs {
     int n, k, ld, rows;  // rows per CTA

@@ -143,6 +143,7 @@ struct nlsp_ctx {
     GraphKey gkey;
     bool use_graph = true;
     bool use_cluster = true;  // single-cluster solver for small systems
+    cudaMemPool_t pool = nullptr;  // scratch of setup calls (salloc / sfree)
     bool coarse_inverse = true;  // coarse solve through A_c^-1 (NLSP_COARSE=chol: substitutions)
     unsigned long long gk_pro = 0, gk_body = 0, gk_epi = 0;  // kernels per graph part
 };
@@ -194,6 +195,20 @@ cudaError_t dalloc(T** p, size_t count) {
 
 void dfree(void* p) {
     if (p) cudaFree(p);
+}
+
+// Scratch of the setup calls comes from the context's stream-ordered pool
+// (release threshold: never), so repeated builds reuse memory instead of paying
+// cudaMalloc/cudaFree of multi-GB buffers (and their implicit device syncs).
+template <class T>
+cudaError_t salloc(nlsp_ctx* c, T** p, size_t count) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    return cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), count * sizeof(T), c->pool, c->s);
+}
+
+void sfree(nlsp_ctx* c, void* p) {
+    if (p) cudaFreeAsync(p, c->s);
 }
 
 nlsp_status bind(nlsp_ctx* ctx) {
@@ -497,6 +512,19 @@ nlsp_status nlsp_ctx_create(int device, nlsp_ctx** out) {
         nlsp_ctx_destroy(ctx);
         return NLSP_E_CUDA;
     }
+    {
+        cudaMemPoolProps pp{};
+        pp.allocType = cudaMemAllocationTypePinned;
+        pp.location.type = cudaMemLocationTypeDevice;
+        pp.location.id = device;
+        unsigned long long keep = ~0ull;
+        if (cudaMemPoolCreate(&ctx->pool, &pp) != cudaSuccess ||
+            cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &keep) != cudaSuccess) {
+            cudaGetLastError();
+            nlsp_ctx_destroy(ctx);
+            return NLSP_E_CUDA;
+        }
+    }
     cudaMemset(ctx->st, 0, sizeof(PcgState));
     ctx->lc.s = ctx->s;
     ctx->lc.num_sms = ctx->num_sms;
@@ -525,6 +553,7 @@ void nlsp_ctx_destroy(nlsp_ctx* ctx) {
         if (ev) cudaEventDestroy(ev);
     if (ctx->s_body) cudaStreamDestroy(ctx->s_body);
     if (ctx->s) cudaStreamDestroy(ctx->s);
+    if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
     delete ctx;
 }
 
@@ -561,8 +590,8 @@ nlsp_status nlsp_csr_upload(nlsp_ctx* ctx, uint64_t n, uint64_t nnz, const uint6
     a->nnz = (long long)nnz;
     unsigned long long *rp64 = nullptr, *ci64 = nullptr;
     auto fail = [&](cudaError_t e, const char* w) {
-        dfree(rp64);
-        dfree(ci64);
+        sfree(ctx, rp64);
+        sfree(ctx, ci64);
         nlsp_csr_destroy(a);
         return cuda_fail(ctx, e, w);
     };
@@ -580,7 +609,7 @@ nlsp_status nlsp_csr_upload(nlsp_ctx* ctx, uint64_t n, uint64_t nnz, const uint6
         if ((r0 & 255) == 0) a->tile_nnz256 = std::max(a->tile_nnz256, span(256));
     }
     if ((e = dalloc(&a->rp, n + 1 + 16)) || (e = dalloc(&a->ci, nnz + 16)) || (e = dalloc(&a->v, nnz + 16)) ||
-        (e = dalloc(&a->diag, n)) || (e = dalloc(&rp64, n + 1)) || (e = dalloc(&ci64, nnz)))
+        (e = dalloc(&a->diag, n)) || (e = salloc(ctx, &rp64, n + 1)) || (e = salloc(ctx, &ci64, nnz)))
         return fail(e, "csr_upload alloc");
     if ((e = cudaMemcpyAsync(rp64, row_ptr, (n + 1) * 8, cudaMemcpyHostToDevice, ctx->s)) ||
         (nnz && (e = cudaMemcpyAsync(ci64, col_idx, nnz * 8, cudaMemcpyHostToDevice, ctx->s))) ||
@@ -598,8 +627,8 @@ nlsp_status nlsp_csr_upload(nlsp_ctx* ctx, uint64_t n, uint64_t nnz, const uint6
                              ctx->s)) ||
         (e = cudaStreamSynchronize(ctx->s)))
         return fail(e, "csr_upload sync");
-    dfree(rp64);
-    dfree(ci64);
+    sfree(ctx, rp64);
+    sfree(ctx, ci64);
     rp64 = ci64 = nullptr;
     const int fl = ctx->flags_host[0];
     if (fl) {
@@ -615,14 +644,14 @@ nlsp_status nlsp_csr_upload(nlsp_ctx* ctx, uint64_t n, uint64_t nnz, const uint6
     {
         int* f = ctx->flags + 2;
         double* tmp = nullptr;
-        if ((e = dalloc(&tmp, n)) || (e = cudaMemsetAsync(f, 0, sizeof(int), ctx->s))) {
-            dfree(tmp);
+        if ((e = salloc(ctx, &tmp, n)) || (e = cudaMemsetAsync(f, 0, sizeof(int), ctx->s))) {
+            sfree(ctx, tmp);
             return fail(e, "csr_upload diag");
         }
         launch_wd(ctx->lc, (int)n, a->diag, 1.0, tmp, f);
         e = cudaMemcpyAsync(ctx->flags_host + 2, f, sizeof(int), cudaMemcpyDeviceToHost, ctx->s);
+        sfree(ctx, tmp);
         if (!e) e = cudaStreamSynchronize(ctx->s);
-        dfree(tmp);
         if (e) return fail(e, "csr_upload diag sync");
         a->diag_ok = ctx->flags_host[2] == 0;
     }
@@ -750,7 +779,7 @@ nlsp_status nlsp_jacobi_sweeps(nlsp_ctx* ctx, const nlsp_csr* a, double omega, u
     st = ensure_ws(ctx, a->n, 1);
     if (st) return st;
     double* wd = nullptr;
-    CU(dalloc(&wd, a->n));
+    CU(salloc(ctx, &wd, a->n));
     launch_wd(ctx->lc, a->n, a->diag, omega, wd, ctx->flags + 3);
     const size_t bytes = (size_t)a->n * 8;
     CU(cudaMemcpyAsync(ctx->zt0, x, bytes, cudaMemcpyHostToDevice, ctx->s));
@@ -766,9 +795,9 @@ nlsp_status nlsp_jacobi_sweeps(nlsp_ctx* ctx, const nlsp_csr* a, double omega, u
         cur = nxt;
     }
     CHECK_LAUNCH();
+    sfree(ctx, wd);
     CU(cudaMemcpyAsync(x, cur, bytes, cudaMemcpyDeviceToHost, ctx->s));
     CU(cudaStreamSynchronize(ctx->s));
-    dfree(wd);
     return NLSP_OK;
 }
 
@@ -781,10 +810,10 @@ static nlsp_status smooth_impl(nlsp_ctx* ctx, const nlsp_csr* a, nlsp_dense* s, 
         return set_err(ctx, NLSP_E_VALIDATION, "jacobi sweep: dimension mismatch");
     if (sweeps == 0 || s->cols == 0 || a->n == 0) return NLSP_OK;
     double *wd = nullptr, *tmp = nullptr;
-    CU(dalloc(&wd, a->n));
-    cudaError_t e = dalloc(&tmp, s->rows * s->cols);
+    CU(salloc(ctx, &wd, a->n));
+    cudaError_t e = salloc(ctx, &tmp, s->rows * s->cols);
     if (e) {
-        dfree(wd);
+        sfree(ctx, wd);
         return cuda_fail(ctx, e, "smooth alloc");
     }
     launch_wd(ctx->lc, a->n, a->diag, omega, wd, ctx->flags + 3);
@@ -799,9 +828,9 @@ static nlsp_status smooth_impl(nlsp_ctx* ctx, const nlsp_csr* a, nlsp_dense* s, 
     e = cudaGetLastError();
     if (!e && cur != s->d)
         e = cudaMemcpyAsync(s->d, cur, s->rows * s->cols * 8, cudaMemcpyDeviceToDevice, ctx->s);
+    sfree(ctx, wd);
+    sfree(ctx, tmp);
     if (!e) e = cudaStreamSynchronize(ctx->s);
-    dfree(wd);
-    dfree(tmp);
     if (e) return cuda_fail(ctx, e, "smooth");
     return NLSP_OK;
 }
@@ -865,16 +894,17 @@ nlsp_status nlsp_svd_basis(nlsp_ctx* ctx, const nlsp_dense* s, uint64_t k, nlsp_
     nlsp_dense* P = nullptr;
     nlsp_status ret = NLSP_OK;
     auto cleanup = [&]() {
-        for (double* p : {part, G, ev, V, sa, sv, sig, W, pmag, pval, sign}) dfree(p);
-        dfree(pidx);
+        for (double* p : {part, G, ev, V, sa, sv, sig, W, pmag, pval, sign}) sfree(ctx, p);
+        sfree(ctx, pidx);
     };
     cudaError_t e;
     const size_t mm = (size_t)m * m;
-    if ((e = dalloc(&part, (size_t)g * mm)) || (e = dalloc(&G, mm)) || (e = dalloc(&ev, m)) ||
-        (e = dalloc(&V, mm)) || (e = dalloc(&sa, mm)) || (e = dalloc(&sv, mm)) ||
-        (e = dalloc(&sig, m)) || (e = dalloc(&W, (size_t)m * k)) ||
-        (e = dalloc(&pmag, (size_t)ctx->num_sms * k)) || (e = dalloc(&pval, (size_t)ctx->num_sms * k)) ||
-        (e = dalloc(&pidx, (size_t)ctx->num_sms * k)) || (e = dalloc(&sign, k))) {
+    if ((e = salloc(ctx, &part, (size_t)g * mm)) || (e = salloc(ctx, &G, mm)) || (e = salloc(ctx, &ev, m)) ||
+        (e = salloc(ctx, &V, mm)) || (e = salloc(ctx, &sa, mm)) || (e = salloc(ctx, &sv, mm)) ||
+        (e = salloc(ctx, &sig, m)) || (e = salloc(ctx, &W, (size_t)m * k)) ||
+        (e = salloc(ctx, &pmag, (size_t)ctx->num_sms * kColsignPerSm * k)) ||
+        (e = salloc(ctx, &pval, (size_t)ctx->num_sms * kColsignPerSm * k)) ||
+        (e = salloc(ctx, &pidx, (size_t)ctx->num_sms * kColsignPerSm * k)) || (e = salloc(ctx, &sign, k))) {
         cleanup();
         return cuda_fail(ctx, e, "svd_basis alloc");
     }
@@ -960,7 +990,7 @@ nlsp_status nlsp_twolevel_build(nlsp_ctx* ctx, const nlsp_csr* a, const nlsp_den
     const int g = gram_grid(ctx->lc, n);
     double *part = nullptr, *G = nullptr, *U = nullptr, *Q1 = nullptr, *Q = nullptr, *Y = nullptr;
     auto cleanup = [&]() {
-        for (double* p : {part, G, U, Q1, Q, Y}) dfree(p);
+        for (double* p : {part, G, U, Q1, Q, Y}) sfree(ctx, p);
     };
     auto fail_cuda = [&](cudaError_t e, const char* w) {
         cleanup();
@@ -969,9 +999,10 @@ nlsp_status nlsp_twolevel_build(nlsp_ctx* ctx, const nlsp_csr* a, const nlsp_den
     };
     cudaError_t e;
     if ((e = dalloc(&m->basis, (size_t)n * m->ld)) || (e = dalloc(&m->L, kk)) ||
-        (e = dalloc(&m->Ainv, kk)) || (e = dalloc(&m->coarse, kk)) || (e = dalloc(&m->wd, n)) || (e = dalloc(&part, (size_t)g * kk)) ||
-        (e = dalloc(&G, kk)) || (e = dalloc(&U, kk)) || (e = dalloc(&Q1, (size_t)n * k)) ||
-        (e = dalloc(&Q, (size_t)n * k)) || (e = dalloc(&Y, (size_t)n * k)))
+        (e = dalloc(&m->Ainv, kk)) || (e = dalloc(&m->coarse, kk)) || (e = dalloc(&m->wd, n)) ||
+        (e = salloc(ctx, &part, (size_t)g * kk)) || (e = salloc(ctx, &G, kk)) || (e = salloc(ctx, &U, kk)) ||
+        (e = salloc(ctx, &Q1, (size_t)n * k)) || (e = salloc(ctx, &Q, (size_t)n * k)) ||
+        (e = salloc(ctx, &Y, (size_t)n * k)))
         return fail_cuda(e, "two-level alloc");
     if ((e = cudaMemsetAsync(ctx->flags, 0, 16 * sizeof(int), ctx->s))) return fail_cuda(e, "memset");
     launch_wd(ctx->lc, (int)n, a->diag, omega, m->wd, ctx->flags + 7);

@@ -8,6 +8,7 @@
 //   k_colsign_*      largest-|entry|-nonnegative column signs (svd.hpp:209-225)
 //   k_chol / k_tri_inv_lower / k_symmetrize   single-CTA k x k kernels
 #include <cfloat>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -404,48 +405,55 @@ __global__ void __launch_bounds__(256) k_dense_mm(long long rows, int m, int kou
 // per CTA: for each column, (max |x|, first row attaining it, x at that row)
 __global__ void k_colmax_partial(long long rows, int k, const double* __restrict__ P,
                                  double* pmag, long long* pidx_out, double* pval) {
+    // thread (sub, j): column j over rows blockIdx * tpc + sub, stepping by
+    // gridDim * tpc, in increasing order (first maximum kept); a CTA step reads
+    // tpc whole rows (coalesced), 4 steps' loads in flight per thread
     extern __shared__ unsigned char smraw[];
     double* bm = reinterpret_cast<double*>(smraw);
     long long* bi = reinterpret_cast<long long*>(bm + blockDim.x);
     double* bv = reinterpret_cast<double*>(bi + blockDim.x);
-    for (int j = 0; j < k; ++j) {
-        double best = -1.0, val = 0.0;
-        long long arg = -1;
-        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < rows;
-             i += (long long)gridDim.x * blockDim.x) {
-            const double x = P[i * k + j];
-            const double mag = fabs(x);
-            if (mag > best) {  // rows visited in increasing order per thread
-                best = mag;
-                arg = i;
-                val = x;
+    const int tpc = blockDim.x / k;
+    const int t = threadIdx.x, j = t % k, sub = t / k;
+    double best = -1.0, val = 0.0;
+    long long arg = -1;
+    if (sub < tpc) {
+        const long long step = (long long)gridDim.x * tpc;
+        for (long long i0 = (long long)blockIdx.x * tpc + sub; i0 < rows; i0 += 4 * step) {
+            double x[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const long long i = i0 + u * step;
+                x[u] = i < rows ? P[i * k + j] : 0.0;
             }
-        }
-        bm[threadIdx.x] = best;
-        bi[threadIdx.x] = arg;
-        bv[threadIdx.x] = val;
-        __syncthreads();
-        for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-            if (threadIdx.x < s) {
-                const double m2 = bm[threadIdx.x + s];
-                const long long i2 = bi[threadIdx.x + s];
-                const bool take = (m2 > bm[threadIdx.x]) ||
-                                  (m2 == bm[threadIdx.x] && i2 >= 0 &&
-                                   (bi[threadIdx.x] < 0 || i2 < bi[threadIdx.x]));
-                if (take) {
-                    bm[threadIdx.x] = m2;
-                    bi[threadIdx.x] = i2;
-                    bv[threadIdx.x] = bv[threadIdx.x + s];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const long long i = i0 + u * step;
+                const double mag = fabs(x[u]);
+                if (i < rows && mag > best) {
+                    best = mag;
+                    arg = i;
+                    val = x[u];
                 }
             }
-            __syncthreads();
         }
-        if (threadIdx.x == 0) {
-            pmag[(long long)blockIdx.x * k + j] = bm[0];
-            pidx_out[(long long)blockIdx.x * k + j] = bi[0];
-            pval[(long long)blockIdx.x * k + j] = bv[0];
+    }
+    bm[t] = best;
+    bi[t] = arg;
+    bv[t] = val;
+    __syncthreads();
+    if (t < k) {
+        for (int q = 1; q < tpc; ++q) {
+            const double m2 = bm[q * k + t];
+            const long long i2 = bi[q * k + t];
+            if (i2 >= 0 && (m2 > best || (m2 == best && (arg < 0 || i2 < arg)))) {
+                best = m2;
+                arg = i2;
+                val = bv[q * k + t];
+            }
         }
-        __syncthreads();
+        pmag[(long long)blockIdx.x * k + t] = best;
+        pidx_out[(long long)blockIdx.x * k + t] = arg;
+        pval[(long long)blockIdx.x * k + t] = val;
     }
 }
 
@@ -469,10 +477,12 @@ __global__ void k_colsign_final(int nparts, int k, const double* pmag, const lon
 }
 
 __global__ void k_colscale(long long rows, int k, double* P, const double* sign) {
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < rows * k;
-         idx += (long long)gridDim.x * blockDim.x) {
-        if (sign[idx % k] < 0.0) P[idx] = -P[idx];
-    }
+    // thread (sub, j) flips column j over its rows only when sign_j < 0
+    const int tpc = blockDim.x / k;
+    const int t = threadIdx.x, j = t % k, sub = t / k;
+    if (sub >= tpc || !(sign[j] < 0.0)) return;
+    const long long step = (long long)gridDim.x * tpc;
+    for (long long i = (long long)blockIdx.x * tpc + sub; i < rows; i += step) P[i * k + j] = -P[i * k + j];
 }
 
 // ------------------------------------------------------- small k x k ops --
@@ -657,6 +667,21 @@ void launch_block_op(const LaunchCtx& c, int mode, int n, const int* rp, const i
 }
 
 // C (ca x cb) = X^T Y; part must hold grid * ca * cb doubles (grid <= kMaxGrid)
+bool launch_gram_dmma(cudaStream_t s, int g, long long rows, int bi, int bj, int lda, int ldb,
+                      const double* X, const double* Y, double* part);
+bool launch_dense_mm_dmma(cudaStream_t s, int num_sms, long long rows, int m, int kout, const double* X,
+                          const double* W, const double* sigma, double* Y);
+
+// FP64 tensor-pipe (DMMA) contractions unless NLSP_DMMA=0 (then the
+// register-tiled FFMA kernels below)
+static bool use_dmma() {
+    static const bool on = [] {
+        const char* e = std::getenv("NLSP_DMMA");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 int gram_grid(const LaunchCtx& c, long long rows) {
     long long g = (rows + 15) / 16;
     const long long cap = (long long)c.num_sms * 2;
@@ -673,6 +698,14 @@ void launch_gram(const LaunchCtx& c, long long rows, int ca, int cb, const doubl
     for (int i0 = 0; i0 < ca; i0 += 128)
         for (int j0 = 0; j0 < cb; j0 += 128) {
             const int bi = ca - i0 < 128 ? ca - i0 : 128, bj = cb - j0 < 128 ? cb - j0 : 128;
+            if (use_dmma() &&
+                launch_gram_dmma(c.s, g, rows, bi, bj, ca, cb, X + i0, Y + j0, part)) {
+                count(c);
+                k_gram_reduce<<<grid_for(c, (long long)bi * bj, 256), 256, 0, c.s>>>(
+                    g, bi, bj, part, C + (long long)i0 * cb + j0, cb);
+                count(c);
+                continue;
+            }
             const int w = bi > bj ? bi : bj;
             const int ti = (w + 15) / 16;
 #define NLSP_G(T)                                                                              \
@@ -714,6 +747,10 @@ void launch_eigh(const LaunchCtx& c, int m, const double* g, double* evals, doub
 
 void launch_dense_mm(const LaunchCtx& c, long long rows, int m, int kout, const double* X,
                      const double* W, const double* sigma, double* Y) {
+    if (use_dmma() && launch_dense_mm_dmma(c.s, c.num_sms, rows, m, kout, X, W, sigma, Y)) {
+        count(c);
+        return;
+    }
     const size_t wbytes = (size_t)m * kout * sizeof(double);
     const int use_shared = wbytes <= 96 * 1024;
     const int g = grid_for(c, rows * 32, 256, 8);
@@ -738,13 +775,13 @@ void launch_dense_mm(const LaunchCtx& c, long long rows, int m, int kout, const 
 
 void launch_colsign(const LaunchCtx& c, long long rows, int k, double* P, double* pmag,
                     long long* pidx_buf, double* pval, double* sign) {
-    const int g = grid_for(c, rows, 256, 1);
+    const int g = grid_for(c, rows, 256, kColsignPerSm);  // pmag / pidx / pval: num_sms * 8 * k
     const size_t smem = 256 * (sizeof(double) * 2 + sizeof(long long));
     k_colmax_partial<<<g, 256, smem, c.s>>>(rows, k, P, pmag, pidx_buf, pval);
     count(c);
     k_colsign_final<<<1, 256, 0, c.s>>>(g, k, pmag, pidx_buf, pval, sign);
     count(c);
-    k_colscale<<<grid_for(c, rows * k, 256), 256, 0, c.s>>>(rows, k, P, sign);
+    k_colscale<<<grid_for(c, rows, 256 / k, 8), 256, 0, c.s>>>(rows, k, P, sign);
     count(c);
 }
 
