@@ -29,13 +29,14 @@ Pu64, Pdbl, Pu8, Pi32 = (C.POINTER(C.c_uint64), C.POINTER(C.c_double), C.POINTER
                          C.POINTER(C.c_int))
 
 STATUS_NAMES = {0: "ok", 1: "validation", 2: "numeric", 3: "not_spd", 4: "rank_deficient",
-                5: "convergence", 9: "other"}
+                5: "convergence", 8: "io", 9: "other"}
 
 
 class OracleError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"{STATUS_NAMES.get(code, code)}: {msg}")
         self.code = code
+        self.message = msg
         self.kind = STATUS_NAMES.get(code, str(code))
 
 
@@ -307,11 +308,20 @@ class Reference:
             "ref_csr_create": (vp, [u64, u64, Pu64, Pu64, Pdbl]),
             "ref_csr_destroy": (None, [vp]),
             "ref_csr_nnz": (u64, [vp]),
+            "ref_csr_dim": (u64, [vp]),
             "ref_csr_export": (None, [vp, Pu64, Pu64, Pdbl]),
             "ref_csr_from_triplets": (vp, [u64, u64, Pu64, Pu64, Pdbl, Pi32]),
             "ref_spmv": (C.c_int, [vp, u64, Pdbl, Pdbl]),
             "ref_fem_instance": (C.c_int, [C.c_int, u64, dbl, u64, Pu64, Pu64, Pu64, Pu64, Pdbl, Pdbl, Pu8]),
             "ref_mix_seed": (u64, [u64, u64]),
+            "ref_save_instance": (C.c_int, [C.c_int, u64, dbl, u64, C.c_char_p]),
+            "ref_load_matrix_market": (vp, [C.c_char_p, Pi32]),
+            "ref_save_matrix_market": (C.c_int, [vp, C.c_char_p]),
+            "ref_load_instance": (vp, [C.c_char_p, Pi32]),
+            "ref_instance_destroy": (None, [vp]),
+            "ref_instance_meta": (None, [vp, Pi32, Pu64, Pu64, Pdbl, Pdbl, Pu64, Pu64, Pu64]),
+            "ref_instance_matrix": (vp, [vp]),
+            "ref_instance_arrays": (None, [vp, Pdbl, Pu8, Pdbl, Pu64, Pdbl]),
             "ref_rng_normal": (None, [u64, u64, Pdbl]),
             "ref_rng_uniform": (None, [u64, u64, dbl, dbl, Pdbl]),
             "ref_rng_u64": (None, [u64, u64, Pu64]),
@@ -388,6 +398,55 @@ class Reference:
                                             C.byref(C.c_uint64()), _u(rp), _u(ci), _d(v), _d(rhs),
                                             mask.ctypes.data_as(Pu8)))
         return (int(n), rp, ci, v), rhs, mask
+
+    # --- on-disk inputs (sparse.hpp:148-194, instance_io.hpp:99-185) ---------
+    def _csr_out(self, h, dim):
+        nnz = self.lib.ref_csr_nnz(h)
+        rp, ci, v = np.empty(dim + 1, np.uint64), np.empty(nnz, np.uint64), np.empty(nnz)
+        self.lib.ref_csr_export(h, _u(rp), _u(ci), _d(v))
+        return (dim, rp, ci, v)
+
+    def save_instance(self, family, grid_n, jitter, seed, path):
+        self._chk(self.lib.ref_save_instance(family, grid_n, jitter, seed, str(path).encode()))
+
+    def load_matrix_market(self, path):
+        """(n, rp, ci, v) or OracleError(status, message)."""
+        st = C.c_int32(0)
+        h = self.lib.ref_load_matrix_market(str(path).encode(), C.byref(st))
+        self._chk(st.value)
+        try:
+            return self._csr_out(h, int(self.lib.ref_csr_dim(h)))
+        finally:
+            self.lib.ref_csr_destroy(h)
+
+    def save_matrix_market(self, a, path):
+        self._chk(self.lib.ref_save_matrix_market(self.handle(a), str(path).encode()))
+
+    def load_instance(self, path):
+        st = C.c_int32(0)
+        h = self.lib.ref_load_instance(str(path).encode(), C.byref(st))
+        self._chk(st.value)
+        try:
+            fam, gn, seed = C.c_int32(0), C.c_uint64(0), C.c_uint64(0)
+            jit, alpha = C.c_double(0), C.c_double(0)
+            n, nv, nt = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0)
+            self.lib.ref_instance_meta(h, C.byref(fam), C.byref(gn), C.byref(seed), C.byref(jit),
+                                       C.byref(alpha), C.byref(n), C.byref(nv), C.byref(nt))
+            n, nv, nt = n.value, nv.value, nt.value
+            cc = 3 if fam.value == 1 else 1
+            rhs, mask = np.empty(n), np.empty(nv, np.uint8)
+            vert, tri, coeff = np.empty((nv, 2)), np.empty((nt, 3), np.uint64), np.empty((nt, cc))
+            self.lib.ref_instance_arrays(h, _d(rhs), mask.ctypes.data_as(Pu8), _d(vert), _u(tri), _d(coeff))
+            mh = self.lib.ref_instance_matrix(h)
+            try:
+                a = self._csr_out(mh, n)
+            finally:
+                self.lib.ref_csr_destroy(mh)
+            return dict(family=fam.value, grid_n=gn.value, seed=seed.value, jitter=jit.value,
+                        alpha=alpha.value, matrix=a, rhs=rhs, mask=mask, vertices=vert, triangles=tri,
+                        coefficients=coeff)
+        finally:
+            self.lib.ref_instance_destroy(h)
 
     def from_triplets(self, n, i, j, v):
         i = np.ascontiguousarray(i, np.uint64)

@@ -45,6 +45,7 @@
 #include "nlsp/dense.hpp"
 #include "nlsp/errors.hpp"
 #include "nlsp/fem.hpp"
+#include "nlsp/instance_io.hpp"
 #include "nlsp/qr.hpp"
 #include "nlsp/rng.hpp"
 #include "nlsp/sa.hpp"
@@ -62,7 +63,7 @@ thread_local std::string g_err;
 
 // status codes shared with include/nlsp_gpu.h (nlsp_status)
 enum { ST_OK = 0, ST_VALIDATION = 1, ST_NUMERIC = 2, ST_NOT_SPD = 3, ST_RANK = 4,
-       ST_CONVERGENCE = 5, ST_OTHER = 9 };
+       ST_CONVERGENCE = 5, ST_IO = 8, ST_OTHER = 9 };
 
 template <class F>
 int guarded(F&& f) {
@@ -84,6 +85,9 @@ int guarded(F&& f) {
     } catch (const NumericError& e) {
         g_err = e.what();
         return ST_NUMERIC;
+    } catch (const IoError& e) {
+        g_err = e.what();
+        return ST_IO;
     } catch (const std::exception& e) {
         g_err = e.what();
         return ST_OTHER;
@@ -129,6 +133,8 @@ void* ref_csr_create(std::uint64_t n, std::uint64_t nnz, const std::uint64_t* rp
 void ref_csr_destroy(void* h) { delete static_cast<SparseCsrMatrix*>(h); }
 
 std::uint64_t ref_csr_nnz(void* h) { return static_cast<SparseCsrMatrix*>(h)->nnz(); }
+
+std::uint64_t ref_csr_dim(void* h) { return static_cast<SparseCsrMatrix*>(h)->dim(); }
 
 // export the (possibly re-normalised) CSR arrays
 void ref_csr_export(void* h, std::uint64_t* rp, std::uint64_t* ci, double* v) {
@@ -183,6 +189,82 @@ int ref_fem_instance(int family, std::uint64_t grid_n, double jitter, std::uint6
             mask[i] = inst.mesh.boundary_mask[i] ? 1 : 0;
         }
     });
+}
+
+// --- on-disk inputs (sparse.hpp:148-194, instance_io.hpp:99-185) ------------
+int ref_save_instance(int family, std::uint64_t grid_n, double jitter, std::uint64_t seed,
+                      const char* dir) {
+    return guarded([&] {
+        auto inst = make_instance(static_cast<PdeFamily>(family), grid_n, jitter, seed);
+        save_instance(inst, dir);
+    });
+}
+
+// load_matrix_market -> CSR handle (ref_csr_export / ref_csr_destroy), or NULL
+// with *status set
+void* ref_load_matrix_market(const char* path, int* status) {
+    SparseCsrMatrix* out = nullptr;
+    *status = guarded([&] { out = new SparseCsrMatrix(load_matrix_market(path)); });
+    return out;
+}
+
+int ref_save_matrix_market(void* h, const char* path) {
+    return guarded([&] { save_matrix_market(*static_cast<SparseCsrMatrix*>(h), path); });
+}
+
+void* ref_load_instance(const char* dir, int* status) {
+    PdeInstance* out = nullptr;
+    *status = guarded([&] { out = new PdeInstance(load_instance(dir)); });
+    return out;
+}
+
+void ref_instance_destroy(void* h) { delete static_cast<PdeInstance*>(h); }
+
+// family, grid_n, seed, jitter, alpha, n (matrix), vertices, triangles
+void ref_instance_meta(void* h, int* family, std::uint64_t* grid_n, std::uint64_t* seed, double* jitter,
+                       double* alpha, std::uint64_t* n, std::uint64_t* nv, std::uint64_t* nt) {
+    const auto& in = *static_cast<PdeInstance*>(h);
+    *family = static_cast<int>(in.family);
+    *grid_n = in.grid_n;
+    *seed = in.seed;
+    *jitter = in.jitter;
+    *alpha = in.coefficients.alpha;
+    *n = in.matrix.dim();
+    *nv = in.mesh.vertices.size();
+    *nt = in.mesh.triangles.size();
+}
+
+// a copy of the matrix as a CSR handle; rhs (n), mask (nv), vertices (nv x 2),
+// triangles (nt x 3), coefficients (nt x 1|3)
+void* ref_instance_matrix(void* h) { return new SparseCsrMatrix(static_cast<PdeInstance*>(h)->matrix); }
+
+void ref_instance_arrays(void* h, double* rhs, std::uint8_t* mask, double* vert, std::uint64_t* tri,
+                         double* coeff) {
+    const auto& in = *static_cast<PdeInstance*>(h);
+    for (std::size_t i = 0; i < in.rhs.size(); ++i) rhs[i] = in.rhs[i];
+    for (std::size_t v = 0; v < in.mesh.vertices.size(); ++v) {
+        mask[v] = in.mesh.boundary_mask[v] ? 1 : 0;
+        vert[2 * v] = in.mesh.vertices[v].x;
+        vert[2 * v + 1] = in.mesh.vertices[v].y;
+    }
+    for (std::size_t t = 0; t < in.mesh.triangles.size(); ++t)
+        for (int q = 0; q < 3; ++q) tri[3 * t + q] = in.mesh.triangles[t].v[q];
+    const auto& c = in.coefficients;
+    switch (in.family) {
+        case PdeFamily::Diffusion:
+            for (std::size_t t = 0; t < c.g.size(); ++t) coeff[t] = c.g[t];
+            break;
+        case PdeFamily::Anisotropic:
+            for (std::size_t t = 0; t < c.tensor.size(); ++t) {
+                coeff[3 * t] = c.tensor[t].k11;
+                coeff[3 * t + 1] = c.tensor[t].k12;
+                coeff[3 * t + 2] = c.tensor[t].k22;
+            }
+            break;
+        case PdeFamily::ScreenedPoisson:
+            for (std::size_t t = 0; t < c.kappa.size(); ++t) coeff[t] = c.kappa[t];
+            break;
+    }
 }
 
 // --- RNG (rng.hpp) ----------------------------------------------------------

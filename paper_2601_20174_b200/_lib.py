@@ -14,6 +14,7 @@ import threading
 HERE = os.path.dirname(os.path.abspath(__file__))
 GPU_LIB_PATH = os.environ.get("NLSP_GPU_LIB") or os.path.join(HERE, "libnlsp_gpu.so")
 INPUTS_LIB_PATH = os.path.join(HERE, "libnlsp_inputs.so")
+IO_LIB_PATH = os.path.join(HERE, "libnlsp_io.so")
 
 c_u64 = C.c_uint64
 c_i32 = C.c_int32
@@ -33,6 +34,7 @@ NLSP_E_RANK_DEFICIENT = 4
 NLSP_E_CONVERGENCE = 5
 NLSP_E_CUDA = 6
 NLSP_E_OOM = 7
+NLSP_E_IO = 8  # nlsp::IoError (include/nlsp_io.h)
 
 PRECOND_IDENTITY = 0
 PRECOND_JACOBI = 1
@@ -132,9 +134,46 @@ INPUT_SYMBOLS = [
     ("nlsp_smoothed_s0", None, [c_u64, c_u64, c_u64, P_u8, P_dbl]),
 ]
 
+
+
+class HostCsrC(C.Structure):
+    """nlsp_host_csr (include/nlsp_io.h)."""
+    _fields_ = [("n", c_u64), ("nnz", c_u64), ("row_ptr", P_u64), ("col_idx", P_u64), ("values", P_dbl)]
+
+
+class InstanceC(C.Structure):
+    """nlsp_instance (include/nlsp_io.h)."""
+    _fields_ = [
+        ("family", C.c_int),
+        ("grid_n", c_u64),
+        ("seed", c_u64),
+        ("jitter", c_dbl),
+        ("alpha", c_dbl),
+        ("matrix", HostCsrC),
+        ("rhs", P_dbl),
+        ("n_vertices", c_u64),
+        ("vertices", P_dbl),
+        ("boundary_mask", P_u8),
+        ("n_triangles", c_u64),
+        ("triangles", P_u64),
+        ("coeff_cols", c_u64),
+        ("coefficients", P_dbl),
+    ]
+
+
+IO_SYMBOLS = [
+    ("nlsp_io_load_matrix_market", C.c_int, [C.c_char_p, C.POINTER(HostCsrC)]),
+    ("nlsp_io_save_matrix_market", C.c_int, [C.POINTER(HostCsrC), C.c_char_p]),
+    ("nlsp_io_csr_free", None, [C.POINTER(HostCsrC)]),
+    ("nlsp_io_load_instance", C.c_int, [C.c_char_p, C.POINTER(InstanceC)]),
+    ("nlsp_io_instance_free", None, [C.POINTER(InstanceC)]),
+    ("nlsp_io_last_error", C.c_char_p, []),
+]
+
 _lock = threading.Lock()
 _gpu = None
 _inputs = None
+_io = None
 
 
 def _bind(lib, table):
@@ -166,6 +205,17 @@ def inputs_lib():
                 raise RuntimeError(f"{INPUTS_LIB_PATH} is missing: build it with `make -C {HERE}`")
             _inputs = _bind(C.CDLL(INPUTS_LIB_PATH), INPUT_SYMBOLS)
         return _inputs
+
+
+def io_lib():
+    """libnlsp_io.so (host C++ loaders, include/nlsp_io.h)."""
+    global _io
+    with _lock:
+        if _io is None:
+            if not os.path.exists(IO_LIB_PATH):
+                raise RuntimeError(f"{IO_LIB_PATH} is missing: build it with `make -C {HERE}`")
+            _io = _bind(C.CDLL(IO_LIB_PATH), IO_SYMBOLS)
+        return _io
 
 
 def dptr(a):

@@ -1,0 +1,126 @@
+"""bench_single's SVD rows (pipeline.hpp:303-346) on an `nlsp gen` instance
+directory — the paper's Tables 1-3 setting at N = 64 (n = 4,225) — GPU vs the
+reference's own CPU code, both timed the way the reference's StopWatch times
+them (host wall clock around each phase, data starting on the host).
+
+GPU arm (this repo): libnlsp_io load_instance -> generate_smoothed_vectors
+(K = 32, s1 = 10, omega = 0.66, seed = smoothing_seed(instance seed)) ->
+svd_basis(rank) -> TwoLevelPreconditioner(nu1 = nu2 = 5) -> pcg(delta = 1e-6,
+10 n), for ranks 4/8/16/32 (ExperimentConfig defaults, experiment.hpp:42-70).
+Reference arm: the same calls through oracle/_ref (the unmodified reference
+headers compiled by oracle/Makefile), one core.
+
+Prints one JSON line per (arm, rank) with smooth / inference / setup / solve /
+total ms (the reference's BenchRow fields) and iterations; --reps R repeats
+and keeps the median per phase.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+K, S1, OMEGA, NU, DELTA = 32, 10, 0.66, 5, 1e-6
+
+
+def gpu_arm(path, ranks, reps):
+    from paper_2601_20174_b200 import instance_io as io
+    from paper_2601_20174_b200 import nlsp
+    ctx = nlsp.default_context()
+    rows = {r: [] for r in ranks}
+    for rep in range(reps + 1):  # rep 0 warms module loading
+        t0 = time.perf_counter()
+        inst = io.load_instance(path)
+        t_load = time.perf_counter() - t0
+        seed = mix_seed(inst.seed, 3)
+        t0 = time.perf_counter()
+        sv = nlsp.generate_smoothed_vectors(inst.matrix, inst.boundary_mask, K, S1, OMEGA, seed)
+        ctx.synchronize()
+        t_smooth = time.perf_counter() - t0
+        for r in ranks:
+            t0 = time.perf_counter()
+            p, _, _ = nlsp.svd_basis(sv.s, r)
+            ctx.synchronize()
+            t_inf = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            m = nlsp.TwoLevelPreconditioner(inst.matrix, p, OMEGA, NU, NU)
+            ctx.synchronize()
+            t_setup = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            res = nlsp.pcg(inst.matrix, inst.rhs, m, DELTA, 10 * inst.matrix.dim())
+            t_solve = time.perf_counter() - t0
+            if rep:
+                rows[r].append(dict(load=t_load, smooth=t_smooth, inference=t_inf, setup=t_setup,
+                                    solve=t_solve, iterations=res.report.iterations,
+                                    converged=res.report.converged))
+    return inst.matrix.dim(), rows
+
+
+def ref_arm(path, ranks, reps):
+    from oracle.oracle import Reference
+    ref = Reference()
+    rows = {r: [] for r in ranks}
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        inst = ref.load_instance(path)
+        t_load = time.perf_counter() - t0
+        a = inst["matrix"]
+        seed = int(ref.lib.ref_mix_seed(inst["seed"], 3))
+        t0 = time.perf_counter()
+        s = ref.generate_smoothed_vectors(a, inst["mask"], K, S1, OMEGA, seed)
+        t_smooth = time.perf_counter() - t0
+        for r in ranks:
+            t0 = time.perf_counter()
+            u, _, _, _ = ref.svd(s)
+            p = np.ascontiguousarray(u[:, :r])
+            t_inf = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            t = ref.twolevel(a, p, OMEGA, NU, NU)
+            t_setup = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            res = ref.pcg(a, inst["rhs"], 2, t, DELTA, 10 * a[0])
+            t_solve = time.perf_counter() - t0
+            rows[r].append(dict(load=t_load, smooth=t_smooth, inference=t_inf, setup=t_setup,
+                                solve=t_solve, iterations=res.iterations, converged=res.converged))
+    return a[0], rows
+
+
+def mix_seed(seed, tag):
+    # rng.hpp mix_seed through the product's host generator library
+    from paper_2601_20174_b200 import _lib as L
+    return int(L.inputs_lib().nlsp_mix_seed(seed, tag))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--instance", default=os.path.join(ROOT, "tests", "golden", "io", "inst_diffusion_n64"))
+    ap.add_argument("--ranks", default="4,8,16,32")
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--impl", choices=["gpu", "reference", "both"], default="both")
+    args = ap.parse_args()
+    ranks = [int(r) for r in args.ranks.split(",")]
+    arms = ["gpu", "reference"] if args.impl == "both" else [args.impl]
+    for arm in arms:
+        n, rows = (gpu_arm if arm == "gpu" else ref_arm)(args.instance, ranks, args.reps)
+        for r in ranks:
+            med = {k: statistics.median(x[k] for x in rows[r]) * 1e3
+                   for k in ("load", "smooth", "inference", "setup", "solve")}
+            out = {"impl": arm, "instance": os.path.basename(args.instance), "n": n, "method": "SVD",
+                   "rank": r, "K": K, "s1": S1, "nu": NU, "delta": DELTA,
+                   "iterations": rows[r][-1]["iterations"], "converged": rows[r][-1]["converged"],
+                   "ms": {k: round(v, 3) for k, v in med.items()},
+                   "total_ms": round(med["smooth"] + med["inference"] + med["setup"] + med["solve"], 3),
+                   "reps": len(rows[r]), "cores": 1 if arm == "reference" else None}
+            print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -13,7 +13,7 @@ import pytest
 from conftest import ROOT
 from paper_2601_20174_b200 import _lib as L
 
-HEADERS = {"nlsp_gpu.h": L.GPU_LIB_PATH, "nlsp_inputs.h": L.INPUTS_LIB_PATH}
+HEADERS = {"nlsp_gpu.h": L.GPU_LIB_PATH, "nlsp_inputs.h": L.INPUTS_LIB_PATH, "nlsp_io.h": L.IO_LIB_PATH}
 
 
 def declared(header):
@@ -39,6 +39,7 @@ def test_library_exports_every_declared_symbol(header):
 def test_ctypes_table_covers_headers():
     assert declared("nlsp_gpu.h") == {n for n, _, _ in L.GPU_SYMBOLS}
     assert declared("nlsp_inputs.h") == {n for n, _, _ in L.INPUT_SYMBOLS}
+    assert declared("nlsp_io.h") == {n for n, _, _ in L.IO_SYMBOLS}
 
 
 def test_gpu_library_is_sm100a():
