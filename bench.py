@@ -152,12 +152,15 @@ def byte_model_literal(n, nnz, k, nu1, nu2):
     return (1 + nu1 + nu2) * csr + 16.0 * n * k + v * n
 
 
-def byte_model(n, nnz, k, nu1, nu2):
+def byte_model(n, nnz, k, nu1, nu2, pass_bytes=None):
     """Algorithmic HBM bytes per PCG iteration of the schedule this library runs
-    (folded cycle): spmv_p (CSR + 32n), update+restriction through
-    W1 (8nk + 48n), nu1+nu2-1 smoothing sweeps (CSR + 24n for the first, CSR + 32n
-    after), prolongation through W2 with r.z (8nk + 24n)."""
-    csr = 12.0 * nnz + 4.0 * (n + 1)
+    (folded cycle): spmv_p (A + 32n), update+restriction through
+    W1 (8nk + 48n), nu1+nu2-1 smoothing sweeps (A + 24n for the first, A + 32n
+    after), prolongation through W2 with r.z (8nk + 24n). A = the matrix bytes
+    one pass streams: CSR 12 nnz + 4(n+1), or the diagonal form's own bytes
+    when the upload detected one (nlsp_csr_format; SURVEY §8d's rule for
+    stencil-specialised kernels)."""
+    csr = 12.0 * nnz + 4.0 * (n + 1) if pass_bytes is None else float(pass_bytes)
     ld = k + (k & 1)
     t = nu1 + nu2
     sweeps = 0.0
@@ -313,7 +316,9 @@ def run_ours(args, dist: Dist):
     dominant = max((k for k in kernels if kernels[k]["bytes_per_launch"] > 0),
                    key=lambda k: kernels[k]["avg_us"] * kernels[k]["launches"])
     dk = kernels[dominant]
-    bytes_iter = byte_model(pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2)
+    fmt_kind, fmt_offsets, pass_bytes = dcsr.format()
+    bytes_iter = byte_model(pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2, pass_bytes)
+    bytes_iter_csr = byte_model(pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2)
     iter_gbs = bytes_iter * iters / (ms_local / 1e3) / 1e9
     traffic = ncu_traffic(dominant, args.config)
     roofline = {"bound": "hbm", "kernel": dominant, "achieved": round(dk["gbs"], 1),
@@ -322,6 +327,9 @@ def run_ours(args, dist: Dist):
                 "bytes_per_launch": dk["bytes_per_launch"], "avg_launch_us": round(dk["avg_us"], 2),
                 "iteration": {"bytes_per_iter": bytes_iter, "achieved": round(iter_gbs, 1),
                               "frac": round(iter_gbs / peak, 4),
+                              "matrix_form": ["csr", "diagonal-constant", "diagonal-values"][fmt_kind],
+                              "matrix_offsets": fmt_offsets, "matrix_bytes_per_pass": pass_bytes,
+                              "csr_model_bytes_per_iter": bytes_iter_csr,
                               "literal_schedule_bytes_per_iter": byte_model_literal(
                                   pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2),
                               "literal_equivalent_gbs": round(byte_model_literal(

@@ -83,6 +83,15 @@ nlsp_status nlsp_csr_upload(nlsp_ctx* ctx, uint64_t n, uint64_t nnz, const uint6
                             const uint64_t* col_idx, const double* values, nlsp_csr** out);
 void nlsp_csr_destroy(nlsp_csr* a);
 void nlsp_csr_dims(const nlsp_csr* a, uint64_t* n, uint64_t* nnz);
+
+/* The device form the solve kernels stream (no reference
+ * counterpart): kind 0 = CSR; 1 = diagonal form with one value per offset
+ * (constant-coefficient stencil: per-row presence bits only); 2 = diagonal
+ * form with per-row values. `offsets` = number of distinct column offsets
+ * (kinds 1, 2), `pass_bytes` = matrix bytes one SpMV pass reads (the byte
+ * model of the roofline). Detected at nlsp_csr_upload; NLSP_DIA=0 keeps CSR.
+ * Results are bitwise those of the CSR kernels (same per-row fma order). */
+nlsp_status nlsp_csr_format(const nlsp_csr* a, int* kind, int* offsets, uint64_t* pass_bytes);
 /* spmv (sparse.hpp:116-128), y = A x; host buffers of length n */
 nlsp_status nlsp_spmv(nlsp_ctx* ctx, const nlsp_csr* a, const double* x, double* y);
 /* device-buffer variant (x, y device pointers of length n) */

@@ -315,6 +315,8 @@ class Reference:
             "ref_fem_instance": (C.c_int, [C.c_int, u64, dbl, u64, Pu64, Pu64, Pu64, Pu64, Pdbl, Pdbl, Pu8]),
             "ref_mix_seed": (u64, [u64, u64]),
             "ref_save_instance": (C.c_int, [C.c_int, u64, dbl, u64, C.c_char_p]),
+            "ref_aggregate_nodes": (C.c_int, [vp, dbl, Pu64, Pu64]),
+            "ref_sa_prolongator": (C.c_int, [vp, dbl, dbl, Pu64, Pdbl]),
             "ref_load_matrix_market": (vp, [C.c_char_p, Pi32]),
             "ref_save_matrix_market": (C.c_int, [vp, C.c_char_p]),
             "ref_load_instance": (vp, [C.c_char_p, Pi32]),
@@ -405,6 +407,22 @@ class Reference:
         rp, ci, v = np.empty(dim + 1, np.uint64), np.empty(nnz, np.uint64), np.empty(nnz)
         self.lib.ref_csr_export(h, _u(rp), _u(ci), _d(v))
         return (dim, rp, ci, v)
+
+    def aggregate_nodes(self, a, theta):
+        """aggregate_nodes (sa.hpp:18-76): (aggregate id per node, count)."""
+        n = _csr(a)[0]
+        agg, nc = np.empty(n, np.uint64), C.c_uint64(0)
+        self._chk(self.lib.ref_aggregate_nodes(self.handle(a), theta, _u(agg), C.byref(nc)))
+        return agg, int(nc.value)
+
+    def sa_prolongator(self, a, theta=0.25, omega=0.66):
+        """sa_prolongator (sa.hpp:78-109): dense n x nc."""
+        n = _csr(a)[0]
+        nc = C.c_uint64(0)
+        self._chk(self.lib.ref_sa_prolongator(self.handle(a), theta, omega, C.byref(nc), None))
+        p = np.empty((n, nc.value))
+        self._chk(self.lib.ref_sa_prolongator(self.handle(a), theta, omega, C.byref(nc), _d(p)))
+        return p
 
     def save_instance(self, family, grid_n, jitter, seed, path):
         self._chk(self.lib.ref_save_instance(family, grid_n, jitter, seed, str(path).encode()))

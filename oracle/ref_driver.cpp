@@ -267,6 +267,26 @@ void ref_instance_arrays(void* h, double* rhs, std::uint8_t* mask, double* vert,
     }
 }
 
+// --- smoothed aggregation (sa.hpp:18-109) -----------------------------------
+// aggregate ids (n) and their count
+int ref_aggregate_nodes(void* h, double theta, std::uint64_t* agg, std::uint64_t* nc) {
+    return guarded([&] {
+        std::size_t c = 0;
+        const auto a = aggregate_nodes(*static_cast<SparseCsrMatrix*>(h), theta, &c);
+        for (std::size_t i = 0; i < a.size(); ++i) agg[i] = a[i];
+        *nc = c;
+    });
+}
+
+// dense P (n x nc, row-major); two-phase: p == NULL queries nc
+int ref_sa_prolongator(void* h, double theta, double omega, std::uint64_t* nc, double* p) {
+    return guarded([&] {
+        const auto m = sa_prolongator(*static_cast<SparseCsrMatrix*>(h), theta, omega);
+        *nc = m.cols();
+        if (p) dense_to(m, p);
+    });
+}
+
 // --- RNG (rng.hpp) ----------------------------------------------------------
 std::uint64_t ref_mix_seed(std::uint64_t seed, std::uint64_t tag) { return mix_seed(seed, tag); }
 

@@ -97,6 +97,7 @@ GPU_SYMBOLS = [
     ("nlsp_csr_upload", C.c_int, [vp, c_u64, c_u64, P_u64, P_u64, P_dbl, C.POINTER(vp)]),
     ("nlsp_csr_destroy", None, [vp]),
     ("nlsp_csr_dims", None, [vp, P_u64, P_u64]),
+    ("nlsp_csr_format", c_i32, [vp, P_i32, P_i32, P_u64]),
     ("nlsp_spmv", C.c_int, [vp, vp, P_dbl, P_dbl]),
     ("nlsp_spmv_device", C.c_int, [vp, vp, vp, vp]),
     ("nlsp_csr_diagonal", C.c_int, [vp, vp, P_dbl]),

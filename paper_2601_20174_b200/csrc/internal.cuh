@@ -42,6 +42,24 @@ enum Ticket : int {
     kTkInit, kTkGeneric
 };
 
+// Diagonal (offset) form of A, detected at upload (nlsp_gpu.cu):
+// when the CSR columns of every row sit at one of d <= 32 fixed offsets from
+// the row, A is stored as per-row presence bits over the sorted offsets plus
+// either one value per offset (kind 1, every entry on an offset bitwise equal:
+// constant-coefficient stencils) or a column-major value slab vals[t n + i]
+// (kind 2). Row sums run over the present offsets in ascending order = the
+// CSR column order, so results are bitwise those of the CSR kernels.
+constexpr int kMaxDia = 32;
+struct DiaArgs {
+    int kind;   // 0: CSR only, 1: constant values, 2: per-row values
+    int d;      // number of offsets
+    int mbytes; // presence-mask bytes per row: 1, 2 or 4
+    int off[kMaxDia];
+    double val[kMaxDia];
+    const void* mask;  // n presence masks (bit t: offset t present)
+    const double* rv;  // kind 2: d x n values (0 where absent)
+};
+
 // Everything a solve kernel needs, passed by value.
 struct SolveArgs {
     int n;
@@ -73,6 +91,7 @@ struct SolveArgs {
     PcgState* st;
     double* partials;    // kMaxGrid * max(k, 4)
     double* e;           // coarse correction, k
+    DiaArgs dia;         // diagonal form of A (dia.kind == 0: CSR kernels)
 };
 
 constexpr int kColsignPerSm = 8;  // CTAs per SM of the column-sign scan

@@ -86,6 +86,10 @@ struct nlsp_csr {
     int max_row;
     int tile_nnz64, tile_nnz128, tile_nnz256;  // max nonzeros of any 64/128/256-row tile
     std::vector<int> rp_host;  // row_ptr kept on the host for small systems (cluster plan)
+    DiaArgs dia{};             // diagonal form (dia.kind == 0: none)
+    void* dia_mask = nullptr;
+    double* dia_rv = nullptr;
+    unsigned long long pass_bytes = 0;  // matrix bytes one solve-kernel pass streams
 };
 
 struct nlsp_dense {
@@ -263,6 +267,7 @@ SolveArgs make_args(nlsp_ctx* c, const nlsp_csr* a, const nlsp_twolevel* m) {
     s.tile_nnz128 = a->tile_nnz128;
     s.tile_nnz256 = a->tile_nnz256;
     s.max_row = a->max_row;
+    s.dia = a->dia;
     s.wd = m ? m->wd : nullptr;
     s.P = m ? m->basis : nullptr;
     s.L = m ? m->L : nullptr;
@@ -571,6 +576,68 @@ nlsp_status nlsp_ctx_synchronize(nlsp_ctx* ctx) {
 }
 
 // ---------------------------------------------------------------------- CSR --
+// Diagonal form of a CSR matrix (DiaArgs, internal.cuh): the sorted set of
+// column offsets (at most kMaxDia), per-row presence bits and either the one
+// value every entry of an offset shares (kind 1) or a d x n value slab (kind 2).
+// Returns false when the offsets do not fit or the form would not stream fewer
+// bytes than the CSR arrays.
+static bool detect_dia(uint64_t n, uint64_t nnz, const uint64_t* rp, const uint64_t* ci,
+                       const double* v, DiaArgs& d, std::vector<unsigned char>& mask,
+                       std::vector<double>& rv) {
+    if (n == 0 || nnz == 0) return false;
+    long long offs[kMaxDia];
+    int D = 0;
+    for (uint64_t i = 0; i < n; ++i)
+        for (uint64_t k = rp[i]; k < rp[i + 1]; ++k) {
+            const long long o = (long long)ci[k] - (long long)i;
+            const long long* at = std::lower_bound(offs, offs + D, o);
+            if (at < offs + D && *at == o) continue;
+            if (D == kMaxDia) return false;
+            const int pos = (int)(at - offs);
+            for (int t = D; t > pos; --t) offs[t] = offs[t - 1];
+            offs[pos] = o;
+            ++D;
+        }
+    const int mb = D <= 8 ? 1 : (D <= 16 ? 2 : 4);
+    double cv[kMaxDia];
+    bool seen[kMaxDia] = {false}, constant = true;
+    mask.assign((size_t)n * mb, 0);
+    for (uint64_t i = 0; i < n; ++i) {
+        unsigned m = 0;
+        for (uint64_t k = rp[i]; k < rp[i + 1]; ++k) {
+            const int t = (int)(std::lower_bound(offs, offs + D, (long long)ci[k] - (long long)i) - offs);
+            m |= 1u << t;
+            if (!seen[t]) {
+                cv[t] = v[k];
+                seen[t] = true;
+            } else if (std::memcmp(&cv[t], &v[k], sizeof(double)) != 0) {
+                constant = false;
+            }
+        }
+        std::memcpy(mask.data() + (size_t)i * mb, &m, mb);  // little endian
+    }
+    const double csr_bytes = 12.0 * (double)nnz + 4.0 * (double)(n + 1);
+    const double dia_bytes = (double)n * (mb + (constant ? 0 : 8 * D));
+    if (!constant && dia_bytes > 0.8 * csr_bytes) return false;
+    if (!constant) {
+        rv.assign((size_t)D * n, 0.0);
+        for (uint64_t i = 0; i < n; ++i)
+            for (uint64_t k = rp[i]; k < rp[i + 1]; ++k) {
+                const int t = (int)(std::lower_bound(offs, offs + D, (long long)ci[k] - (long long)i) - offs);
+                rv[(size_t)t * n + i] = v[k];
+            }
+    }
+    d = DiaArgs{};
+    d.kind = constant ? 1 : 2;
+    d.d = D;
+    d.mbytes = mb;
+    for (int t = 0; t < D; ++t) {
+        d.off[t] = (int)offs[t];
+        d.val[t] = constant ? cv[t] : 0.0;
+    }
+    return true;
+}
+
 nlsp_status nlsp_csr_upload(nlsp_ctx* ctx, uint64_t n, uint64_t nnz, const uint64_t* row_ptr,
                             const uint64_t* col_idx, const double* values, nlsp_csr** out) {
     if (!out) return set_err(ctx, NLSP_E_VALIDATION, "csr_upload: null out");
@@ -640,6 +707,28 @@ nlsp_status nlsp_csr_upload(nlsp_ctx* ctx, uint64_t n, uint64_t nnz, const uint6
     }
     a->max_row = ctx->flags_host[1];
     if (n <= 65536) a->rp_host.assign(row_ptr, row_ptr + n + 1);
+    a->pass_bytes = 12ull * nnz + 4ull * (n + 1);
+    {
+        const char* de = std::getenv("NLSP_DIA");
+        std::vector<unsigned char> mask;
+        std::vector<double> rv;
+        DiaArgs d{};
+        if (!(de && de[0] == '0') && detect_dia(n, nnz, row_ptr, col_idx, values, d, mask, rv)) {
+            if ((e = dalloc(reinterpret_cast<unsigned char**>(&a->dia_mask), mask.size() + 16)) ||
+                (e = cudaMemcpyAsync(a->dia_mask, mask.data(), mask.size(), cudaMemcpyHostToDevice, ctx->s)))
+                return fail(e, "csr_upload diagonal form");
+            if (d.kind == 2) {
+                if ((e = dalloc(&a->dia_rv, rv.size())) ||
+                    (e = cudaMemcpyAsync(a->dia_rv, rv.data(), rv.size() * 8, cudaMemcpyHostToDevice, ctx->s)))
+                    return fail(e, "csr_upload diagonal values");
+            }
+            if ((e = cudaStreamSynchronize(ctx->s))) return fail(e, "csr_upload diagonal sync");
+            d.mask = a->dia_mask;
+            d.rv = a->dia_rv;
+            a->dia = d;
+            a->pass_bytes = (unsigned long long)n * (d.mbytes + (d.kind == 2 ? 8ull * d.d : 0ull));
+        }
+    }
     // diag_ok: any A_ii <= 0 ?
     {
         int* f = ctx->flags + 2;
@@ -666,7 +755,17 @@ void nlsp_csr_destroy(nlsp_csr* a) {
     dfree(a->ci);
     dfree(a->v);
     dfree(a->diag);
+    dfree(a->dia_mask);
+    dfree(a->dia_rv);
     delete a;
+}
+
+nlsp_status nlsp_csr_format(const nlsp_csr* a, int* kind, int* offsets, uint64_t* pass_bytes) {
+    if (!a) return NLSP_E_VALIDATION;
+    if (kind) *kind = a->dia.kind;
+    if (offsets) *offsets = a->dia.kind ? a->dia.d : 0;
+    if (pass_bytes) *pass_bytes = a->pass_bytes;
+    return NLSP_OK;
 }
 
 void nlsp_csr_dims(const nlsp_csr* a, uint64_t* n, uint64_t* nnz) {
@@ -1200,16 +1299,17 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
     };
     const double n = a->n, nnz = (double)a->nnz, k = m ? m->k : 0;
     const double csr = 12.0 * nnz + 4.0 * (n + 1);
+    const double pass = (double)a->pass_bytes;  // CSR, or the diagonal form when detected
     // algorithmic bytes per launch; slots by name below
     enum { kSpmvP = 0, kUpd, kRes, kPro, kPost, kUR, kSmooth, kCtl, kSlots };
     std::vector<Acc> acc = {
-        {"spmv_p", csr + 32.0 * n},                  // reads z, p; writes p, q
+        {"spmv_p", pass + 32.0 * n},                 // reads z, p; writes p, q
         {"update", (mode == 0 ? 48.0 : (mode == 1 ? 56.0 : 64.0)) * n},
         {"restrict", csr + 8.0 * n * k + 16.0 * n},  // literal: P, r, w (implicit z1)
         {"prolong", 8.0 * n * k + 24.0 * n},         // literal: P, r, w; writes z2
-        {"post_sweep", csr + 32.0 * n},              // z2, r, w; writes z
+        {"post_sweep", pass + 32.0 * n},             // z2, r, w; writes z
         {"update_restrict", 8.0 * n * k + 48.0 * n}, // folded: W1, x, p, q, r; writes x, r
-        {"smooth", csr + ((m && m->nu1 + m->nu2 == 2) ? 24.0 : 32.0) * n},  // folded sweeps
+        {"smooth", pass + ((m && m->nu1 + m->nu2 == 2) ? 24.0 : 32.0) * n},  // folded sweeps
         {"loop_ctl", 0.0},
     };
     if ((int)acc.size() != kSlots) return -1;

@@ -796,6 +796,52 @@ struct OpPlain {
     __device__ __forceinline__ void finish(PcgState*, const double*) const {}
 };
 
+// ====================================================== diagonal-form rows ==
+// The SpMV family over the diagonal form of A (DiaArgs, internal.cuh): one
+// thread per row, presence bits of the row, gathers x[i + off_t] for the
+// present offsets (consecutive rows -> coalesced), then the fma chain in
+// ascending offset order = CSR column order, so y is bitwise the CSR kernels'
+// y. Matrix bytes per row: the mask (1-4 B) for constant-coefficient stencils,
+// + 8 d for per-row values, instead of 12 nnz/n + 4 for CSR.
+// (Measured alternatives: lane shuffles for offsets within a
+// warp and shared-memory windows per offset cluster both cut L2 requests but
+// lost the memory-level parallelism of this form: 1.6x / 1.6x slower at C4.)
+template <int MAXD, typename MT, bool RV, int SKIP, class Op>
+__global__ void __launch_bounds__(kThreads) k_spmv_dia(SolveArgs a, Op op) {
+    PcgState* st = a.st;
+    if (SKIP == 1 && st->done) return;
+    if (SKIP == 2 && st->error) return;
+    op.init(a);
+    constexpr int NVS = Op::NV > 0 ? Op::NV : 1;
+    double s[NVS];
+#pragma unroll
+    for (int j = 0; j < NVS; ++j) s[j] = 0.0;
+    const MT* __restrict__ mask = static_cast<const MT*>(a.dia.mask);
+    const int n = a.n, d = a.dia.d;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const unsigned m = mask[i];
+        double g[MAXD], vv[MAXD];
+#pragma unroll
+        for (int t = 0; t < MAXD; ++t) {
+            const bool on = t < d && ((m >> t) & 1u);
+            g[t] = on ? op(i + a.dia.off[t]) : 0.0;
+            if (RV) vv[t] = on ? __ldcs(a.dia.rv + (size_t)t * n + i) : 0.0;
+        }
+        double y = 0.0;
+#pragma unroll
+        for (int t = 0; t < MAXD; ++t)
+            if (t < d && ((m >> t) & 1u)) y = fma(RV ? vv[t] : a.dia.val[t], g[t], y);
+        op.row(i, y, s);
+    }
+    if constexpr (Op::NV > 0) {
+        double v[Op::NV], tot[Op::NV];
+#pragma unroll
+        for (int j = 0; j < Op::NV; ++j) v[j] = s[j];
+        if (grid_reduce<Op::NV>(v, a.partials, &st->counter[Op::TICKET], tot) && threadIdx.x == 0)
+            op.finish(st, tot);
+    }
+}
+
 // SKIP: 0 never, 1 when st->done (solve kernels), 2 when st->error (true residual)
 // G lanes per row (transposed mapping), U row steps per warp and tile:
 // TR = 8 warps * U * (32 / G) rows per staged tile.
@@ -1263,6 +1309,28 @@ void launch_spmv_op(const LaunchCtx& c, const SolveArgs& a, const Op& op) {
     else launch_tma(c, k_spmv_tma<G, U, S, SKIP, 16, Op>, nt, sm, a, op);
 }
 
+template <int SKIP, class Op>
+void launch_dia_op(const LaunchCtx& c, const SolveArgs& a, const Op& op) {
+    auto go = [&](auto kern) {
+        const int g = occ_grid(c, reinterpret_cast<const void*>(kern), a.n, kThreads);
+        kern<<<g, kThreads, 0, c.s>>>(a, op);
+    };
+    const bool rv = a.dia.kind == 2;
+    if (a.dia.d <= 8) {
+        if (rv) go(k_spmv_dia<8, unsigned char, true, SKIP, Op>);
+        else go(k_spmv_dia<8, unsigned char, false, SKIP, Op>);
+    } else if (a.dia.d <= 16) {
+        if (rv) go(k_spmv_dia<16, unsigned short, true, SKIP, Op>);
+        else go(k_spmv_dia<16, unsigned short, false, SKIP, Op>);
+    } else if (a.dia.d <= 24) {
+        if (rv) go(k_spmv_dia<24, unsigned int, true, SKIP, Op>);
+        else go(k_spmv_dia<24, unsigned int, false, SKIP, Op>);
+    } else {
+        if (rv) go(k_spmv_dia<32, unsigned int, true, SKIP, Op>);
+        else go(k_spmv_dia<32, unsigned int, false, SKIP, Op>);
+    }
+}
+
 // Staged tiles must fit in shared memory (227 KB per CTA); matrices with very
 // long rows (a tile's nonzeros beyond the budget) take the direct-load kernels.
 constexpr size_t kStageBudget = 200 * 1024;
@@ -1270,7 +1338,8 @@ bool spmv_tma_ok(const SolveArgs& a) { return NLSP_TMA && spmv_stage_smem(a) <= 
 bool restrict_tma_ok(const SolveArgs& a) { return NLSP_TMA && restrict_stage_smem(a) <= kStageBudget; }
 
 void launch_spmv_p(const LaunchCtx& c, const SolveArgs& a) {
-    if (spmv_tma_ok(a)) launch_spmv_op<1>(c, a, OpSpmvP{});
+    if (a.dia.kind) launch_dia_op<1>(c, a, OpSpmvP{});
+    else if (spmv_tma_ok(a)) launch_spmv_op<1>(c, a, OpSpmvP{});
     else launch_rows<kU>(c, k_spmv_p, a.n, a);
     count(c);
 }
@@ -1289,7 +1358,8 @@ void launch_loop_ctl(const LaunchCtx& c, PcgState* st, cudaGraphConditionalHandl
 }
 
 void launch_true_res(const LaunchCtx& c, const SolveArgs& a) {
-    if (spmv_tma_ok(a)) launch_spmv_op<2>(c, a, OpTrueRes{a.x, a.b});
+    if (a.dia.kind) launch_dia_op<2>(c, a, OpTrueRes{a.x, a.b});
+    else if (spmv_tma_ok(a)) launch_spmv_op<2>(c, a, OpTrueRes{a.x, a.b});
     else launch_rows<kU>(c, k_true_res, a.n, a);
     count(c);
 }
@@ -1302,7 +1372,8 @@ void launch_spmv(const LaunchCtx& c, int n, const int* rp, const int* ci, const 
 
 // y = A x through the TMA-staged engine (the product path of nlsp_spmv)
 void launch_spmv_args(const LaunchCtx& c, const SolveArgs& a, const double* x, double* y) {
-    if (spmv_tma_ok(a)) launch_spmv_op<0>(c, a, OpPlain{x, y});
+    if (a.dia.kind) launch_dia_op<0>(c, a, OpPlain{x, y});
+    else if (spmv_tma_ok(a)) launch_spmv_op<0>(c, a, OpPlain{x, y});
     else launch_rows<kU>(c, k_spmv, a.n, a.n, a.rp, a.ci, a.v, x, y);
     count(c);
 }
@@ -1373,6 +1444,19 @@ void launch_prolong(const LaunchCtx& c, const SolveArgs& a, int zmode, bool rz, 
 // sweep with z_in = implicit w D^-1 r (first pre-sweep) or a buffer
 void launch_sweep(const LaunchCtx& c, const SolveArgs& a, bool implicit_in, const double* zin,
                   double* zout, bool rz) {
+    if (a.dia.kind) {
+        if (implicit_in) {
+            const GWdr gw{a.wd, a.r};
+            if (rz) launch_dia_op<1>(c, a, OpSweep<GWdr, true>{gw, a.r, a.wd, zout});
+            else launch_dia_op<1>(c, a, OpSweep<GWdr, false>{gw, a.r, a.wd, zout});
+        } else {
+            const GPlain gp{zin};
+            if (rz) launch_dia_op<1>(c, a, OpSweep<GPlain, true>{gp, a.r, a.wd, zout});
+            else launch_dia_op<1>(c, a, OpSweep<GPlain, false>{gp, a.r, a.wd, zout});
+        }
+        count(c);
+        return;
+    }
     if (spmv_tma_ok(a)) {
         if (implicit_in) {
             const GWdr gw{a.wd, a.r};

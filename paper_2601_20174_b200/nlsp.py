@@ -236,6 +236,13 @@ class DeviceCsr:
                                                 C.byref(h)))
         return DeviceCsr(ctx, h, a.dim(), a.nnz())
 
+    def format(self):
+        """(kind, offsets, pass_bytes) of nlsp_csr_format: 0 CSR, 1 constant
+        diagonal form, 2 diagonal form with per-row values."""
+        kind, offs, pb = C.c_int32(0), C.c_int32(0), C.c_uint64(0)
+        _check(self.ctx, L.gpu_lib().nlsp_csr_format(self.handle, C.byref(kind), C.byref(offs), C.byref(pb)))
+        return int(kind.value), int(offs.value), int(pb.value)
+
     def __del__(self):
         try:
             if self.handle:

@@ -42,6 +42,8 @@ PATHS = {
     # coarse solve by the reference's triangular substitutions instead of A_c^-1
     "chol": {"NLSP_CLUSTER": "0", "NLSP_COARSE": "chol"},
     "cluster_chol": {"NLSP_CLUSTER": "1", "NLSP_COARSE": "chol"},
+    # the SpMV family over CSR instead of the detected diagonal form
+    "graph_csr": {"NLSP_CLUSTER": "0", "NLSP_DIA": "0"},
 }
 
 
@@ -69,3 +71,26 @@ def test_execution_paths_match_reference(tmp_path, case):
     assert res["cluster"][0]["launches"] == 2  # state init + the cluster kernel
     assert res["graph"][0]["iterations"] == res["host"][0]["iterations"]
     assert np.array_equal(res["graph"][1], res["host"][1])
+    # the diagonal form sums every row in CSR column order: bitwise the CSR path
+    assert res["graph"][0]["iterations"] == res["graph_csr"][0]["iterations"]
+    assert np.array_equal(res["graph"][1], res["graph_csr"][1])
+
+
+EXPECTED_FORM = {"c1_default": 1, "scaled_C2": 2, "scaled_C3": 1, "scaled_C4": 1, "scaled_C5": 0,
+                 "fem_diffusion": 0}
+
+
+@pytest.mark.parametrize("case", sorted(EXPECTED_FORM))
+def test_detected_matrix_form(nlsp, case):
+    from conftest import csr_from_golden
+    d = golden(case)
+    a = csr_from_golden(d)
+    kind, offsets, pass_bytes = a.device().format()
+    assert kind == EXPECTED_FORM[case]
+    n, nnz = a.dim(), a.nnz()
+    if kind == 0:
+        assert pass_bytes == 12 * nnz + 4 * (n + 1)
+    else:
+        mb = 1 if offsets <= 8 else (2 if offsets <= 16 else 4)
+        assert pass_bytes == n * (mb + (8 * offsets if kind == 2 else 0))
+        assert pass_bytes < 12 * nnz + 4 * (n + 1)
