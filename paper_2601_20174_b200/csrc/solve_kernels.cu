@@ -32,6 +32,9 @@ namespace nlsp {
 #ifndef NLSP_KUP
 #define NLSP_KUP 2
 #endif
+#ifndef NLSP_KUPRO
+#define NLSP_KUPRO 2
+#endif
 #ifndef NLSP_BLOCKROWS
 #define NLSP_BLOCKROWS 0
 #endif
@@ -623,10 +626,22 @@ __global__ void __launch_bounds__(kThreads) k_prolong(SolveArgs a, const double*
         }
     }
     double s[1] = {0.0};
-    ROW_BATCH_BEGIN(a.n, kUP)
-        double2 pv[kUP][PPL];
+    constexpr int UPR = NLSP_KUPRO;
+    ROW_BATCH_BEGIN(a.n, UPR)
+        // the row's scalars first (independent of the basis stream), then the
+        // W2 rows, so both are in flight together
+        double zpv[UPR], rrv[UPR];
 #pragma unroll
-        for (int u = 0; u < kUP; ++u) {
+        for (int u = 0; u < UPR; ++u) {
+            const int rw = valid[u] ? row[u] : 0;
+            if (ZMODE == 0) zpv[u] = 0.0;
+            else if (ZMODE == 1) zpv[u] = a.wd[rw] * a.r[rw];
+            else zpv[u] = zpre[rw];
+            rrv[u] = RZ ? a.r[rw] : 0.0;
+        }
+        double2 pv[UPR][PPL];
+#pragma unroll
+        for (int u = 0; u < UPR; ++u) {
             const double* prow = a.P + (long long)row[u] * ld;
 #pragma unroll
             for (int t = 0; t < PPL; ++t) {
@@ -634,9 +649,9 @@ __global__ void __launch_bounds__(kThreads) k_prolong(SolveArgs a, const double*
                 pv[u][t] = (valid[u] && pi < pairs) ? ld_stream2(prow + 2 * pi) : make_double2(0.0, 0.0);
             }
         }
-        double sum[kUP];
+        double sum[UPR];
 #pragma unroll
-        for (int u = 0; u < kUP; ++u) {
+        for (int u = 0; u < UPR; ++u) {
             double part = 0.0;
 #pragma unroll
             for (int t = 0; t < PPL; ++t) {
@@ -647,16 +662,11 @@ __global__ void __launch_bounds__(kThreads) k_prolong(SolveArgs a, const double*
         }
         if (l == 0) {
 #pragma unroll
-            for (int u = 0; u < kUP; ++u) {
+            for (int u = 0; u < UPR; ++u) {
                 if (!valid[u]) continue;
-                const int rw = row[u];
-                double zp;
-                if (ZMODE == 0) zp = 0.0;
-                else if (ZMODE == 1) zp = a.wd[rw] * a.r[rw];
-                else zp = zpre[rw];
-                const double zi = zp + sum[u];
-                zout[rw] = zi;
-                if (RZ) s[0] = fma(a.r[rw], zi, s[0]);
+                const double zi = zpv[u] + sum[u];
+                zout[row[u]] = zi;
+                if (RZ) s[0] = fma(rrv[u], zi, s[0]);
             }
         }
     ROW_BATCH_END
@@ -1397,7 +1407,7 @@ static void restrict_ppl(const LaunchCtx& c, const SolveArgs& a, int zmode, cons
 template <int PPL>
 static void prolong_ppl(const LaunchCtx& c, const SolveArgs& a, int zmode, bool rz,
                         const double* zpre, double* zout, cudaGraphConditionalHandle h, int ctl) {
-#define NLSP_PRO(Z, R) launch_rows<kUP>(c, k_prolong<PPL, Z, R>, a.n, a, zpre, zout, h, ctl)
+#define NLSP_PRO(Z, R) launch_rows<NLSP_KUPRO>(c, k_prolong<PPL, Z, R>, a.n, a, zpre, zout, h, ctl)
     if (zmode == 0) { if (rz) NLSP_PRO(0, true); else NLSP_PRO(0, false); }
     else if (zmode == 1) { if (rz) NLSP_PRO(1, true); else NLSP_PRO(1, false); }
     else { if (rz) NLSP_PRO(2, true); else NLSP_PRO(2, false); }
