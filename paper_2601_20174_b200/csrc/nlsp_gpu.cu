@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -190,11 +191,42 @@ nlsp_status map_dev_error(nlsp_ctx* c, int code, const char* where) {
     }
 }
 
+// Handle-owned device memory (matrices, bases, workspaces) comes from one
+// stream-ordered pool per device that never releases memory to the OS, so
+// rebuilding a preconditioner or re-uploading a matrix reuses pages instead of
+// mapping multi-GB allocations anew (tens to hundreds of ms at C4). Allocation
+// is ordered on the legacy stream and completed before use; cudaFree of a pool
+// allocation synchronises the device and returns the block to the pool.
+static cudaMemPool_t device_pool() {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    if (!pools[dev]) {
+        cudaMemPoolProps pp{};
+        pp.allocType = cudaMemAllocationTypePinned;
+        pp.location.type = cudaMemLocationTypeDevice;
+        pp.location.id = dev;
+        unsigned long long keep = ~0ull;
+        if (cudaMemPoolCreate(&pools[dev], &pp) != cudaSuccess ||
+            cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep) != cudaSuccess) {
+            cudaGetLastError();
+            pools[dev] = nullptr;
+        }
+    }
+    return pools[dev];
+}
+
 template <class T>
 cudaError_t dalloc(T** p, size_t count) {
     *p = nullptr;
     if (count == 0) count = 1;
-    return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+    cudaMemPool_t pool = device_pool();
+    if (!pool) return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+    cudaError_t e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), count * sizeof(T), pool, 0);
+    if (!e) e = cudaStreamSynchronize(0);
+    return e;
 }
 
 void dfree(void* p) {

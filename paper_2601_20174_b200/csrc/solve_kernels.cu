@@ -740,12 +740,17 @@ struct OpSpmvP {
         q = a.q;
     }
     __device__ __forceinline__ double operator()(int j) const { return g(j); }
-    __device__ __forceinline__ void row(int i, double y, double* s) const {
-        const double pi = g(i);
-        pc[i] = pi;
+    // own-row operands, loadable before the row's gathers complete
+    struct Pre {
+        double pi;
+    };
+    __device__ __forceinline__ Pre pre(int i) const { return Pre{g(i)}; }
+    __device__ __forceinline__ void row(int i, double y, double* s, const Pre& p) const {
+        pc[i] = p.pi;
         q[i] = y;
-        s[0] = fma(pi, y, s[0]);
+        s[0] = fma(p.pi, y, s[0]);
     }
+    __device__ __forceinline__ void row(int i, double y, double* s) const { row(i, y, s, pre(i)); }
     __device__ __forceinline__ void finish(PcgState* st, const double* tot) const {
         const double pap = tot[0];
         st->pap = pap;
@@ -767,12 +772,16 @@ struct OpSweep {
     const double* wd;
     double* zout;
     __device__ __forceinline__ double operator()(int j) const { return g(j); }
-    __device__ __forceinline__ void row(int i, double y, double* s) const {
-        const double ri = r[i];
-        const double zi = fma(wd[i], ri - y, g(i));
+    struct Pre {
+        double ri, wi, gi;
+    };
+    __device__ __forceinline__ Pre pre(int i) const { return Pre{r[i], wd[i], g(i)}; }
+    __device__ __forceinline__ void row(int i, double y, double* s, const Pre& p) const {
+        const double zi = fma(p.wi, p.ri - y, p.gi);
         zout[i] = zi;
-        if (RZ) s[0] = fma(ri, zi, s[0]);
+        if (RZ) s[0] = fma(p.ri, zi, s[0]);
     }
+    __device__ __forceinline__ void row(int i, double y, double* s) const { row(i, y, s, pre(i)); }
     __device__ __forceinline__ void init(const SolveArgs&) {}
     __device__ __forceinline__ void finish(PcgState* st, const double* tot) const {
         st->rz_new = tot[0];
@@ -785,10 +794,15 @@ struct OpTrueRes {
     const double* x;
     const double* b;
     __device__ __forceinline__ double operator()(int j) const { return x[j]; }
-    __device__ __forceinline__ void row(int i, double y, double* s) const {
-        const double d = b[i] - y;
+    struct Pre {
+        double bi;
+    };
+    __device__ __forceinline__ Pre pre(int i) const { return Pre{b[i]}; }
+    __device__ __forceinline__ void row(int i, double y, double* s, const Pre& p) const {
+        const double d = p.bi - y;
         s[0] = fma(d, d, s[0]);
     }
+    __device__ __forceinline__ void row(int i, double y, double* s) const { row(i, y, s, pre(i)); }
     __device__ __forceinline__ void init(const SolveArgs&) {}
     __device__ __forceinline__ void finish(PcgState* st, const double* tot) const {
         st->true_res = sqrt(tot[0]) / st->bnorm;
@@ -801,6 +815,9 @@ struct OpPlain {
     const double* x;
     double* y;
     __device__ __forceinline__ double operator()(int j) const { return x[j]; }
+    struct Pre {};
+    __device__ __forceinline__ Pre pre(int) const { return Pre{}; }
+    __device__ __forceinline__ void row(int i, double yy, double*, const Pre&) const { y[i] = yy; }
     __device__ __forceinline__ void row(int i, double yy, double*) const { y[i] = yy; }
     __device__ __forceinline__ void init(const SolveArgs&) {}
     __device__ __forceinline__ void finish(PcgState*, const double*) const {}
@@ -830,6 +847,7 @@ __global__ void __launch_bounds__(kThreads) k_spmv_dia(SolveArgs a, Op op) {
     const int n = a.n, d = a.dia.d;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const unsigned m = mask[i];
+        const typename Op::Pre pr = op.pre(i);  // own-row operands in flight with the gathers
         double g[MAXD], vv[MAXD];
 #pragma unroll
         for (int t = 0; t < MAXD; ++t) {
@@ -841,7 +859,7 @@ __global__ void __launch_bounds__(kThreads) k_spmv_dia(SolveArgs a, Op op) {
 #pragma unroll
         for (int t = 0; t < MAXD; ++t)
             if (t < d && ((m >> t) & 1u)) y = fma(RV ? vv[t] : a.dia.val[t], g[t], y);
-        op.row(i, y, s);
+        op.row(i, y, s, pr);
     }
     if constexpr (Op::NV > 0) {
         double v[Op::NV], tot[Op::NV];
