@@ -175,6 +175,29 @@ typedef struct {
 int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twolevel* m,
                      const double* b_dev, uint64_t iters, nlsp_kernel_stat* stats, int cap);
 
+/* ---- NLSS basis: MLP inference --------------------------- */
+typedef struct nlsp_mlp nlsp_mlp;
+
+/* MlpModel (mlp.hpp:47-320) on the device from its widths and flat parameter
+ * buffer in the reference's layout (nlsp_io_mlp_load / nlsp_io_mlp_init,
+ * include/nlsp_io.h). VALIDATION on fewer than 2 widths or a count mismatch. */
+nlsp_status nlsp_mlp_upload(nlsp_ctx* ctx, const uint64_t* widths, uint64_t nwidths,
+                            const double* params, uint64_t nparams, nlsp_mlp** out);
+void nlsp_mlp_destroy(nlsp_mlp* m);
+
+/* MlpModel::forward (mlp.hpp:113-161): host vectors of the input / output
+ * width; hidden layers Linear -> LayerNorm(gain, offset) -> GELU. */
+nlsp_status nlsp_mlp_forward(nlsp_ctx* ctx, const nlsp_mlp* m, const double* in, double* out);
+
+/* infer_basis(model, S) (train.hpp:52-62): Q (n x r, r = output width / n) =
+ * orthonormalize(reshape_column_major(forward(vec_colmajor(S / ||S||_F)))).
+ * The orthonormalisation is CholeskyQR2 (same Q as the reference's two-pass
+ * MGS up to rounding); RANK_DEFICIENT when a column's post-elimination norm
+ * falls below 1e-10 (orthonormalize.hpp:52-54), VALIDATION on width mismatch
+ * or ||S||_F = 0. */
+nlsp_status nlsp_mlp_infer_basis(nlsp_ctx* ctx, const nlsp_mlp* m, const nlsp_dense* s,
+                                 nlsp_dense** q_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -77,6 +77,30 @@ typedef struct {
 int nlsp_io_load_instance(const char* dir, nlsp_instance* out);
 void nlsp_io_instance_free(nlsp_instance* inst);
 
+/* MlpModel (mlp.hpp:47-320): layer widths and the flat parameter buffer in
+ * the reference's order — per layer l: W_l (fan_out x fan_in, row-major), b_l,
+ * and for hidden layers the LayerNorm gain_l, offset_l. */
+typedef struct {
+    uint64_t nwidths;
+    uint64_t* widths;
+    uint64_t nparams;
+    double* params;
+    char* manifest;  /* NUL-terminated checkpoint manifest text (may be empty) */
+} nlsp_host_mlp;
+
+/* MlpModel::load(path) (mlp.hpp:276-303): "NLSPCKP1" checkpoint; the Adam
+ * state is read past, not kept. IoError on bad magic / count / truncation. */
+int nlsp_io_mlp_load(const char* path, nlsp_host_mlp* out);
+
+/* MlpModel::save(path, manifest) (mlp.hpp:255-274) with zero Adam state. */
+int nlsp_io_mlp_save(const nlsp_host_mlp* m, const char* path);
+
+/* MlpModel(widths, seed) (mlp.hpp:57-88): the reference's seeded He
+ * initialisation (Rng(mix_seed(seed, 0x6d6c70)), bit-identical), gains 1. */
+int nlsp_io_mlp_init(const uint64_t* widths, uint64_t nwidths, uint64_t seed, nlsp_host_mlp* out);
+
+void nlsp_io_mlp_free(nlsp_host_mlp* m);
+
 /* Message of the last failed call on this thread. */
 const char* nlsp_io_last_error(void);
 

@@ -316,6 +316,10 @@ class Reference:
             "ref_mix_seed": (u64, [u64, u64]),
             "ref_save_instance": (C.c_int, [C.c_int, u64, dbl, u64, C.c_char_p]),
             "ref_aggregate_nodes": (C.c_int, [vp, dbl, Pu64, Pu64]),
+            "ref_mlp_create_save": (C.c_int, [Pu64, u64, u64, C.c_char_p]),
+            "ref_mlp_params": (C.c_int, [C.c_char_p, Pu64, Pdbl]),
+            "ref_mlp_forward": (C.c_int, [C.c_char_p, Pdbl, Pdbl]),
+            "ref_infer_basis": (C.c_int, [C.c_char_p, u64, u64, Pdbl, Pdbl, Pu64, Pdbl]),
             "ref_sa_prolongator": (C.c_int, [vp, dbl, dbl, Pu64, Pdbl]),
             "ref_load_matrix_market": (vp, [C.c_char_p, Pi32]),
             "ref_save_matrix_market": (C.c_int, [vp, C.c_char_p]),
@@ -407,6 +411,34 @@ class Reference:
         rp, ci, v = np.empty(dim + 1, np.uint64), np.empty(nnz, np.uint64), np.empty(nnz)
         self.lib.ref_csr_export(h, _u(rp), _u(ci), _d(v))
         return (dim, rp, ci, v)
+
+    # --- MLP inference (mlp.hpp, train.hpp) --------------------------------
+    def mlp_create_save(self, widths, seed, path):
+        w = np.ascontiguousarray(widths, np.uint64)
+        self._chk(self.lib.ref_mlp_create_save(_u(w), w.size, seed, str(path).encode()))
+
+    def mlp_params(self, path):
+        np_ = C.c_uint64(0)
+        self._chk(self.lib.ref_mlp_params(str(path).encode(), C.byref(np_), None))
+        out = np.empty(np_.value)
+        self._chk(self.lib.ref_mlp_params(str(path).encode(), C.byref(np_), _d(out)))
+        return out
+
+    def mlp_forward(self, path, x, out_width):
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.empty(out_width)
+        self._chk(self.lib.ref_mlp_forward(str(path).encode(), _d(x), _d(y)))
+        return y
+
+    def infer_basis(self, path, s, r):
+        """infer_basis (train.hpp:52-62) -> (q n x r, ms of the call)."""
+        s = np.ascontiguousarray(s, np.float64)
+        n, k = s.shape
+        q = np.empty((n, r))
+        rr, ms = C.c_uint64(0), C.c_double(0)
+        self._chk(self.lib.ref_infer_basis(str(path).encode(), n, k, _d(s), _d(q), C.byref(rr), C.byref(ms)))
+        assert rr.value == r
+        return q, float(ms.value)
 
     def aggregate_nodes(self, a, theta):
         """aggregate_nodes (sa.hpp:18-76): (aggregate id per node, count)."""

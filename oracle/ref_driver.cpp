@@ -46,6 +46,8 @@
 #include "nlsp/errors.hpp"
 #include "nlsp/fem.hpp"
 #include "nlsp/instance_io.hpp"
+#include "nlsp/mlp.hpp"
+#include "nlsp/train.hpp"
 #include "nlsp/qr.hpp"
 #include "nlsp/rng.hpp"
 #include "nlsp/sa.hpp"
@@ -284,6 +286,48 @@ int ref_sa_prolongator(void* h, double theta, double omega, std::uint64_t* nc, d
         const auto m = sa_prolongator(*static_cast<SparseCsrMatrix*>(h), theta, omega);
         *nc = m.cols();
         if (p) dense_to(m, p);
+    });
+}
+
+// --- MLP inference (mlp.hpp:57-161, train.hpp:52-62) -------------------------
+int ref_mlp_create_save(const std::uint64_t* widths, std::uint64_t nw, std::uint64_t seed,
+                        const char* path) {
+    return guarded([&] {
+        MlpModel m(std::vector<std::size_t>(widths, widths + nw), seed);
+        m.save(path, "created by oracle/ref_driver.cpp");
+    });
+}
+
+// parameters of a checkpoint (two-phase: params == NULL queries the count)
+int ref_mlp_params(const char* path, std::uint64_t* np, double* params) {
+    return guarded([&] {
+        const auto m = MlpModel::load(path);
+        *np = m.num_params();
+        if (params) std::copy(m.params().begin(), m.params().end(), params);
+    });
+}
+
+int ref_mlp_forward(const char* path, const double* in, double* out) {
+    return guarded([&] {
+        const auto m = MlpModel::load(path);
+        const std::vector<double> x(in, in + m.input_width());
+        const auto y = m.forward(x);
+        std::copy(y.begin(), y.end(), out);
+    });
+}
+
+// infer_basis(model, S) (train.hpp:52-62): S n x k row-major -> q n x r row-major
+int ref_infer_basis(const char* path, std::uint64_t n, std::uint64_t k, const double* s, double* q,
+                    std::uint64_t* r_out, double* ms) {
+    return guarded([&] {
+        const auto m = MlpModel::load(path);
+        const auto sm = dense_from(n, k, s);
+        const auto t0 = std::chrono::steady_clock::now();
+        const auto b = infer_basis(m, sm);
+        const auto t1 = std::chrono::steady_clock::now();
+        if (ms) *ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        *r_out = b.cols();
+        if (q) dense_to(b, q);
     });
 }
 

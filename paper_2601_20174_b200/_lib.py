@@ -98,6 +98,10 @@ GPU_SYMBOLS = [
     ("nlsp_csr_destroy", None, [vp]),
     ("nlsp_csr_dims", None, [vp, P_u64, P_u64]),
     ("nlsp_csr_format", c_i32, [vp, P_i32, P_i32, P_u64]),
+    ("nlsp_mlp_upload", c_i32, [vp, P_u64, c_u64, P_dbl, c_u64, C.POINTER(vp)]),
+    ("nlsp_mlp_destroy", None, [vp]),
+    ("nlsp_mlp_forward", c_i32, [vp, vp, P_dbl, P_dbl]),
+    ("nlsp_mlp_infer_basis", c_i32, [vp, vp, vp, C.POINTER(vp)]),
     ("nlsp_spmv", C.c_int, [vp, vp, P_dbl, P_dbl]),
     ("nlsp_spmv_device", C.c_int, [vp, vp, vp, vp]),
     ("nlsp_csr_diagonal", C.c_int, [vp, vp, P_dbl]),
@@ -162,12 +166,22 @@ class InstanceC(C.Structure):
     ]
 
 
+class HostMlpC(C.Structure):
+    """nlsp_host_mlp (include/nlsp_io.h)."""
+    _fields_ = [("nwidths", c_u64), ("widths", P_u64), ("nparams", c_u64), ("params", P_dbl),
+                ("manifest", C.c_char_p)]
+
+
 IO_SYMBOLS = [
     ("nlsp_io_load_matrix_market", C.c_int, [C.c_char_p, C.POINTER(HostCsrC)]),
     ("nlsp_io_save_matrix_market", C.c_int, [C.POINTER(HostCsrC), C.c_char_p]),
     ("nlsp_io_csr_free", None, [C.POINTER(HostCsrC)]),
     ("nlsp_io_load_instance", C.c_int, [C.c_char_p, C.POINTER(InstanceC)]),
     ("nlsp_io_instance_free", None, [C.POINTER(InstanceC)]),
+    ("nlsp_io_mlp_load", C.c_int, [C.c_char_p, C.POINTER(HostMlpC)]),
+    ("nlsp_io_mlp_save", C.c_int, [C.POINTER(HostMlpC), C.c_char_p]),
+    ("nlsp_io_mlp_init", C.c_int, [P_u64, c_u64, c_u64, C.POINTER(HostMlpC)]),
+    ("nlsp_io_mlp_free", None, [C.POINTER(HostMlpC)]),
     ("nlsp_io_last_error", C.c_char_p, []),
 ]
 

@@ -14,6 +14,8 @@
 // reference writes, instead of a comparison sort of all triplets.
 #include "nlsp_io.h"
 
+#include "host_rng.hpp"
+
 #include <algorithm>
 #include <cerrno>
 #include <cmath>
@@ -467,6 +469,123 @@ void load_instance(const std::string& dir, nlsp_instance* inst) {
     inst->alpha = inst->family == 2 ? to_double(m.get("alpha")) : 0.0;
 }
 
+// --- MlpModel checkpoints and initialisation (mlp.hpp:57-88, 255-303) -------
+uint64_t mlp_param_count(const std::vector<uint64_t>& w) {
+    if (w.size() < 2) throw ValidationError("mlp: need at least input and output widths");
+    uint64_t total = 0;
+    for (size_t l = 0; l + 1 < w.size(); ++l) {
+        total += w[l] * w[l + 1] + w[l + 1];
+        if (l + 2 < w.size()) total += 2 * w[l + 1];
+    }
+    return total;
+}
+
+void mlp_fill(nlsp_host_mlp* out, const std::vector<uint64_t>& w, uint64_t np, const std::string& manifest) {
+    out->nwidths = w.size();
+    out->widths = alloc_n<uint64_t>(w.size());
+    std::copy(w.begin(), w.end(), out->widths);
+    out->nparams = np;
+    out->params = alloc_n<double>(np);
+    out->manifest = alloc_n<char>(manifest.size() + 1);
+    std::memcpy(out->manifest, manifest.c_str(), manifest.size() + 1);
+}
+
+void mlp_load(const std::string& path, nlsp_host_mlp* out) {
+    std::string buf;
+    if (!read_file(path, buf)) throw IoError("cannot open for read: " + path);
+    size_t pos = 0;
+    bool ok = true;
+    auto get = [&](void* dst, size_t bytes) {
+        if (pos + bytes > buf.size()) {
+            ok = false;
+            const size_t have = pos < buf.size() ? buf.size() - pos : 0;
+            std::memset(dst, 0, bytes);
+            if (have) std::memcpy(dst, buf.data() + pos, have);
+            pos = buf.size();
+            return;
+        }
+        std::memcpy(dst, buf.data() + pos, bytes);
+        pos += bytes;
+    };
+    auto get_u64 = [&]() {
+        uint64_t v = 0;
+        get(&v, 8);
+        return v;
+    };
+    char magic[8] = {};
+    get(magic, 8);
+    if (!ok || std::string(magic, 8) != "NLSPCKP1") throw IoError("bad checkpoint magic: " + path);
+    const uint64_t nw = get_u64();
+    if (!ok || nw > (buf.size() / 8)) throw IoError("truncated checkpoint: " + path);
+    std::vector<uint64_t> w(nw);
+    for (auto& x : w) x = get_u64();
+    const uint64_t expect = mlp_param_count(w);  // ValidationError for < 2 widths (the ctor's)
+    const uint64_t np = get_u64();
+    if (np != expect) throw IoError("checkpoint parameter count mismatch: " + path);
+    if (np > buf.size() / 8) throw IoError("truncated checkpoint: " + path);
+    mlp_fill(out, w, np, "");
+    get(out->params, 8 * np);
+    pos += 16 * np;  // Adam m, v (not kept)
+    if (pos > buf.size()) {
+        ok = false;
+        pos = buf.size();
+    }
+    (void)get_u64();  // adam step
+    const uint64_t mlen = get_u64();
+    if (!ok || mlen > buf.size() - pos) throw IoError("truncated checkpoint: " + path);
+    std::free(out->manifest);
+    out->manifest = alloc_n<char>(mlen + 1);
+    std::memcpy(out->manifest, buf.data() + pos, mlen);
+    out->manifest[mlen] = '\0';
+}
+
+void mlp_save(const nlsp_host_mlp* m, const std::string& path) {
+    FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw IoError("cannot open for write: " + path);
+    bool ok = std::fwrite("NLSPCKP1", 1, 8, f) == 8;
+    auto put = [&](const void* p, size_t bytes) { ok = ok && std::fwrite(p, 1, bytes, f) == bytes; };
+    auto put_u64 = [&](uint64_t v) { put(&v, 8); };
+    put_u64(m->nwidths);
+    for (uint64_t l = 0; l < m->nwidths; ++l) put_u64(m->widths[l]);
+    put_u64(m->nparams);
+    put(m->params, 8 * m->nparams);
+    std::vector<double> zeros(std::min<uint64_t>(m->nparams, 1 << 20), 0.0);
+    for (int rep = 0; rep < 2; ++rep)
+        for (uint64_t done = 0; done < m->nparams;) {
+            const uint64_t c = std::min<uint64_t>(zeros.size(), m->nparams - done);
+            put(zeros.data(), 8 * c);
+            done += c;
+        }
+    put_u64(0);
+    const size_t mlen = m->manifest ? std::strlen(m->manifest) : 0;
+    put_u64(mlen);
+    if (mlen) put(m->manifest, mlen);
+    if (std::fclose(f) != 0 || !ok) throw IoError("write failed: " + path);
+}
+
+void mlp_init(const uint64_t* widths, uint64_t nw, uint64_t seed, nlsp_host_mlp* out) {
+    std::vector<uint64_t> w(widths, widths + nw);
+    const uint64_t np = mlp_param_count(w);
+    mlp_fill(out, w, np, "");
+    std::fill(out->params, out->params + np, 0.0);
+    // one Rng(mix_seed(seed, 0x6d6c70)) stream across the layers' weights, in order
+    uint64_t nweights = 0;
+    for (size_t l = 0; l + 1 < w.size(); ++l) nweights += w[l] * w[l + 1];
+    std::vector<double> z(nweights);
+    nlsp_host::normal_stream(nlsp_host::mix_seed(seed, 0x6d6c70), nweights, z.data());
+    uint64_t off = 0, zi = 0;
+    for (size_t l = 0; l + 1 < w.size(); ++l) {
+        const uint64_t fi = w[l], fo = w[l + 1];
+        const double sd = std::sqrt(2.0 / static_cast<double>(fi));
+        for (uint64_t i = 0; i < fi * fo; ++i) out->params[off + i] = 0.0 + sd * z[zi++];  // normal(0, sd)
+        off += fi * fo + fo;
+        if (l + 2 < w.size()) {
+            for (uint64_t i = 0; i < fo; ++i) out->params[off + i] = 1.0;  // gain
+            off += 2 * fo;
+        }
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -519,6 +638,44 @@ void nlsp_io_instance_free(nlsp_instance* inst) {
     inst->rhs = inst->vertices = inst->coefficients = nullptr;
     inst->boundary_mask = nullptr;
     inst->triangles = nullptr;
+}
+
+int nlsp_io_mlp_load(const char* path, nlsp_host_mlp* out) {
+    if (!path || !out) {
+        g_err = "mlp load: null argument";
+        return NLSP_IO_E_VALIDATION;
+    }
+    *out = nlsp_host_mlp{};
+    const int st = guarded([&] { mlp_load(path, out); });
+    if (st) nlsp_io_mlp_free(out);
+    return st;
+}
+
+int nlsp_io_mlp_save(const nlsp_host_mlp* m, const char* path) {
+    if (!path || !m || !m->widths || !m->params) {
+        g_err = "mlp save: null argument";
+        return NLSP_IO_E_VALIDATION;
+    }
+    return guarded([&] { mlp_save(m, path); });
+}
+
+int nlsp_io_mlp_init(const uint64_t* widths, uint64_t nwidths, uint64_t seed, nlsp_host_mlp* out) {
+    if (!widths || !out) {
+        g_err = "mlp init: null argument";
+        return NLSP_IO_E_VALIDATION;
+    }
+    *out = nlsp_host_mlp{};
+    const int st = guarded([&] { mlp_init(widths, nwidths, seed, out); });
+    if (st) nlsp_io_mlp_free(out);
+    return st;
+}
+
+void nlsp_io_mlp_free(nlsp_host_mlp* m) {
+    if (!m) return;
+    std::free(m->widths);
+    std::free(m->params);
+    std::free(m->manifest);
+    *m = nlsp_host_mlp{};
 }
 
 const char* nlsp_io_last_error(void) { return g_err.c_str(); }

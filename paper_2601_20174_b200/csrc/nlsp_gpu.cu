@@ -66,6 +66,12 @@ void launch_tri_inv_t(const LaunchCtx&, int, const double*, double*);
 void launch_symmetrize(const LaunchCtx&, int, double*);
 void launch_sigma(const LaunchCtx&, int, int, const double*, const double*, double*, double*,
                   int*);
+// mlp.cu
+int mlp_splitk_parts(const LaunchCtx&, int, int);
+void launch_mlp_layer(const LaunchCtx&, const double*, const double*, const double*, const double*,
+                      int, int, bool, const double*, double*, double*);
+void launch_mlp_input(const LaunchCtx&, int, int, const double*, double*, int, double*, int*);
+void launch_unflatten(const LaunchCtx&, int, int, const double*, double*);
 }  // namespace nlsp
 
 using namespace nlsp;
@@ -1407,3 +1413,199 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------- MLP inference (8f.4) --
+struct nlsp_mlp {
+    unsigned long long id;
+    int device;
+    std::vector<uint64_t> w;  // layer widths
+    struct Off {
+        size_t w, b, gain, offset;
+    };
+    std::vector<Off> off;
+    double* params = nullptr;
+    uint64_t np = 0;
+};
+
+nlsp_status nlsp_mlp_upload(nlsp_ctx* ctx, const uint64_t* widths, uint64_t nwidths, const double* params,
+                            uint64_t nparams, nlsp_mlp** out) {
+    if (!out) return set_err(ctx, NLSP_E_VALIDATION, "mlp: null out");
+    *out = nullptr;
+    nlsp_status st = bind(ctx);
+    if (st) return st;
+    if (!widths || !params || nwidths < 2)
+        return set_err(ctx, NLSP_E_VALIDATION, "mlp: need at least input and output widths");
+    auto* m = new nlsp_mlp();
+    m->id = g_next_id++;
+    m->device = ctx->device;
+    m->w.assign(widths, widths + nwidths);
+    size_t total = 0;
+    for (size_t l = 0; l + 1 < m->w.size(); ++l) {
+        if (m->w[l] == 0 || m->w[l + 1] == 0 || m->w[l] >= (1ull << 31) || m->w[l + 1] >= (1ull << 31)) {
+            delete m;
+            return set_err(ctx, NLSP_E_VALIDATION, "mlp: layer widths must be in [1, 2^31)");
+        }
+        nlsp_mlp::Off o{};
+        o.w = total;
+        total += m->w[l] * m->w[l + 1];
+        o.b = total;
+        total += m->w[l + 1];
+        if (l + 2 < m->w.size()) {
+            o.gain = total;
+            total += m->w[l + 1];
+            o.offset = total;
+            total += m->w[l + 1];
+        }
+        m->off.push_back(o);
+    }
+    if (total != nparams) {
+        delete m;
+        return set_err(ctx, NLSP_E_VALIDATION, "mlp: parameter count does not match the widths");
+    }
+    m->np = nparams;
+    cudaError_t e = dalloc(&m->params, nparams);
+    if (!e) e = cudaMemcpyAsync(m->params, params, nparams * 8, cudaMemcpyHostToDevice, ctx->s);
+    if (!e) e = cudaStreamSynchronize(ctx->s);
+    if (e) {
+        nlsp_mlp_destroy(m);
+        return cuda_fail(ctx, e, "mlp upload");
+    }
+    *out = m;
+    return NLSP_OK;
+}
+
+void nlsp_mlp_destroy(nlsp_mlp* m) {
+    if (!m) return;
+    cudaSetDevice(m->device);
+    dfree(m->params);
+    delete m;
+}
+
+// forward pass on device vectors; scratch from the context pool
+static nlsp_status mlp_forward_dev(nlsp_ctx* ctx, const nlsp_mlp* m, const double* x, double* y) {
+    uint64_t maxw = 0, maxs = 0;
+    const size_t L = m->w.size() - 1;
+    for (size_t l = 0; l < L; ++l) {
+        const int fi = (int)m->w[l], fo = (int)m->w[l + 1];
+        if (l + 1 < L) maxw = std::max<uint64_t>(maxw, fo);
+        uint64_t sc = fo;
+        if (fi > 4096) sc = (uint64_t)mlp_splitk_parts(ctx->lc, fi, fo) * fo;
+        maxs = std::max(maxs, sc);
+    }
+    double *a = nullptr, *b = nullptr, *scr = nullptr;
+    cudaError_t e;
+    if ((e = salloc(ctx, &a, std::max<uint64_t>(maxw, 1))) || (e = salloc(ctx, &b, std::max<uint64_t>(maxw, 1))) ||
+        (e = salloc(ctx, &scr, maxs))) {
+        sfree(ctx, a);
+        sfree(ctx, b);
+        return cuda_fail(ctx, e, "mlp scratch");
+    }
+    const double* cur = x;
+    for (size_t l = 0; l < L; ++l) {
+        const bool hidden = l + 1 < L;
+        double* dst = hidden ? ((cur == a) ? b : a) : y;
+        const auto& o = m->off[l];
+        launch_mlp_layer(ctx->lc, m->params + o.w, m->params + o.b, hidden ? m->params + o.gain : nullptr,
+                         hidden ? m->params + o.offset : nullptr, (int)m->w[l], (int)m->w[l + 1], hidden, cur,
+                         dst, scr);
+        cur = dst;
+    }
+    sfree(ctx, a);
+    sfree(ctx, b);
+    sfree(ctx, scr);
+    CU(cudaGetLastError());
+    return NLSP_OK;
+}
+
+nlsp_status nlsp_mlp_forward(nlsp_ctx* ctx, const nlsp_mlp* m, const double* in, double* out) {
+    nlsp_status st = bind(ctx);
+    if (st) return st;
+    if (!m || !in || !out) return set_err(ctx, NLSP_E_VALIDATION, "mlp forward: null argument");
+    const uint64_t wi = m->w.front(), wo = m->w.back();
+    double *x = nullptr, *y = nullptr;
+    cudaError_t e;
+    if ((e = salloc(ctx, &x, wi)) || (e = salloc(ctx, &y, wo))) {
+        sfree(ctx, x);
+        return cuda_fail(ctx, e, "mlp forward alloc");
+    }
+    CU(cudaMemcpyAsync(x, in, wi * 8, cudaMemcpyHostToDevice, ctx->s));
+    st = mlp_forward_dev(ctx, m, x, y);
+    if (!st) CU(cudaMemcpyAsync(out, y, wo * 8, cudaMemcpyDeviceToHost, ctx->s));
+    sfree(ctx, x);
+    sfree(ctx, y);
+    CU(cudaStreamSynchronize(ctx->s));
+    return st;
+}
+
+nlsp_status nlsp_mlp_infer_basis(nlsp_ctx* ctx, const nlsp_mlp* m, const nlsp_dense* s, nlsp_dense** q_out) {
+    if (!q_out) return set_err(ctx, NLSP_E_VALIDATION, "infer_basis: null out");
+    *q_out = nullptr;
+    nlsp_status st = bind(ctx);
+    if (st) return st;
+    if (!m || !s) return set_err(ctx, NLSP_E_VALIDATION, "infer_basis: null argument");
+    const uint64_t n = s->rows, K = s->cols;
+    if (n * K != m->w.front()) return set_err(ctx, NLSP_E_VALIDATION, "mlp forward: width mismatch");
+    const uint64_t r = m->w.back() / n;
+    if (r * n != m->w.back()) return set_err(ctx, NLSP_E_VALIDATION, "reshape: length mismatch");
+    if (n < r) return set_err(ctx, NLSP_E_VALIDATION, "orthonormalize: requires rows >= cols");
+    if (r > 256) return set_err(ctx, NLSP_E_VALIDATION, "infer_basis: at most 256 basis columns");
+    const int g = gram_grid(ctx->lc, (long long)n);
+    const int nparts = ctx->num_sms * 2;
+    const size_t rr = (size_t)r * r;
+    double *part = nullptr, *x = nullptr, *raw = nullptr, *P = nullptr, *G = nullptr, *gp = nullptr,
+           *Lf = nullptr, *U = nullptr, *Q1 = nullptr;
+    auto cleanup = [&]() {
+        for (double* p : {part, x, raw, P, G, gp, Lf, U, Q1}) sfree(ctx, p);
+    };
+    cudaError_t e;
+    if ((e = salloc(ctx, &part, nparts)) || (e = salloc(ctx, &x, n * K)) || (e = salloc(ctx, &raw, n * r)) ||
+        (e = salloc(ctx, &P, n * r)) || (e = salloc(ctx, &G, rr)) || (e = salloc(ctx, &gp, (size_t)g * rr)) ||
+        (e = salloc(ctx, &Lf, rr)) || (e = salloc(ctx, &U, rr)) || (e = salloc(ctx, &Q1, n * r))) {
+        cleanup();
+        return cuda_fail(ctx, e, "infer_basis alloc");
+    }
+    CU(cudaMemsetAsync(ctx->flags, 0, 16 * sizeof(int), ctx->s));
+    // x = vec(S / ||S||_F), forward, reshape (train.hpp:52-61)
+    launch_mlp_input(ctx->lc, (int)n, (int)K, s->d, part, nparts, x, ctx->flags + 11);
+    st = mlp_forward_dev(ctx, m, x, raw);
+    if (st) {
+        cleanup();
+        return st;
+    }
+    launch_unflatten(ctx->lc, (int)n, (int)r, raw, P);
+    // orthonormalize_differentiable (orthonormalize.hpp:25-59) as CholeskyQR2:
+    // the first pass's pivots are MGS's post-elimination norms (absolute 1e-10 test)
+    nlsp_dense* Q = nullptr;
+    st = dense_alloc(ctx, n, r, &Q);
+    if (st) {
+        cleanup();
+        return st;
+    }
+    launch_gram(ctx->lc, (long long)n, (int)r, (int)r, P, P, gp, G);
+    launch_chol(ctx->lc, (int)r, G, Lf, -1e-10, ctx->flags + 12);
+    launch_tri_inv_t(ctx->lc, (int)r, Lf, U);
+    launch_dense_mm(ctx->lc, (long long)n, (int)r, (int)r, P, U, nullptr, Q1);
+    launch_gram(ctx->lc, (long long)n, (int)r, (int)r, Q1, Q1, gp, G);
+    launch_chol(ctx->lc, (int)r, G, Lf, 0.0, ctx->flags + 13);
+    launch_tri_inv_t(ctx->lc, (int)r, Lf, U);
+    launch_dense_mm(ctx->lc, (long long)n, (int)r, (int)r, Q1, U, nullptr, Q->d);
+    e = cudaGetLastError();
+    if (!e) e = cudaMemcpyAsync(ctx->flags_host, ctx->flags, 16 * sizeof(int), cudaMemcpyDeviceToHost, ctx->s);
+    if (!e) e = cudaStreamSynchronize(ctx->s);
+    cleanup();
+    if (e) {
+        nlsp_dense_destroy(Q);
+        return cuda_fail(ctx, e, "infer_basis");
+    }
+    const int* f = ctx->flags_host;
+    if (f[11]) {
+        nlsp_dense_destroy(Q);
+        return set_err(ctx, NLSP_E_VALIDATION, "infer_basis: zero vector set");
+    }
+    if (f[12] || f[13]) {
+        nlsp_dense_destroy(Q);
+        return set_err(ctx, NLSP_E_RANK_DEFICIENT, "orthonormalize: a column vanished after elimination");
+    }
+    *q_out = Q;
+    return NLSP_OK;
+}

@@ -517,7 +517,9 @@ __global__ void __launch_bounds__(256) k_chol(int k, const double* __restrict__ 
         if (tid < s) red[tid] += red[tid + s];
         __syncthreads();
     }
-    const double rank_tol = rank_rel > 0.0 ? rank_rel * sqrt(fmax(red[0], 0.0)) : 0.0;
+    // rank_rel > 0: tolerance relative to sqrt(trace) (qr_thin); < 0: absolute
+    // |rank_rel| on the pivots (orthonormalize_differentiable's 1e-10 norm test)
+    const double rank_tol = rank_rel > 0.0 ? rank_rel * sqrt(fmax(red[0], 0.0)) : -rank_rel;
     if (tid == 0) fail = 0;
     __syncthreads();
     for (int idx = tid; idx < k * k; idx += nt) {
@@ -534,10 +536,10 @@ __global__ void __launch_bounds__(256) k_chol(int k, const double* __restrict__ 
             double d = A[j * k + j];
             for (int q = 0; q < j; ++q) d = fma(-L[j * k + q], L[j * k + q], d);
             if (d <= 0.0) {
-                fail = rank_rel > 0.0 ? 2 : 1;
+                fail = rank_rel != 0.0 ? 2 : 1;
             } else {
                 const double sd = sqrt(d);
-                if (rank_rel > 0.0 && sd < rank_tol) fail = 2;
+                if (rank_rel != 0.0 && sd < rank_tol) fail = 2;
                 djj = sd;
                 L[j * k + j] = sd;
             }

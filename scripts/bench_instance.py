@@ -10,9 +10,14 @@ svd_basis(rank) -> TwoLevelPreconditioner(nu1 = nu2 = 5) -> pcg(delta = 1e-6,
 Reference arm: the same calls through oracle/_ref (the unmodified reference
 headers compiled by oracle/Makefile), one core.
 
-Prints one JSON line per (arm, rank) with smooth / inference / setup / solve /
-total ms (the reference's BenchRow fields) and iterations; --reps R repeats
-and keeps the median per phase.
+With --nlss, the NLSS rows too: an (untrained) MlpModel of the default widths
+(train.hpp:28-32, seed 77, bit-identical initialisation in both arms), its
+basis from infer_basis (train.hpp:52-62) — the MLP forward on the device here,
+the reference's forward + MGS on one core there.
+
+Prints one JSON line per (arm, method, rank) with smooth / inference / setup /
+solve / total ms (the reference's BenchRow fields) and iterations; --reps R
+repeats and keeps the median per phase.
 """
 from __future__ import annotations
 
@@ -31,11 +36,20 @@ sys.path.insert(0, ROOT)
 K, S1, OMEGA, NU, DELTA = 32, 10, 0.66, 5, 1e-6
 
 
-def gpu_arm(path, ranks, reps):
+MLP_SEED = 77
+
+
+def gpu_arm(path, ranks, reps, nlss=False):
     from paper_2601_20174_b200 import instance_io as io
+    from paper_2601_20174_b200 import mlp
     from paper_2601_20174_b200 import nlsp
     ctx = nlsp.default_context()
-    rows = {r: [] for r in ranks}
+    rows = {("SVD", r): [] for r in ranks}
+    if nlss:
+        rows.update({("NLSS", r): [] for r in ranks})
+        n0 = io.load_instance(path).matrix.dim()
+        model = mlp.MlpModel.init([n0 * K] + mlp.default_hidden_widths(n0) + [n0 * K], MLP_SEED)
+        model.device(ctx)
     for rep in range(reps + 1):  # rep 0 warms module loading
         t0 = time.perf_counter()
         inst = io.load_instance(path)
@@ -45,9 +59,13 @@ def gpu_arm(path, ranks, reps):
         sv = nlsp.generate_smoothed_vectors(inst.matrix, inst.boundary_mask, K, S1, OMEGA, seed)
         ctx.synchronize()
         t_smooth = time.perf_counter() - t0
-        for r in ranks:
+        for method, r in rows:
             t0 = time.perf_counter()
-            p, _, _ = nlsp.svd_basis(sv.s, r)
+            if method == "SVD":
+                p, _, _ = nlsp.svd_basis(sv.s, r)
+            else:
+                q = mlp.infer_basis(model, sv.s)
+                p = np.ascontiguousarray(q.numpy()[:, :r])  # first_cols (dense.hpp:158-164)
             ctx.synchronize()
             t_inf = time.perf_counter() - t0
             t0 = time.perf_counter()
@@ -58,16 +76,24 @@ def gpu_arm(path, ranks, reps):
             res = nlsp.pcg(inst.matrix, inst.rhs, m, DELTA, 10 * inst.matrix.dim())
             t_solve = time.perf_counter() - t0
             if rep:
-                rows[r].append(dict(load=t_load, smooth=t_smooth, inference=t_inf, setup=t_setup,
-                                    solve=t_solve, iterations=res.report.iterations,
-                                    converged=res.report.converged))
+                rows[(method, r)].append(dict(load=t_load, smooth=t_smooth, inference=t_inf, setup=t_setup,
+                                              solve=t_solve, iterations=res.report.iterations,
+                                              converged=res.report.converged))
     return inst.matrix.dim(), rows
 
 
-def ref_arm(path, ranks, reps):
+def ref_arm(path, ranks, reps, nlss=False):
+    import tempfile
     from oracle.oracle import Reference
     ref = Reference()
-    rows = {r: [] for r in ranks}
+    rows = {("SVD", r): [] for r in ranks}
+    ckpt = None
+    if nlss:
+        rows.update({("NLSS", r): [] for r in ranks})
+        n0 = ref.load_instance(path)["matrix"][0]
+        from paper_2601_20174_b200 import mlp
+        ckpt = os.path.join(tempfile.mkdtemp(), "model.ckpt")
+        ref.mlp_create_save([n0 * K] + mlp.default_hidden_widths(n0) + [n0 * K], MLP_SEED, ckpt)
     for _ in range(reps):
         t0 = time.perf_counter()
         inst = ref.load_instance(path)
@@ -77,19 +103,25 @@ def ref_arm(path, ranks, reps):
         t0 = time.perf_counter()
         s = ref.generate_smoothed_vectors(a, inst["mask"], K, S1, OMEGA, seed)
         t_smooth = time.perf_counter() - t0
-        for r in ranks:
+        for method, r in rows:
             t0 = time.perf_counter()
-            u, _, _, _ = ref.svd(s)
+            if method == "SVD":
+                u, _, _, _ = ref.svd(s)
+                t_inf = time.perf_counter() - t0
+            else:
+                u, ms = ref.infer_basis(ckpt, s, K)  # timed inside (checkpoint load excluded)
+                t_inf = ms / 1e3
             p = np.ascontiguousarray(u[:, :r])
-            t_inf = time.perf_counter() - t0
             t0 = time.perf_counter()
             t = ref.twolevel(a, p, OMEGA, NU, NU)
             t_setup = time.perf_counter() - t0
             t0 = time.perf_counter()
             res = ref.pcg(a, inst["rhs"], 2, t, DELTA, 10 * a[0])
             t_solve = time.perf_counter() - t0
-            rows[r].append(dict(load=t_load, smooth=t_smooth, inference=t_inf, setup=t_setup,
-                                solve=t_solve, iterations=res.iterations, converged=res.converged))
+            rows[(method, r)].append(dict(load=t_load, smooth=t_smooth, inference=t_inf, setup=t_setup,
+                                          solve=t_solve, iterations=res.iterations, converged=res.converged))
+    if ckpt:
+        os.remove(ckpt)
     return a[0], rows
 
 
@@ -105,20 +137,21 @@ def main():
     ap.add_argument("--ranks", default="4,8,16,32")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--impl", choices=["gpu", "reference", "both"], default="both")
+    ap.add_argument("--nlss", action="store_true", help="also the NLSS (MLP inference) rows")
     args = ap.parse_args()
     ranks = [int(r) for r in args.ranks.split(",")]
     arms = ["gpu", "reference"] if args.impl == "both" else [args.impl]
     for arm in arms:
-        n, rows = (gpu_arm if arm == "gpu" else ref_arm)(args.instance, ranks, args.reps)
-        for r in ranks:
-            med = {k: statistics.median(x[k] for x in rows[r]) * 1e3
+        n, rows = (gpu_arm if arm == "gpu" else ref_arm)(args.instance, ranks, args.reps, args.nlss)
+        for (method, r), rr in rows.items():
+            med = {k: statistics.median(x[k] for x in rr) * 1e3
                    for k in ("load", "smooth", "inference", "setup", "solve")}
-            out = {"impl": arm, "instance": os.path.basename(args.instance), "n": n, "method": "SVD",
+            out = {"impl": arm, "instance": os.path.basename(args.instance), "n": n, "method": method,
                    "rank": r, "K": K, "s1": S1, "nu": NU, "delta": DELTA,
-                   "iterations": rows[r][-1]["iterations"], "converged": rows[r][-1]["converged"],
+                   "iterations": rr[-1]["iterations"], "converged": rr[-1]["converged"],
                    "ms": {k: round(v, 3) for k, v in med.items()},
                    "total_ms": round(med["smooth"] + med["inference"] + med["setup"] + med["solve"], 3),
-                   "reps": len(rows[r]), "cores": 1 if arm == "reference" else None}
+                   "reps": len(rr), "cores": 1 if arm == "reference" else None}
             print(json.dumps(out), flush=True)
 
 

@@ -13,6 +13,6 @@ done
 wait
 for spec in "$@"; do
   tag=${spec%%:*}
-  nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $D/variants/libnlsp_gpu_$tag.so $D/build/variants/solve_$tag.o $D/build/setup_kernels.o $D/build/setup_dmma.o $D/build/cluster_solve.o $D/build/nlsp_gpu.o -lcudart
+  nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $D/variants/libnlsp_gpu_$tag.so $D/build/variants/solve_$tag.o $D/build/setup_kernels.o $D/build/setup_dmma.o $D/build/mlp.o $D/build/cluster_solve.o $D/build/nlsp_gpu.o -lcudart
 done
 ls $D/variants
