@@ -175,6 +175,21 @@ typedef struct {
 int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twolevel* m,
                      const double* b_dev, uint64_t iters, nlsp_kernel_stat* stats, int cap);
 
+/* ---- smoothed aggregation: the SA coarse space ------------ */
+/* aggregate_nodes(a, theta) (sa.hpp:18-76) on the host CSR (reference
+ * layout): one aggregate id per node and their count. Needs no device. */
+nlsp_status nlsp_sa_aggregate(uint64_t n, uint64_t nnz, const uint64_t* row_ptr, const uint64_t* col_idx,
+                              const double* values, double theta, uint64_t* agg, uint64_t* nc);
+
+/* sa_prolongator(a, theta, omega) (sa.hpp:78-109): P = (I - omega D^-1 A) T,
+ * dense n x n_c on the device (T the normalised aggregate indicator). The
+ * aggregation runs on the host, the assembly on the device. NUMERIC for a
+ * non-positive diagonal or no aggregates. Feed P to nlsp_twolevel_build
+ * (coarse dimensions up to 2048). */
+nlsp_status nlsp_sa_prolongator(nlsp_ctx* ctx, uint64_t n, uint64_t nnz, const uint64_t* row_ptr,
+                                const uint64_t* col_idx, const double* values, double theta, double omega,
+                                nlsp_dense** p_out);
+
 /* ---- NLSS basis: MLP inference --------------------------- */
 typedef struct nlsp_mlp nlsp_mlp;
 

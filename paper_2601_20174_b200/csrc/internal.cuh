@@ -17,7 +17,11 @@ constexpr int kThreads = 256;      // CTA size of the row kernels
 constexpr int kGroup = 8;          // lanes per CSR row / basis row
 constexpr int kRowsPerWarp = 32 / kGroup;
 constexpr int kMaxGrid = 148 * 8;  // upper bound on row-kernel grids (partials sizing)
-constexpr int kMaxCoarse = 1024;   // largest supported coarse dimension k
+constexpr int kMaxCoarse = 2048;   // largest supported coarse dimension k
+constexpr int kWideK = 256;        // k above this: the wide restriction / prolongation kernels
+constexpr int kWideGrid = 144;     // CTAs of the wide restriction (partials: grid * (k + 1))
+// c = W1^T r of the wide path lives at the tail of the partials buffer
+constexpr long long kWideCOffset = (long long)kMaxGrid * 256 - (kMaxCoarse + 8);
 
 enum DevError : int {
     kErrNone = 0,

@@ -66,6 +66,9 @@ void launch_tri_inv_t(const LaunchCtx&, int, const double*, double*);
 void launch_symmetrize(const LaunchCtx&, int, double*);
 void launch_sigma(const LaunchCtx&, int, int, const double*, const double*, double*, double*,
                   int*);
+// setup_kernels.cu (SA)
+void launch_sa_assemble(const LaunchCtx&, int, int, const int*, const int*, const double*, const int*,
+                        const double*, const double*, double, double*);
 // mlp.cu
 int mlp_splitk_parts(const LaunchCtx&, int, int);
 void launch_mlp_layer(const LaunchCtx&, const double*, const double*, const double*, const double*,
@@ -253,6 +256,9 @@ void sfree(nlsp_ctx* c, void* p) {
     if (p) cudaFreeAsync(p, c->s);
 }
 
+// per-CTA partial size of launch_gram: it tiles C in blocks of <= 128 x 128
+size_t gram_tile(int ca, int cb) { return (size_t)std::min(ca, 128) * (size_t)std::min(cb, 128); }
+
 nlsp_status bind(nlsp_ctx* ctx) {
     if (!ctx) return NLSP_E_VALIDATION;
     CU(cudaSetDevice(ctx->device));
@@ -309,7 +315,7 @@ SolveArgs make_args(nlsp_ctx* c, const nlsp_csr* a, const nlsp_twolevel* m) {
     s.wd = m ? m->wd : nullptr;
     s.P = m ? m->basis : nullptr;
     s.L = m ? m->L : nullptr;
-    s.Ainv = (m && c->coarse_inverse) ? m->Ainv : nullptr;
+    s.Ainv = (m && (c->coarse_inverse || m->k > kWideK)) ? m->Ainv : nullptr;
     s.W1 = m ? m->W1 : nullptr;
     s.W2 = m ? m->W2 : nullptr;
     s.k = m ? m->k : 0;
@@ -1036,7 +1042,7 @@ nlsp_status nlsp_svd_basis(nlsp_ctx* ctx, const nlsp_dense* s, uint64_t k, nlsp_
     };
     cudaError_t e;
     const size_t mm = (size_t)m * m;
-    if ((e = salloc(ctx, &part, (size_t)g * mm)) || (e = salloc(ctx, &G, mm)) || (e = salloc(ctx, &ev, m)) ||
+    if ((e = salloc(ctx, &part, (size_t)g * gram_tile(m, m))) || (e = salloc(ctx, &G, mm)) || (e = salloc(ctx, &ev, m)) ||
         (e = salloc(ctx, &V, mm)) || (e = salloc(ctx, &sa, mm)) || (e = salloc(ctx, &sv, mm)) ||
         (e = salloc(ctx, &sig, m)) || (e = salloc(ctx, &W, (size_t)m * k)) ||
         (e = salloc(ctx, &pmag, (size_t)ctx->num_sms * kColsignPerSm * k)) ||
@@ -1108,7 +1114,8 @@ nlsp_status nlsp_twolevel_build(nlsp_ctx* ctx, const nlsp_csr* a, const nlsp_den
         return set_err(ctx, NLSP_E_VALIDATION, "two-level: basis row count must match matrix dimension");
     const int k = (int)basis->cols;
     const long long n = a->n;
-    if (k > 256) return set_err(ctx, NLSP_E_VALIDATION, "two-level: coarse dimension above 256 unsupported");
+    if (k > kMaxCoarse)
+        return set_err(ctx, NLSP_E_VALIDATION, "two-level: coarse dimension above 2048 unsupported");
     if ((long long)k > n) return set_err(ctx, NLSP_E_VALIDATION, "qr_thin: requires rows >= cols");
     auto* m = new nlsp_twolevel();
     m->id = g_next_id++;
@@ -1121,7 +1128,8 @@ nlsp_status nlsp_twolevel_build(nlsp_ctx* ctx, const nlsp_csr* a, const nlsp_den
     m->omega = omega;
     {
         const char* cyc = std::getenv("NLSP_CYCLE");
-        m->folded = !(cyc && std::strcmp(cyc, "literal") == 0);
+        // wide coarse spaces (k > 256) run the folded cycle only
+        m->folded = !(cyc && std::strcmp(cyc, "literal") == 0) || k > kWideK;
     }
     const size_t kk = (size_t)k * k;
     const int g = gram_grid(ctx->lc, n);
@@ -1137,7 +1145,7 @@ nlsp_status nlsp_twolevel_build(nlsp_ctx* ctx, const nlsp_csr* a, const nlsp_den
     cudaError_t e;
     if ((e = dalloc(&m->basis, (size_t)n * m->ld)) || (e = dalloc(&m->L, kk)) ||
         (e = dalloc(&m->Ainv, kk)) || (e = dalloc(&m->coarse, kk)) || (e = dalloc(&m->wd, n)) ||
-        (e = salloc(ctx, &part, (size_t)g * kk)) || (e = salloc(ctx, &G, kk)) || (e = salloc(ctx, &U, kk)) ||
+        (e = salloc(ctx, &part, (size_t)g * gram_tile(k, k))) || (e = salloc(ctx, &G, kk)) || (e = salloc(ctx, &U, kk)) ||
         (e = salloc(ctx, &Q1, (size_t)n * k)) || (e = salloc(ctx, &Q, (size_t)n * k)) ||
         (e = salloc(ctx, &Y, (size_t)n * k)))
         return fail_cuda(e, "two-level alloc");
@@ -1559,7 +1567,7 @@ nlsp_status nlsp_mlp_infer_basis(nlsp_ctx* ctx, const nlsp_mlp* m, const nlsp_de
     };
     cudaError_t e;
     if ((e = salloc(ctx, &part, nparts)) || (e = salloc(ctx, &x, n * K)) || (e = salloc(ctx, &raw, n * r)) ||
-        (e = salloc(ctx, &P, n * r)) || (e = salloc(ctx, &G, rr)) || (e = salloc(ctx, &gp, (size_t)g * rr)) ||
+        (e = salloc(ctx, &P, n * r)) || (e = salloc(ctx, &G, rr)) || (e = salloc(ctx, &gp, (size_t)g * gram_tile((int)r, (int)r))) ||
         (e = salloc(ctx, &Lf, rr)) || (e = salloc(ctx, &U, rr)) || (e = salloc(ctx, &Q1, n * r))) {
         cleanup();
         return cuda_fail(ctx, e, "infer_basis alloc");
@@ -1607,5 +1615,161 @@ nlsp_status nlsp_mlp_infer_basis(nlsp_ctx* ctx, const nlsp_mlp* m, const nlsp_de
         return set_err(ctx, NLSP_E_RANK_DEFICIENT, "orthonormalize: a column vanished after elimination");
     }
     *q_out = Q;
+    return NLSP_OK;
+}
+
+// ------------------------------------------------- smoothed aggregation (8f.3) --
+// aggregate_nodes (sa.hpp:18-76), restated on the host: the greedy passes are
+// sequential by construction (each pass reads the ids it has just assigned).
+static void sa_aggregate_host(uint64_t n, const uint64_t* rp, const uint64_t* ci, const double* v,
+                              double theta, std::vector<uint64_t>& agg, uint64_t& nc) {
+    const uint64_t kUnset = ~0ull;
+    std::vector<double> diag(n, 0.0);
+    for (uint64_t i = 0; i < n; ++i)
+        for (uint64_t k = rp[i]; k < rp[i + 1]; ++k)
+            if (ci[k] == i) {
+                diag[i] = v[k];
+                break;
+            }
+    std::vector<uint64_t> sstart(n + 1, 0), strong;
+    strong.reserve(rp[n]);
+    for (uint64_t i = 0; i < n; ++i) {
+        sstart[i] = strong.size();
+        for (uint64_t k = rp[i]; k < rp[i + 1]; ++k) {
+            const uint64_t j = ci[k];
+            if (j == i) continue;
+            if (std::abs(v[k]) >= theta * std::sqrt(std::abs(diag[i] * diag[j]))) strong.push_back(j);
+        }
+    }
+    sstart[n] = strong.size();
+    agg.assign(n, kUnset);
+    uint64_t next = 0;
+    for (uint64_t i = 0; i < n; ++i) {  // pass 1: seeds with untouched strong neighbourhoods
+        if (agg[i] != kUnset || sstart[i] == sstart[i + 1]) continue;
+        bool touched = false;
+        for (uint64_t s2 = sstart[i]; s2 < sstart[i + 1]; ++s2)
+            if (agg[strong[s2]] != kUnset) {
+                touched = true;
+                break;
+            }
+        if (touched) continue;
+        agg[i] = next;
+        for (uint64_t s2 = sstart[i]; s2 < sstart[i + 1]; ++s2) agg[strong[s2]] = next;
+        ++next;
+    }
+    for (uint64_t i = 0; i < n; ++i) {  // pass 2: strongest neighbouring aggregate
+        if (agg[i] != kUnset) continue;
+        double best = -1.0;
+        uint64_t best_agg = kUnset;
+        for (uint64_t k = rp[i]; k < rp[i + 1]; ++k) {
+            const uint64_t j = ci[k];
+            if (j == i || agg[j] == kUnset) continue;
+            bool is_strong = false;
+            for (uint64_t s2 = sstart[i]; s2 < sstart[i + 1]; ++s2)
+                if (strong[s2] == j) {
+                    is_strong = true;
+                    break;
+                }
+            if (!is_strong) continue;
+            if (std::abs(v[k]) > best) {
+                best = std::abs(v[k]);
+                best_agg = agg[j];
+            }
+        }
+        if (best_agg != kUnset) agg[i] = best_agg;
+    }
+    for (uint64_t i = 0; i < n; ++i) {  // pass 3: the rest
+        if (agg[i] != kUnset) continue;
+        agg[i] = next;
+        for (uint64_t s2 = sstart[i]; s2 < sstart[i + 1]; ++s2)
+            if (agg[strong[s2]] == kUnset) agg[strong[s2]] = next;
+        ++next;
+    }
+    nc = next;
+}
+
+nlsp_status nlsp_sa_aggregate(uint64_t n, uint64_t nnz, const uint64_t* row_ptr, const uint64_t* col_idx,
+                              const double* values, double theta, uint64_t* agg, uint64_t* nc) {
+    if (!row_ptr || !agg || !nc || (nnz && (!col_idx || !values))) return NLSP_E_VALIDATION;
+    if (row_ptr[0] != 0 || row_ptr[n] != nnz) return NLSP_E_VALIDATION;
+    std::vector<uint64_t> a;
+    uint64_t c = 0;
+    sa_aggregate_host(n, row_ptr, col_idx, values, theta, a, c);
+    std::copy(a.begin(), a.end(), agg);
+    *nc = c;
+    return NLSP_OK;
+}
+
+nlsp_status nlsp_sa_prolongator(nlsp_ctx* ctx, uint64_t n, uint64_t nnz, const uint64_t* row_ptr,
+                                const uint64_t* col_idx, const double* values, double theta, double omega,
+                                nlsp_dense** p_out) {
+    if (!p_out) return set_err(ctx, NLSP_E_VALIDATION, "sa_prolongator: null out");
+    *p_out = nullptr;
+    nlsp_status st = bind(ctx);
+    if (st) return st;
+    if (!row_ptr || (nnz && (!col_idx || !values)) || row_ptr[0] != 0 || row_ptr[n] != nnz)
+        return set_err(ctx, NLSP_E_VALIDATION, "sa_prolongator: bad CSR arrays");
+    if (n >= (1ull << 31) || nnz >= (1ull << 31))
+        return set_err(ctx, NLSP_E_VALIDATION, "sa_prolongator: n and nnz must be < 2^31");
+    for (uint64_t k = 0; k < nnz; ++k)
+        if (col_idx[k] >= n) return set_err(ctx, NLSP_E_VALIDATION, "sa_prolongator: column index out of range");
+    std::vector<uint64_t> agg;
+    uint64_t nc = 0;
+    sa_aggregate_host(n, row_ptr, col_idx, values, theta, agg, nc);
+    if (nc == 0) return set_err(ctx, NLSP_E_NUMERIC, "sa_prolongator: no aggregates formed");
+    // t_c = 1 / sqrt(|aggregate c|); A_ii > 0 (sa.hpp:84-99)
+    std::vector<uint64_t> size(nc, 0);
+    for (uint64_t i = 0; i < n; ++i) ++size[agg[i]];
+    std::vector<double> tval(nc), diag(n, 0.0);
+    for (uint64_t c = 0; c < nc; ++c) tval[c] = 1.0 / std::sqrt(static_cast<double>(size[c]));
+    std::vector<int> rp32(n + 1), ci32(std::max<uint64_t>(nnz, 1)), agg32(n);
+    for (uint64_t i = 0; i <= n; ++i) rp32[i] = (int)row_ptr[i];
+    for (uint64_t k = 0; k < nnz; ++k) ci32[k] = (int)col_idx[k];
+    for (uint64_t i = 0; i < n; ++i) {
+        agg32[i] = (int)agg[i];
+        for (uint64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k)
+            if (col_idx[k] == i) {
+                diag[i] = values[k];
+                break;
+            }
+        if (diag[i] <= 0.0) return set_err(ctx, NLSP_E_NUMERIC, "sa_prolongator: non-positive diagonal");
+    }
+    nlsp_dense* P = nullptr;
+    st = dense_alloc(ctx, n, nc, &P);
+    if (st) return st;
+    int *drp = nullptr, *dci = nullptr, *dagg = nullptr;
+    double *dv = nullptr, *dt = nullptr, *dd = nullptr;
+    auto cleanup = [&]() {
+        sfree(ctx, drp);
+        sfree(ctx, dci);
+        sfree(ctx, dagg);
+        sfree(ctx, dv);
+        sfree(ctx, dt);
+        sfree(ctx, dd);
+    };
+    cudaError_t e;
+    if ((e = salloc(ctx, &drp, n + 1)) || (e = salloc(ctx, &dci, std::max<uint64_t>(nnz, 1))) ||
+        (e = salloc(ctx, &dagg, n)) || (e = salloc(ctx, &dv, std::max<uint64_t>(nnz, 1))) ||
+        (e = salloc(ctx, &dt, nc)) || (e = salloc(ctx, &dd, n)) ||
+        (e = cudaMemcpyAsync(drp, rp32.data(), (n + 1) * 4, cudaMemcpyHostToDevice, ctx->s)) ||
+        (nnz && (e = cudaMemcpyAsync(dci, ci32.data(), nnz * 4, cudaMemcpyHostToDevice, ctx->s))) ||
+        (nnz && (e = cudaMemcpyAsync(dv, values, nnz * 8, cudaMemcpyHostToDevice, ctx->s))) ||
+        (e = cudaMemcpyAsync(dagg, agg32.data(), n * 4, cudaMemcpyHostToDevice, ctx->s)) ||
+        (e = cudaMemcpyAsync(dt, tval.data(), nc * 8, cudaMemcpyHostToDevice, ctx->s)) ||
+        (e = cudaMemcpyAsync(dd, diag.data(), n * 8, cudaMemcpyHostToDevice, ctx->s)) ||
+        (e = cudaMemsetAsync(P->d, 0, n * nc * 8, ctx->s))) {
+        cleanup();
+        nlsp_dense_destroy(P);
+        return cuda_fail(ctx, e, "sa_prolongator upload");
+    }
+    launch_sa_assemble(ctx->lc, (int)n, (int)nc, drp, dci, dv, dagg, dt, dd, omega, P->d);
+    e = cudaGetLastError();
+    cleanup();
+    if (!e) e = cudaStreamSynchronize(ctx->s);
+    if (e) {
+        nlsp_dense_destroy(P);
+        return cuda_fail(ctx, e, "sa_prolongator");
+    }
+    *p_out = P;
     return NLSP_OK;
 }

@@ -377,26 +377,28 @@ __global__ void __launch_bounds__(256) k_dense_mm(long long rows, int m, int kou
     const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
     for (long long row = wid; row < rows; row += nw) {
         const double* xr = X + row * m;
-        double acc[T];
+        for (int c0 = 0; c0 < kout; c0 += 32 * T) {  // column blocks (kout > 32 T)
+            double acc[T];
 #pragma unroll
-        for (int t = 0; t < T; ++t) acc[t] = 0.0;
-        for (int l0 = 0; l0 < m; l0 += 32) {
-            const double xl = (l0 + lane < m) ? xr[l0 + lane] : 0.0;
-            const int lim = min(32, m - l0);
-            for (int u = 0; u < lim; ++u) {
-                const double s = __shfl_sync(0xffffffffu, xl, u);
-                const double* wr = W + (long long)(l0 + u) * kout;
+            for (int t = 0; t < T; ++t) acc[t] = 0.0;
+            for (int l0 = 0; l0 < m; l0 += 32) {
+                const double xl = (l0 + lane < m) ? xr[l0 + lane] : 0.0;
+                const int lim = min(32, m - l0);
+                for (int u = 0; u < lim; ++u) {
+                    const double s = __shfl_sync(0xffffffffu, xl, u);
+                    const double* wr = W + (long long)(l0 + u) * kout;
 #pragma unroll
-                for (int t = 0; t < T; ++t) {
-                    const int j = lane + 32 * t;
-                    if (j < kout) acc[t] = fma(s, wr[j], acc[t]);
+                    for (int t = 0; t < T; ++t) {
+                        const int j = c0 + lane + 32 * t;
+                        if (j < kout) acc[t] = fma(s, wr[j], acc[t]);
+                    }
                 }
             }
-        }
 #pragma unroll
-        for (int t = 0; t < T; ++t) {
-            const int j = lane + 32 * t;
-            if (j < kout) Y[row * kout + j] = sigma ? acc[t] / sigma[j] : acc[t];
+            for (int t = 0; t < T; ++t) {
+                const int j = c0 + lane + 32 * t;
+                if (j < kout) Y[row * kout + j] = sigma ? acc[t] / sigma[j] : acc[t];
+            }
         }
     }
 }
@@ -483,6 +485,27 @@ __global__ void k_colscale(long long rows, int k, double* P, const double* sign)
     if (sub >= tpc || !(sign[j] < 0.0)) return;
     const long long step = (long long)gridDim.x * tpc;
     for (long long i = (long long)blockIdx.x * tpc + sub; i < rows; i += step) P[i * k + j] = -P[i * k + j];
+}
+
+// ----------------------------------------------------- smoothed aggregation --
+// P = (I - omega D^-1 A) T (sa.hpp:78-109): row i starts at T(i, agg_i) and
+// subtracts (omega / A_ii) a_ij T(j, agg_j) in the row's CSR order, contracted
+// like the reference's default build (p(i, col) -= scaled * t(j, col)).
+__global__ void k_sa_assemble(int n, int nc, const int* __restrict__ rp, const int* __restrict__ ci,
+                              const double* __restrict__ v, const int* __restrict__ agg,
+                              const double* __restrict__ tval, const double* __restrict__ diag,
+                              double omega, double* __restrict__ P) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        double* row = P + i * nc;
+        row[agg[i]] = tval[agg[i]];
+        const double w = omega / diag[i];
+        for (int k = rp[i]; k < rp[i + 1]; ++k) {
+            const int col = agg[ci[k]];
+            const double scaled = w * v[k];
+            row[col] = fma(-scaled, tval[col], row[col]);
+        }
+    }
 }
 
 // ------------------------------------------------------- small k x k ops --
@@ -784,6 +807,12 @@ void launch_colsign(const LaunchCtx& c, long long rows, int k, double* P, double
     k_colsign_final<<<1, 256, 0, c.s>>>(g, k, pmag, pidx_buf, pval, sign);
     count(c);
     k_colscale<<<grid_for(c, rows, 256 / k, 8), 256, 0, c.s>>>(rows, k, P, sign);
+    count(c);
+}
+
+void launch_sa_assemble(const LaunchCtx& c, int n, int nc, const int* rp, const int* ci, const double* v,
+                        const int* agg, const double* tval, const double* diag, double omega, double* P) {
+    k_sa_assemble<<<grid_for(c, n, 128), 128, 0, c.s>>>(n, nc, rp, ci, v, agg, tval, diag, omega, P);
     count(c);
 }
 

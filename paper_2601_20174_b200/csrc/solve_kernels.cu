@@ -1198,6 +1198,163 @@ __global__ void __launch_bounds__(kTmaThreads) k_update_restrict_tma(SolveArgs a
     restrict_finish<PPL, kTmaThreads, UPDATE>(acc, rr, a);
 }
 
+// ================================================ wide coarse spaces (k > 256) ==
+// Coarse dimensions beyond the 8-lane register tiles (e.g. the SA prolongator's
+// emergent n_c, sa.hpp:78-109). Same arithmetic as the narrow kernels; the
+// coarse solve runs as its own multi-CTA mat-vec with A_c^-1.
+
+// x += alpha p, r -= alpha q, ||r||^2, c = W1^T r_new (UPDATE) or c = W1^T r.
+// Each CTA walks a contiguous row chunk; warp 0 forms 32 residuals at a time,
+// every thread accumulates columns tid + 256 t over them (coalesced W1 rows).
+// Last CTA: fixed-order sum of the partials into c, history + convergence.
+template <bool UPDATE>
+__global__ void __launch_bounds__(kThreads) k_update_restrict_wide(SolveArgs a) {
+    constexpr int KT = kMaxCoarse / kThreads;  // accumulators per thread
+    PcgState* st = a.st;
+    if (st->done) return;
+    const int ld = a.k + (a.k & 1);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ double rn_s[32];
+    __shared__ double red_s[kThreads / 32];
+    __shared__ int is_last;
+    const double alpha = UPDATE ? st->alpha : 0.0;
+    const double* p = (st->it & 1) ? a.p1 : a.p0;
+    const long long chunk = ((long long)a.n + gridDim.x - 1) / gridDim.x;
+    const long long r0 = blockIdx.x * chunk, r1 = min((long long)a.n, r0 + chunk);
+    double acc[KT];
+#pragma unroll
+    for (int t = 0; t < KT; ++t) acc[t] = 0.0;
+    double rr = 0.0;
+    for (long long base = r0; base < r1; base += 32) {
+        const int rows = (int)min(32LL, r1 - base);
+        if (warp == 0) {
+            double rnew = 0.0;
+            if (lane < rows) {
+                const long long i = base + lane;
+                if (UPDATE) {
+                    rnew = fma(-alpha, a.q[i], a.r[i]);
+                    a.x[i] = fma(alpha, p[i], a.x[i]);
+                    a.r[i] = rnew;
+                    rr = fma(rnew, rnew, rr);
+                } else {
+                    rnew = a.r[i];
+                }
+            }
+            rn_s[lane] = rnew;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int ii = 0; ii < rows; ++ii) {
+            const double rv = rn_s[ii];
+            const double* w = a.W1 + (base + ii) * ld;
+#pragma unroll
+            for (int t = 0; t < KT; ++t) {
+                const int j = tid + kThreads * t;
+                if (j < ld) acc[t] = fma(__ldcs(w + j), rv, acc[t]);
+            }
+        }
+        __syncthreads();
+    }
+    // CTA partial: ld columns (+ ||r||^2) -> partials[blockIdx * (ld + 1) + .]
+    double* part = a.partials + (long long)blockIdx.x * (ld + 1);
+#pragma unroll
+    for (int t = 0; t < KT; ++t) {
+        const int j = tid + kThreads * t;
+        if (j < ld) part[j] = acc[t];
+    }
+    if (UPDATE) {
+        rr = warp_sum(rr);
+        if (tid == 0) part[ld] = rr;  // warp 0 holds every ||r||^2 term
+    }
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        const unsigned int tk = atomicAdd(&st->counter[kTkRestrict], 1u);
+        is_last = (tk == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    double* c = a.partials + kWideCOffset;
+    for (int j = tid; j < ld + (UPDATE ? 1 : 0); j += kThreads) {
+        double t = 0.0;
+        for (int b = 0; b < (int)gridDim.x; ++b) t += __ldcg(a.partials + (long long)b * (ld + 1) + j);
+        c[j] = t;
+        if (UPDATE && j == ld) red_s[0] = t;
+    }
+    __syncthreads();
+    if (UPDATE && tid == 0) {
+        const double rrt = red_s[0];
+        const double rel = sqrt(rrt) / st->bnorm;
+        st->rr = rrt;
+        st->last_rel = rel;
+        a.hist[st->it] = rel;
+        st->iterations = st->it + 1;
+        if (rel < st->delta) {
+            st->converged = 1;
+            st->done = 1;
+        }
+    }
+    if (tid == 0) st->counter[kTkRestrict] = 0u;
+}
+
+// e = A_c^-1 c (two_level.hpp:73): a warp per output row
+__global__ void __launch_bounds__(kThreads) k_coarse_gemv(SolveArgs a, int skip_done) {
+    if (skip_done && a.st->done) return;
+    const int k = a.k, lane = threadIdx.x & 31;
+    const double* c = a.partials + kWideCOffset;
+    const long long warps = (long long)gridDim.x * (kThreads / 32);
+    for (long long i = blockIdx.x * (long long)(kThreads / 32) + (threadIdx.x >> 5); i < k; i += warps) {
+        const double* row = a.Ainv + i * k;
+        double s = 0.0;
+        for (int j = lane; j < k; j += 32) s = fma(__ldg(row + j), __ldcg(c + j), s);
+        s = warp_sum(s);
+        if (lane == 0) a.e[i] = s;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (k & 1)) a.e[k] = 0.0;  // padded column
+}
+
+// z = z_pre + W2 e (two_level.hpp:74-78), r.z; ctl: loop control as k_prolong
+template <int ZMODE, bool RZ>
+__global__ void __launch_bounds__(kThreads) k_prolong_wide(SolveArgs a, const double* zpre, double* zout,
+                                                         cudaGraphConditionalHandle h, int ctl) {
+    PcgState* st = a.st;
+    if (st->done) {
+        if (ctl && blockIdx.x == 0 && threadIdx.x == 0) loop_ctl_body(st, h, ctl == 2);
+        return;
+    }
+    __shared__ double es[kMaxCoarse + 2];
+    const int ld = a.k + (a.k & 1);
+    for (int j = threadIdx.x; j < ld; j += kThreads) es[j] = a.e[j];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    double s[1] = {0.0};
+    const long long warps = (long long)gridDim.x * (kThreads / 32);
+    for (long long i = blockIdx.x * (long long)(kThreads / 32) + (threadIdx.x >> 5); i < a.n; i += warps) {
+        double zp;
+        if (ZMODE == 0) zp = 0.0;
+        else if (ZMODE == 1) zp = a.wd[i] * a.r[i];
+        else zp = zpre[i];
+        const double ri = RZ ? a.r[i] : 0.0;
+        const double* w = a.P + i * ld;
+        double acc = 0.0;
+        for (int j = lane; j < ld; j += 32) acc = fma(__ldcs(w + j), es[j], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) {
+            const double zi = zp + acc;
+            zout[i] = zi;
+            if (RZ) s[0] = fma(ri, zi, s[0]);
+        }
+    }
+    if (RZ) {
+        double tot[1];
+        if (grid_reduce<1>(s, a.partials, &st->counter[kTkProlong], tot) && threadIdx.x == 0) {
+            st->rz_new = tot[0];
+            if (ctl) loop_ctl_body(st, h, ctl == 2);
+        }
+    }
+}
+
 // ======================================================== host launchers ==
 
 namespace {
@@ -1463,6 +1620,15 @@ void launch_restrict(const LaunchCtx& c, const SolveArgs& a, int zmode, const do
 // ctl: 0 plain, 1 / 2 also the loop control of k_loop_ctl (2: graph WHILE body)
 void launch_prolong(const LaunchCtx& c, const SolveArgs& a, int zmode, bool rz, const double* zpre,
                     double* zout, cudaGraphConditionalHandle h = 0, int ctl = 0) {
+    if (a.k > kWideK) {
+#define NLSP_PW(Z, R) launch_rows<1>(c, k_prolong_wide<Z, R>, (long long)a.n * 8, a, zpre, zout, h, ctl)
+        if (zmode == 0) { if (rz) NLSP_PW(0, true); else NLSP_PW(0, false); }
+        else if (zmode == 1) { if (rz) NLSP_PW(1, true); else NLSP_PW(1, false); }
+        else { if (rz) NLSP_PW(2, true); else NLSP_PW(2, false); }
+#undef NLSP_PW
+        count(c);
+        return;
+    }
 #define CALL(P) prolong_ppl<P>(c, a, zmode, rz, zpre, zout, h, ctl)
     NLSP_PPL_SWITCH(ppl_for(a.k), CALL)
 #undef CALL
@@ -1576,6 +1742,19 @@ static void update_restrict_ppl(const LaunchCtx& c, const SolveArgs& a, bool upd
 // update = true: x/r update + ||r|| + convergence + c = W1^T r + coarse solve;
 // update = false: c = W1^T r + coarse solve
 void launch_update_restrict(const LaunchCtx& c, const SolveArgs& a, bool update) {
+    if (a.k > kWideK) {
+        // c = W1^T r (+ the x / r update and convergence test), then e = A_c^-1 c
+        long long g = (long long)c.num_sms;
+        if (g > kWideGrid) g = kWideGrid;
+        const long long need = ((long long)a.n + 31) / 32;
+        if (g > need) g = need;
+        if (update) k_update_restrict_wide<true><<<(int)g, kThreads, 0, c.s>>>(a);
+        else k_update_restrict_wide<false><<<(int)g, kThreads, 0, c.s>>>(a);
+        count(c);
+        k_coarse_gemv<<<(a.k + 7) / 8, kThreads, 0, c.s>>>(a, update ? 1 : 0);
+        count(c);
+        return;
+    }
 #define CALL(P) update_restrict_ppl<P>(c, a, update)
     NLSP_PPL_SWITCH(ppl_for(a.k), CALL)
 #undef CALL

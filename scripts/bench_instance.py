@@ -15,6 +15,11 @@ With --nlss, the NLSS rows too: an (untrained) MlpModel of the default widths
 basis from infer_basis (train.hpp:52-62) — the MLP forward on the device here,
 the reference's forward + MGS on one core there.
 
+With --sa, the SA row too (pipeline.hpp:316-317: sa_prolongator(A, 0.25, 0.66),
+its emergent coarse dimension n_c — 2 009 at N = 64 — through the wide
+kernels). The reference's SA constructor (dense MGS of n x n_c) takes minutes
+at N = 64, so its arm runs SA only for n <= 1089 unless --sa-ref.
+
 Prints one JSON line per (arm, method, rank) with smooth / inference / setup /
 solve / total ms (the reference's BenchRow fields) and iterations; --reps R
 repeats and keeps the median per phase.
@@ -39,12 +44,15 @@ K, S1, OMEGA, NU, DELTA = 32, 10, 0.66, 5, 1e-6
 MLP_SEED = 77
 
 
-def gpu_arm(path, ranks, reps, nlss=False):
+def gpu_arm(path, ranks, reps, nlss=False, with_sa=False):
     from paper_2601_20174_b200 import instance_io as io
     from paper_2601_20174_b200 import mlp
     from paper_2601_20174_b200 import nlsp
+    from paper_2601_20174_b200 import sa
     ctx = nlsp.default_context()
     rows = {("SVD", r): [] for r in ranks}
+    if with_sa:
+        rows[("SA", 0)] = []
     if nlss:
         rows.update({("NLSS", r): [] for r in ranks})
         n0 = io.load_instance(path).matrix.dim()
@@ -63,6 +71,8 @@ def gpu_arm(path, ranks, reps, nlss=False):
             t0 = time.perf_counter()
             if method == "SVD":
                 p, _, _ = nlsp.svd_basis(sv.s, r)
+            elif method == "SA":
+                p = sa.sa_prolongator(inst.matrix, 0.25, OMEGA)
             else:
                 q = mlp.infer_basis(model, sv.s)
                 p = np.ascontiguousarray(q.numpy()[:, :r])  # first_cols (dense.hpp:158-164)
@@ -76,17 +86,20 @@ def gpu_arm(path, ranks, reps, nlss=False):
             res = nlsp.pcg(inst.matrix, inst.rhs, m, DELTA, 10 * inst.matrix.dim())
             t_solve = time.perf_counter() - t0
             if rep:
-                rows[(method, r)].append(dict(load=t_load, smooth=t_smooth, inference=t_inf, setup=t_setup,
-                                              solve=t_solve, iterations=res.report.iterations,
-                                              converged=res.report.converged))
+                rows[(method, r)].append(dict(load=t_load, smooth=0.0 if method == "SA" else t_smooth,
+                                              inference=t_inf, setup=t_setup, solve=t_solve,
+                                              iterations=res.report.iterations,
+                                              converged=res.report.converged, coarse_dim=m.coarse_dim()))
     return inst.matrix.dim(), rows
 
 
-def ref_arm(path, ranks, reps, nlss=False):
+def ref_arm(path, ranks, reps, nlss=False, with_sa=False):
     import tempfile
     from oracle.oracle import Reference
     ref = Reference()
     rows = {("SVD", r): [] for r in ranks}
+    if with_sa:
+        rows[("SA", 0)] = []
     ckpt = None
     if nlss:
         rows.update({("NLSS", r): [] for r in ranks})
@@ -103,10 +116,14 @@ def ref_arm(path, ranks, reps, nlss=False):
         t0 = time.perf_counter()
         s = ref.generate_smoothed_vectors(a, inst["mask"], K, S1, OMEGA, seed)
         t_smooth = time.perf_counter() - t0
-        for method, r in rows:
+        for method, r in list(rows):
             t0 = time.perf_counter()
             if method == "SVD":
                 u, _, _, _ = ref.svd(s)
+                t_inf = time.perf_counter() - t0
+            elif method == "SA":
+                u = ref.sa_prolongator(a, 0.25, OMEGA)
+                r = u.shape[1]
                 t_inf = time.perf_counter() - t0
             else:
                 u, ms = ref.infer_basis(ckpt, s, K)  # timed inside (checkpoint load excluded)
@@ -118,8 +135,10 @@ def ref_arm(path, ranks, reps, nlss=False):
             t0 = time.perf_counter()
             res = ref.pcg(a, inst["rhs"], 2, t, DELTA, 10 * a[0])
             t_solve = time.perf_counter() - t0
-            rows[(method, r)].append(dict(load=t_load, smooth=t_smooth, inference=t_inf, setup=t_setup,
-                                          solve=t_solve, iterations=res.iterations, converged=res.converged))
+            key = (method, 0) if method == "SA" else (method, r)
+            rows[key].append(dict(load=t_load, smooth=0.0 if method == "SA" else t_smooth, inference=t_inf,
+                                  setup=t_setup, solve=t_solve, iterations=res.iterations,
+                                  converged=res.converged, coarse_dim=r))
     if ckpt:
         os.remove(ckpt)
     return a[0], rows
@@ -138,16 +157,22 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--impl", choices=["gpu", "reference", "both"], default="both")
     ap.add_argument("--nlss", action="store_true", help="also the NLSS (MLP inference) rows")
+    ap.add_argument("--sa", action="store_true", help="also the SA row")
+    ap.add_argument("--sa-ref", action="store_true", help="run the reference SA row at any size")
     args = ap.parse_args()
     ranks = [int(r) for r in args.ranks.split(",")]
     arms = ["gpu", "reference"] if args.impl == "both" else [args.impl]
     for arm in arms:
-        n, rows = (gpu_arm if arm == "gpu" else ref_arm)(args.instance, ranks, args.reps, args.nlss)
+        sa_here = args.sa
+        if arm == "reference" and args.sa and not args.sa_ref:
+            from paper_2601_20174_b200 import instance_io as io
+            sa_here = io.load_instance(args.instance).matrix.dim() <= 1089
+        n, rows = (gpu_arm if arm == "gpu" else ref_arm)(args.instance, ranks, args.reps, args.nlss, sa_here)
         for (method, r), rr in rows.items():
             med = {k: statistics.median(x[k] for x in rr) * 1e3
                    for k in ("load", "smooth", "inference", "setup", "solve")}
             out = {"impl": arm, "instance": os.path.basename(args.instance), "n": n, "method": method,
-                   "rank": r, "K": K, "s1": S1, "nu": NU, "delta": DELTA,
+                   "rank": r if method != "SA" else rr[-1]["coarse_dim"], "K": K, "s1": S1, "nu": NU, "delta": DELTA,
                    "iterations": rr[-1]["iterations"], "converged": rr[-1]["converged"],
                    "ms": {k: round(v, 3) for k, v in med.items()},
                    "total_ms": round(med["smooth"] + med["inference"] + med["setup"] + med["solve"], 3),
