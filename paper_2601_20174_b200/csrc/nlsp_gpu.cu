@@ -1143,7 +1143,7 @@ nlsp_status nlsp_twolevel_build(nlsp_ctx* ctx, const nlsp_csr* a, const nlsp_den
         return cuda_fail(ctx, e, w);
     };
     cudaError_t e;
-    if ((e = dalloc(&m->basis, (size_t)n * m->ld)) || (e = dalloc(&m->L, kk)) ||
+    if ((e = dalloc(&m->basis, (size_t)n * m->ld)) || (e = dalloc(&m->L, kk + 8)) ||
         (e = dalloc(&m->Ainv, kk)) || (e = dalloc(&m->coarse, kk)) || (e = dalloc(&m->wd, n)) ||
         (e = salloc(ctx, &part, (size_t)g * gram_tile(k, k))) || (e = salloc(ctx, &G, kk)) || (e = salloc(ctx, &U, kk)) ||
         (e = salloc(ctx, &Q1, (size_t)n * k)) || (e = salloc(ctx, &Q, (size_t)n * k)) ||

@@ -598,6 +598,107 @@ __global__ void k_tri_inv_lower_t(int k, const double* __restrict__ L, double* _
     }
 }
 
+// ---- wide k x k factorizations (k > 256, e.g. the SA coarse space) --------
+// Same entrywise formulas as k_chol / k_tri_inv_lower_t, with the inner sums
+// split across a warp: the Cholesky runs one launch per column (the column's
+// rows in parallel across the grid), the triangular inverse a warp per column.
+__global__ void __launch_bounds__(1024) k_chol_prep(int k, const double* __restrict__ A, double* __restrict__ L,
+                                                    double rank_rel, double* tol, int* status) {
+    __shared__ double red[32];
+    __shared__ int fail;
+    const int tid = threadIdx.x;
+    double mx = 0.0, tr = 0.0;
+    for (long long idx = tid; idx < (long long)k * k; idx += blockDim.x) {
+        mx = fmax(mx, fabs(A[idx]));
+        L[idx] = 0.0;
+    }
+    for (int i = tid; i < k; i += blockDim.x) tr += A[(long long)i * k + i];
+    // block max / sum
+    for (int o = 16; o; o >>= 1) {
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        tr += __shfl_xor_sync(0xffffffffu, tr, o);
+    }
+    if (tid == 0) fail = 0;
+    if ((tid & 31) == 0) red[tid >> 5] = mx;
+    __syncthreads();
+    double scale = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) scale = fmax(scale, red[w]);
+    __syncthreads();
+    if ((tid & 31) == 0) red[tid >> 5] = tr;
+    __syncthreads();
+    double trace = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) trace += red[w];
+    scale = scale > 0.0 ? scale : 1.0;
+    for (long long idx = tid; idx < (long long)k * k; idx += blockDim.x) {
+        const long long i = idx / k, j = idx % k;
+        if (j > i && fabs(A[i * k + j] - A[j * k + i]) > 1e-10 * scale) atomicOr(&fail, 1);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        *tol = rank_rel > 0.0 ? rank_rel * sqrt(fmax(trace, 0.0)) : -rank_rel;
+        *status = fail ? kErrNotSpd : 0;
+    }
+}
+
+// column j: d = A_jj - sum_q L_jq^2 (every CTA, warp 0), then rows i > j
+__global__ void __launch_bounds__(256) k_chol_col(int k, int j, const double* __restrict__ A,
+                                                  double* __restrict__ L, double rank_rel,
+                                                  const double* tol, int* status) {
+    __shared__ double djj;
+    __shared__ int bad;
+    if (*status) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double* lj = L + (long long)j * k;
+    if (warp == 0) {
+        double s = 0.0;
+        for (int q = lane; q < j; q += 32) s = fma(lj[q], lj[q], s);
+        s = warp_sum(s);
+        if (lane == 0) {
+            const double d = A[(long long)j * k + j] - s;
+            bad = 0;
+            if (d <= 0.0) {
+                bad = rank_rel != 0.0 ? kErrRank : kErrNotSpd;
+            } else {
+                const double sd = sqrt(d);
+                if (rank_rel != 0.0 && sd < *tol) bad = kErrRank;
+                djj = sd;
+            }
+        }
+    }
+    __syncthreads();
+    if (bad) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) *status = bad;
+        return;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) L[(long long)j * k + j] = djj;
+    const int warps = gridDim.x * (blockDim.x >> 5);
+    for (int i = j + 1 + blockIdx.x * (blockDim.x >> 5) + warp; i < k; i += warps) {
+        const double* li = L + (long long)i * k;
+        double s = 0.0;
+        for (int q = lane; q < j; q += 32) s = fma(li[q], lj[q], s);
+        s = warp_sum(s);
+        if (lane == 0) L[(long long)i * k + j] = (A[(long long)i * k + j] - s) / djj;
+    }
+}
+
+// U = (L^-1)^T, a warp per column j of L^-1 (row j of U): forward substitution
+__global__ void __launch_bounds__(256) k_tri_inv_warp(int k, const double* __restrict__ L, double* __restrict__ U) {
+    const int lane = threadIdx.x & 31;
+    const int warps = gridDim.x * (blockDim.x >> 5);
+    for (int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < k; j += warps) {
+        double* u = U + (long long)j * k;
+        for (int q = lane; q < j; q += 32) u[q] = 0.0;
+        for (int i = j; i < k; ++i) {
+            const double* li = L + (long long)i * k;
+            double s = 0.0;
+            for (int q = j + lane; q < i; q += 32) s = fma(li[q], u[q], s);
+            s = warp_sum(s);
+            if (lane == 0) u[i] = ((i == j ? 1.0 : 0.0) - s) / li[i];
+            __syncwarp();
+        }
+    }
+}
+
 // A_c^-1 = L^-T L^-1 from U = (L^-1)^T: (A_c^-1)_ab = sum_{m >= max(a,b)} U_am U_bm
 // (the coarse solve of the two-level cycle becomes one k x k mat-vec)
 __global__ void k_coarse_inverse(int k, const double* __restrict__ U, double* __restrict__ Ainv) {
@@ -708,7 +809,8 @@ static bool use_dmma() {
 }
 
 int gram_grid(const LaunchCtx& c, long long rows) {
-    long long g = (rows + 15) / 16;
+    // at least 256 rows per CTA: fewer partials to reduce for short, wide Grams
+    long long g = (rows + 255) / 256;
     const long long cap = (long long)c.num_sms * 2;
     if (g > cap) g = cap;
     if (g < 1) g = 1;
@@ -818,12 +920,26 @@ void launch_sa_assemble(const LaunchCtx& c, int n, int nc, const int* rp, const 
 
 void launch_chol(const LaunchCtx& c, int k, const double* A, double* L, double rank_rel,
                  int* status) {
-    k_chol<<<1, 256, 0, c.s>>>(k, A, L, rank_rel, status);
+    if (k <= 256) {
+        k_chol<<<1, 256, 0, c.s>>>(k, A, L, rank_rel, status);
+        count(c);
+        return;
+    }
+    // wide: one launch per column; the rank tolerance sits just past the
+    // factor (callers allocate L with k*k + 8 doubles for k > 256)
+    double* tol = L + (long long)k * k;
+    k_chol_prep<<<1, 1024, 0, c.s>>>(k, A, L, rank_rel, tol, status);
     count(c);
+    const int grid = (k + 63) / 64;  // 8 warps per CTA, ~8 rows per warp
+    for (int j = 0; j < k; ++j) {
+        k_chol_col<<<grid, 256, 0, c.s>>>(k, j, A, L, rank_rel, tol, status);
+        count(c);
+    }
 }
 
 void launch_tri_inv_t(const LaunchCtx& c, int k, const double* L, double* U) {
-    k_tri_inv_lower_t<<<(k + 127) / 128, 128, 0, c.s>>>(k, L, U);
+    if (k <= 256) k_tri_inv_lower_t<<<(k + 127) / 128, 128, 0, c.s>>>(k, L, U);
+    else k_tri_inv_warp<<<(k + 7) / 8, 256, 0, c.s>>>(k, L, U);
     count(c);
 }
 
