@@ -93,3 +93,27 @@ def test_wide_coarse_space_apply_and_pcg(nlsp, k, nu):
     res = nlsp.pcg(a, b, m, 1e-8, 10 * n)
     assert res.report.converged
     assert np.linalg.norm(b - A @ res.solution) <= 1e-7 * np.linalg.norm(b)
+
+
+G64 = np.load(os.path.join(GOLDEN, "sa", "sa_n64.npz"))
+
+
+def test_aggregates_n64_match_reference():
+    inst = io.load_instance(os.path.join(GOLDEN, "io", "inst_diffusion_n64"))
+    agg, nc = sa.aggregate_nodes(inst.matrix, 0.25)
+    assert nc == int(G64["nc"]) == 2009
+    assert np.array_equal(agg, G64["agg"])
+
+
+@pytest.mark.gpu
+def test_sa_row_n64_matches_reference(nlsp):
+    """The paper's N = 64 SA row: n_c = 2 009 (the reference's constructor
+    took 575 s on one core to make this golden)."""
+    inst = io.load_instance(os.path.join(GOLDEN, "io", "inst_diffusion_n64"))
+    p = sa.sa_prolongator(inst.matrix, 0.25, 0.66)
+    m = nlsp.TwoLevelPreconditioner(inst.matrix, p, 0.66, 5, 5)
+    assert m.coarse_dim() == 2009
+    res = nlsp.pcg(inst.matrix, inst.rhs, m, 1e-6, 10 * inst.matrix.dim())
+    assert res.report.converged
+    assert abs(res.report.iterations - int(G64["iterations"])) <= 2
+    assert np.linalg.norm(res.solution - G64["x"]) <= 1e-9 * np.linalg.norm(G64["x"])
