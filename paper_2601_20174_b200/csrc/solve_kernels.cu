@@ -32,6 +32,9 @@ namespace nlsp {
 #ifndef NLSP_KUP
 #define NLSP_KUP 2
 #endif
+#ifndef NLSP_DIA_EXACT
+#define NLSP_DIA_EXACT 1
+#endif
 #ifndef NLSP_KUPRO
 #define NLSP_KUPRO 2
 #endif
@@ -833,7 +836,9 @@ struct OpPlain {
 // (Measured alternatives: lane shuffles for offsets within a
 // warp and shared-memory windows per offset cluster both cut L2 requests but
 // lost the memory-level parallelism of this form: 1.6x / 1.6x slower at C4.)
-template <int MAXD, typename MT, bool RV, int SKIP, class Op>
+// EXACT: MAXD is the offset count itself (the common 5 / 7 / 9-point forms),
+// and rows with every offset present (the interior) take an unpredicated path.
+template <int MAXD, typename MT, bool RV, int SKIP, bool EXACT, class Op>
 __global__ void __launch_bounds__(kThreads) k_spmv_dia(SolveArgs a, Op op) {
     PcgState* st = a.st;
     if (SKIP == 1 && st->done) return;
@@ -844,21 +849,33 @@ __global__ void __launch_bounds__(kThreads) k_spmv_dia(SolveArgs a, Op op) {
 #pragma unroll
     for (int j = 0; j < NVS; ++j) s[j] = 0.0;
     const MT* __restrict__ mask = static_cast<const MT*>(a.dia.mask);
-    const int n = a.n, d = a.dia.d;
+    const int n = a.n, d = EXACT ? MAXD : a.dia.d;
+    constexpr unsigned kFull = MAXD >= 32 ? ~0u : ((1u << MAXD) - 1u);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const unsigned m = mask[i];
         const typename Op::Pre pr = op.pre(i);  // own-row operands in flight with the gathers
-        double g[MAXD], vv[MAXD];
-#pragma unroll
-        for (int t = 0; t < MAXD; ++t) {
-            const bool on = t < d && ((m >> t) & 1u);
-            g[t] = on ? op(i + a.dia.off[t]) : 0.0;
-            if (RV) vv[t] = on ? __ldcs(a.dia.rv + (size_t)t * n + i) : 0.0;
-        }
         double y = 0.0;
+        if (EXACT && m == kFull) {
+            double g[MAXD], vv[MAXD];
 #pragma unroll
-        for (int t = 0; t < MAXD; ++t)
-            if (t < d && ((m >> t) & 1u)) y = fma(RV ? vv[t] : a.dia.val[t], g[t], y);
+            for (int t = 0; t < MAXD; ++t) {
+                g[t] = op(i + a.dia.off[t]);
+                if (RV) vv[t] = __ldcs(a.dia.rv + (size_t)t * n + i);
+            }
+#pragma unroll
+            for (int t = 0; t < MAXD; ++t) y = fma(RV ? vv[t] : a.dia.val[t], g[t], y);
+        } else {
+            double g[MAXD], vv[MAXD];
+#pragma unroll
+            for (int t = 0; t < MAXD; ++t) {
+                const bool on = t < d && ((m >> t) & 1u);
+                g[t] = on ? op(i + a.dia.off[t]) : 0.0;
+                if (RV) vv[t] = on ? __ldcs(a.dia.rv + (size_t)t * n + i) : 0.0;
+            }
+#pragma unroll
+            for (int t = 0; t < MAXD; ++t)
+                if (t < d && ((m >> t) & 1u)) y = fma(RV ? vv[t] : a.dia.val[t], g[t], y);
+        }
         op.row(i, y, s, pr);
     }
     if constexpr (Op::NV > 0) {
@@ -1501,19 +1518,16 @@ void launch_dia_op(const LaunchCtx& c, const SolveArgs& a, const Op& op) {
         kern<<<g, kThreads, 0, c.s>>>(a, op);
     };
     const bool rv = a.dia.kind == 2;
-    if (a.dia.d <= 8) {
-        if (rv) go(k_spmv_dia<8, unsigned char, true, SKIP, Op>);
-        else go(k_spmv_dia<8, unsigned char, false, SKIP, Op>);
-    } else if (a.dia.d <= 16) {
-        if (rv) go(k_spmv_dia<16, unsigned short, true, SKIP, Op>);
-        else go(k_spmv_dia<16, unsigned short, false, SKIP, Op>);
-    } else if (a.dia.d <= 24) {
-        if (rv) go(k_spmv_dia<24, unsigned int, true, SKIP, Op>);
-        else go(k_spmv_dia<24, unsigned int, false, SKIP, Op>);
-    } else {
-        if (rv) go(k_spmv_dia<32, unsigned int, true, SKIP, Op>);
-        else go(k_spmv_dia<32, unsigned int, false, SKIP, Op>);
-    }
+#define NLSP_DIA_GO(D, MT, EX) \
+    do { if (rv) go(k_spmv_dia<D, MT, true, SKIP, EX, Op>); else go(k_spmv_dia<D, MT, false, SKIP, EX, Op>); } while (0)
+    if (NLSP_DIA_EXACT && a.dia.d == 5) NLSP_DIA_GO(5, unsigned char, true);
+    else if (NLSP_DIA_EXACT && a.dia.d == 7) NLSP_DIA_GO(7, unsigned char, true);
+    else if (NLSP_DIA_EXACT && a.dia.d == 9) NLSP_DIA_GO(9, unsigned short, true);
+    else if (a.dia.d <= 8) NLSP_DIA_GO(8, unsigned char, false);
+    else if (a.dia.d <= 16) NLSP_DIA_GO(16, unsigned short, false);
+    else if (a.dia.d <= 24) NLSP_DIA_GO(24, unsigned int, false);
+    else NLSP_DIA_GO(32, unsigned int, false);
+#undef NLSP_DIA_GO
 }
 
 // Staged tiles must fit in shared memory (227 KB per CTA); matrices with very
