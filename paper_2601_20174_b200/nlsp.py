@@ -423,8 +423,11 @@ class TwoLevelPreconditioner:
 
     kind = L.PRECOND_TWOLEVEL
 
-    def __init__(self, a: SparseCsrMatrix, basis_any, omega: float, nu1: int, nu2: int):
-        dev = _dev(a)
+    def __init__(self, a: SparseCsrMatrix, basis_any, omega: float, nu1: int, nu2: int,
+                 ctx: Context | None = None):
+        # the context of a device-resident basis unless one is given
+        ctx = ctx or (basis_any.ctx if isinstance(basis_any, DeviceDense) else None)
+        dev = _dev(a, ctx)
         self.ctx = dev.ctx
         if not isinstance(basis_any, DeviceDense):
             basis_any = np.asarray(basis_any, dtype=np.float64)
