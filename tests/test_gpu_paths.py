@@ -94,3 +94,42 @@ def test_detected_matrix_form(nlsp, case):
         mb = 1 if offsets <= 8 else (2 if offsets <= 16 else 4)
         assert pass_bytes == n * (mb + (8 * offsets if kind == 2 else 0))
         assert pass_bytes < 12 * nnz + 4 * (n + 1)
+
+
+@pytest.fixture(scope="module")
+def graph_ctx(nlsp):
+    os.environ["NLSP_CLUSTER"] = "0"
+    try:
+        return nlsp.Context(0)
+    finally:
+        os.environ.pop("NLSP_CLUSTER", None)
+
+
+@pytest.mark.parametrize("path", ["cluster", "graph"])
+def test_two_level_edge_cases_on_both_paths(nlsp, graph_ctx, path):
+    """pcg's contract (two_level.hpp:141-191) with the two-level operator on the
+    single-cluster solver and on the graph loop: zero RHS, max_iters hit, zero
+    iterations, NotSpdError from p^T A p <= 0."""
+    ctx = nlsp.default_context() if path == "cluster" else graph_ctx
+    d = golden("c1_default")
+    a = nlsp.SparseCsrMatrix(int(d["n"]), d["row_ptr"], d["col_idx"], d["values"])
+    basis = nlsp.DeviceDense.upload(np.ascontiguousarray(d["P"]), ctx)
+    m = nlsp.TwoLevelPreconditioner(a, basis, float(d["omega"]), 1, 1)
+    with pytest.raises(nlsp.ValidationError):
+        nlsp.pcg(a, np.zeros(a.dim()), m, 1e-8, 100)
+    res = nlsp.pcg(a, d["rhs"], m, 1e-14, 3)
+    assert not res.report.converged and res.report.iterations == 3
+    assert len(res.report.residual_history) == 3
+    res0 = nlsp.pcg(a, d["rhs"], m, 1e-8, 0)
+    assert res0.report.iterations == 0 and not res0.report.converged
+    assert np.all(res0.solution == 0.0) and abs(res0.report.true_relative_residual - 1.0) < 1e-15
+    # indefinite A with a positive diagonal: the smoother and A_c build, p^T A p
+    # turns negative
+    n = 6
+    dense = np.diag(np.full(n, 1.0)) + np.diag(np.full(n - 1, 1.5), 1) + np.diag(np.full(n - 1, 1.5), -1)
+    ii, jj = np.nonzero(dense)
+    ai = nlsp.SparseCsrMatrix.from_coo(n, ii, jj, dense[ii, jj])
+    bi = nlsp.DeviceDense.upload(np.eye(n)[:, :1].copy(), ctx)
+    mi = nlsp.TwoLevelPreconditioner(ai, bi, 0.66, 1, 1)
+    with pytest.raises(nlsp.NotSpdError):
+        nlsp.pcg(ai, np.arange(1.0, n + 1.0), mi, 1e-10, 50)
