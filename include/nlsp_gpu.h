@@ -175,6 +175,18 @@ typedef struct {
 int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twolevel* m,
                      const double* b_dev, uint64_t iters, nlsp_kernel_stat* stats, int cap);
 
+/* ---- many small systems at once ------------------------------------------ */
+/* count independent two-level PCG solves (the reference's harness runs its
+ * test instances through parallel_for, pipeline.hpp:356) in ONE launch: one
+ * single-cluster solver per system that fits one (n <= 65536, k <= 256,
+ * folded cycle), the others one by one through nlsp_pcg. Host b[i], x[i];
+ * reps[i] / statuses[i] per system (either may be NULL). Returns the first
+ * failing status (NOT_SPD, VALIDATION for a zero right-hand side), else OK. */
+nlsp_status nlsp_pcg_batch(nlsp_ctx* ctx, uint64_t count, const nlsp_csr* const* a,
+                           const nlsp_twolevel* const* m, const double* const* b, double delta,
+                           uint64_t max_iters, double* const* x, nlsp_solve_report* reps,
+                           nlsp_status* statuses);
+
 /* ---- smoothed aggregation: the SA coarse space ------------ */
 /* aggregate_nodes(a, theta) (sa.hpp:18-76) on the host CSR (reference
  * layout): one aggregate id per node and their count. Needs no device. */

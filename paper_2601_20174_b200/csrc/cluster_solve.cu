@@ -109,7 +109,7 @@ __device__ __forceinline__ double ell_row(const unsigned* ea, const double* ev, 
 
 }  // namespace
 
-__global__ void __launch_bounds__(kClusterThreads, 1) k_cluster_pcg(ClusterArgs a) {
+__device__ __forceinline__ void cluster_pcg_body(const ClusterArgs& a) {
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ __align__(16) unsigned char sm[];
     __shared__ double wsc[kClusterWarps];
@@ -383,6 +383,16 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster_pcg(ClusterArgs 
     cl.sync();  // no CTA exits while others may still read its shared memory
 }
 
+__global__ void __launch_bounds__(kClusterThreads, 1) k_cluster_pcg(ClusterArgs a) { cluster_pcg_body(a); }
+
+// Independent systems in ONE launch, one cluster each (nlsp_pcg_batch): the
+// cluster index selects the system's arguments.
+__global__ void __launch_bounds__(kClusterThreads, 1) k_cluster_pcg_batch(const ClusterArgs* __restrict__ args) {
+    cg::cluster_group cl = cg::this_cluster();
+    const ClusterArgs a = args[blockIdx.x / cl.num_blocks()];
+    cluster_pcg_body(a);
+}
+
 // Cluster size and rows per CTA for an n x n system with rows of at most
 // `width` nonzeros, or 0 when the slices do not fit in shared memory. Prefers
 // the smallest cluster whose CTAs hold at most one row per thread.
@@ -429,6 +439,57 @@ cudaError_t launch_cluster_pcg(cudaStream_t s, const ClusterArgs& a, int ncta, s
     e = cudaOccupancyMaxActiveClusters(&nclusters, k_cluster_pcg, &cfg);
     if (e || nclusters < 1) return e ? e : cudaErrorInvalidConfiguration;
     return cudaLaunchKernelEx(&cfg, k_cluster_pcg, a);
+}
+
+// Common cluster size for a batch: the largest any system needs, each
+// system's rows re-split over it; returns 0 if any system does not fit.
+int cluster_plan_batch(int count, const int* n, const int* k, const int* width, const bool* two_w, int* rows,
+                       size_t* smem_out) {
+    // the smallest cluster each system fits in: many systems share the SMs,
+    // so fewer SMs per system beat fewer rows per thread
+    int ncta = 1;
+    for (int i = 0; i < count; ++i) {
+        int c = 0;
+        for (int t = 1; t <= kMaxClusterCtas && !c; t *= 2) {
+            const int R = (n[i] + t - 1) / t;
+            if (ClusterLayout(R, std::max(width[i], 1), k[i] + (k[i] & 1), k[i], two_w[i], t).bytes <= 200 * 1024)
+                c = t;
+        }
+        if (!c || k[i] > 256) return 0;
+        ncta = std::max(ncta, c);
+    }
+    size_t smem = 0;
+    for (int i = 0; i < count; ++i) {
+        rows[i] = (n[i] + ncta - 1) / ncta;
+        const ClusterLayout Lo(rows[i], std::max(width[i], 1), k[i] + (k[i] & 1), k[i], two_w[i], ncta);
+        if (Lo.bytes > 200 * 1024) return 0;
+        smem = std::max<size_t>(smem, Lo.bytes);
+    }
+    *smem_out = smem;
+    return ncta;
+}
+
+cudaError_t launch_cluster_pcg_batch(cudaStream_t s, const ClusterArgs* dargs, int count, int ncta, size_t smem) {
+    cudaError_t e = cudaFuncSetAttribute(k_cluster_pcg_batch, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e) return e;
+    e = cudaFuncSetAttribute(k_cluster_pcg_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e) return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(count * ncta);
+    cfg.blockDim = dim3(kClusterThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = ncta;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    e = cudaOccupancyMaxActiveClusters(&nclusters, k_cluster_pcg_batch, &cfg);
+    if (e || nclusters < 1) return e ? e : cudaErrorInvalidConfiguration;
+    return cudaLaunchKernelEx(&cfg, k_cluster_pcg_batch, dargs);
 }
 
 }  // namespace nlsp

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -45,6 +46,9 @@ int ppl_for(int k);
 int cluster_plan(int n, int k, int width, bool two_w, int* rows_out,
                  size_t* smem_out);
 cudaError_t launch_cluster_pcg(cudaStream_t s, const ClusterArgs& a, int ncta, size_t smem);
+int cluster_plan_batch(int count, const int* n, const int* k, const int* width, const bool* two_w, int* rows,
+                       size_t* smem_out);
+cudaError_t launch_cluster_pcg_batch(cudaStream_t s, const ClusterArgs* dargs, int count, int ncta, size_t smem);
 // setup_kernels.cu
 void launch_csr_import(const LaunchCtx&, int, long long, const unsigned long long*,
                        const unsigned long long*, const double*, int*, int*, double*, int*, int*);
@@ -1771,5 +1775,137 @@ nlsp_status nlsp_sa_prolongator(nlsp_ctx* ctx, uint64_t n, uint64_t nnz, const u
         return cuda_fail(ctx, e, "sa_prolongator");
     }
     *p_out = P;
+    return NLSP_OK;
+}
+
+// ------------------------------------------------------------- batched solves --
+// Many independent small systems in one launch: one single-cluster solver per
+// system (the reference's harness runs its test instances through parallel_for,
+// pipeline.hpp:356). Systems that do not fit a cluster are solved one by one.
+nlsp_status nlsp_pcg_batch(nlsp_ctx* ctx, uint64_t count, const nlsp_csr* const* a,
+                           const nlsp_twolevel* const* m, const double* const* b, double delta,
+                           uint64_t max_iters, double* const* x, nlsp_solve_report* reps,
+                           nlsp_status* statuses) {
+    nlsp_status st = bind(ctx);
+    if (st) return st;
+    if (count == 0) return NLSP_OK;
+    if (!a || !m || !b || !x) return set_err(ctx, NLSP_E_VALIDATION, "pcg_batch: null array");
+    if (max_iters > (1ull << 26)) return set_err(ctx, NLSP_E_VALIDATION, "pcg_batch: max_iters too large");
+    std::vector<int> in_batch, ns, ks, ws, rows;
+    std::vector<char> tw;
+    for (uint64_t i = 0; i < count; ++i) {
+        if (!a[i] || !m[i] || !b[i] || !x[i]) return set_err(ctx, NLSP_E_VALIDATION, "pcg_batch: null system");
+        st = check_pcg_args(ctx, a[i], NLSP_PRECOND_TWOLEVEL, m[i]);
+        if (st) return st;
+        int r = 0;
+        size_t sm = 0;
+        const bool fits = m[i]->folded && ctx->use_cluster && !a[i]->rp_host.empty() &&
+                          cluster_plan(a[i]->n, m[i]->k, a[i]->max_row, m[i]->W2 != m[i]->W1, &r, &sm) > 0;
+        if (fits) {
+            in_batch.push_back((int)i);
+            ns.push_back(a[i]->n);
+            ks.push_back(m[i]->k);
+            ws.push_back(a[i]->max_row);
+            tw.push_back(m[i]->W2 != m[i]->W1);
+        }
+    }
+    nlsp_status first = NLSP_OK;
+    auto record = [&](uint64_t i, nlsp_status s_i) {
+        if (statuses) statuses[i] = s_i;
+        if (s_i && !first) first = s_i;
+    };
+    const int cnt = (int)in_batch.size();
+    if (cnt) {
+        rows.resize(cnt);
+        size_t smem = 0;
+        std::vector<bool> twb(tw.begin(), tw.end());
+        std::unique_ptr<bool[]> twa(new bool[cnt]);
+        for (int j = 0; j < cnt; ++j) twa[j] = twb[j];
+        const int ncta = cluster_plan_batch(cnt, ns.data(), ks.data(), ws.data(), twa.get(), rows.data(), &smem);
+        if (!ncta) return set_err(ctx, NLSP_E_VALIDATION, "pcg_batch: systems do not fit one cluster size");
+        // per-system state, history, b, x in one pool allocation each
+        std::vector<size_t> voff(cnt + 1, 0);
+        for (int j = 0; j < cnt; ++j) voff[j + 1] = voff[j] + (size_t)ns[j] + 16;
+        PcgState* dst = nullptr;
+        double *dhist = nullptr, *db = nullptr, *dx = nullptr;
+        ClusterArgs* dargs = nullptr;
+        const size_t hcap = std::max<uint64_t>(max_iters, 1);
+        auto cleanup = [&]() {
+            sfree(ctx, dst);
+            sfree(ctx, dhist);
+            sfree(ctx, db);
+            sfree(ctx, dx);
+            sfree(ctx, dargs);
+        };
+        cudaError_t e;
+        if ((e = salloc(ctx, &dst, cnt)) || (e = salloc(ctx, &dhist, (size_t)cnt * hcap)) ||
+            (e = salloc(ctx, &db, voff[cnt])) || (e = salloc(ctx, &dx, voff[cnt])) ||
+            (e = salloc(ctx, &dargs, cnt))) {
+            cleanup();
+            return cuda_fail(ctx, e, "pcg_batch alloc");
+        }
+        std::vector<ClusterArgs> args(cnt);
+        CU(cudaEventRecord(ctx->ev2, ctx->s));
+        for (int j = 0; j < cnt; ++j) {
+            const uint64_t i = in_batch[j];
+            const nlsp_csr* A = a[i];
+            const nlsp_twolevel* M = m[i];
+            CU(cudaMemcpyAsync(db + voff[j], b[i], (size_t)A->n * 8, cudaMemcpyHostToDevice, ctx->s));
+            launch_state_init(ctx->lc, dst + j, delta, (long long)max_iters);
+            const SolveArgs sa = make_args(ctx, A, M);
+            args[j] = ClusterArgs{A->n, M->k, M->ld, rows[j], (int)M->nu1, (int)M->nu2, A->max_row, A->rp, A->ci, A->v,
+                                  M->wd, M->W1, M->W2, M->L, sa.Ainv, db + voff[j], dx + voff[j],
+                                  dhist + (size_t)j * hcap, dst + j};
+        }
+        CU(cudaMemcpyAsync(dargs, args.data(), sizeof(ClusterArgs) * cnt, cudaMemcpyHostToDevice, ctx->s));
+        CU(cudaEventRecord(ctx->ev0, ctx->s));
+        e = launch_cluster_pcg_batch(ctx->s, dargs, cnt, ncta, smem);
+        if (e) {
+            cleanup();
+            return cuda_fail(ctx, e, "pcg_batch launch");
+        }
+        ctx->launches += 1 + cnt;
+        CU(cudaEventRecord(ctx->ev1, ctx->s));
+        std::vector<PcgState> hs(cnt);
+        CU(cudaMemcpyAsync(hs.data(), dst, sizeof(PcgState) * cnt, cudaMemcpyDeviceToHost, ctx->s));
+        for (int j = 0; j < cnt; ++j)
+            CU(cudaMemcpyAsync(x[in_batch[j]], dx + voff[j], (size_t)ns[j] * 8, cudaMemcpyDeviceToHost, ctx->s));
+        CU(cudaEventRecord(ctx->ev3, ctx->s));
+        CU(cudaStreamSynchronize(ctx->s));
+        float ms = 0.f, tot = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+        cudaEventElapsedTime(&tot, ctx->ev2, ctx->ev3);
+        for (int j = 0; j < cnt; ++j) {
+            const uint64_t i = in_batch[j];
+            const PcgState& p = hs[j];
+            if (reps) {
+                nlsp_solve_report& r = reps[i];
+                std::memset(&r, 0, sizeof(r));
+                r.iterations = (uint64_t)p.iterations;
+                r.converged = p.converged;
+                r.precond_kind = NLSP_PRECOND_TWOLEVEL;
+                r.true_relative_residual = p.true_res;
+                r.final_relative_residual = p.last_rel;
+                r.solve_ms = ms;  // the batch's device time
+                r.total_ms = tot;
+                r.coarse_dim = (uint64_t)m[i]->k;
+                r.kernel_launches = 1;
+                r.h2d_bytes = (uint64_t)ns[j] * 8;
+                r.d2h_bytes = (uint64_t)ns[j] * 8 + sizeof(PcgState);
+            }
+            record(i, p.error == kErrNotSpd ? NLSP_E_NOT_SPD : (p.error ? NLSP_E_VALIDATION : NLSP_OK));
+        }
+        cleanup();
+        CU(cudaStreamSynchronize(ctx->s));
+    }
+    // the rest one by one on the general path
+    for (uint64_t i = 0; i < count; ++i) {
+        if (std::find(in_batch.begin(), in_batch.end(), (int)i) != in_batch.end()) continue;
+        nlsp_solve_report local{};
+        const nlsp_status s_i = nlsp_pcg(ctx, a[i], NLSP_PRECOND_TWOLEVEL, m[i], b[i], delta, max_iters, x[i],
+                                         reps ? &reps[i] : &local, nullptr);
+        record(i, s_i);
+    }
+    if (first) return set_err(ctx, first, "pcg_batch: at least one system failed (see statuses)");
     return NLSP_OK;
 }

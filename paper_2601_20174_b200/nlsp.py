@@ -550,3 +550,46 @@ def pcg(a: SparseCsrMatrix, b, m, delta: float, max_iters: int) -> PcgResult:
                     coarse_dim=int(rep.coarse_dim), kernel_launches=int(rep.kernel_launches),
                     method={0: "plain", 1: "jacobi", 2: "two_level"}[kind])
     return PcgResult(x, r)
+
+
+def pcg_batch(systems, delta: float, max_iters: int, return_statuses: bool = False):
+    """Independent two-level PCG solves in one launch (nlsp_pcg_batch): one
+    single-cluster solver per system. `systems` is a sequence of (a, b, m) with
+    m a TwoLevelPreconditioner; returns a list of PcgResult (no residual
+    history), plus the per-system statuses when asked."""
+    systems = list(systems)
+    count = len(systems)
+    if count == 0:
+        return ([], []) if return_statuses else []
+    ctx = systems[0][2].ctx
+    keep = []
+    ah, mh, bp, xp = (C.c_void_p * count)(), (C.c_void_p * count)(), (L.P_dbl * count)(), (L.P_dbl * count)()
+    xs = []
+    for i, (a, b, m) in enumerate(systems):
+        if getattr(m, "kind", None) != L.PRECOND_TWOLEVEL:
+            raise ValidationError("pcg_batch: two-level preconditioners only")
+        if m.ctx is not ctx:
+            raise ValidationError("pcg_batch: all systems must share one context")
+        bb = np.ascontiguousarray(b, dtype=np.float64)
+        if bb.shape != (a.dim(),):
+            raise ValidationError("pcg: dimension mismatch")
+        dev = _dev(a, ctx)
+        x = np.empty(a.dim())
+        keep += [bb, dev]
+        xs.append(x)
+        ah[i], mh[i] = dev.handle, m.handle
+        bp[i], xp[i] = L.dptr(bb), L.dptr(x)
+    reps = (L.SolveReportC * count)()
+    sts = (C.c_int32 * count)()
+    st = L.gpu_lib().nlsp_pcg_batch(ctx.handle, count, ah, mh, bp, delta, int(max_iters), xp, reps, sts)
+    if st and not return_statuses:
+        _check(ctx, st)
+    out = []
+    for i in range(count):
+        r = reps[i]
+        out.append(PcgResult(xs[i], SolveReport(iterations=int(r.iterations), converged=bool(r.converged),
+                                                true_relative_residual=float(r.true_relative_residual),
+                                                solve_ms=float(r.solve_ms), total_ms=float(r.total_ms),
+                                                coarse_dim=int(r.coarse_dim),
+                                                kernel_launches=int(r.kernel_launches), method="two_level")))
+    return (out, [int(s) for s in sts]) if return_statuses else out

@@ -20,6 +20,12 @@ its emergent coarse dimension n_c — 2 009 at N = 64 — through the wide
 kernels). The reference's SA constructor (dense MGS of n x n_c) takes minutes
 at N = 64, so its arm runs SA only for n <= 1089 unless --sa-ref.
 
+With --batch B, a throughput line per arm instead: B solves of the instance's
+SVD rank-8 system (the reference harness solves its test instances
+concurrently, pipeline.hpp:356) — nlsp_pcg_batch (one single-cluster solver
+per system, all in one launch) vs the reference's pcg on every host core
+(one single-threaded solve per core, repeated to B).
+
 Prints one JSON line per (arm, method, rank) with smooth / inference / setup /
 solve / total ms (the reference's BenchRow fields) and iterations; --reps R
 repeats and keeps the median per phase.
@@ -144,6 +150,50 @@ def ref_arm(path, ranks, reps, nlss=False, with_sa=False):
     return a[0], rows
 
 
+def batch_arm(arm, path, count, reps):
+    import os as _os
+    if arm == "gpu":
+        from paper_2601_20174_b200 import instance_io as io
+        from paper_2601_20174_b200 import nlsp
+        ctx = nlsp.default_context()
+        inst = io.load_instance(path)
+        sv = nlsp.generate_smoothed_vectors(inst.matrix, inst.boundary_mask, K, S1, OMEGA, mix_seed(inst.seed, 3))
+        p, _, _ = nlsp.svd_basis(sv.s, 8)
+        m = nlsp.TwoLevelPreconditioner(inst.matrix, p, OMEGA, NU, NU)
+        systems = [(inst.matrix, inst.rhs, m)] * count
+        nlsp.pcg_batch(systems, DELTA, 10 * inst.matrix.dim())  # warm
+        ts = []
+        for _ in range(reps):
+            ctx.synchronize()
+            t0 = time.perf_counter()
+            res = nlsp.pcg_batch(systems, DELTA, 10 * inst.matrix.dim())
+            ts.append(time.perf_counter() - t0)
+        n, iters, dev_ms = inst.matrix.dim(), res[0].report.iterations, res[0].report.solve_ms
+        cores = None
+    else:
+        from oracle.oracle import Reference
+        ref = Reference()
+        inst = ref.load_instance(path)
+        a = inst["matrix"]
+        s = ref.generate_smoothed_vectors(a, inst["mask"], K, S1, OMEGA, int(ref.lib.ref_mix_seed(inst["seed"], 3)))
+        u, _, _, _ = ref.svd(s)
+        t = ref.twolevel(a, np.ascontiguousarray(u[:, :8]), OMEGA, NU, NU)
+        cores = _os.cpu_count() or 1
+        ts = []
+        for _ in range(reps):
+            done, t0 = 0, time.perf_counter()
+            while done < count:
+                th = min(cores, count - done)
+                _, iters = ref.pcg_parallel(a, inst["rhs"], 2, t, DELTA, 10 * a[0], th)
+                done += th
+            ts.append(time.perf_counter() - t0)
+        n, dev_ms = a[0], None
+    wall = statistics.median(ts)
+    return {"impl": arm, "instance": os.path.basename(path), "n": n, "method": "SVD", "rank": 8, "batch": count,
+            "iterations": iters, "wall_ms": round(wall * 1e3, 3), "solves_per_s": round(count / wall, 2),
+            "device_ms": dev_ms, "cores": cores, "reps": reps}
+
+
 def mix_seed(seed, tag):
     # rng.hpp mix_seed through the product's host generator library
     from paper_2601_20174_b200 import _lib as L
@@ -159,9 +209,14 @@ def main():
     ap.add_argument("--nlss", action="store_true", help="also the NLSS (MLP inference) rows")
     ap.add_argument("--sa", action="store_true", help="also the SA row")
     ap.add_argument("--sa-ref", action="store_true", help="run the reference SA row at any size")
+    ap.add_argument("--batch", type=int, default=0, help="throughput of B concurrent solves")
     args = ap.parse_args()
     ranks = [int(r) for r in args.ranks.split(",")]
     arms = ["gpu", "reference"] if args.impl == "both" else [args.impl]
+    if args.batch:
+        for arm in arms:
+            print(json.dumps(batch_arm(arm, args.instance, args.batch, args.reps)), flush=True)
+        return
     for arm in arms:
         sa_here = args.sa
         if arm == "reference" and args.sa and not args.sa_ref:

@@ -133,3 +133,23 @@ def test_two_level_edge_cases_on_both_paths(nlsp, graph_ctx, path):
     mi = nlsp.TwoLevelPreconditioner(ai, bi, 0.66, 1, 1)
     with pytest.raises(nlsp.NotSpdError):
         nlsp.pcg(ai, np.arange(1.0, n + 1.0), mi, 1e-10, 50)
+
+
+def test_pcg_batch_matches_reference(nlsp):
+    """nlsp_pcg_batch: many systems of different sizes / coarse dimensions /
+    smoothing in one launch (one cluster each), each against the reference."""
+    names = ["c1_default", "scaled_C2", "scaled_C3", "scaled_C4", "scaled_C5", "c1_default"]
+    systems, goldens = [], []
+    for nm in names:
+        d = golden(nm)
+        a = nlsp.SparseCsrMatrix(int(d["n"]), d["row_ptr"], d["col_idx"], d["values"])
+        m = nlsp.TwoLevelPreconditioner(a, d["P"], float(d["omega"]), int(d["nu1"]), int(d["nu2"]))
+        systems.append((a, d["rhs"], m))
+        goldens.append(d)
+    res = nlsp.pcg_batch(systems, 1e-8, 10 * max(int(g["n"]) for g in goldens))
+    for r, d in zip(res, goldens):
+        assert r.report.converged
+        assert abs(r.report.iterations - int(d["iterations"])) <= 2
+        assert np.linalg.norm(r.solution - d["x"]) <= 1e-9 * np.linalg.norm(d["x"])
+    # the same system twice gives the same answer
+    assert np.array_equal(res[0].solution, res[-1].solution)
