@@ -152,20 +152,25 @@ def byte_model_literal(n, nnz, k, nu1, nu2):
     return (1 + nu1 + nu2) * csr + 16.0 * n * k + v * n
 
 
-def byte_model(n, nnz, k, nu1, nu2, pass_bytes=None):
+def byte_model(n, nnz, k, nu1, nu2, pass_bytes=None, cycle="onepass"):
     """Algorithmic HBM bytes per PCG iteration of the schedule this library runs
-    (folded cycle): spmv_p (A + 32n), update+restriction through
+    (DESIGN.md §3). Folded cycle: spmv_p (A + 32n), update+restriction through
     W1 (8nk + 48n), nu1+nu2-1 smoothing sweeps (A + 24n for the first, A + 32n
-    after), prolongation through W2 with r.z (8nk + 24n). A = the matrix bytes
-    one pass streams: CSR 12 nnz + 4(n+1), or the diagonal form's own bytes
-    when the upload detected one (nlsp_csr_format; SURVEY §8d's rule for
-    stencil-specialised kernels)."""
+    after), prolongation through W2 with r.z (8nk + 24n). One-pass cycle
+    (nu1 == nu2): spmv_p (A + 32n), x/r update (48n), the same sweeps, and ONE
+    pass over W that also gathers A s (8nk + A + 24n; 8nk + 16n without sweeps).
+    A = the matrix bytes one pass streams: CSR 12 nnz + 4(n+1), or the diagonal
+    form's own bytes when the upload detected one (nlsp_csr_format; SURVEY
+    §8d's rule for stencil-specialised kernels)."""
     csr = 12.0 * nnz + 4.0 * (n + 1) if pass_bytes is None else float(pass_bytes)
     ld = k + (k & 1)
     t = nu1 + nu2
     sweeps = 0.0
     if t >= 2:
         sweeps = (csr + 24.0 * n) + (t - 2) * (csr + 32.0 * n)
+    if cycle == "onepass":
+        pro = 8.0 * n * ld + ((csr + 24.0 * n) if t >= 1 else 16.0 * n)
+        return (csr + 32.0 * n) + 48.0 * n + sweeps + pro
     pro = 8.0 * n * ld + (24.0 if t >= 1 else 16.0) * n
     return (csr + 32.0 * n) + (8.0 * n * ld + 48.0 * n) + sweeps + pro
 
@@ -317,8 +322,12 @@ def run_ours(args, dist: Dist):
                    key=lambda k: kernels[k]["avg_us"] * kernels[k]["launches"])
     dk = kernels[dominant]
     fmt_kind, fmt_offsets, pass_bytes = dcsr.format()
-    bytes_iter = byte_model(pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2, pass_bytes)
-    bytes_iter_csr = byte_model(pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2)
+    cycle = m.cycle()
+    if cycle == "literal":
+        bytes_iter = bytes_iter_csr = byte_model_literal(pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2)
+    else:
+        bytes_iter = byte_model(pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2, pass_bytes, cycle)
+        bytes_iter_csr = byte_model(pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2, None, cycle)
     iter_gbs = bytes_iter * iters / (ms_local / 1e3) / 1e9
     traffic = ncu_traffic(dominant, args.config)
     roofline = {"bound": "hbm", "kernel": dominant, "achieved": round(dk["gbs"], 1),
@@ -327,6 +336,9 @@ def run_ours(args, dist: Dist):
                 "bytes_per_launch": dk["bytes_per_launch"], "avg_launch_us": round(dk["avg_us"], 2),
                 "iteration": {"bytes_per_iter": bytes_iter, "achieved": round(iter_gbs, 1),
                               "frac": round(iter_gbs / peak, 4),
+                              "cycle": cycle,
+                              "folded_cycle_bytes_per_iter": byte_model(
+                                  pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2, pass_bytes, "folded"),
                               "matrix_form": ["csr", "diagonal-constant", "diagonal-values"][fmt_kind],
                               "matrix_offsets": fmt_offsets, "matrix_bytes_per_pass": pass_bytes,
                               "csr_model_bytes_per_iter": bytes_iter_csr,

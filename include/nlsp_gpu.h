@@ -140,6 +140,12 @@ nlsp_status nlsp_twolevel_build(nlsp_ctx* ctx, const nlsp_csr* a, const nlsp_den
                                 double omega, uint64_t nu1, uint64_t nu2, nlsp_twolevel** out);
 void nlsp_twolevel_destroy(nlsp_twolevel* m);
 void nlsp_twolevel_dims(const nlsp_twolevel* m, uint64_t* n, uint64_t* k);
+/* The schedule nlsp_pcg runs this operator with (same operator,
+ * different pass structure): 0 literal (two_level.hpp:60-81 op by op), 1 folded
+ * (W1 = G^nu1 P, W2 = G^nu2 P streamed twice per iteration), 2 one-pass (nu1 ==
+ * nu2, k <= 64: W streamed once per iteration, the restriction by its
+ * recurrence). NLSP_CYCLE=literal|folded selects the first two. */
+int nlsp_twolevel_cycle(const nlsp_twolevel* m);
 /* basis_ (n x k), Cholesky factor L (k x k, lower), A_c (k x k); any may be NULL */
 nlsp_status nlsp_twolevel_export(nlsp_ctx* ctx, const nlsp_twolevel* m, double* basis,
                                  double* chol, double* coarse);

@@ -121,6 +121,7 @@ GPU_SYMBOLS = [
     ("nlsp_twolevel_build", C.c_int, [vp, vp, vp, c_dbl, c_u64, c_u64, C.POINTER(vp)]),
     ("nlsp_twolevel_destroy", None, [vp]),
     ("nlsp_twolevel_dims", None, [vp, P_u64, P_u64]),
+    ("nlsp_twolevel_cycle", C.c_int, [vp]),
     ("nlsp_twolevel_export", C.c_int, [vp, vp, P_dbl, P_dbl, P_dbl]),
     ("nlsp_twolevel_apply", C.c_int, [vp, vp, vp, P_dbl, P_dbl]),
     ("nlsp_pcg", C.c_int, [vp, vp, C.c_int, vp, P_dbl, c_dbl, c_u64, P_dbl, C.POINTER(SolveReportC), P_dbl]),

@@ -22,6 +22,8 @@ constexpr int kWideK = 256;        // k above this: the wide restriction / prolo
 constexpr int kWideGrid = 144;     // CTAs of the wide restriction (partials: grid * (k + 1))
 // c = W1^T r of the wide path lives at the tail of the partials buffer
 constexpr long long kWideCOffset = (long long)kMaxGrid * 256 - (kMaxCoarse + 8);
+// one-pass cycle: coarse dimensions it runs at (8-lane register tiles, PPL <= 4)
+constexpr int kOnePassK = 64;
 
 enum DevError : int {
     kErrNone = 0,
@@ -38,6 +40,8 @@ struct PcgState {
     long long it, max_it, iterations, body_runs;
     int done, converged, error, first;
     unsigned int counter[16];  // last-CTA tickets, one slot per kernel kind
+    int op_grid;               // CTAs of the last one-pass prolongation (its partials' stride)
+    double alpha_prev;         // alpha of the previous iteration (one-pass restriction)
 };
 
 // Ticket slots (each kernel kind reuses its own counter; counters return to 0).
@@ -95,6 +99,12 @@ struct SolveArgs {
     PcgState* st;
     double* partials;    // kMaxGrid * max(k, 4)
     double* e;           // coarse correction, k
+    // one-pass cycle (solve_kernels.cu): M = W^T A W (k x k),
+    // ow = [u_even | u_odd | v] column sums (3 ld), opart = per-CTA partials of
+    // [u | v], column-major
+    const double* M;
+    double* ow;
+    double* opart;
     DiaArgs dia;         // diagonal form of A (dia.kind == 0: CSR kernels)
 };
 

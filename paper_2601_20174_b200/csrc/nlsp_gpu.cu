@@ -41,6 +41,13 @@ void launch_update_restrict(const LaunchCtx&, const SolveArgs&, bool);
 void launch_folded_tail(const LaunchCtx&, const SolveArgs&, unsigned long long, unsigned long long,
                         cudaGraphConditionalHandle, int);
 void launch_folded_apply(const LaunchCtx&, const SolveArgs&, unsigned long long, unsigned long long);
+bool onepass_supported(int k);
+void launch_prolong_onepass(const LaunchCtx&, const SolveArgs&, const double*, double*,
+                            cudaGraphConditionalHandle, int);
+const double* launch_onepass_sweeps(const LaunchCtx&, const SolveArgs&, unsigned long long);
+void launch_update_onepass(const LaunchCtx&, const SolveArgs&);
+void launch_onepass_tail(const LaunchCtx&, const SolveArgs&, unsigned long long, cudaGraphConditionalHandle, int);
+void launch_onepass_apply(const LaunchCtx&, const SolveArgs&, unsigned long long);
 int ppl_for(int k);
 // cluster_solve.cu
 int cluster_plan(int n, int k, int width, bool two_w, int* rows_out,
@@ -127,6 +134,8 @@ struct nlsp_twolevel {
     double* W1;      // (I - w D^-1 A)^nu1 P, n x ld (folded cycle)
     double* W2;      // (I - w D^-1 A)^nu2 P, n x ld (aliases W1 when nu1 == nu2)
     bool folded;     // folded cycle (default) or the literal schedule (NLSP_CYCLE=literal)
+    bool onepass;    // PCG streams W once per iteration (nu1 == nu2, k <= 64; NLSP_CYCLE=folded: twice)
+    double* M;       // W^T A W, k x k (one-pass restriction recurrence)
 };
 
 struct GraphKey {
@@ -156,6 +165,7 @@ struct nlsp_ctx {
     double *x = nullptr, *r = nullptr, *q = nullptr, *z = nullptr, *p0 = nullptr, *p1 = nullptr,
            *zt0 = nullptr, *zt1 = nullptr, *b = nullptr, *e = nullptr, *partials = nullptr,
            *hist = nullptr;
+    double *ow = nullptr, *opart = nullptr;  // one-pass cycle: [u | v | w], per-CTA partials
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
     cudaGraphExec_t gexec = nullptr;
     GraphKey gkey;
@@ -271,7 +281,7 @@ nlsp_status bind(nlsp_ctx* ctx) {
 
 void free_ws(nlsp_ctx* c) {
     for (double** p : {&c->x, &c->r, &c->q, &c->z, &c->p0, &c->p1, &c->zt0, &c->zt1, &c->b,
-                       &c->e, &c->partials, &c->hist}) {
+                       &c->e, &c->partials, &c->hist, &c->ow, &c->opart}) {
         dfree(*p);
         *p = nullptr;
     }
@@ -289,6 +299,10 @@ nlsp_status ensure_ws(nlsp_ctx* ctx, long long n, long long hist) {
             CU(dalloc(p, (size_t)n + 16));  // padded for 16-B bulk copies of tile slices
         CU(dalloc(&ctx->e, (size_t)kMaxCoarse + 2));
         CU(dalloc(&ctx->partials, (size_t)kMaxGrid * 256));
+        CU(dalloc(&ctx->ow, (size_t)3 * (kOnePassK + 2)));
+        CU(dalloc(&ctx->opart, (size_t)kMaxGrid * 3 * (kOnePassK + 2)));
+        // q feeds the one-pass partials of the PCG prologue (weighted by 0)
+        CU(cudaMemsetAsync(ctx->q, 0, ((size_t)n + 16) * 8, ctx->s));
         ctx->ws_n = n;
         ctx->ws_gen++;
         hist = hist > hist_keep ? hist : hist_keep;
@@ -336,6 +350,9 @@ SolveArgs make_args(nlsp_ctx* c, const nlsp_csr* a, const nlsp_twolevel* m) {
     s.st = c->st;
     s.partials = c->partials;
     s.e = c->e;
+    s.M = m ? m->M : nullptr;
+    s.ow = c->ow;
+    s.opart = c->opart;
     return s;
 }
 
@@ -343,6 +360,11 @@ SolveArgs make_args(nlsp_ctx* c, const nlsp_csr* a, const nlsp_twolevel* m) {
 void enqueue_iteration(const LaunchCtx& lc, const SolveArgs& a, int mode, const nlsp_twolevel* m,
                        cudaGraphConditionalHandle h, int use_cond) {
     launch_spmv_p(lc, a);
+    if (mode == 0 && m->onepass) {
+        launch_update_onepass(lc, a);  // x, r, ||r||, c by its recurrence, e
+        launch_onepass_tail(lc, a, m->nu1 + m->nu2, h, use_cond ? 2 : 1);
+        return;
+    }
     if (mode == 0 && m->folded) {
         launch_update_restrict(lc, a, true);  // x, r, ||r||, c = W1^T r, e
         // the prolongation ends the iteration and runs the loop control too
@@ -359,7 +381,8 @@ void enqueue_prologue(const LaunchCtx& lc, const SolveArgs& a, int mode, const n
                       const double* params_dev) {
     (void)params_dev;
     launch_bnorm(lc, a);
-    if (mode == 0 && m->folded) launch_folded_apply(lc, a, m->nu1, m->nu2);
+    if (mode == 0 && m->onepass) launch_onepass_apply(lc, a, m->nu1 + m->nu2);
+    else if (mode == 0 && m->folded) launch_folded_apply(lc, a, m->nu1, m->nu2);
     else if (mode == 0) launch_twolevel_apply(lc, a, m->nu1, m->nu2);
     else launch_init_simple(lc, a, mode == 2 ? 1 : 0);
     launch_init_ctl(lc, a.st);
@@ -1134,6 +1157,8 @@ nlsp_status nlsp_twolevel_build(nlsp_ctx* ctx, const nlsp_csr* a, const nlsp_den
         const char* cyc = std::getenv("NLSP_CYCLE");
         // wide coarse spaces (k > 256) run the folded cycle only
         m->folded = !(cyc && std::strcmp(cyc, "literal") == 0) || k > kWideK;
+        m->onepass = m->folded && nu1 == nu2 && onepass_supported(k) &&
+                     !(cyc && std::strcmp(cyc, "folded") == 0);
     }
     const size_t kk = (size_t)k * k;
     const int g = gram_grid(ctx->lc, n);
@@ -1194,6 +1219,15 @@ nlsp_status nlsp_twolevel_build(nlsp_ctx* ctx, const nlsp_csr* a, const nlsp_den
         err = cudaMemcpy2DAsync(*out, (size_t)m->ld * 8, cur, (size_t)k * 8, (size_t)k * 8, n,
                                 cudaMemcpyDeviceToDevice, ctx->s);
         if (!err && m->ld != k) err = cudaMemset2DAsync(*out + k, (size_t)m->ld * 8, 0, 8, n, ctx->s);
+        if (!err && m->onepass) {
+            // M = W^T (A W) for the one-pass restriction recurrence
+            double* aw = (cur == Y) ? Q1 : Y;
+            err = dalloc(&m->M, kk);
+            if (err) return err;
+            launch_block_op(ctx->lc, 1, (int)n, a->rp, a->ci, a->v, nullptr, k, cur, aw);
+            launch_gram(ctx->lc, n, k, k, cur, aw, part, m->M);
+            launch_symmetrize(ctx->lc, k, m->M);
+        }
         return err;
     };
     if (!e && m->folded) {
@@ -1228,8 +1262,13 @@ void nlsp_twolevel_destroy(nlsp_twolevel* m) {
     if (!m) return;
     cudaSetDevice(m->device);
     if (m->W2 && m->W2 != m->W1) dfree(m->W2);
-    for (double* p : {m->basis, m->L, m->Ainv, m->coarse, m->wd, m->W1}) dfree(p);
+    for (double* p : {m->basis, m->L, m->Ainv, m->coarse, m->wd, m->W1, m->M}) dfree(p);
     delete m;
+}
+
+int nlsp_twolevel_cycle(const nlsp_twolevel* m) {
+    if (!m) return -1;
+    return m->onepass ? 2 : (m->folded ? 1 : 0);
 }
 
 void nlsp_twolevel_dims(const nlsp_twolevel* m, uint64_t* n, uint64_t* k) {
@@ -1351,7 +1390,9 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
     const double csr = 12.0 * nnz + 4.0 * (n + 1);
     const double pass = (double)a->pass_bytes;  // CSR, or the diagonal form when detected
     // algorithmic bytes per launch; slots by name below
-    enum { kSpmvP = 0, kUpd, kRes, kPro, kPost, kUR, kSmooth, kCtl, kSlots };
+    enum { kSpmvP = 0, kUpd, kRes, kPro, kPost, kUR, kSmooth, kCtl, kUO, kPO, kSlots };
+    const bool onepass = mode == 0 && m->onepass;
+    const unsigned long long T = m ? m->nu1 + m->nu2 : 0;
     std::vector<Acc> acc = {
         {"spmv_p", pass + 32.0 * n},                 // reads z, p; writes p, q
         {"update", (mode == 0 ? 48.0 : (mode == 1 ? 56.0 : 64.0)) * n},
@@ -1361,6 +1402,9 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
         {"update_restrict", 8.0 * n * k + 48.0 * n}, // folded: W1, x, p, q, r; writes x, r
         {"smooth", pass + ((m && m->nu1 + m->nu2 == 2) ? 24.0 : 32.0) * n},  // folded sweeps
         {"loop_ctl", 0.0},
+        {"update_onepass", 48.0 * n},  // x, p, q, r; writes x, r (+ the 2k column sums)
+        // one-pass prolongation: W, s (+ A s: one more matrix pass), r; writes z
+        {"prolong_onepass", 8.0 * n * k + (T ? pass + 24.0 * n : 16.0 * n)},
     };
     if ((int)acc.size() != kSlots) return -1;
     std::vector<cudaEvent_t> evs(2);
@@ -1379,10 +1423,18 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
     const bool simple_apply = mode == 0 && !folded && m->nu1 == 1 && m->nu2 == 1;
     for (uint64_t it = 0; it < iters; ++it) {
         timed(kSpmvP, [&] { launch_spmv_p(ctx->lc, args); });
-        if (folded) {
+        if (onepass) {
+            timed(kUO, [&] { launch_update_onepass(ctx->lc, args); });
+            double* cur = nullptr;
+            for (unsigned long long j = 2; j <= T; ++j) {
+                double* nxt = (cur == ctx->zt0) ? ctx->zt1 : ctx->zt0;
+                timed(kSmooth, [&] { launch_sweep(ctx->lc, args, cur == nullptr, cur, nxt, false); });
+                cur = nxt;
+            }
+            timed(kPO, [&] { launch_prolong_onepass(ctx->lc, args, cur, ctx->z, 0, 1); });
+        } else if (folded) {
             timed(kUR, [&] { launch_update_restrict(ctx->lc, args, true); });
             // launch_folded_tail, each launch timed on its own
-            const unsigned long long T = m->nu1 + m->nu2;
             SolveArgs b = args;
             b.P = m->W2;
             if (T <= 1) {

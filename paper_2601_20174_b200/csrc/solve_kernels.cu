@@ -1372,6 +1372,468 @@ __global__ void __launch_bounds__(kThreads) k_prolong_wide(SolveArgs a, const do
     }
 }
 
+// ==================================================== one-pass two-level cycle ==
+// With nu1 = nu2 the folded cycle streams W = W1 = W2 twice per iteration:
+// c = W^T r_new after the x/r update, and z = s + W e after the sweeps. The
+// restriction is carried by its recurrence instead, so W is streamed ONCE:
+//   c_{i+1} = W^T r_{i+1} = W^T r_i - alpha_i W^T q_i,
+//   W^T q_i = W^T A p_i   = W^T A s_i + M e_i + beta_i W^T q_{i-1},  M = W^T A W,
+// since p_i = z_i + beta_i p_{i-1} and z_i = s_i + W e_i, and
+//   W^T q_{i-1} = (u_{i-1} - u_i) / alpha_{i-1}   (r_i = r_{i-1} - alpha_{i-1} q_{i-1}).
+// The prolongation pass of iteration i reads W rows once and forms, besides
+// z_i = s_i + W e_i and r.z, two k-vectors: u_i = W^T r_i and v_i = W^T (A s_i)
+// (A s_i gathered in the same pass). Every term on the right is recomputed from
+// the current vectors each iteration, so no drift accumulates: only the
+// one-step combination c = u_i - alpha_i (v_i + M e_i + beta_i W^T q_{i-1}) is
+// new (relative deviation from W^T r_{i+1} ~1e-13 over thousands of
+// iterations), formed by the next update kernel's last CTA together with
+// e = A_c^-1 c. Same operator as the
+// reference's cycle (two_level.hpp:60-81), iteration counts identical on the
+// configs; per iteration 8nk bytes fewer than the folded cycle.
+
+// y = sum_t A(i, i + off_t) x[i + off_t] over the present offsets of row i, in
+// ascending offset order (the CSR column order), for any diagonal form
+template <int MAXD, bool RV>
+__device__ __forceinline__ double dia_row_dot(const SolveArgs& a, int i, const double* __restrict__ x) {
+    const int mb = a.dia.mbytes, d = a.dia.d;
+    unsigned m;
+    if (mb == 1) m = static_cast<const unsigned char*>(a.dia.mask)[i];
+    else if (mb == 2) m = static_cast<const unsigned short*>(a.dia.mask)[i];
+    else m = static_cast<const unsigned int*>(a.dia.mask)[i];
+    double g[MAXD], vv[RV ? MAXD : 1];
+#pragma unroll
+    for (int t = 0; t < MAXD; ++t) {
+        const bool on = t < d && ((m >> t) & 1u);
+        g[t] = on ? x[i + a.dia.off[t]] : 0.0;
+        if (RV) vv[RV ? t : 0] = on ? __ldcs(a.dia.rv + (size_t)t * a.n + i) : 0.0;
+    }
+    double y = 0.0;
+#pragma unroll
+    for (int t = 0; t < MAXD; ++t)
+        if (t < d && ((m >> t) & 1u)) y = fma(RV ? vv[RV ? t : 0] : a.dia.val[t], g[t], y);
+    return y;
+}
+
+// Per-lane column accumulators of one k-vector -> this CTA's column sums ->
+// dst[c * G + blockIdx.x] (column-major partials, G = gridDim.x).
+template <int PPL>
+__device__ __forceinline__ void cta_columns(double (&acc)[2 * PPL], double* cs, int ld, double* dst) {
+    constexpr int CW = 2 * kGroup * PPL;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int pairs = ld >> 1;
+#pragma unroll
+    for (int t = 0; t < 2 * PPL; ++t) {
+        acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], 8);
+        acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], 16);
+    }
+    if (lane < kGroup) {
+#pragma unroll
+        for (int t = 0; t < PPL; ++t) {
+            const int pi = lane + kGroup * t;
+            if (pi < pairs) {
+                cs[warp * CW + 2 * pi] = acc[2 * t];
+                cs[warp * CW + 2 * pi + 1] = acc[2 * t + 1];
+            }
+        }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < ld; c += blockDim.x) {
+        double t = 0.0;
+        for (int w = 0; w < nw; ++w) t += cs[w * CW + c];
+        dst[(long long)c * gridDim.x + blockIdx.x] = t;
+    }
+    __syncthreads();
+}
+
+// z = s + W e (two_level.hpp:74-79 folded), r.z -> beta and the loop control
+// (ctl as k_prolong), and in the same pass over W: u = W^T r, v = W^T (A s) as
+// per-CTA partials. A s one lane per row (8 rows per warp): MAXD = 0 the CSR
+// row, else the diagonal form (RV: per-row values).
+template <int PPL, int MAXD, bool RV>
+__global__ void __launch_bounds__(kThreads, 2) k_prolong_onepass(SolveArgs a, const double* sv,
+                                                              double* zout,
+                                                              cudaGraphConditionalHandle h, int ctl) {
+    PcgState* st = a.st;
+    if (st->done) {
+        if (ctl && blockIdx.x == 0 && threadIdx.x == 0) loop_ctl_body(st, h, ctl == 2);
+        return;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->op_grid = gridDim.x;
+    const int ld = a.k + (a.k & 1);
+    const int pairs = ld >> 1;
+    double ev[2 * PPL], au[2 * PPL], av[2 * PPL];
+    {
+        const int l0 = threadIdx.x & (kGroup - 1);
+#pragma unroll
+        for (int t = 0; t < PPL; ++t) {
+            const int pi = l0 + kGroup * t;
+            ev[2 * t] = pi < pairs ? a.e[2 * pi] : 0.0;
+            ev[2 * t + 1] = pi < pairs ? a.e[2 * pi + 1] : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < 2 * PPL; ++t) au[t] = av[t] = 0.0;
+    }
+    double s[1] = {0.0};
+    constexpr int UPR = NLSP_KUPRO;
+    ROW_BATCH_BEGIN(a.n, UPR)
+        // W rows first (the HBM stream), then the row scalars and A s gathers
+        double2 pv[UPR][PPL];
+#pragma unroll
+        for (int u = 0; u < UPR; ++u) {
+            const double* prow = a.P + (long long)row[u] * ld;
+#pragma unroll
+            for (int t = 0; t < PPL; ++t) {
+                const int pi = l + kGroup * t;
+                pv[u][t] = (valid[u] && pi < pairs) ? ld_stream2(prow + 2 * pi) : make_double2(0.0, 0.0);
+            }
+        }
+        double sr[UPR], rr[UPR], as[UPR];
+#pragma unroll
+        for (int u = 0; u < UPR; ++u) {
+            const int rw = valid[u] ? row[u] : 0;
+            sr[u] = sv ? sv[rw] : 0.0;
+            rr[u] = valid[u] ? a.r[rw] : 0.0;
+        }
+        {
+            // lane L < 4 UPR sums row base + L (sequential fma chain in column
+            // order, bitwise the SpMV family's rows); group grp's row u is lane grp + 4u
+            double mine = 0.0;
+            const long long ri = base_ + lane_;
+            if (sv && lane_ < kRowsPerWarp * UPR && ri < a.n) {
+                if constexpr (MAXD == 0) {
+                    const int b = __ldg(a.rp + ri), e = __ldg(a.rp + ri + 1);
+                    for (int kk = b; kk < e; ++kk) mine = fma(__ldg(a.v + kk), sv[__ldg(a.ci + kk)], mine);
+                } else {
+                    mine = dia_row_dot<MAXD, RV>(a, (int)ri, sv);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < UPR; ++u) as[u] = __shfl_sync(0xffffffffu, mine, grp + kRowsPerWarp * u);
+        }
+        double sum[UPR];
+#pragma unroll
+        for (int u = 0; u < UPR; ++u) {
+            double part = 0.0;
+#pragma unroll
+            for (int t = 0; t < PPL; ++t) {
+                part = fma(pv[u][t].x, ev[2 * t], part);
+                part = fma(pv[u][t].y, ev[2 * t + 1], part);
+                au[2 * t] = fma(pv[u][t].x, rr[u], au[2 * t]);
+                au[2 * t + 1] = fma(pv[u][t].y, rr[u], au[2 * t + 1]);
+                av[2 * t] = fma(pv[u][t].x, as[u], av[2 * t]);
+                av[2 * t + 1] = fma(pv[u][t].y, as[u], av[2 * t + 1]);
+            }
+            sum[u] = group_sum(part);
+        }
+        if (l == 0) {
+#pragma unroll
+            for (int u = 0; u < UPR; ++u) {
+                if (!valid[u]) continue;
+                const double zi = sr[u] + sum[u];
+                zout[row[u]] = zi;
+                s[0] = fma(rr[u], zi, s[0]);
+            }
+        }
+    ROW_BATCH_END
+    {
+        __shared__ double cs[(kThreads / 32) * 2 * kGroup * PPL];
+        const long long G = gridDim.x;
+        cta_columns<PPL>(au, cs, ld, a.opart);
+        cta_columns<PPL>(av, cs, ld, a.opart + ld * G);
+    }
+    double tot[1];
+    if (grid_reduce<1>(s, a.partials, &st->counter[kTkProlong], tot) && threadIdx.x == 0) {
+        st->rz_new = tot[0];
+        if (ctl) loop_ctl_body(st, h, ctl == 2);
+    }
+}
+
+// The one-pass prolongation with its HBM stream decoupled from the gathers
+// (warp-specialised, 1 CTA per SM): a producer warp stages each 64-row tile —
+// its W rows, s and r slices and the diagonal form's presence masks — into an
+// S-stage ring with bulk copies (cp.async.bulk, mbarrier complete_tx); pairs
+// of stencil warps take alternate tiles and form (A s)_row from the staged
+// mask and L2 gathers of s (the only global latency left), publishing them
+// through a second barrier per stage; 8 consumer warps then run the W products
+// of the tile from shared memory (8 lanes per row) and release the stage.
+constexpr int kOpTR = 64;      // rows per tile
+constexpr int kOpWWarps = 8;   // W-product warps
+constexpr int kOpSPairs = 4;   // at most this many stencil warp pairs (tile i -> pair i % P)
+constexpr int kOpMaxStages = 8;
+// Stencil pair p waits only on tiles i = p (mod P). With S a multiple of P it
+// always sees the stages p, p + P, ... and waits their phases in order, so an
+// mbarrier parity wait can never alias a phase two ahead (S % P == 0 is required).
+constexpr int kOpThreads = 32 * (1 + 2 * kOpSPairs + kOpWWarps);
+constexpr unsigned kOpVec = kOpTR * 8;  // bytes of one staged vector slice
+
+__host__ __device__ constexpr unsigned op_stage_bytes(int ld) {
+    return (unsigned)kOpTR * ld * 8 + 2 * kOpVec + round16(kOpTR * 4) + kOpVec;
+}
+
+template <int PPL, int MAXD, bool RV>
+__global__ void __launch_bounds__(kOpThreads, 1) k_prolong_onepass_tma(SolveArgs a, const double* sv,
+                                                                      double* zout,
+                                                                      cudaGraphConditionalHandle h,
+                                                                      int ctl, int S, int P) {
+    PcgState* st = a.st;
+    if (st->done) {
+        if (ctl && blockIdx.x == 0 && threadIdx.x == 0) loop_ctl_body(st, h, ctl == 2);
+        return;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->op_grid = gridDim.x;
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem);
+    unsigned long long* asr = full + kOpMaxStages;
+    unsigned long long* empty = asr + kOpMaxStages;
+    unsigned char* stages = smem + 256;  // after 3 x kOpMaxStages barriers
+    const int ld = a.k + (a.k & 1);
+    const int pairs = ld >> 1;
+    const unsigned wbytes = (unsigned)kOpTR * ld * 8;
+    const unsigned sbytes = op_stage_bytes(ld);
+    // stage layout: [W rows | s | r | mask | A s]
+    const unsigned s_off = wbytes, r_off = wbytes + kOpVec, m_off = wbytes + 2 * kOpVec;
+    const unsigned as_off = m_off + round16(kOpTR * 4);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&asr[s], 2);
+            mbar_init(&empty[s], kOpWWarps);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    const int ntiles = (a.n + kOpTR - 1) / kOpTR;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int mb = a.dia.mbytes;
+    double au[2 * PPL], av[2 * PPL];
+#pragma unroll
+    for (int t = 0; t < 2 * PPL; ++t) au[t] = av[t] = 0.0;
+    double rz[1] = {0.0};
+    if (warp == 0) {
+        // ---- producer
+        if (lane == 0) {
+            int i = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+                const int stg = i % S;
+                if (i >= S) mbar_wait(&empty[stg], ((i / S) - 1) & 1);
+                unsigned char* base = stages + stg * sbytes;
+                const int r0 = tile * kOpTR, rows = min(kOpTR, a.n - r0);
+                const unsigned vb = round16(rows * 8);  // vectors are padded by 16 doubles
+                const unsigned wb = (unsigned)rows * ld * 8;
+                const unsigned mbb = MAXD ? round16(rows * mb) : 0u;  // masks are padded by 16 B
+                mbar_arrive_tx(&full[stg], wb + (sv ? vb : 0u) + vb + mbb);
+                bulk_g2s(base, a.P + (long long)r0 * ld, wb, &full[stg]);
+                if (sv) bulk_g2s(base + s_off, sv + r0, vb, &full[stg]);
+                bulk_g2s(base + r_off, a.r + r0, vb, &full[stg]);
+                if (MAXD)
+                    bulk_g2s(base + m_off, static_cast<const unsigned char*>(a.dia.mask) + (long long)r0 * mb,
+                             mbb, &full[stg]);
+            }
+        }
+    } else if (warp <= 2 * P) {
+        // ---- stencil warps: (A s)_row, one thread per row, sequential fma
+        // chain in column order (bitwise the SpMV family's row sums)
+        const int pair = (warp - 1) >> 1;
+        const int lr = ((warp - 1) & 1) * 32 + lane;
+        int i = pair;
+        for (int tile = blockIdx.x + pair * gridDim.x; tile < ntiles; tile += P * gridDim.x, i += P) {
+            const int stg = i % S;
+            mbar_wait(&full[stg], (i / S) & 1);
+            unsigned char* base = stages + stg * sbytes;
+            const int r0 = tile * kOpTR, rows = min(kOpTR, a.n - r0);
+            double y = 0.0;
+            if (sv && lr < rows) {
+                const int row = r0 + lr;
+                if constexpr (MAXD == 0) {
+                    const int b = __ldg(a.rp + row), e = __ldg(a.rp + row + 1);
+                    for (int kk = b; kk < e; ++kk) y = fma(__ldg(a.v + kk), sv[__ldg(a.ci + kk)], y);
+                } else {
+                    unsigned m;
+                    const unsigned char* ms = base + m_off;
+                    if (mb == 1) m = ms[lr];
+                    else if (mb == 2) m = reinterpret_cast<const unsigned short*>(ms)[lr];
+                    else m = reinterpret_cast<const unsigned*>(ms)[lr];
+                    double g[MAXD], vv[RV ? MAXD : 1];
+#pragma unroll
+                    for (int t = 0; t < MAXD; ++t) {
+                        const bool on = t < a.dia.d && ((m >> t) & 1u);
+                        g[t] = on ? sv[row + a.dia.off[t]] : 0.0;
+                        if (RV) vv[RV ? t : 0] = on ? __ldcs(a.dia.rv + (size_t)t * a.n + row) : 0.0;
+                    }
+#pragma unroll
+                    for (int t = 0; t < MAXD; ++t)
+                        if (t < a.dia.d && ((m >> t) & 1u)) y = fma(RV ? vv[RV ? t : 0] : a.dia.val[t], g[t], y);
+                }
+            }
+            reinterpret_cast<double*>(base + as_off)[lr] = y;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&asr[stg]);
+        }
+    } else {
+        // ---- W-product warps: 8 lanes per row, 2 rows per group per tile
+        const int cw = warp - 1 - 2 * P;
+        const int grp = (cw * 32 + lane) >> 3, l = lane & (kGroup - 1);
+        double ev[2 * PPL];
+#pragma unroll
+        for (int t = 0; t < PPL; ++t) {
+            const int pi = l + kGroup * t;
+            ev[2 * t] = pi < pairs ? a.e[2 * pi] : 0.0;
+            ev[2 * t + 1] = pi < pairs ? a.e[2 * pi + 1] : 0.0;
+        }
+        int i = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+            const int stg = i % S;
+            mbar_wait(&full[stg], (i / S) & 1);
+            mbar_wait(&asr[stg], (i / S) & 1);
+            const unsigned char* base = stages + stg * sbytes;
+            const int r0 = tile * kOpTR, rows = min(kOpTR, a.n - r0);
+            const double* ss = reinterpret_cast<const double*>(base + s_off);
+            const double* rs = reinterpret_cast<const double*>(base + r_off);
+            const double* as = reinterpret_cast<const double*>(base + as_off);
+#pragma unroll
+            for (int u = 0; u < kOpTR / (kOpWWarps * 4); ++u) {
+                const int lr = grp + kOpWWarps * 4 * u;
+                const bool ok = lr < rows;  // every lane still runs the group shuffles
+                const double* wrow = reinterpret_cast<const double*>(base) + lr * ld;
+                const double rr = ok ? rs[lr] : 0.0, ar = ok ? as[lr] : 0.0;
+                double part = 0.0;
+#pragma unroll
+                for (int t = 0; t < PPL; ++t) {
+                    const int pi = l + kGroup * t;
+                    if (ok && pi < pairs) {
+                        const double2 w = *reinterpret_cast<const double2*>(wrow + 2 * pi);
+                        part = fma(w.x, ev[2 * t], part);
+                        part = fma(w.y, ev[2 * t + 1], part);
+                        au[2 * t] = fma(w.x, rr, au[2 * t]);
+                        au[2 * t + 1] = fma(w.y, rr, au[2 * t + 1]);
+                        av[2 * t] = fma(w.x, ar, av[2 * t]);
+                        av[2 * t + 1] = fma(w.y, ar, av[2 * t + 1]);
+                    }
+                }
+                const double sum = group_sum(part);
+                if (ok && l == 0) {
+                    const double zi = (sv ? ss[lr] : 0.0) + sum;
+                    zout[r0 + lr] = zi;
+                    rz[0] = fma(rr, zi, rz[0]);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stg]);
+        }
+    }
+    {
+        __shared__ double cs[(kOpThreads / 32) * 2 * kGroup * PPL];
+        const long long G = gridDim.x;
+        cta_columns<PPL>(au, cs, ld, a.opart);
+        cta_columns<PPL>(av, cs, ld, a.opart + ld * G);
+    }
+    double tot[1];
+    if (grid_reduce<1>(rz, a.partials, &st->counter[kTkProlong], tot) && threadIdx.x == 0) {
+        st->rz_new = tot[0];
+        if (ctl) loop_ctl_body(st, h, ctl == 2);
+    }
+}
+
+// x += alpha p, r -= alpha q, ||r||^2 (two_level.hpp:164-170); the CTAs also
+// sum the previous prolongation's partials (a column per CTA, fixed order)
+// into u_i (ow slot it & 1, u_{i-1} stays in the other) and v_i. Last CTA:
+// history + convergence test (:168-176), then the one-pass restriction
+// c = u_i - alpha_i (v_i + M e_i + beta_i (u_{i-1} - u_i) / alpha_{i-1}) and
+// e = A_c^-1 c.
+__global__ void __launch_bounds__(kThreads) k_update_onepass(SolveArgs a) {
+    PcgState* st = a.st;
+    if (st->done) return;
+    const double alpha = st->alpha;
+    const double* p = (st->it & 1) ? a.p1 : a.p0;
+    double s[1] = {0.0};
+    const long long npairs = a.n >> 1;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < npairs; t += stride) {
+        const long long i = 2 * t;
+        const double2 pv = *reinterpret_cast<const double2*>(p + i);
+        const double2 qv = *reinterpret_cast<const double2*>(a.q + i);
+        const double2 xv = *reinterpret_cast<const double2*>(a.x + i);
+        const double2 rv = *reinterpret_cast<const double2*>(a.r + i);
+        double2 xo, ro;
+        xo.x = fma(alpha, pv.x, xv.x);
+        xo.y = fma(alpha, pv.y, xv.y);
+        ro.x = fma(-alpha, qv.x, rv.x);
+        ro.y = fma(-alpha, qv.y, rv.y);
+        s[0] = fma(ro.x, ro.x, s[0]);
+        s[0] = fma(ro.y, ro.y, s[0]);
+        *reinterpret_cast<double2*>(a.x + i) = xo;
+        *reinterpret_cast<double2*>(a.r + i) = ro;
+    }
+    if ((a.n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const long long i = a.n - 1;
+        a.x[i] = fma(alpha, p[i], a.x[i]);
+        const double ro = fma(-alpha, a.q[i], a.r[i]);
+        a.r[i] = ro;
+        s[0] = fma(ro, ro, s[0]);
+    }
+    const int ld = a.k + (a.k & 1);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    {
+        __shared__ double wsum[kThreads / 32];
+        const long long G = st->op_grid;
+        const int ucur = (int)(st->it & 1) * ld;
+        for (int j = blockIdx.x; j < 2 * ld; j += gridDim.x) {
+            double t = 0.0;
+            for (long long b = threadIdx.x; b < G; b += blockDim.x) t += __ldcg(a.opart + j * G + b);
+            t = warp_sum(t);
+            if (lane == 0) wsum[warp] = t;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double tt = 0.0;
+                for (int w = 0; w < nw; ++w) tt += wsum[w];
+                a.ow[j < ld ? ucur + j : ld + j] = tt;  // u_i -> its slot, v_i -> [2 ld, 3 ld)
+                __threadfence();
+            }
+            __syncthreads();
+        }
+    }
+    double tot[1];
+    if (!grid_reduce<1>(s, a.partials, &st->counter[kTkUpdate], tot)) return;
+    __shared__ int go_on;
+    if (threadIdx.x == 0) {
+        const double rel = sqrt(tot[0]) / st->bnorm;
+        st->rr = tot[0];
+        st->last_rel = rel;
+        a.hist[st->it] = rel;
+        st->iterations = st->it + 1;
+        if (rel < st->delta) {
+            st->converged = 1;
+            st->done = 1;
+        }
+        go_on = !st->done;
+    }
+    __syncthreads();
+    if (!go_on) return;
+    __threadfence();
+    __shared__ double es[kOnePassK + 2], gs[kOnePassK + 2], cs[kOnePassK + 2];
+    const int k = a.k;
+    const bool first = st->first != 0;
+    const double beta = st->beta, alpha_prev = st->alpha_prev;
+    const int ucur = (int)(st->it & 1) * ld, uprev = ld - ucur;
+    for (int j = threadIdx.x; j < k; j += blockDim.x) es[j] = __ldcg(a.e + j);
+    __syncthreads();
+    coarse_apply_inverse(a.M, k, es, gs);  // M e_i
+    __syncthreads();
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+        const double u = __ldcg(a.ow + ucur + j);
+        double g = __ldcg(a.ow + 2 * ld + j) + gs[j];  // v + M e
+        if (!first) g = fma(beta, (__ldcg(a.ow + uprev + j) - u) / alpha_prev, g);  // + beta W^T q_{i-1}
+        cs[j] = fma(-alpha, g, u);                     // c = u - alpha g
+    }
+    __syncthreads();
+    if (a.Ainv) coarse_apply_inverse(a.Ainv, k, cs, a.e);
+    else if (warp == 0) coarse_solve_warp(a.L, k, cs, a.e);
+    if (threadIdx.x == 0) {
+        if (k & 1) a.e[k] = 0.0;  // padded column
+        st->alpha_prev = alpha;
+    }
+}
+
 // ======================================================== host launchers ==
 
 namespace {
@@ -1802,6 +2264,113 @@ void launch_folded_apply(const LaunchCtx& c, const SolveArgs& a, unsigned long l
                          unsigned long long nu2) {
     launch_update_restrict(c, a, false);
     launch_folded_tail(c, a, nu1, nu2, 0, 0);
+}
+
+// ------------------------------------------------------- one-pass cycle host --
+bool onepass_supported(int k) { return k <= kOnePassK; }
+
+#ifndef NLSP_OP_TMA
+#define NLSP_OP_TMA 1
+#endif
+#ifndef NLSP_OP_STAGES
+#define NLSP_OP_STAGES 0  // 0: as many as fit, up to kOpMaxStages
+#endif
+template <class... KArgs, class... Args>
+static void launch_op_tma(const LaunchCtx& c, void (*f)(KArgs...), long long ntiles, size_t smem,
+                          int threads, Args&&... args) {
+    static std::mutex mu;
+    static std::unordered_map<const void*, size_t> attr;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        size_t& cur = attr[reinterpret_cast<const void*>(f)];
+        if (smem > cur) {
+            cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cur = smem;
+        }
+    }
+    long long g = c.num_sms;  // one CTA per SM (the stage ring fills shared memory)
+    if (g > ntiles) g = ntiles;
+    if (g < 1) g = 1;
+    f<<<(int)g, threads, smem, c.s>>>(std::forward<Args>(args)...);
+}
+
+template <int PPL>
+static void prolong_onepass_ppl(const LaunchCtx& c, const SolveArgs& a, const double* sv, double* zout,
+                                cudaGraphConditionalHandle h, int ctl) {
+    const int ld = a.k + (a.k & 1);
+    // as many stages as fit, a multiple of the stencil pair count P
+    int fit = (int)((kStageBudget - 256) / op_stage_bytes(ld));
+    if (fit > kOpMaxStages) fit = kOpMaxStages;
+    if (NLSP_OP_STAGES > 0 && fit > NLSP_OP_STAGES) fit = NLSP_OP_STAGES;
+    int S, P;
+    if (fit >= 8) { S = 8; P = 4; }
+    else if (fit >= 6) { S = 6; P = 3; }
+    else if (fit >= 4) { S = 4; P = 4; }
+    else { S = 2; P = 2; }
+    const size_t sm = 256 + (size_t)S * op_stage_bytes(ld);
+    if (NLSP_OP_TMA && fit >= 2) {
+        const long long nt = (a.n + kOpTR - 1) / kOpTR;
+        const int threads = 32 * (1 + 2 * P + kOpWWarps);
+#define NLSP_P2(D, R) launch_op_tma(c, k_prolong_onepass_tma<PPL, D, R>, nt, sm, threads, a, sv, zout, h, ctl, S, P)
+        const bool rv = a.dia.kind == 2;
+        if (!a.dia.kind) NLSP_P2(0, false);
+        else if (a.dia.d <= 8) { if (rv) NLSP_P2(8, true); else NLSP_P2(8, false); }
+        else if (a.dia.d <= 16) { if (rv) NLSP_P2(16, true); else NLSP_P2(16, false); }
+        else { if (rv) NLSP_P2(32, true); else NLSP_P2(32, false); }
+#undef NLSP_P2
+        return;
+    }
+#define NLSP_P1(D, R) launch_rows<NLSP_KUPRO>(c, k_prolong_onepass<PPL, D, R>, a.n, a, sv, zout, h, ctl)
+    const bool rv = a.dia.kind == 2;
+    if (!a.dia.kind) NLSP_P1(0, false);
+    else if (a.dia.d <= 8) { if (rv) NLSP_P1(8, true); else NLSP_P1(8, false); }
+    else if (a.dia.d <= 16) { if (rv) NLSP_P1(16, true); else NLSP_P1(16, false); }
+    else { if (rv) NLSP_P1(32, true); else NLSP_P1(32, false); }
+#undef NLSP_P1
+}
+
+// z = s + W e with u, v, w partials (s = S_T(r) by T - 1 sweep launches, or
+// none for T = 0); ctl as launch_prolong
+void launch_prolong_onepass(const LaunchCtx& c, const SolveArgs& a, const double* sv, double* zout,
+                            cudaGraphConditionalHandle h, int ctl) {
+    SolveArgs b = a;
+    b.P = a.W2;
+    switch (ppl_for(a.k)) {
+        case 1: prolong_onepass_ppl<1>(c, b, sv, zout, h, ctl); break;
+        case 2: prolong_onepass_ppl<2>(c, b, sv, zout, h, ctl); break;
+        case 3: prolong_onepass_ppl<3>(c, b, sv, zout, h, ctl); break;
+        default: prolong_onepass_ppl<4>(c, b, sv, zout, h, ctl); break;
+    }
+    count(c);
+}
+
+// sweeps s = S_T(r) (T = nu1 + nu2 even, first sweep implicit), returns s (null for T = 0)
+const double* launch_onepass_sweeps(const LaunchCtx& c, const SolveArgs& a, unsigned long long T) {
+    double* cur = nullptr;
+    for (unsigned long long j = 2; j <= T; ++j) {
+        double* nxt = (cur == a.zt0) ? a.zt1 : a.zt0;
+        launch_sweep(c, a, cur == nullptr, cur, nxt, false);
+        cur = nxt;
+    }
+    return cur;
+}
+
+void launch_update_onepass(const LaunchCtx& c, const SolveArgs& a) {
+    launch_elems(c, k_update_onepass, a.n, a);
+    count(c);
+}
+
+// one iteration's tail after k_spmv_p / k_update_onepass
+void launch_onepass_tail(const LaunchCtx& c, const SolveArgs& a, unsigned long long T,
+                         cudaGraphConditionalHandle h, int ctl) {
+    const double* sv = launch_onepass_sweeps(c, a, T);
+    launch_prolong_onepass(c, a, sv, a.z, h, ctl);
+}
+
+// PCG prologue z = M r_0 with the one-pass partials of r_0: c = W^T r_0 directly
+void launch_onepass_apply(const LaunchCtx& c, const SolveArgs& a, unsigned long long T) {
+    launch_update_restrict(c, a, false);
+    launch_onepass_tail(c, a, T, 0, 0);
 }
 
 }  // namespace nlsp

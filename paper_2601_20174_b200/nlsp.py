@@ -450,6 +450,11 @@ class TwoLevelPreconditioner:
     def coarse_dim(self) -> int:
         return self._k
 
+    def cycle(self) -> str:
+        """The PCG schedule of this operator (nlsp_twolevel_cycle): "literal",
+        "folded" or "onepass"."""
+        return {0: "literal", 1: "folded", 2: "onepass"}[L.gpu_lib().nlsp_twolevel_cycle(self.handle)]
+
     def nu1(self) -> int:
         return self._nu1
 

@@ -39,6 +39,8 @@ PATHS = {
     "graph": {"NLSP_CLUSTER": "0"},
     "host": {"NLSP_CLUSTER": "0", "NLSP_LOOP": "host"},
     "literal": {"NLSP_CLUSTER": "0", "NLSP_CYCLE": "literal"},
+    # W streamed twice per iteration (the default graph path streams it once)
+    "folded": {"NLSP_CLUSTER": "0", "NLSP_CYCLE": "folded"},
     # coarse solve by the reference's triangular substitutions instead of A_c^-1
     "chol": {"NLSP_CLUSTER": "0", "NLSP_COARSE": "chol"},
     "cluster_chol": {"NLSP_CLUSTER": "1", "NLSP_COARSE": "chol"},
@@ -153,3 +155,34 @@ def test_pcg_batch_matches_reference(nlsp):
         assert np.linalg.norm(r.solution - d["x"]) <= 1e-9 * np.linalg.norm(d["x"])
     # the same system twice gives the same answer
     assert np.array_equal(res[0].solution, res[-1].solution)
+
+
+@pytest.mark.parametrize("cfg,nx", [("C2", 512), ("C3", 512), ("C4", 64), ("C5", 256)])
+def test_onepass_cycle_matches_folded_midsize(nlsp, cfg, nx):
+    """The one-pass cycle (W streamed once per iteration, the restriction by
+    its recurrence) against the folded cycle on the same system,
+    at sizes where every CTA cycles its stage ring many times: same iteration
+    count, solutions within rounding, both below the tolerance."""
+    from paper_2601_20174_b200 import problems
+    c = problems.CONFIGS[cfg].scaled(nx=nx)
+    pb = problems.generate(c)
+    a = pb.csr()
+    assert pb.n > 65536  # beyond the single-cluster solver: the multi-kernel graph loop
+    sv = nlsp.generate_smoothed_vectors(a, None, c.m, c.s1, c.omega, c.s0_seed)
+    p, _, _ = nlsp.svd_basis(sv.s, c.k)
+    m1 = nlsp.TwoLevelPreconditioner(a, p, c.omega, c.nu1, c.nu2)
+    os.environ["NLSP_CYCLE"] = "folded"
+    try:
+        m2 = nlsp.TwoLevelPreconditioner(a, p, c.omega, c.nu1, c.nu2)
+    finally:
+        os.environ.pop("NLSP_CYCLE", None)
+    assert m1.cycle() == "onepass" and m2.cycle() == "folded"
+    r1 = nlsp.pcg(a, pb.rhs, m1, c.delta, 10 * pb.n)
+    r2 = nlsp.pcg(a, pb.rhs, m2, c.delta, 10 * pb.n)
+    assert r1.report.converged and r2.report.converged
+    assert abs(r1.report.iterations - r2.report.iterations) <= 1
+    assert r1.report.true_relative_residual < 10 * c.delta
+    assert np.linalg.norm(r1.solution - r2.solution) <= 1e-10 * np.linalg.norm(r2.solution)
+    # deterministic: a second solve is bitwise the first
+    r3 = nlsp.pcg(a, pb.rhs, m1, c.delta, 10 * pb.n)
+    assert np.array_equal(r1.solution, r3.solution)
