@@ -158,7 +158,8 @@ def byte_model(n, nnz, k, nu1, nu2, pass_bytes=None, cycle="onepass"):
     W1 (8nk + 48n), nu1+nu2-1 smoothing sweeps (A + 24n for the first, A + 32n
     after), prolongation through W2 with r.z (8nk + 24n). One-pass cycle
     (nu1 == nu2): spmv_p (A + 32n), x/r update (48n), the same sweeps, and ONE
-    pass over W that also gathers A s (8nk + A + 24n; 8nk + 16n without sweeps).
+    pass over W that also gathers A s (8nk + A + 24n; 8nk + 16n without sweeps);
+    at nu1 = nu2 = 1 the update and the sweeps are one kernel (A + 64n).
     A = the matrix bytes one pass streams: CSR 12 nnz + 4(n+1), or the diagonal
     form's own bytes when the upload detected one (nlsp_csr_format; SURVEY
     §8d's rule for stencil-specialised kernels)."""
@@ -170,6 +171,8 @@ def byte_model(n, nnz, k, nu1, nu2, pass_bytes=None, cycle="onepass"):
         sweeps = (csr + 24.0 * n) + (t - 2) * (csr + 32.0 * n)
     if cycle == "onepass":
         pro = 8.0 * n * ld + ((csr + 24.0 * n) if t >= 1 else 16.0 * n)
+        if t == 2:  # x/r update fused with the sweeps: A + 64n (x, p, q, r, w; writes x, r', s)
+            return (csr + 32.0 * n) + (csr + 64.0 * n) + pro
         return (csr + 32.0 * n) + 48.0 * n + sweeps + pro
     pro = 8.0 * n * ld + (24.0 if t >= 1 else 16.0) * n
     return (csr + 32.0 * n) + (8.0 * n * ld + 48.0 * n) + sweeps + pro

@@ -75,6 +75,7 @@ struct SolveArgs {
     const int* ci;
     const double* v;
     const double* wd;    // omega * (1 / A_ii)    (two-level smoother)
+    double wdc;          // wd when it is one constant (constant-coefficient diagonal form), else 0
     const double* diag;  // A_ii                   (Jacobi preconditioner)
     const double* P;     // basis, n x k row-major, ld = k
     const double* L;     // Cholesky factor of A_c, k x k row-major
@@ -88,6 +89,7 @@ struct SolveArgs {
     int max_row;      // longest CSR row
     double* x;
     double* r;
+    double* r1;          // second residual buffer (fused update + sweep, by iteration parity)
     double* q;
     double* z;
     double* p0;

@@ -43,7 +43,11 @@ void launch_folded_tail(const LaunchCtx&, const SolveArgs&, unsigned long long, 
 void launch_folded_apply(const LaunchCtx&, const SolveArgs&, unsigned long long, unsigned long long);
 bool onepass_supported(int k);
 void launch_prolong_onepass(const LaunchCtx&, const SolveArgs&, const double*, double*,
-                            cudaGraphConditionalHandle, int);
+                            cudaGraphConditionalHandle, int, int);
+bool update_sweep_ok(const SolveArgs&, unsigned long long);
+void launch_update_sweep(const LaunchCtx&, const SolveArgs&);
+void launch_onepass_iteration_tail(const LaunchCtx&, const SolveArgs&, unsigned long long,
+                                   cudaGraphConditionalHandle, int);
 const double* launch_onepass_sweeps(const LaunchCtx&, const SolveArgs&, unsigned long long);
 void launch_update_onepass(const LaunchCtx&, const SolveArgs&);
 void launch_onepass_tail(const LaunchCtx&, const SolveArgs&, unsigned long long, cudaGraphConditionalHandle, int);
@@ -162,7 +166,7 @@ struct nlsp_ctx {
     // workspace (sized for ws_n rows, ws_ld coarse columns, ws_hist history)
     long long ws_n = 0, ws_hist = 0;
     long long ws_gen = 0;
-    double *x = nullptr, *r = nullptr, *q = nullptr, *z = nullptr, *p0 = nullptr, *p1 = nullptr,
+    double *x = nullptr, *r = nullptr, *r1 = nullptr, *q = nullptr, *z = nullptr, *p0 = nullptr, *p1 = nullptr,
            *zt0 = nullptr, *zt1 = nullptr, *b = nullptr, *e = nullptr, *partials = nullptr,
            *hist = nullptr;
     double *ow = nullptr, *opart = nullptr;  // one-pass cycle: [u | v | w], per-CTA partials
@@ -280,7 +284,7 @@ nlsp_status bind(nlsp_ctx* ctx) {
 }
 
 void free_ws(nlsp_ctx* c) {
-    for (double** p : {&c->x, &c->r, &c->q, &c->z, &c->p0, &c->p1, &c->zt0, &c->zt1, &c->b,
+    for (double** p : {&c->x, &c->r, &c->r1, &c->q, &c->z, &c->p0, &c->p1, &c->zt0, &c->zt1, &c->b,
                        &c->e, &c->partials, &c->hist, &c->ow, &c->opart}) {
         dfree(*p);
         *p = nullptr;
@@ -294,7 +298,7 @@ nlsp_status ensure_ws(nlsp_ctx* ctx, long long n, long long hist) {
     if (n > ctx->ws_n) {
         const long long hist_keep = ctx->ws_hist;
         free_ws(ctx);
-        for (double** p : {&ctx->x, &ctx->r, &ctx->q, &ctx->z, &ctx->p0, &ctx->p1, &ctx->zt0,
+        for (double** p : {&ctx->x, &ctx->r, &ctx->r1, &ctx->q, &ctx->z, &ctx->p0, &ctx->p1, &ctx->zt0,
                            &ctx->zt1, &ctx->b})
             CU(dalloc(p, (size_t)n + 16));  // padded for 16-B bulk copies of tile slices
         CU(dalloc(&ctx->e, (size_t)kMaxCoarse + 2));
@@ -331,6 +335,13 @@ SolveArgs make_args(nlsp_ctx* c, const nlsp_csr* a, const nlsp_twolevel* m) {
     s.max_row = a->max_row;
     s.dia = a->dia;
     s.wd = m ? m->wd : nullptr;
+    s.wdc = 0.0;
+    if (m && a->dia.kind == 1) {
+        // every stored entry on an offset is bitwise equal, so every row's
+        // omega * (1 / A_ii) (k_wd) is this one value
+        for (int t = 0; t < a->dia.d; ++t)
+            if (a->dia.off[t] == 0 && a->dia.val[t] > 0.0) s.wdc = m->omega * (1.0 / a->dia.val[t]);
+    }
     s.P = m ? m->basis : nullptr;
     s.L = m ? m->L : nullptr;
     s.Ainv = (m && (c->coarse_inverse || m->k > kWideK)) ? m->Ainv : nullptr;
@@ -339,6 +350,7 @@ SolveArgs make_args(nlsp_ctx* c, const nlsp_csr* a, const nlsp_twolevel* m) {
     s.k = m ? m->k : 0;
     s.x = c->x;
     s.r = c->r;
+    s.r1 = c->r1;
     s.q = c->q;
     s.z = c->z;
     s.p0 = c->p0;
@@ -361,8 +373,8 @@ void enqueue_iteration(const LaunchCtx& lc, const SolveArgs& a, int mode, const 
                        cudaGraphConditionalHandle h, int use_cond) {
     launch_spmv_p(lc, a);
     if (mode == 0 && m->onepass) {
-        launch_update_onepass(lc, a);  // x, r, ||r||, c by its recurrence, e
-        launch_onepass_tail(lc, a, m->nu1 + m->nu2, h, use_cond ? 2 : 1);
+        // x, r, ||r||, c by its recurrence, e (+ the sweeps when fused); prolongation
+        launch_onepass_iteration_tail(lc, a, m->nu1 + m->nu2, h, use_cond ? 2 : 1);
         return;
     }
     if (mode == 0 && m->folded) {
@@ -1390,7 +1402,7 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
     const double csr = 12.0 * nnz + 4.0 * (n + 1);
     const double pass = (double)a->pass_bytes;  // CSR, or the diagonal form when detected
     // algorithmic bytes per launch; slots by name below
-    enum { kSpmvP = 0, kUpd, kRes, kPro, kPost, kUR, kSmooth, kCtl, kUO, kPO, kSlots };
+    enum { kSpmvP = 0, kUpd, kRes, kPro, kPost, kUR, kSmooth, kCtl, kUO, kPO, kUS, kSlots };
     const bool onepass = mode == 0 && m->onepass;
     const unsigned long long T = m ? m->nu1 + m->nu2 : 0;
     std::vector<Acc> acc = {
@@ -1405,6 +1417,8 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
         {"update_onepass", 48.0 * n},  // x, p, q, r; writes x, r (+ the 2k column sums)
         // one-pass prolongation: W, s (+ A s: one more matrix pass), r; writes z
         {"prolong_onepass", 8.0 * n * k + (T ? pass + 24.0 * n : 16.0 * n)},
+        // x/r update fused with the T = 2 sweeps: A, x, p, q, r, w; writes x, r', s
+        {"update_sweep", pass + 64.0 * n},
     };
     if ((int)acc.size() != kSlots) return -1;
     std::vector<cudaEvent_t> evs(2);
@@ -1423,7 +1437,10 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
     const bool simple_apply = mode == 0 && !folded && m->nu1 == 1 && m->nu2 == 1;
     for (uint64_t it = 0; it < iters; ++it) {
         timed(kSpmvP, [&] { launch_spmv_p(ctx->lc, args); });
-        if (onepass) {
+        if (onepass && update_sweep_ok(args, T)) {
+            timed(kUS, [&] { launch_update_sweep(ctx->lc, args); });
+            timed(kPO, [&] { launch_prolong_onepass(ctx->lc, args, ctx->zt0, ctx->z, 0, 1, 1); });
+        } else if (onepass) {
             timed(kUO, [&] { launch_update_onepass(ctx->lc, args); });
             double* cur = nullptr;
             for (unsigned long long j = 2; j <= T; ++j) {
@@ -1431,7 +1448,7 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
                 timed(kSmooth, [&] { launch_sweep(ctx->lc, args, cur == nullptr, cur, nxt, false); });
                 cur = nxt;
             }
-            timed(kPO, [&] { launch_prolong_onepass(ctx->lc, args, cur, ctx->z, 0, 1); });
+            timed(kPO, [&] { launch_prolong_onepass(ctx->lc, args, cur, ctx->z, 0, 1, 0); });
         } else if (folded) {
             timed(kUR, [&] { launch_update_restrict(ctx->lc, args, true); });
             // launch_folded_tail, each launch timed on its own

@@ -17,6 +17,7 @@
 // the row's k basis entries as 16-B loads, so the SpMV result of a row is
 // already in the registers of the lanes that stream that row of P.
 #include <mutex>
+#include <type_traits>
 #include <unordered_map>
 #include <utility>
 
@@ -69,11 +70,17 @@ struct GPupd {
     }
 };
 // first pre-sweep from z = 0: z_j = (w dinv_j)(r_j - 0) (smoothing.hpp:40 with x = 0)
-struct GWdr {
+// CW: w D^-1 is the constant wc (constant-coefficient diagonal form, bitwise
+// equal to every wd[j]), so only r is gathered
+template <bool CW = false>
+struct GWdrT {
     const double* wd;
     const double* r;
-    __device__ __forceinline__ double operator()(int j) const { return wd[j] * r[j]; }
+    double wc = 0.0;
+    __device__ __forceinline__ double operator()(int j) const { return (CW ? wc : wd[j]) * r[j]; }
 };
+using GWdr = GWdrT<false>;
+
 
 // y[u] = sum_k v_k g(col_k) for the U rows row[u] of this 8-lane group; every
 // lane of the group returns the full sums. All row_ptr loads, then all
@@ -730,6 +737,13 @@ __device__ __host__ __forceinline__ int tile_nnz_for(const SolveArgs& a, int TR)
 // Row epilogues of the SpMV-family kernels (same arithmetic as the direct
 // kernels above). Each provides the gather, the per-row update (run by lane 0
 // of the row's group) and, with NV > 0, the last-CTA finish.
+// Ops with CTA_HOOKS run cta_pre(a) in every CTA before the grid sum and
+// cta_last(a, tot) with the whole last CTA (instead of finish by one thread).
+template <class Op, class = void>
+struct HasCtaHooks : std::false_type {};
+template <class Op>
+struct HasCtaHooks<Op, std::void_t<decltype(Op::CTA_HOOKS)>> : std::bool_constant<Op::CTA_HOOKS> {};
+
 struct OpSpmvP {
     static constexpr int NV = 1;
     static constexpr int TICKET = kTkSpmvP;
@@ -766,7 +780,7 @@ struct OpSpmvP {
     }
 };
 
-template <class Gat, bool RZ>
+template <class Gat, bool RZ, bool CW = false>
 struct OpSweep {
     static constexpr int NV = RZ ? 1 : 0;
     static constexpr int TICKET = kTkSweep;
@@ -774,11 +788,12 @@ struct OpSweep {
     const double* r;
     const double* wd;
     double* zout;
+    double wc = 0.0;  // constant w D^-1 (see GWdr)
     __device__ __forceinline__ double operator()(int j) const { return g(j); }
     struct Pre {
         double ri, wi, gi;
     };
-    __device__ __forceinline__ Pre pre(int i) const { return Pre{r[i], wd[i], g(i)}; }
+    __device__ __forceinline__ Pre pre(int i) const { return Pre{r[i], CW ? wc : wd[i], g(i)}; }
     __device__ __forceinline__ void row(int i, double y, double* s, const Pre& p) const {
         const double zi = fma(p.wi, p.ri - y, p.gi);
         zout[i] = zi;
@@ -882,8 +897,12 @@ __global__ void __launch_bounds__(kThreads) k_spmv_dia(SolveArgs a, Op op) {
         double v[Op::NV], tot[Op::NV];
 #pragma unroll
         for (int j = 0; j < Op::NV; ++j) v[j] = s[j];
-        if (grid_reduce<Op::NV>(v, a.partials, &st->counter[Op::TICKET], tot) && threadIdx.x == 0)
+        if constexpr (HasCtaHooks<Op>::value) {
+            op.cta_pre(a);
+            if (grid_reduce<Op::NV>(v, a.partials, &st->counter[Op::TICKET], tot)) op.cta_last(a, tot);
+        } else if (grid_reduce<Op::NV>(v, a.partials, &st->counter[Op::TICKET], tot) && threadIdx.x == 0) {
             op.finish(st, tot);
+        }
     }
 }
 
@@ -942,8 +961,12 @@ __global__ void __launch_bounds__(kTmaThreads) k_spmv_tma(SolveArgs a, Op op) {
         double v[Op::NV], tot[Op::NV];
 #pragma unroll
         for (int j = 0; j < Op::NV; ++j) v[j] = s[j];
-        if (grid_reduce<Op::NV>(v, a.partials, &st->counter[Op::TICKET], tot) && threadIdx.x == 0)
+        if constexpr (HasCtaHooks<Op>::value) {
+            op.cta_pre(a);
+            if (grid_reduce<Op::NV>(v, a.partials, &st->counter[Op::TICKET], tot)) op.cta_last(a, tot);
+        } else if (grid_reduce<Op::NV>(v, a.partials, &st->counter[Op::TICKET], tot) && threadIdx.x == 0) {
             op.finish(st, tot);
+        }
     }
 }
 
@@ -1452,13 +1475,16 @@ __device__ __forceinline__ void cta_columns(double (&acc)[2 * PPL], double* cs, 
 template <int PPL, int MAXD, bool RV>
 __global__ void __launch_bounds__(kThreads, 2) k_prolong_onepass(SolveArgs a, const double* sv,
                                                               double* zout,
-                                                              cudaGraphConditionalHandle h, int ctl) {
+                                                              cudaGraphConditionalHandle h, int ctl,
+                                                              int rsel) {
     PcgState* st = a.st;
     if (st->done) {
         if (ctl && blockIdx.x == 0 && threadIdx.x == 0) loop_ctl_body(st, h, ctl == 2);
         return;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) st->op_grid = gridDim.x;
+    // rsel: the residual the fused update + sweep wrote (r[(it + 1) & 1]), else r
+    const double* rv = (rsel && !(st->it & 1)) ? a.r1 : a.r;
     const int ld = a.k + (a.k & 1);
     const int pairs = ld >> 1;
     double ev[2 * PPL], au[2 * PPL], av[2 * PPL];
@@ -1492,7 +1518,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_prolong_onepass(SolveArgs a, co
         for (int u = 0; u < UPR; ++u) {
             const int rw = valid[u] ? row[u] : 0;
             sr[u] = sv ? sv[rw] : 0.0;
-            rr[u] = valid[u] ? a.r[rw] : 0.0;
+            rr[u] = valid[u] ? rv[rw] : 0.0;
         }
         {
             // lane L < 4 UPR sums row base + L (sequential fma chain in column
@@ -1574,13 +1600,15 @@ template <int PPL, int MAXD, bool RV>
 __global__ void __launch_bounds__(kOpThreads, 1) k_prolong_onepass_tma(SolveArgs a, const double* sv,
                                                                       double* zout,
                                                                       cudaGraphConditionalHandle h,
-                                                                      int ctl, int S, int P) {
+                                                                      int ctl, int S, int P, int rsel) {
     PcgState* st = a.st;
     if (st->done) {
         if (ctl && blockIdx.x == 0 && threadIdx.x == 0) loop_ctl_body(st, h, ctl == 2);
         return;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) st->op_grid = gridDim.x;
+    // rsel: the residual the fused update + sweep wrote (r[(it + 1) & 1]), else r
+    const double* rv = (rsel && !(st->it & 1)) ? a.r1 : a.r;
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned long long* full = reinterpret_cast<unsigned long long*>(smem);
     unsigned long long* asr = full + kOpMaxStages;
@@ -1624,7 +1652,7 @@ __global__ void __launch_bounds__(kOpThreads, 1) k_prolong_onepass_tma(SolveArgs
                 mbar_arrive_tx(&full[stg], wb + (sv ? vb : 0u) + vb + mbb);
                 bulk_g2s(base, a.P + (long long)r0 * ld, wb, &full[stg]);
                 if (sv) bulk_g2s(base + s_off, sv + r0, vb, &full[stg]);
-                bulk_g2s(base + r_off, a.r + r0, vb, &full[stg]);
+                bulk_g2s(base + r_off, rv + r0, vb, &full[stg]);
                 if (MAXD)
                     bulk_g2s(base + m_off, static_cast<const unsigned char*>(a.dia.mask) + (long long)r0 * mb,
                              mbb, &full[stg]);
@@ -1734,12 +1762,81 @@ __global__ void __launch_bounds__(kOpThreads, 1) k_prolong_onepass_tma(SolveArgs
     }
 }
 
-// x += alpha p, r -= alpha q, ||r||^2 (two_level.hpp:164-170); the CTAs also
-// sum the previous prolongation's partials (a column per CTA, fixed order)
-// into u_i (ow slot it & 1, u_{i-1} stays in the other) and v_i. Last CTA:
-// history + convergence test (:168-176), then the one-pass restriction
+// Every CTA: sum columns of the previous one-pass prolongation's partials (a
+// column per CTA, fixed order) into u_i (ow slot it & 1; u_{i-1} stays in the
+// other) and v_i (ow + 2 ld).
+__device__ void onepass_colsums(const SolveArgs& a) {
+    const PcgState* st = a.st;
+    const int ld = a.k + (a.k & 1);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __shared__ double wsum[32];
+    const long long G = st->op_grid;
+    const int ucur = (int)(st->it & 1) * ld;
+    for (int j = blockIdx.x; j < 2 * ld; j += gridDim.x) {
+        double t = 0.0;
+        for (long long b = threadIdx.x; b < G; b += blockDim.x) t += __ldcg(a.opart + j * G + b);
+        t = warp_sum(t);
+        if (lane == 0) wsum[warp] = t;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double tt = 0.0;
+            for (int w = 0; w < nw; ++w) tt += wsum[w];
+            a.ow[j < ld ? ucur + j : ld + j] = tt;  // u_i -> its slot, v_i -> [2 ld, 3 ld)
+            __threadfence();
+        }
+        __syncthreads();
+    }
+}
+
+// The last CTA of the x/r update (whole CTA; rrt = ||r_{i+1}||^2): history +
+// convergence test (two_level.hpp:168-176), then the one-pass restriction
 // c = u_i - alpha_i (v_i + M e_i + beta_i (u_{i-1} - u_i) / alpha_{i-1}) and
 // e = A_c^-1 c.
+__device__ void onepass_last(const SolveArgs& a, double rrt, double alpha) {
+    PcgState* st = a.st;
+    __shared__ int go_on;
+    if (threadIdx.x == 0) {
+        const double rel = sqrt(rrt) / st->bnorm;
+        st->rr = rrt;
+        st->last_rel = rel;
+        a.hist[st->it] = rel;
+        st->iterations = st->it + 1;
+        if (rel < st->delta) {
+            st->converged = 1;
+            st->done = 1;
+        }
+        go_on = !st->done;
+    }
+    __syncthreads();
+    if (!go_on) return;
+    __threadfence();
+    __shared__ double es[kOnePassK + 2], gs[kOnePassK + 2], cs[kOnePassK + 2];
+    const int k = a.k, ld = a.k + (a.k & 1);
+    const int warp = threadIdx.x >> 5;
+    const bool first = st->first != 0;
+    const double beta = st->beta, alpha_prev = st->alpha_prev;
+    const int ucur = (int)(st->it & 1) * ld, uprev = ld - ucur;
+    for (int j = threadIdx.x; j < k; j += blockDim.x) es[j] = __ldcg(a.e + j);
+    __syncthreads();
+    coarse_apply_inverse(a.M, k, es, gs);  // M e_i
+    __syncthreads();
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+        const double u = __ldcg(a.ow + ucur + j);
+        double g = __ldcg(a.ow + 2 * ld + j) + gs[j];  // v + M e
+        if (!first) g = fma(beta, (__ldcg(a.ow + uprev + j) - u) / alpha_prev, g);  // + beta W^T q_{i-1}
+        cs[j] = fma(-alpha, g, u);                     // c = u - alpha g
+    }
+    __syncthreads();
+    if (a.Ainv) coarse_apply_inverse(a.Ainv, k, cs, a.e);
+    else if (warp == 0) coarse_solve_warp(a.L, k, cs, a.e);
+    if (threadIdx.x == 0) {
+        if (k & 1) a.e[k] = 0.0;  // padded column
+        st->alpha_prev = alpha;
+    }
+}
+
+// x += alpha p, r -= alpha q, ||r||^2 (two_level.hpp:164-170), with the
+// one-pass column sums and, in the last CTA, the one-pass restriction.
 __global__ void __launch_bounds__(kThreads) k_update_onepass(SolveArgs a) {
     PcgState* st = a.st;
     if (st->done) return;
@@ -1771,68 +1868,66 @@ __global__ void __launch_bounds__(kThreads) k_update_onepass(SolveArgs a) {
         a.r[i] = ro;
         s[0] = fma(ro, ro, s[0]);
     }
-    const int ld = a.k + (a.k & 1);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    {
-        __shared__ double wsum[kThreads / 32];
-        const long long G = st->op_grid;
-        const int ucur = (int)(st->it & 1) * ld;
-        for (int j = blockIdx.x; j < 2 * ld; j += gridDim.x) {
-            double t = 0.0;
-            for (long long b = threadIdx.x; b < G; b += blockDim.x) t += __ldcg(a.opart + j * G + b);
-            t = warp_sum(t);
-            if (lane == 0) wsum[warp] = t;
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                double tt = 0.0;
-                for (int w = 0; w < nw; ++w) tt += wsum[w];
-                a.ow[j < ld ? ucur + j : ld + j] = tt;  // u_i -> its slot, v_i -> [2 ld, 3 ld)
-                __threadfence();
-            }
-            __syncthreads();
-        }
-    }
+    onepass_colsums(a);
     double tot[1];
-    if (!grid_reduce<1>(s, a.partials, &st->counter[kTkUpdate], tot)) return;
-    __shared__ int go_on;
-    if (threadIdx.x == 0) {
-        const double rel = sqrt(tot[0]) / st->bnorm;
-        st->rr = tot[0];
-        st->last_rel = rel;
-        a.hist[st->it] = rel;
-        st->iterations = st->it + 1;
-        if (rel < st->delta) {
-            st->converged = 1;
-            st->done = 1;
-        }
-        go_on = !st->done;
-    }
-    __syncthreads();
-    if (!go_on) return;
-    __threadfence();
-    __shared__ double es[kOnePassK + 2], gs[kOnePassK + 2], cs[kOnePassK + 2];
-    const int k = a.k;
-    const bool first = st->first != 0;
-    const double beta = st->beta, alpha_prev = st->alpha_prev;
-    const int ucur = (int)(st->it & 1) * ld, uprev = ld - ucur;
-    for (int j = threadIdx.x; j < k; j += blockDim.x) es[j] = __ldcg(a.e + j);
-    __syncthreads();
-    coarse_apply_inverse(a.M, k, es, gs);  // M e_i
-    __syncthreads();
-    for (int j = threadIdx.x; j < k; j += blockDim.x) {
-        const double u = __ldcg(a.ow + ucur + j);
-        double g = __ldcg(a.ow + 2 * ld + j) + gs[j];  // v + M e
-        if (!first) g = fma(beta, (__ldcg(a.ow + uprev + j) - u) / alpha_prev, g);  // + beta W^T q_{i-1}
-        cs[j] = fma(-alpha, g, u);                     // c = u - alpha g
-    }
-    __syncthreads();
-    if (a.Ainv) coarse_apply_inverse(a.Ainv, k, cs, a.e);
-    else if (warp == 0) coarse_solve_warp(a.L, k, cs, a.e);
-    if (threadIdx.x == 0) {
-        if (k & 1) a.e[k] = 0.0;  // padded column
-        st->alpha_prev = alpha;
-    }
+    if (grid_reduce<1>(s, a.partials, &st->counter[kTkUpdate], tot)) onepass_last(a, tot[0], alpha);
 }
+
+// The x/r update fused with the smoothing sweeps of the one-pass cycle at
+// nu1 = nu2 = 1 (T = 2): s = s1 + w D^-1 (r_new - A s1), s1 = w D^-1 r_new,
+// with r_new = r - alpha q formed inside the gather (bitwise the values the
+// separate update writes). r is double-buffered by iteration parity (the
+// gathers read the old residual while rows write the new one): read r[it & 1],
+// write r[(it + 1) & 1]. Plus x += alpha p, ||r_new||^2 and the one-pass hooks.
+template <bool CW>
+struct OpUpdSweep {
+    static constexpr int NV = 1;
+    static constexpr int TICKET = kTkUpdate;
+    static constexpr bool CTA_HOOKS = true;
+    double alpha;
+    const double* rc;
+    double* rn;
+    const double* q;
+    const double* wd;
+    const double* p;
+    double* x;
+    double* sout;
+    double wc;  // constant w D^-1 (see GWdr), else 0
+    __device__ __forceinline__ void init(const SolveArgs& a) {
+        const bool odd = a.st->it & 1;
+        wc = a.wdc;
+        alpha = a.st->alpha;
+        rc = odd ? a.r1 : a.r;
+        rn = odd ? a.r : a.r1;
+        q = a.q;
+        wd = a.wd;
+        p = odd ? a.p1 : a.p0;
+        x = a.x;
+        sout = a.zt0;
+    }
+    __device__ __forceinline__ double operator()(int j) const {
+        return (CW ? wc : wd[j]) * fma(-alpha, q[j], rc[j]);
+    }
+    struct Pre {
+        double ri, wi, xi, pi;
+    };
+    __device__ __forceinline__ Pre pre(int i) const {
+        return Pre{fma(-alpha, q[i], rc[i]), CW ? wc : wd[i], x[i], p[i]};
+    }
+    __device__ __forceinline__ void row(int i, double y, double* s, const Pre& pr) const {
+        const double gi = pr.wi * pr.ri;
+        sout[i] = fma(pr.wi, pr.ri - y, gi);
+        rn[i] = pr.ri;
+        x[i] = fma(alpha, pr.pi, pr.xi);
+        s[0] = fma(pr.ri, pr.ri, s[0]);
+    }
+    __device__ __forceinline__ void row(int i, double y, double* s) const { row(i, y, s, pre(i)); }
+    __device__ __forceinline__ void cta_pre(const SolveArgs& a) const { onepass_colsums(a); }
+    __device__ __forceinline__ void cta_last(const SolveArgs& a, const double* tot) const {
+        onepass_last(a, tot[0], alpha);
+    }
+    __device__ __forceinline__ void finish(PcgState*, const double*) const {}
+};
 
 // ======================================================== host launchers ==
 
@@ -2115,7 +2210,17 @@ void launch_prolong(const LaunchCtx& c, const SolveArgs& a, int zmode, bool rz, 
 void launch_sweep(const LaunchCtx& c, const SolveArgs& a, bool implicit_in, const double* zin,
                   double* zout, bool rz) {
     if (a.dia.kind) {
-        if (implicit_in) {
+        if (a.wdc != 0.0) {
+            if (implicit_in) {
+                const GWdrT<true> gw{a.wd, a.r, a.wdc};
+                if (rz) launch_dia_op<1>(c, a, OpSweep<GWdrT<true>, true, true>{gw, a.r, a.wd, zout, a.wdc});
+                else launch_dia_op<1>(c, a, OpSweep<GWdrT<true>, false, true>{gw, a.r, a.wd, zout, a.wdc});
+            } else {
+                const GPlain gp{zin};
+                if (rz) launch_dia_op<1>(c, a, OpSweep<GPlain, true, true>{gp, a.r, a.wd, zout, a.wdc});
+                else launch_dia_op<1>(c, a, OpSweep<GPlain, false, true>{gp, a.r, a.wd, zout, a.wdc});
+            }
+        } else if (implicit_in) {
             const GWdr gw{a.wd, a.r};
             if (rz) launch_dia_op<1>(c, a, OpSweep<GWdr, true>{gw, a.r, a.wd, zout});
             else launch_dia_op<1>(c, a, OpSweep<GWdr, false>{gw, a.r, a.wd, zout});
@@ -2296,7 +2401,7 @@ static void launch_op_tma(const LaunchCtx& c, void (*f)(KArgs...), long long nti
 
 template <int PPL>
 static void prolong_onepass_ppl(const LaunchCtx& c, const SolveArgs& a, const double* sv, double* zout,
-                                cudaGraphConditionalHandle h, int ctl) {
+                                cudaGraphConditionalHandle h, int ctl, int rsel) {
     const int ld = a.k + (a.k & 1);
     // as many stages as fit, a multiple of the stencil pair count P
     int fit = (int)((kStageBudget - 256) / op_stage_bytes(ld));
@@ -2311,7 +2416,7 @@ static void prolong_onepass_ppl(const LaunchCtx& c, const SolveArgs& a, const do
     if (NLSP_OP_TMA && fit >= 2) {
         const long long nt = (a.n + kOpTR - 1) / kOpTR;
         const int threads = 32 * (1 + 2 * P + kOpWWarps);
-#define NLSP_P2(D, R) launch_op_tma(c, k_prolong_onepass_tma<PPL, D, R>, nt, sm, threads, a, sv, zout, h, ctl, S, P)
+#define NLSP_P2(D, R) launch_op_tma(c, k_prolong_onepass_tma<PPL, D, R>, nt, sm, threads, a, sv, zout, h, ctl, S, P, rsel)
         const bool rv = a.dia.kind == 2;
         if (!a.dia.kind) NLSP_P2(0, false);
         else if (a.dia.d <= 8) { if (rv) NLSP_P2(8, true); else NLSP_P2(8, false); }
@@ -2320,7 +2425,7 @@ static void prolong_onepass_ppl(const LaunchCtx& c, const SolveArgs& a, const do
 #undef NLSP_P2
         return;
     }
-#define NLSP_P1(D, R) launch_rows<NLSP_KUPRO>(c, k_prolong_onepass<PPL, D, R>, a.n, a, sv, zout, h, ctl)
+#define NLSP_P1(D, R) launch_rows<NLSP_KUPRO>(c, k_prolong_onepass<PPL, D, R>, a.n, a, sv, zout, h, ctl, rsel)
     const bool rv = a.dia.kind == 2;
     if (!a.dia.kind) NLSP_P1(0, false);
     else if (a.dia.d <= 8) { if (rv) NLSP_P1(8, true); else NLSP_P1(8, false); }
@@ -2332,15 +2437,26 @@ static void prolong_onepass_ppl(const LaunchCtx& c, const SolveArgs& a, const do
 // z = s + W e with u, v, w partials (s = S_T(r) by T - 1 sweep launches, or
 // none for T = 0); ctl as launch_prolong
 void launch_prolong_onepass(const LaunchCtx& c, const SolveArgs& a, const double* sv, double* zout,
-                            cudaGraphConditionalHandle h, int ctl) {
+                            cudaGraphConditionalHandle h, int ctl, int rsel) {
     SolveArgs b = a;
     b.P = a.W2;
     switch (ppl_for(a.k)) {
-        case 1: prolong_onepass_ppl<1>(c, b, sv, zout, h, ctl); break;
-        case 2: prolong_onepass_ppl<2>(c, b, sv, zout, h, ctl); break;
-        case 3: prolong_onepass_ppl<3>(c, b, sv, zout, h, ctl); break;
-        default: prolong_onepass_ppl<4>(c, b, sv, zout, h, ctl); break;
+        case 1: prolong_onepass_ppl<1>(c, b, sv, zout, h, ctl, rsel); break;
+        case 2: prolong_onepass_ppl<2>(c, b, sv, zout, h, ctl, rsel); break;
+        case 3: prolong_onepass_ppl<3>(c, b, sv, zout, h, ctl, rsel); break;
+        default: prolong_onepass_ppl<4>(c, b, sv, zout, h, ctl, rsel); break;
     }
+    count(c);
+}
+
+// the x/r update fused with the T = 2 sweeps (OpUpdSweep): s -> zt0
+bool update_sweep_ok(const SolveArgs& a, unsigned long long T) {
+    return T == 2 && (a.dia.kind || spmv_tma_ok(a));
+}
+void launch_update_sweep(const LaunchCtx& c, const SolveArgs& a) {
+    if (a.dia.kind && a.wdc != 0.0) launch_dia_op<1>(c, a, OpUpdSweep<true>{});
+    else if (a.dia.kind) launch_dia_op<1>(c, a, OpUpdSweep<false>{});
+    else launch_spmv_op<1>(c, a, OpUpdSweep<false>{});
     count(c);
 }
 
@@ -2364,7 +2480,19 @@ void launch_update_onepass(const LaunchCtx& c, const SolveArgs& a) {
 void launch_onepass_tail(const LaunchCtx& c, const SolveArgs& a, unsigned long long T,
                          cudaGraphConditionalHandle h, int ctl) {
     const double* sv = launch_onepass_sweeps(c, a, T);
-    launch_prolong_onepass(c, a, sv, a.z, h, ctl);
+    launch_prolong_onepass(c, a, sv, a.z, h, ctl, 0);
+}
+
+// one iteration after k_spmv_p: fused update + sweeps (T = 2) when possible
+void launch_onepass_iteration_tail(const LaunchCtx& c, const SolveArgs& a, unsigned long long T,
+                                   cudaGraphConditionalHandle h, int ctl) {
+    if (update_sweep_ok(a, T)) {
+        launch_update_sweep(c, a);
+        launch_prolong_onepass(c, a, a.zt0, a.z, h, ctl, 1);
+        return;
+    }
+    launch_update_onepass(c, a);
+    launch_onepass_tail(c, a, T, h, ctl);
 }
 
 // PCG prologue z = M r_0 with the one-pass partials of r_0: c = W^T r_0 directly
