@@ -16,6 +16,7 @@
 // (4 rows per warp): the 8 lanes read a row's nonzeros as one coalesced run and
 // the row's k basis entries as 16-B loads, so the SpMV result of a row is
 // already in the registers of the lanes that stream that row of P.
+#include <cstdlib>
 #include <mutex>
 #include <type_traits>
 #include <unordered_map>
@@ -2412,6 +2413,16 @@ static void prolong_onepass_ppl(const LaunchCtx& c, const SolveArgs& a, const do
     else if (fit >= 6) { S = 6; P = 3; }
     else if (fit >= 4) { S = 4; P = 4; }
     else { S = 2; P = 2; }
+    {
+        // development overrides (A/B runs): NLSP_OP_P stencil pairs, NLSP_OP_S stages
+        static const int env_p = std::getenv("NLSP_OP_P") ? std::atoi(std::getenv("NLSP_OP_P")) : 0;
+        static const int env_s = std::getenv("NLSP_OP_S") ? std::atoi(std::getenv("NLSP_OP_S")) : 0;
+        if (env_p >= 1 && env_p <= kOpSPairs) P = env_p;
+        if (env_s >= 2) S = env_s < fit ? env_s : fit;
+        S -= S % P;  // the ring depth must be a multiple of P (see kOpSPairs)
+        if (S < P) S = P;
+        if (S > fit) S = fit, P = 1;
+    }
     const size_t sm = 256 + (size_t)S * op_stage_bytes(ld);
     if (NLSP_OP_TMA && fit >= 2) {
         const long long nt = (a.n + kOpTR - 1) / kOpTR;
