@@ -144,6 +144,15 @@ __device__ __forceinline__ double group_sum(double v) {
     return v;
 }
 
+// Programmatic dependent launch: wait until the preceding grid has completed
+// and its memory is visible (a no-op without PDL), then let the next grid be
+// scheduled. Called first thing by every kernel that may be launched with
+// LaunchCtx::pdl.
+__device__ __forceinline__ void pdl_entry() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Streaming 16-B load that does not allocate in L1 (basis rows, CSR arrays).
 __device__ __forceinline__ double2 ld_stream2(const double* p) {
     double2 r;
@@ -161,5 +170,8 @@ struct LaunchCtx {
     cudaStream_t s;
     int num_sms;
     unsigned long long* launches;  // incremented per kernel launch
+    // launch with programmatic stream serialization (PDL): the kernel may be
+    // scheduled while its predecessor drains; it must start with pdl_entry()
+    bool pdl = false;
 };
 }  // namespace nlsp

@@ -368,13 +368,19 @@ SolveArgs make_args(nlsp_ctx* c, const nlsp_csr* a, const nlsp_twolevel* m) {
     return s;
 }
 
+const bool g_pdl = !(std::getenv("NLSP_PDL") && std::strcmp(std::getenv("NLSP_PDL"), "0") == 0);
+
 // One PCG iteration (the WHILE body). mode: 0 two-level, 1 identity, 2 Jacobi.
 void enqueue_iteration(const LaunchCtx& lc, const SolveArgs& a, int mode, const nlsp_twolevel* m,
                        cudaGraphConditionalHandle h, int use_cond) {
     launch_spmv_p(lc, a);
     if (mode == 0 && m->onepass) {
-        // x, r, ||r||, c by its recurrence, e (+ the sweeps when fused); prolongation
-        launch_onepass_iteration_tail(lc, a, m->nu1 + m->nu2, h, use_cond ? 2 : 1);
+        // x, r, ||r||, c by its recurrence, e (+ the sweeps when fused); prolongation.
+        // Each of these kernels starts with pdl_entry(): launched with PDL, it is
+        // scheduled while its predecessor drains (NLSP_PDL=0: plain launches)
+        LaunchCtx lp = lc;
+        lp.pdl = g_pdl;
+        launch_onepass_iteration_tail(lp, a, m->nu1 + m->nu2, h, use_cond ? 2 : 1);
         return;
     }
     if (mode == 0 && m->folded) {

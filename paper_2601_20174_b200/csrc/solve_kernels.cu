@@ -282,6 +282,7 @@ __global__ void k_init_ctl(PcgState* st) {
 // p = z + beta p (written to the other ping-pong buffer), q = A p, p.q;
 // last CTA: p^T A p <= 0 -> NotSpdError (two_level.hpp:159-163), alpha = rz / pap
 __global__ void __launch_bounds__(kThreads, NLSP_MINB_S) k_spmv_p(SolveArgs a) {
+    pdl_entry();
     PcgState* st = a.st;
     if (st->done) return;
     const bool odd = st->it & 1;
@@ -398,6 +399,7 @@ __global__ void k_loop_ctl(PcgState* st, cudaGraphConditionalHandle h, int use_c
 // z_in given by the gather (implicit first sweep or a buffer); RZ: r.z_out
 template <class Gat, bool RZ>
 __global__ void __launch_bounds__(kThreads, NLSP_MINB_S) k_sweep(SolveArgs a, Gat g, double* zout) {
+    pdl_entry();
     PcgState* st = a.st;
     if (st->done) return;
     double s[1] = {0.0};
@@ -856,6 +858,7 @@ struct OpPlain {
 // and rows with every offset present (the interior) take an unpredicated path.
 template <int MAXD, typename MT, bool RV, int SKIP, bool EXACT, class Op>
 __global__ void __launch_bounds__(kThreads) k_spmv_dia(SolveArgs a, Op op) {
+    pdl_entry();
     PcgState* st = a.st;
     if (SKIP == 1 && st->done) return;
     if (SKIP == 2 && st->error) return;
@@ -912,6 +915,7 @@ __global__ void __launch_bounds__(kThreads) k_spmv_dia(SolveArgs a, Op op) {
 // TR = 8 warps * U * (32 / G) rows per staged tile.
 template <int G, int U, int S, int SKIP, int CHW, class Op>
 __global__ void __launch_bounds__(kTmaThreads) k_spmv_tma(SolveArgs a, Op op) {
+    pdl_entry();
     constexpr int R = 32 / G;
     constexpr int TR = kConsumerWarps * U * R;
     constexpr int CH = CHW;  // nonzeros per lane per pass (G * CH per row)
@@ -1478,6 +1482,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_prolong_onepass(SolveArgs a, co
                                                               double* zout,
                                                               cudaGraphConditionalHandle h, int ctl,
                                                               int rsel) {
+    pdl_entry();
     PcgState* st = a.st;
     if (st->done) {
         if (ctl && blockIdx.x == 0 && threadIdx.x == 0) loop_ctl_body(st, h, ctl == 2);
@@ -1602,6 +1607,7 @@ __global__ void __launch_bounds__(kOpThreads, 1) k_prolong_onepass_tma(SolveArgs
                                                                       double* zout,
                                                                       cudaGraphConditionalHandle h,
                                                                       int ctl, int S, int P, int rsel) {
+    pdl_entry();
     PcgState* st = a.st;
     if (st->done) {
         if (ctl && blockIdx.x == 0 && threadIdx.x == 0) loop_ctl_body(st, h, ctl == 2);
@@ -1839,6 +1845,7 @@ __device__ void onepass_last(const SolveArgs& a, double rrt, double alpha) {
 // x += alpha p, r -= alpha q, ||r||^2 (two_level.hpp:164-170), with the
 // one-pass column sums and, in the last CTA, the one-pass restriction.
 __global__ void __launch_bounds__(kThreads) k_update_onepass(SolveArgs a) {
+    pdl_entry();
     PcgState* st = a.st;
     if (st->done) return;
     const double alpha = st->alpha;
@@ -1933,6 +1940,25 @@ struct OpUpdSweep {
 // ======================================================== host launchers ==
 
 namespace {
+// <<<g, b, smem, c.s>>>, or with programmatic stream serialization when c.pdl
+template <class... KArgs, class... Args>
+void klaunch(const LaunchCtx& c, void (*f)(KArgs...), dim3 g, dim3 b, size_t smem, Args&&... args) {
+    if (!c.pdl) {
+        f<<<g, b, smem, c.s>>>(std::forward<Args>(args)...);
+        return;
+    }
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = g;
+    cfg.blockDim = b;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, f, std::forward<Args>(args)...);
+}
 // Persistent, occupancy-sized grids: min(work, resident CTAs on all SMs).
 int occ_blocks(const void* f) {
     static std::mutex mu;
@@ -1959,7 +1985,7 @@ int occ_grid(const LaunchCtx& c, const void* f, long long units, long long per_c
 template <int U, class... KArgs, class... Args>
 void launch_rows(const LaunchCtx& c, void (*f)(KArgs...), long long n, Args&&... args) {
     const int g = occ_grid(c, reinterpret_cast<const void*>(f), n, (kThreads / 32) * kRowsPerWarp * U);
-    f<<<g, kThreads, 0, c.s>>>(std::forward<Args>(args)...);
+    klaunch(c, f, g, kThreads, 0, std::forward<Args>(args)...);
 }
 // TMA-staged kernels: one CTA = 8 consumer warps + 1 producer warp, dynamic
 // shared memory for the stage ring, grid = min(tiles, resident CTAs).
@@ -1994,13 +2020,13 @@ void launch_tma(const LaunchCtx& c, void (*f)(KArgs...), long long ntiles, size_
     if (g > kMaxGrid) g = kMaxGrid;
     if (g > ntiles) g = ntiles;
     if (g < 1) g = 1;
-    f<<<(int)g, kTmaThreads, smem, c.s>>>(std::forward<Args>(args)...);
+    klaunch(c, f, (int)g, kTmaThreads, smem, std::forward<Args>(args)...);
 }
 // element kernels: units = elements (2 per thread)
 template <class... KArgs, class... Args>
 void launch_elems(const LaunchCtx& c, void (*f)(KArgs...), long long n, Args&&... args) {
     const int g = occ_grid(c, reinterpret_cast<const void*>(f), n, 2LL * kThreads);
-    f<<<g, kThreads, 0, c.s>>>(std::forward<Args>(args)...);
+    klaunch(c, f, g, kThreads, 0, std::forward<Args>(args)...);
 }
 inline void count(const LaunchCtx& c) { ++*c.launches; }
 }  // namespace
@@ -2073,7 +2099,7 @@ template <int SKIP, class Op>
 void launch_dia_op(const LaunchCtx& c, const SolveArgs& a, const Op& op) {
     auto go = [&](auto kern) {
         const int g = occ_grid(c, reinterpret_cast<const void*>(kern), a.n, kThreads);
-        kern<<<g, kThreads, 0, c.s>>>(a, op);
+        klaunch(c, kern, g, kThreads, 0, a, op);
     };
     const bool rv = a.dia.kind == 2;
 #define NLSP_DIA_GO(D, MT, EX) \
@@ -2397,7 +2423,7 @@ static void launch_op_tma(const LaunchCtx& c, void (*f)(KArgs...), long long nti
     long long g = c.num_sms;  // one CTA per SM (the stage ring fills shared memory)
     if (g > ntiles) g = ntiles;
     if (g < 1) g = 1;
-    f<<<(int)g, threads, smem, c.s>>>(std::forward<Args>(args)...);
+    klaunch(c, f, (int)g, threads, smem, std::forward<Args>(args)...);
 }
 
 template <int PPL>

@@ -107,6 +107,61 @@ def graph_ctx(nlsp):
         os.environ.pop("NLSP_CLUSTER", None)
 
 
+@pytest.fixture(scope="module")
+def graph_chol_ctx(nlsp):
+    os.environ["NLSP_CLUSTER"] = "0"
+    os.environ["NLSP_COARSE"] = "chol"
+    try:
+        return nlsp.Context(0)
+    finally:
+        os.environ.pop("NLSP_CLUSTER", None)
+        os.environ.pop("NLSP_COARSE", None)
+
+
+@pytest.mark.parametrize("coarse", ["inverse", "chol"])
+def test_graph_loop_cycles_match_oracle(nlsp, oracle, graph_ctx, graph_chol_ctx, coarse):
+    """The multi-kernel graph loop (the path of every n > 65 536 system) on the
+    variants of the two-level operator: nu1 = nu2 in {0, 1, 2} run the one-pass
+    cycle (no sweeps / fused update + sweeps / update then three sweeps),
+    nu1 != nu2 the folded one; even and odd coarse dimensions (odd k pads W with
+    a zero column); the coarse solve by A_c^-1 or by the triangular
+    substitutions. Each against the reference oracle."""
+    from conftest import csr_from_golden
+    ctx = graph_ctx if coarse == "inverse" else graph_chol_ctx
+    d = golden("scaled_C3")
+    a = csr_from_golden(d)
+    ao = (a.dim(), a.row_ptr(), a.col_idx(), a.values())
+    kmax = d["P"].shape[1]
+    for nu1, nu2, k in [(1, 1, kmax), (2, 2, kmax), (1, 1, 7), (2, 2, 7), (0, 1, kmax), (3, 1, kmax - 1)]:
+        p = np.ascontiguousarray(d["P"][:, :k])
+        m = nlsp.TwoLevelPreconditioner(a, nlsp.DeviceDense.upload(p, ctx), 2 / 3, nu1, nu2)
+        assert m.cycle() == ("onepass" if nu1 == nu2 else "folded"), (nu1, nu2, k)
+        t = oracle.twolevel(ao, p, 2 / 3, nu1, nu2)
+        res = nlsp.pcg(a, d["rhs"], m, 1e-8, 10 * a.dim())
+        ro = oracle.pcg(ao, d["rhs"], 2, t, 1e-8, 10 * a.dim())
+        assert res.report.converged, (nu1, nu2, k)
+        assert abs(res.report.iterations - ro.iterations) <= 2, (nu1, nu2, k, res.report.iterations, ro.iterations)
+        assert res.report.true_relative_residual < 1e-7
+        assert np.linalg.norm(res.solution - ro.x) <= 1e-9 * np.linalg.norm(ro.x), (nu1, nu2, k)
+        assert res.report.kernel_launches > 2  # not the single-cluster solver
+    # nu1 = nu2 = 0: z = W A_c^-1 W^T r is singular (rank k) and PCG breaks down
+    # once the k-dimensional Krylov space is spent (r.z -> 0); the one-pass
+    # schedule (no sweeps, v = 0) against the folded one over the first iterations
+    p = np.ascontiguousarray(d["P"])
+    m1 = nlsp.TwoLevelPreconditioner(a, nlsp.DeviceDense.upload(p, ctx), 2 / 3, 0, 0)
+    os.environ["NLSP_CYCLE"] = "folded"
+    try:
+        m2 = nlsp.TwoLevelPreconditioner(a, nlsp.DeviceDense.upload(p, ctx), 2 / 3, 0, 0)
+    finally:
+        os.environ.pop("NLSP_CYCLE", None)
+    assert m1.cycle() == "onepass" and m2.cycle() == "folded"
+    r1 = nlsp.pcg(a, d["rhs"], m1, 1e-8, 3)
+    r2 = nlsp.pcg(a, d["rhs"], m2, 1e-8, 3)
+    assert r1.report.iterations == r2.report.iterations == 3
+    assert np.allclose(r1.report.residual_history, r2.report.residual_history, rtol=1e-9, atol=0)
+    assert np.linalg.norm(r1.solution - r2.solution) <= 1e-9 * np.linalg.norm(r2.solution)
+
+
 @pytest.mark.parametrize("path", ["cluster", "graph"])
 def test_two_level_edge_cases_on_both_paths(nlsp, graph_ctx, path):
     """pcg's contract (two_level.hpp:141-191) with the two-level operator on the
