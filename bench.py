@@ -152,14 +152,16 @@ def byte_model_literal(n, nnz, k, nu1, nu2):
     return (1 + nu1 + nu2) * csr + 16.0 * n * k + v * n
 
 
-def byte_model(n, nnz, k, nu1, nu2, pass_bytes=None, cycle="onepass"):
+def byte_model(n, nnz, k, nu1, nu2, pass_bytes=None, cycle="onepass", const_wd=False):
     """Algorithmic HBM bytes per PCG iteration of the schedule this library runs
     (DESIGN.md §3). Folded cycle: spmv_p (A + 32n), update+restriction through
     W1 (8nk + 48n), nu1+nu2-1 smoothing sweeps (A + 24n for the first, A + 32n
     after), prolongation through W2 with r.z (8nk + 24n). One-pass cycle
     (nu1 == nu2): spmv_p (A + 32n), x/r update (48n), the same sweeps, and ONE
     pass over W that also gathers A s (8nk + A + 24n; 8nk + 16n without sweeps);
-    at nu1 = nu2 = 1 the update and the sweeps are one kernel (A + 64n).
+    the update and the first two sweeps are one kernel (A + 64n), later sweeps
+    A + 32n. const_wd: the constant-coefficient diagonal form, whose w D^-1 is
+    one kernel parameter (8n less per sweep pass).
     A = the matrix bytes one pass streams: CSR 12 nnz + 4(n+1), or the diagonal
     form's own bytes when the upload detected one (nlsp_csr_format; SURVEY
     §8d's rule for stencil-specialised kernels)."""
@@ -169,11 +171,14 @@ def byte_model(n, nnz, k, nu1, nu2, pass_bytes=None, cycle="onepass"):
     sweeps = 0.0
     if t >= 2:
         sweeps = (csr + 24.0 * n) + (t - 2) * (csr + 32.0 * n)
+    wd = 0.0 if const_wd else 8.0
     if cycle == "onepass":
         pro = 8.0 * n * ld + ((csr + 24.0 * n) if t >= 1 else 16.0 * n)
-        if t == 2:  # x/r update fused with the sweeps: A + 64n (x, p, q, r, w; writes x, r', s)
-            return (csr + 32.0 * n) + (csr + 64.0 * n) + pro
-        return (csr + 32.0 * n) + 48.0 * n + sweeps + pro
+        if t >= 2:  # x/r update fused with two sweeps (x, p, q, r, w; writes x, r', s), then t - 2 sweeps
+            return (csr + 32.0 * n) + (csr + (56.0 + wd) * n) + (t - 2) * (csr + (24.0 + wd) * n) + pro
+        return (csr + 32.0 * n) + 48.0 * n + pro
+    if t >= 2 and const_wd:
+        sweeps -= 8.0 * n * (t - 1)
     pro = 8.0 * n * ld + (24.0 if t >= 1 else 16.0) * n
     return (csr + 32.0 * n) + (8.0 * n * ld + 48.0 * n) + sweeps + pro
 
@@ -329,7 +334,7 @@ def run_ours(args, dist: Dist):
     if cycle == "literal":
         bytes_iter = bytes_iter_csr = byte_model_literal(pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2)
     else:
-        bytes_iter = byte_model(pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2, pass_bytes, cycle)
+        bytes_iter = byte_model(pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2, pass_bytes, cycle, fmt_kind == 1)
         bytes_iter_csr = byte_model(pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2, None, cycle)
     iter_gbs = bytes_iter * iters / (ms_local / 1e3) / 1e9
     traffic = ncu_traffic(dominant, args.config)
@@ -341,7 +346,7 @@ def run_ours(args, dist: Dist):
                               "frac": round(iter_gbs / peak, 4),
                               "cycle": cycle,
                               "folded_cycle_bytes_per_iter": byte_model(
-                                  pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2, pass_bytes, "folded"),
+                                  pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2, pass_bytes, "folded", fmt_kind == 1),
                               "matrix_form": ["csr", "diagonal-constant", "diagonal-values"][fmt_kind],
                               "matrix_offsets": fmt_offsets, "matrix_bytes_per_pass": pass_bytes,
                               "csr_model_bytes_per_iter": bytes_iter_csr,

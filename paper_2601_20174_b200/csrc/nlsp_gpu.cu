@@ -45,6 +45,7 @@ bool onepass_supported(int k);
 void launch_prolong_onepass(const LaunchCtx&, const SolveArgs&, const double*, double*,
                             cudaGraphConditionalHandle, int, int);
 bool update_sweep_ok(const SolveArgs&, unsigned long long);
+void launch_sweeps_rpar(const LaunchCtx&, const SolveArgs&, unsigned long long, double**);
 void launch_update_sweep(const LaunchCtx&, const SolveArgs&);
 void launch_onepass_iteration_tail(const LaunchCtx&, const SolveArgs&, unsigned long long,
                                    cudaGraphConditionalHandle, int);
@@ -1418,13 +1419,14 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
         {"prolong", 8.0 * n * k + 24.0 * n},         // literal: P, r, w; writes z2
         {"post_sweep", pass + 32.0 * n},             // z2, r, w; writes z
         {"update_restrict", 8.0 * n * k + 48.0 * n}, // folded: W1, x, p, q, r; writes x, r
-        {"smooth", pass + ((m && m->nu1 + m->nu2 == 2) ? 24.0 : 32.0) * n},  // folded sweeps
+        // sweeps (the first from zero: r, w, s; later: s, r, w, s'), w not read when constant
+        {"smooth", pass + ((m && m->nu1 + m->nu2 == 2) ? 24.0 : 32.0) * n - (args.wdc != 0.0 ? 8.0 * n : 0.0)},
         {"loop_ctl", 0.0},
         {"update_onepass", 48.0 * n},  // x, p, q, r; writes x, r (+ the 2k column sums)
         // one-pass prolongation: W, s (+ A s: one more matrix pass), r; writes z
         {"prolong_onepass", 8.0 * n * k + (T ? pass + 24.0 * n : 16.0 * n)},
         // x/r update fused with the T = 2 sweeps: A, x, p, q, r, w; writes x, r', s
-        {"update_sweep", pass + 64.0 * n},
+        {"update_sweep", pass + (args.wdc != 0.0 ? 56.0 : 64.0) * n},
     };
     if ((int)acc.size() != kSlots) return -1;
     std::vector<cudaEvent_t> evs(2);
@@ -1445,7 +1447,13 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
         timed(kSpmvP, [&] { launch_spmv_p(ctx->lc, args); });
         if (onepass && update_sweep_ok(args, T)) {
             timed(kUS, [&] { launch_update_sweep(ctx->lc, args); });
-            timed(kPO, [&] { launch_prolong_onepass(ctx->lc, args, ctx->zt0, ctx->z, 0, 1, 1); });
+            double* cur = ctx->zt0;
+            for (unsigned long long j = 3; j <= T; ++j) {
+                double* c1 = cur;
+                timed(kSmooth, [&] { launch_sweeps_rpar(ctx->lc, args, 3, &c1); });  // one sweep
+                cur = c1;
+            }
+            timed(kPO, [&] { launch_prolong_onepass(ctx->lc, args, cur, ctx->z, 0, 1, 1); });
         } else if (onepass) {
             timed(kUO, [&] { launch_update_onepass(ctx->lc, args); });
             double* cur = nullptr;

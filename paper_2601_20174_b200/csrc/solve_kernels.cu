@@ -791,7 +791,8 @@ struct OpSweep {
     const double* r;
     const double* wd;
     double* zout;
-    double wc = 0.0;  // constant w D^-1 (see GWdr)
+    double wc = 0.0;    // constant w D^-1 (see GWdr)
+    bool rpar = false;  // r = the residual the fused update + sweep wrote (r[(it + 1) & 1])
     __device__ __forceinline__ double operator()(int j) const { return g(j); }
     struct Pre {
         double ri, wi, gi;
@@ -803,7 +804,9 @@ struct OpSweep {
         if (RZ) s[0] = fma(p.ri, zi, s[0]);
     }
     __device__ __forceinline__ void row(int i, double y, double* s) const { row(i, y, s, pre(i)); }
-    __device__ __forceinline__ void init(const SolveArgs&) {}
+    __device__ __forceinline__ void init(const SolveArgs& a) {
+        if (rpar) r = (a.st->it & 1) ? a.r : a.r1;
+    }
     __device__ __forceinline__ void finish(PcgState* st, const double* tot) const {
         st->rz_new = tot[0];
     }
@@ -2486,9 +2489,29 @@ void launch_prolong_onepass(const LaunchCtx& c, const SolveArgs& a, const double
     count(c);
 }
 
-// the x/r update fused with the T = 2 sweeps (OpUpdSweep): s -> zt0
+// the x/r update fused with the first two sweeps (OpUpdSweep): s -> zt0
 bool update_sweep_ok(const SolveArgs& a, unsigned long long T) {
-    return T == 2 && (a.dia.kind || spmv_tma_ok(a));
+    return T >= 2 && (a.dia.kind || spmv_tma_ok(a));
+}
+
+// a later sweep s_out = s_in + w D^-1 (r' - A s_in) after the fused update,
+// r' = r[(it + 1) & 1]
+static void launch_sweep_rpar(const LaunchCtx& c, const SolveArgs& a, const double* zin, double* zout) {
+    const GPlain gp{zin};
+    if (a.dia.kind && a.wdc != 0.0)
+        launch_dia_op<1>(c, a, OpSweep<GPlain, false, true>{gp, a.r, a.wd, zout, a.wdc, true});
+    else if (a.dia.kind)
+        launch_dia_op<1>(c, a, OpSweep<GPlain, false>{gp, a.r, a.wd, zout, 0.0, true});
+    else
+        launch_spmv_op<1>(c, a, OpSweep<GPlain, false>{gp, a.r, a.wd, zout, 0.0, true});
+    count(c);
+}
+void launch_sweeps_rpar(const LaunchCtx& c, const SolveArgs& a, unsigned long long T, double** cur) {
+    for (unsigned long long j = 3; j <= T; ++j) {
+        double* nxt = (*cur == a.zt0) ? a.zt1 : a.zt0;
+        launch_sweep_rpar(c, a, *cur, nxt);
+        *cur = nxt;
+    }
 }
 void launch_update_sweep(const LaunchCtx& c, const SolveArgs& a) {
     if (a.dia.kind && a.wdc != 0.0) launch_dia_op<1>(c, a, OpUpdSweep<true>{});
@@ -2524,8 +2547,10 @@ void launch_onepass_tail(const LaunchCtx& c, const SolveArgs& a, unsigned long l
 void launch_onepass_iteration_tail(const LaunchCtx& c, const SolveArgs& a, unsigned long long T,
                                    cudaGraphConditionalHandle h, int ctl) {
     if (update_sweep_ok(a, T)) {
-        launch_update_sweep(c, a);
-        launch_prolong_onepass(c, a, a.zt0, a.z, h, ctl, 1);
+        launch_update_sweep(c, a);  // s_2 -> zt0
+        double* cur = a.zt0;
+        launch_sweeps_rpar(c, a, T, &cur);
+        launch_prolong_onepass(c, a, cur, a.z, h, ctl, 1);
         return;
     }
     launch_update_onepass(c, a);
