@@ -874,26 +874,29 @@ __global__ void __launch_bounds__(kThreads) k_spmv_dia(SolveArgs a, Op op) {
     const int n = a.n, d = EXACT ? MAXD : a.dia.d;
     constexpr unsigned kFull = MAXD >= 32 ? ~0u : ((1u << MAXD) - 1u);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        // Every gather is issued unconditionally (index clamped into [0, n))
+        // together with the mask and the own-row operands: no load waits on the
+        // mask, so a row costs one memory latency, not two. Absent offsets are
+        // then skipped by the mask, so y is unchanged (bitwise the CSR row sum).
         const unsigned m = mask[i];
         const typename Op::Pre pr = op.pre(i);  // own-row operands in flight with the gathers
+        double g[MAXD], vv[MAXD];
+#pragma unroll
+        for (int t = 0; t < MAXD; ++t) {
+            if (t < d) {
+                const int j = min(max(i + a.dia.off[t], 0), n - 1);
+                g[t] = op(j);
+                if (RV) vv[t] = __ldcs(a.dia.rv + (size_t)t * n + i);  // 0 where absent
+            } else {
+                g[t] = 0.0;
+                if (RV) vv[t] = 0.0;
+            }
+        }
         double y = 0.0;
         if (EXACT && m == kFull) {
-            double g[MAXD], vv[MAXD];
-#pragma unroll
-            for (int t = 0; t < MAXD; ++t) {
-                g[t] = op(i + a.dia.off[t]);
-                if (RV) vv[t] = __ldcs(a.dia.rv + (size_t)t * n + i);
-            }
 #pragma unroll
             for (int t = 0; t < MAXD; ++t) y = fma(RV ? vv[t] : a.dia.val[t], g[t], y);
         } else {
-            double g[MAXD], vv[MAXD];
-#pragma unroll
-            for (int t = 0; t < MAXD; ++t) {
-                const bool on = t < d && ((m >> t) & 1u);
-                g[t] = on ? op(i + a.dia.off[t]) : 0.0;
-                if (RV) vv[t] = on ? __ldcs(a.dia.rv + (size_t)t * n + i) : 0.0;
-            }
 #pragma unroll
             for (int t = 0; t < MAXD; ++t)
                 if (t < d && ((m >> t) & 1u)) y = fma(RV ? vv[t] : a.dia.val[t], g[t], y);
