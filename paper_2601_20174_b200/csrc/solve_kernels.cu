@@ -37,6 +37,12 @@ namespace nlsp {
 #ifndef NLSP_DIA_EXACT
 #define NLSP_DIA_EXACT 1
 #endif
+#ifndef NLSP_DIA_ROWS
+#define NLSP_DIA_ROWS 1
+#endif
+#ifndef NLSP_DIA_MINB
+#define NLSP_DIA_MINB 1
+#endif
 #ifndef NLSP_KUPRO
 #define NLSP_KUPRO 2
 #endif
@@ -860,7 +866,7 @@ struct OpPlain {
 // EXACT: MAXD is the offset count itself (the common 5 / 7 / 9-point forms),
 // and rows with every offset present (the interior) take an unpredicated path.
 template <int MAXD, typename MT, bool RV, int SKIP, bool EXACT, class Op>
-__global__ void __launch_bounds__(kThreads) k_spmv_dia(SolveArgs a, Op op) {
+__global__ void __launch_bounds__(kThreads, NLSP_DIA_MINB) k_spmv_dia(SolveArgs a, Op op) {
     pdl_entry();
     PcgState* st = a.st;
     if (SKIP == 1 && st->done) return;
@@ -873,35 +879,50 @@ __global__ void __launch_bounds__(kThreads) k_spmv_dia(SolveArgs a, Op op) {
     const MT* __restrict__ mask = static_cast<const MT*>(a.dia.mask);
     const int n = a.n, d = EXACT ? MAXD : a.dia.d;
     constexpr unsigned kFull = MAXD >= 32 ? ~0u : ((1u << MAXD) - 1u);
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    // NLSP_DIA_ROWS rows per thread and step (rows i + r * stride): all their
+    // loads are in flight together
+    constexpr int RW = NLSP_DIA_ROWS;
+    const int stride = gridDim.x * blockDim.x;
+    for (int i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += RW * stride) {
         // Every gather is issued unconditionally (index clamped into [0, n))
         // together with the mask and the own-row operands: no load waits on the
         // mask, so a row costs one memory latency, not two. Absent offsets are
         // then skipped by the mask, so y is unchanged (bitwise the CSR row sum).
-        const unsigned m = mask[i];
-        const typename Op::Pre pr = op.pre(i);  // own-row operands in flight with the gathers
-        double g[MAXD], vv[MAXD];
+        unsigned m[RW];
+        typename Op::Pre pr[RW];
+        double g[RW][MAXD], vv[RW][MAXD];
 #pragma unroll
-        for (int t = 0; t < MAXD; ++t) {
-            if (t < d) {
-                const int j = min(max(i + a.dia.off[t], 0), n - 1);
-                g[t] = op(j);
-                if (RV) vv[t] = __ldcs(a.dia.rv + (size_t)t * n + i);  // 0 where absent
-            } else {
-                g[t] = 0.0;
-                if (RV) vv[t] = 0.0;
+        for (int rr = 0; rr < RW; ++rr) {
+            const int i = min(i0 + rr * stride, n - 1);
+            m[rr] = mask[i];
+            pr[rr] = op.pre(i);  // own-row operands in flight with the gathers
+#pragma unroll
+            for (int t = 0; t < MAXD; ++t) {
+                if (t < d) {
+                    const int j = min(max(i + a.dia.off[t], 0), n - 1);
+                    g[rr][t] = op(j);
+                    if (RV) vv[rr][t] = __ldcs(a.dia.rv + (size_t)t * n + i);  // 0 where absent
+                } else {
+                    g[rr][t] = 0.0;
+                    if (RV) vv[rr][t] = 0.0;
+                }
             }
         }
-        double y = 0.0;
-        if (EXACT && m == kFull) {
 #pragma unroll
-            for (int t = 0; t < MAXD; ++t) y = fma(RV ? vv[t] : a.dia.val[t], g[t], y);
-        } else {
+        for (int rr = 0; rr < RW; ++rr) {
+            const int i = i0 + rr * stride;
+            if (rr > 0 && i >= n) break;
+            double y = 0.0;
+            if (EXACT && m[rr] == kFull) {
 #pragma unroll
-            for (int t = 0; t < MAXD; ++t)
-                if (t < d && ((m >> t) & 1u)) y = fma(RV ? vv[t] : a.dia.val[t], g[t], y);
+                for (int t = 0; t < MAXD; ++t) y = fma(RV ? vv[rr][t] : a.dia.val[t], g[rr][t], y);
+            } else {
+#pragma unroll
+                for (int t = 0; t < MAXD; ++t)
+                    if (t < d && ((m[rr] >> t) & 1u)) y = fma(RV ? vv[rr][t] : a.dia.val[t], g[rr][t], y);
+            }
+            op.row(i, y, s, pr[rr]);
         }
-        op.row(i, y, s, pr);
     }
     if constexpr (Op::NV > 0) {
         double v[Op::NV], tot[Op::NV];
