@@ -43,6 +43,9 @@ namespace nlsp {
 #ifndef NLSP_DIA_MINB
 #define NLSP_DIA_MINB 1
 #endif
+#ifndef NLSP_DIA_BLOCK
+#define NLSP_DIA_BLOCK 0
+#endif
 #ifndef NLSP_KUPRO
 #define NLSP_KUPRO 2
 #endif
@@ -882,8 +885,17 @@ __global__ void __launch_bounds__(kThreads, NLSP_DIA_MINB) k_spmv_dia(SolveArgs 
     // NLSP_DIA_ROWS rows per thread and step (rows i + r * stride): all their
     // loads are in flight together
     constexpr int RW = NLSP_DIA_ROWS;
+#if NLSP_DIA_BLOCK
+    // each CTA sweeps one contiguous chunk of rows in passes of blockDim rows:
+    // the near neighbours (i +- 1, i +- nx) were just touched by this CTA (L1)
+    const int stride = blockDim.x;
+    const int chunk = ((n + gridDim.x - 1) / gridDim.x + blockDim.x - 1) / blockDim.x * blockDim.x;
+    const int cbeg = blockIdx.x * chunk, cend = min(n, cbeg + chunk);
+    for (int i0 = cbeg + threadIdx.x; i0 < cend; i0 += RW * stride) {
+#else
     const int stride = gridDim.x * blockDim.x;
     for (int i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += RW * stride) {
+#endif
         // Every gather is issued unconditionally (index clamped into [0, n))
         // together with the mask and the own-row operands: no load waits on the
         // mask, so a row costs one memory latency, not two. Absent offsets are
@@ -911,7 +923,11 @@ __global__ void __launch_bounds__(kThreads, NLSP_DIA_MINB) k_spmv_dia(SolveArgs 
 #pragma unroll
         for (int rr = 0; rr < RW; ++rr) {
             const int i = i0 + rr * stride;
+#if NLSP_DIA_BLOCK
+            if (rr > 0 && i >= cend) break;
+#else
             if (rr > 0 && i >= n) break;
+#endif
             double y = 0.0;
             if (EXACT && m[rr] == kFull) {
 #pragma unroll
@@ -1625,8 +1641,14 @@ constexpr int kOpMaxStages = 8;
 constexpr int kOpThreads = 32 * (1 + 2 * kOpSPairs + kOpWWarps);
 constexpr unsigned kOpVec = kOpTR * 8;  // bytes of one staged vector slice
 
-__host__ __device__ constexpr unsigned op_stage_bytes(int ld) {
-    return (unsigned)kOpTR * ld * 8 + 2 * kOpVec + round16(kOpTR * 4) + kOpVec;
+// CSR matrices also stage the tile's row_ptr slice and its runs of values and
+// column indices (at most tile_nnz nonzeros), so the stencil warps only gather s
+__host__ __device__ constexpr unsigned op_csr_bytes(int tile_nnz) {
+    return round16((kOpTR + 4) * 4) + round16((tile_nnz + 2) * 8) + round16((tile_nnz + 8) * 4);
+}
+__host__ __device__ constexpr unsigned op_stage_bytes(int ld, int tile_nnz = -1) {
+    return (unsigned)kOpTR * ld * 8 + 2 * kOpVec + round16(kOpTR * 4) + kOpVec +
+           (tile_nnz >= 0 ? op_csr_bytes(tile_nnz) : 0u);
 }
 
 template <int PPL, int MAXD, bool RV>
@@ -1651,10 +1673,13 @@ __global__ void __launch_bounds__(kOpThreads, 1) k_prolong_onepass_tma(SolveArgs
     const int ld = a.k + (a.k & 1);
     const int pairs = ld >> 1;
     const unsigned wbytes = (unsigned)kOpTR * ld * 8;
-    const unsigned sbytes = op_stage_bytes(ld);
-    // stage layout: [W rows | s | r | mask | A s]
+    const unsigned sbytes = op_stage_bytes(ld, MAXD ? -1 : a.tile_nnz64);
+    // stage layout: [W rows | s | r | mask | A s | CSR: row_ptr | values | columns]
     const unsigned s_off = wbytes, r_off = wbytes + kOpVec, m_off = wbytes + 2 * kOpVec;
     const unsigned as_off = m_off + round16(kOpTR * 4);
+    const unsigned rp_off = as_off + kOpVec;
+    const unsigned v_off = rp_off + round16((kOpTR + 4) * 4);
+    const unsigned c_off = v_off + round16((a.tile_nnz64 + 2) * 8);
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
@@ -1672,24 +1697,73 @@ __global__ void __launch_bounds__(kOpThreads, 1) k_prolong_onepass_tma(SolveArgs
     for (int t = 0; t < 2 * PPL; ++t) au[t] = av[t] = 0.0;
     double rz[1] = {0.0};
     if (warp == 0) {
-        // ---- producer
-        if (lane == 0) {
+        // ---- producer (diagonal form): lane 0 issues each tile's bulk copies
+        if (MAXD != 0 && lane == 0) {
             int i = 0;
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
                 const int stg = i % S;
                 if (i >= S) mbar_wait(&empty[stg], ((i / S) - 1) & 1);
-                unsigned char* base = stages + stg * sbytes;
+                unsigned char* base_s = stages + stg * sbytes;
                 const int r0 = tile * kOpTR, rows = min(kOpTR, a.n - r0);
                 const unsigned vb = round16(rows * 8);  // vectors are padded by 16 doubles
                 const unsigned wb = (unsigned)rows * ld * 8;
-                const unsigned mbb = MAXD ? round16(rows * mb) : 0u;  // masks are padded by 16 B
+                const unsigned mbb = round16(rows * mb);  // masks are padded by 16 B
                 mbar_arrive_tx(&full[stg], wb + (sv ? vb : 0u) + vb + mbb);
-                bulk_g2s(base, a.P + (long long)r0 * ld, wb, &full[stg]);
-                if (sv) bulk_g2s(base + s_off, sv + r0, vb, &full[stg]);
-                bulk_g2s(base + r_off, rv + r0, vb, &full[stg]);
+                bulk_g2s(base_s, a.P + (long long)r0 * ld, wb, &full[stg]);
+                if (sv) bulk_g2s(base_s + s_off, sv + r0, vb, &full[stg]);
+                bulk_g2s(base_s + r_off, rv + r0, vb, &full[stg]);
+                bulk_g2s(base_s + m_off, static_cast<const unsigned char*>(a.dia.mask) + (long long)r0 * mb,
+                         mbb, &full[stg]);
+            }
+        }
+        // ---- producer (CSR): the 32 lanes load the row_ptr bounds of 32
+        // upcoming tiles at once, lane 0 issues each tile's bulk copies
+        if (MAXD == 0)
+        for (int base = 0;; base += 32) {
+            if ((long long)blockIdx.x + (long long)base * gridDim.x >= ntiles) break;
+            int b0 = 0, b1 = 0;
+            if (MAXD == 0) {
+                const long long my = (long long)blockIdx.x + (long long)(base + lane) * gridDim.x;
+                if (my < ntiles) {
+                    const int r0 = (int)my * kOpTR;
+                    b0 = __ldg(a.rp + r0);
+                    b1 = __ldg(a.rp + min(r0 + kOpTR, a.n));
+                }
+            }
+            for (int j = 0; j < 32; ++j) {
+                const int i = base + j;
+                const long long tile = (long long)blockIdx.x + (long long)i * gridDim.x;
+                if (tile >= ntiles) break;
+                const int a0 = __shfl_sync(0xffffffffu, b0, j), a1 = __shfl_sync(0xffffffffu, b1, j);
+                if (lane != 0) continue;
+                const int stg = i % S;
+                if (i >= S) mbar_wait(&empty[stg], ((i / S) - 1) & 1);
+                unsigned char* base_s = stages + stg * sbytes;
+                const int r0 = (int)tile * kOpTR, rows = min(kOpTR, a.n - r0);
+                const unsigned vb = round16(rows * 8);  // vectors are padded by 16 doubles
+                const unsigned wb = (unsigned)rows * ld * 8;
+                const unsigned mbb = MAXD ? round16(rows * mb) : 0u;  // masks are padded by 16 B
+                unsigned cb = 0, cvb = 0, ccb = 0;
+                int s0 = 0, c0 = 0;
+                if (MAXD == 0) {  // row_ptr slice, values and columns from 16-B aligned starts
+                    s0 = a0 & ~1;
+                    c0 = a0 & ~3;
+                    cb = ((rows + 1 + 3) & ~3) * 4;
+                    cvb = ((a1 - s0 + 1) & ~1) * 8;
+                    ccb = ((a1 - c0 + 3) & ~3) * 4;
+                }
+                mbar_arrive_tx(&full[stg], wb + (sv ? vb : 0u) + vb + mbb + cb + cvb + ccb);
+                bulk_g2s(base_s, a.P + (long long)r0 * ld, wb, &full[stg]);
+                if (sv) bulk_g2s(base_s + s_off, sv + r0, vb, &full[stg]);
+                bulk_g2s(base_s + r_off, rv + r0, vb, &full[stg]);
                 if (MAXD)
-                    bulk_g2s(base + m_off, static_cast<const unsigned char*>(a.dia.mask) + (long long)r0 * mb,
+                    bulk_g2s(base_s + m_off, static_cast<const unsigned char*>(a.dia.mask) + (long long)r0 * mb,
                              mbb, &full[stg]);
+                if (MAXD == 0) {
+                    bulk_g2s(base_s + rp_off, a.rp + r0, cb, &full[stg]);
+                    if (cvb) bulk_g2s(base_s + v_off, a.v + s0, cvb, &full[stg]);
+                    if (ccb) bulk_g2s(base_s + c_off, a.ci + c0, ccb, &full[stg]);
+                }
             }
         }
     } else if (warp <= 2 * P) {
@@ -1707,8 +1781,13 @@ __global__ void __launch_bounds__(kOpThreads, 1) k_prolong_onepass_tma(SolveArgs
             if (sv && lr < rows) {
                 const int row = r0 + lr;
                 if constexpr (MAXD == 0) {
-                    const int b = __ldg(a.rp + row), e = __ldg(a.rp + row + 1);
-                    for (int kk = b; kk < e; ++kk) y = fma(__ldg(a.v + kk), sv[__ldg(a.ci + kk)], y);
+                    // the staged row: values from a 16-B aligned start s0, columns from c0
+                    const int* rps = reinterpret_cast<const int*>(base + rp_off);
+                    const double* vs = reinterpret_cast<const double*>(base + v_off);
+                    const int* cs_ = reinterpret_cast<const int*>(base + c_off);
+                    const int a0 = rps[0], s0 = a0 & ~1, c0 = a0 & ~3;
+                    const int b = rps[lr], e = rps[lr + 1];
+                    for (int kk = b; kk < e; ++kk) y = fma(vs[kk - s0], sv[cs_[kk - c0]], y);
                 } else {
                     unsigned m;
                     const unsigned char* ms = base + m_off;
@@ -2458,7 +2537,8 @@ static void prolong_onepass_ppl(const LaunchCtx& c, const SolveArgs& a, const do
                                 cudaGraphConditionalHandle h, int ctl, int rsel) {
     const int ld = a.k + (a.k & 1);
     // as many stages as fit, a multiple of the stencil pair count P
-    int fit = (int)((kStageBudget - 256) / op_stage_bytes(ld));
+    const int tnz = a.dia.kind ? -1 : a.tile_nnz64;
+    int fit = (int)((kStageBudget - 256) / op_stage_bytes(ld, tnz));
     if (fit > kOpMaxStages) fit = kOpMaxStages;
     if (NLSP_OP_STAGES > 0 && fit > NLSP_OP_STAGES) fit = NLSP_OP_STAGES;
     int S, P;
@@ -2476,7 +2556,7 @@ static void prolong_onepass_ppl(const LaunchCtx& c, const SolveArgs& a, const do
         if (S < P) S = P;
         if (S > fit) S = fit, P = 1;
     }
-    const size_t sm = 256 + (size_t)S * op_stage_bytes(ld);
+    const size_t sm = 256 + (size_t)S * op_stage_bytes(ld, tnz);
     if (NLSP_OP_TMA && fit >= 2) {
         const long long nt = (a.n + kOpTR - 1) / kOpTR;
         const int threads = 32 * (1 + 2 * P + kOpWWarps);
