@@ -3,7 +3,8 @@ tens of minutes to hours per solve here, so parity is checked
 through size-independent properties, each recomputed independently on the host
 (scipy.sparse): the recurrence stop and the true residual, the basis is
 orthonormal, A_c = P^T A P, the operator is linear / symmetric / positive, and
-repeated solves are bitwise deterministic."""
+repeated solves are bitwise deterministic; and the one-pass PCG schedule
+matches the folded one (itself pinned to the reference at scaled sizes)."""
 from __future__ import annotations
 
 import numpy as np
@@ -20,7 +21,7 @@ def scipy_csr(pb):
                          shape=(pb.n, pb.n))
 
 
-@pytest.mark.parametrize("name", ["C2", "C4", "C5"])
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
 def test_full_size_solve_properties(nlsp, name):
     cfg = problems.CONFIGS[name]
     pb = problems.generate(cfg)
@@ -50,6 +51,20 @@ def test_full_size_solve_properties(nlsp, name):
     # determinism
     res2 = nlsp.pcg(a, pb.rhs, m, cfg.delta, 10 * pb.n)
     assert res2.report.iterations == rep.iterations and np.array_equal(res2.solution, res.solution)
+    # the one-pass schedule (W streamed once per iteration) against the folded
+    # one (W twice, restriction direct) on the full-size system
+    assert m.cycle() == "onepass"
+    import os
+    os.environ["NLSP_CYCLE"] = "folded"
+    try:
+        mf = nlsp.TwoLevelPreconditioner(a, p, cfg.omega, cfg.nu1, cfg.nu2)
+    finally:
+        os.environ.pop("NLSP_CYCLE", None)
+    assert mf.cycle() == "folded"
+    resf = nlsp.pcg(a, pb.rhs, mf, cfg.delta, 10 * pb.n)
+    assert abs(resf.report.iterations - rep.iterations) <= 1
+    assert np.linalg.norm(resf.solution - res.solution) <= 1e-10 * np.linalg.norm(resf.solution)
+    del mf
     # operator: linear, symmetric, positive (two_level.hpp:17-20)
     rng = np.random.default_rng(0)
     x, y = rng.standard_normal(pb.n), rng.standard_normal(pb.n)
