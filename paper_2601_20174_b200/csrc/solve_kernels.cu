@@ -1631,7 +1631,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_prolong_onepass(SolveArgs a, co
 // mask and L2 gathers of s (the only global latency left), publishing them
 // through a second barrier per stage; 8 consumer warps then run the W products
 // of the tile from shared memory (8 lanes per row) and release the stage.
-constexpr int kOpTR = 64;      // rows per tile
+#ifndef NLSP_OP_TR
+#define NLSP_OP_TR 64
+#endif
+constexpr int kOpTR = NLSP_OP_TR;  // rows per tile (64 or 128)
+static_assert(kOpTR == 64 || kOpTR == 128, "one-pass tiles are 64 or 128 rows");
 constexpr int kOpWWarps = 8;   // W-product warps
 constexpr int kOpSPairs = 4;   // at most this many stencil warp pairs (tile i -> pair i % P)
 constexpr int kOpMaxStages = 8;
@@ -1673,13 +1677,14 @@ __global__ void __launch_bounds__(kOpThreads, 1) k_prolong_onepass_tma(SolveArgs
     const int ld = a.k + (a.k & 1);
     const int pairs = ld >> 1;
     const unsigned wbytes = (unsigned)kOpTR * ld * 8;
-    const unsigned sbytes = op_stage_bytes(ld, MAXD ? -1 : a.tile_nnz64);
+    const int tile_nnz = kOpTR == 64 ? a.tile_nnz64 : a.tile_nnz128;
+    const unsigned sbytes = op_stage_bytes(ld, MAXD ? -1 : tile_nnz);
     // stage layout: [W rows | s | r | mask | A s | CSR: row_ptr | values | columns]
     const unsigned s_off = wbytes, r_off = wbytes + kOpVec, m_off = wbytes + 2 * kOpVec;
     const unsigned as_off = m_off + round16(kOpTR * 4);
     const unsigned rp_off = as_off + kOpVec;
     const unsigned v_off = rp_off + round16((kOpTR + 4) * 4);
-    const unsigned c_off = v_off + round16((a.tile_nnz64 + 2) * 8);
+    const unsigned c_off = v_off + round16((tile_nnz + 2) * 8);
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
@@ -1770,13 +1775,14 @@ __global__ void __launch_bounds__(kOpThreads, 1) k_prolong_onepass_tma(SolveArgs
         // ---- stencil warps: (A s)_row, one thread per row, sequential fma
         // chain in column order (bitwise the SpMV family's row sums)
         const int pair = (warp - 1) >> 1;
-        const int lr = ((warp - 1) & 1) * 32 + lane;
+        const int lr0 = ((warp - 1) & 1) * 32 + lane;
         int i = pair;
         for (int tile = blockIdx.x + pair * gridDim.x; tile < ntiles; tile += P * gridDim.x, i += P) {
             const int stg = i % S;
             mbar_wait(&full[stg], (i / S) & 1);
             unsigned char* base = stages + stg * sbytes;
             const int r0 = tile * kOpTR, rows = min(kOpTR, a.n - r0);
+            for (int lr = lr0; lr < kOpTR; lr += 64) {
             double y = 0.0;
             if (sv && lr < rows) {
                 const int row = r0 + lr;
@@ -1807,6 +1813,7 @@ __global__ void __launch_bounds__(kOpThreads, 1) k_prolong_onepass_tma(SolveArgs
                 }
             }
             reinterpret_cast<double*>(base + as_off)[lr] = y;
+            }
             __syncwarp();
             if (lane == 0) mbar_arrive(&asr[stg]);
         }
@@ -2537,7 +2544,7 @@ static void prolong_onepass_ppl(const LaunchCtx& c, const SolveArgs& a, const do
                                 cudaGraphConditionalHandle h, int ctl, int rsel) {
     const int ld = a.k + (a.k & 1);
     // as many stages as fit, a multiple of the stencil pair count P
-    const int tnz = a.dia.kind ? -1 : a.tile_nnz64;
+    const int tnz = a.dia.kind ? -1 : (kOpTR == 64 ? a.tile_nnz64 : a.tile_nnz128);
     int fit = (int)((kStageBudget - 256) / op_stage_bytes(ld, tnz));
     if (fit > kOpMaxStages) fit = kOpMaxStages;
     if (NLSP_OP_STAGES > 0 && fit > NLSP_OP_STAGES) fit = NLSP_OP_STAGES;
