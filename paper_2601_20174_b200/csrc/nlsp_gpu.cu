@@ -65,6 +65,8 @@ cudaError_t launch_cluster_pcg_batch(cudaStream_t s, const ClusterArgs* dargs, i
 void launch_csr_import(const LaunchCtx&, int, long long, const unsigned long long*,
                        const unsigned long long*, const double*, int*, int*, double*, int*, int*);
 void launch_wd(const LaunchCtx&, int, const double*, double, double*, int*);
+bool launch_block_op_dia(const LaunchCtx&, int, int, const DiaArgs&, const double*, int, const double*,
+                         double*);
 void launch_block_op(const LaunchCtx&, int, int, const int*, const int*, const double*,
                      const double*, int, const double*, double*);
 int gram_grid(const LaunchCtx&, long long);
@@ -1009,7 +1011,8 @@ static nlsp_status smooth_impl(nlsp_ctx* ctx, const nlsp_csr* a, nlsp_dense* s, 
     double* cur = s->d;
     double* other = tmp;
     for (uint64_t k = 0; k < sweeps; ++k) {
-        launch_block_op(ctx->lc, 0, a->n, a->rp, a->ci, a->v, wd, (int)s->cols, cur, other);
+        if (!launch_block_op_dia(ctx->lc, 0, a->n, a->dia, wd, (int)s->cols, cur, other))
+            launch_block_op(ctx->lc, 0, a->n, a->rp, a->ci, a->v, wd, (int)s->cols, cur, other);
         double* t = cur;
         cur = other;
         other = t;
@@ -1210,7 +1213,8 @@ nlsp_status nlsp_twolevel_build(nlsp_ctx* ctx, const nlsp_csr* a, const nlsp_den
     launch_tri_inv_t(ctx->lc, k, m->L, U);
     launch_dense_mm(ctx->lc, n, k, k, Q1, U, nullptr, Q);
     // Galerkin A_c = Q^T (A Q), exact symmetrisation, Cholesky (two_level.hpp:33-52)
-    launch_block_op(ctx->lc, 1, (int)n, a->rp, a->ci, a->v, nullptr, k, Q, Y);
+    if (!launch_block_op_dia(ctx->lc, 1, (int)n, a->dia, nullptr, k, Q, Y))
+        launch_block_op(ctx->lc, 1, (int)n, a->rp, a->ci, a->v, nullptr, k, Q, Y);
     launch_gram(ctx->lc, n, k, k, Q, Y, part, m->coarse);
     launch_symmetrize(ctx->lc, k, m->coarse);
     launch_chol(ctx->lc, k, m->coarse, m->L, 0.0, ctx->flags + 10);
@@ -1231,7 +1235,8 @@ nlsp_status nlsp_twolevel_build(nlsp_ctx* ctx, const nlsp_csr* a, const nlsp_den
         double* other = Y;  // Y and Q1 are free scratch (n x k) at this point
         for (unsigned long long s = 0; s < nu; ++s) {
             double* dst = (cur == Y) ? Q1 : Y;
-            launch_block_op(ctx->lc, 0, (int)n, a->rp, a->ci, a->v, m->wd, k, cur, dst);
+            if (!launch_block_op_dia(ctx->lc, 0, (int)n, a->dia, m->wd, k, cur, dst))
+                launch_block_op(ctx->lc, 0, (int)n, a->rp, a->ci, a->v, m->wd, k, cur, dst);
             cur = dst;
         }
         (void)other;
@@ -1243,7 +1248,8 @@ nlsp_status nlsp_twolevel_build(nlsp_ctx* ctx, const nlsp_csr* a, const nlsp_den
             double* aw = (cur == Y) ? Q1 : Y;
             err = dalloc(&m->M, kk);
             if (err) return err;
-            launch_block_op(ctx->lc, 1, (int)n, a->rp, a->ci, a->v, nullptr, k, cur, aw);
+            if (!launch_block_op_dia(ctx->lc, 1, (int)n, a->dia, nullptr, k, cur, aw))
+                launch_block_op(ctx->lc, 1, (int)n, a->rp, a->ci, a->v, nullptr, k, cur, aw);
             launch_gram(ctx->lc, n, k, k, cur, aw, part, m->M);
             launch_symmetrize(ctx->lc, k, m->M);
         }

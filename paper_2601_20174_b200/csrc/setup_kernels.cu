@@ -112,6 +112,59 @@ __global__ void __launch_bounds__(256) k_block_sweep(int n, const int* __restric
     }
 }
 
+// The same block sweep over the diagonal form of A (exact 5/7/9-offset
+// patterns): the offsets are kernel parameters, so every neighbour row of x is
+// loaded at once (clamped rows, no column-index load in front of them), then
+// each output entry accumulates the present offsets in ascending order (= the
+// CSR column order): bitwise the CSR kernel's result.
+template <int D, int T, int MODE>
+__global__ void __launch_bounds__(256) k_block_sweep_dia(int n, DiaArgs dia, const double* __restrict__ wd,
+                                                         int m, const double* __restrict__ in,
+                                                         double* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+    const int mb = dia.mbytes;
+    for (int c0 = 0; c0 < m; c0 += 32 * T) {
+        for (long long row = wid; row < n; row += nw) {
+            unsigned msk;
+            if (mb == 1) msk = static_cast<const unsigned char*>(dia.mask)[row];
+            else if (mb == 2) msk = static_cast<const unsigned short*>(dia.mask)[row];
+            else msk = static_cast<const unsigned*>(dia.mask)[row];
+            double xv[D][T], av[D];
+#pragma unroll
+            for (int t = 0; t < D; ++t) {
+                const long long nb = min(max(row + dia.off[t], 0LL), (long long)n - 1);
+                av[t] = dia.kind == 2 ? dia.rv[(size_t)t * n + row] : dia.val[t];
+                const double* xr = in + nb * m;
+#pragma unroll
+                for (int u = 0; u < T; ++u) {
+                    const int j = c0 + lane + 32 * u;
+                    xv[t][u] = j < m ? xr[j] : 0.0;
+                }
+            }
+            double acc[T];
+#pragma unroll
+            for (int u = 0; u < T; ++u) acc[u] = 0.0;
+#pragma unroll
+            for (int t = 0; t < D; ++t)
+                if ((msk >> t) & 1u) {
+#pragma unroll
+                    for (int u = 0; u < T; ++u) acc[u] = fma(av[t], xv[t][u], acc[u]);
+                }
+#pragma unroll
+            for (int u = 0; u < T; ++u) {
+                const int j = c0 + lane + 32 * u;
+                if (j < m) {
+                    const long long o = row * m + j;
+                    if (MODE == 0) out[o] = fma(wd[row], 0.0 - acc[u], in[o]);
+                    else out[o] = acc[u];
+                }
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------ Gram --
 // C = X^T Y for tall X (rows x ca), Y (rows x cb), row-major. 256 threads as a
 // 16 x 16 grid; thread (ti, tj) owns a TI x TJ block of C. Row tiles of X and Y
@@ -790,6 +843,37 @@ void launch_block_op(const LaunchCtx& c, int mode, int n, const int* rp, const i
     else NLSP_BS(32, 4);
 #undef NLSP_BS
     count(c);
+}
+
+// the diagonal-form block sweep for the exact 5/7/9-offset forms and m > 16;
+// false: not applicable (the caller uses the CSR kernel)
+bool launch_block_op_dia(const LaunchCtx& c, int mode, int n, const DiaArgs& dia, const double* wd, int m,
+                         const double* in, double* out) {
+    static const bool on = !(std::getenv("NLSP_BSWEEP_DIA") && std::atoi(std::getenv("NLSP_BSWEEP_DIA")) == 0);
+    // measured: faster than the CSR kernel for constant coefficients and wide
+    // blocks (C4 smoothing, m = 128: 3.66 -> 2.68 ms per sweep; C3, m = 96:
+    // -10 %), slower for per-row values (C2 +57 %) and m <= 64 (the builds, +9 %)
+    if (!on || dia.kind != 1 || m <= 64 || m > 128 || !(dia.d == 5 || dia.d == 7 || dia.d == 9)) return false;
+    const int g = grid_for(c, (long long)n * 32, 256, 8);
+#define NLSP_BD(D, T)                                                                                   \
+    do {                                                                                                \
+        if (mode == 0) k_block_sweep_dia<D, T, 0><<<g, 256, 0, c.s>>>(n, dia, wd, m, in, out);          \
+        else k_block_sweep_dia<D, T, 1><<<g, 256, 0, c.s>>>(n, dia, wd, m, in, out);                    \
+    } while (0)
+#define NLSP_BDT(D)                  \
+    do {                             \
+        if (m <= 32) NLSP_BD(D, 1);  \
+        else if (m <= 64) NLSP_BD(D, 2); \
+        else if (m <= 96) NLSP_BD(D, 3); \
+        else NLSP_BD(D, 4);          \
+    } while (0)
+    if (dia.d == 5) NLSP_BDT(5);
+    else if (dia.d == 7) NLSP_BDT(7);
+    else NLSP_BDT(9);
+#undef NLSP_BDT
+#undef NLSP_BD
+    count(c);
+    return true;
 }
 
 // C (ca x cb) = X^T Y; part must hold grid * ca * cb doubles (grid <= kMaxGrid)

@@ -146,6 +146,29 @@ def test_smoothed_vectors_match_reference(nlsp, name):
         assert np.all(s[mask.astype(bool)] == 0.0)  # SmoothedVectors.BoundaryRowsStayExactlyZero
 
 
+@pytest.mark.parametrize("name,m", [("scaled_C4", 128), ("scaled_C3", 96), ("c1_default", 80)])
+def test_wide_smoothing_diagonal_form_matches_csr_and_reference(nlsp, oracle, name, m):
+    """m > 64 on a constant-coefficient stencil runs the diagonal-form block
+    sweep (k_block_sweep_dia): bitwise the CSR block sweep (upload with
+    NLSP_DIA=0), and within rounding of the reference's smoothing."""
+    import os
+    d = golden(name)
+    a = csr_from_golden(d)
+    assert a.device().format()[0] == 1
+    os.environ["NLSP_DIA"] = "0"
+    try:
+        a_csr = csr_from_golden(d)
+        assert a_csr.device().format()[0] == 0
+    finally:
+        os.environ.pop("NLSP_DIA", None)
+    s_dia = nlsp.generate_smoothed_vectors(a, None, m, 10, 2 / 3, 11).s.numpy()
+    s_csr = nlsp.generate_smoothed_vectors(a_csr, None, m, 10, 2 / 3, 11).s.numpy()
+    assert np.array_equal(s_dia, s_csr)
+    so = oracle.generate_smoothed_vectors((a.dim(), a.row_ptr(), a.col_idx(), a.values()), None,
+                                          m, 10, 2 / 3, 11)
+    assert np.abs(s_dia - so).max() <= 1e-13 * np.abs(so).max()
+
+
 def test_zero_sweeps_returns_raw_gaussians(nlsp, oracle):
     d = golden("fem_diffusion")
     a = csr_from_golden(d)
