@@ -344,13 +344,16 @@ __global__ void __launch_bounds__(1024) k_eigh(EighArgs args, int use_shared) {
             const int np = mp / 2;
             const int nblocks = np * (np + 1) / 2;
             for (int bi = tid; bi < nblocks; bi += nt) {
-                // decode bi -> (u, w) with u <= w
-                int u = 0, rem = bi;
-                while (rem >= np - u) {
-                    rem -= np - u;
-                    ++u;
-                }
-                const int w = u + rem;
+                // decode bi -> (u, w) with u <= w: row u of the upper triangle
+                // starts at u np - u (u - 1) / 2 (closed form, then a +-1 fix-up)
+                const double b2 = 2.0 * np + 1.0;
+                int u = (int)((b2 - sqrt(b2 * b2 - 8.0 * bi)) * 0.5);
+                auto row_start = [&](int uu) { return uu * np - (uu * (uu - 1)) / 2; };
+                if (u < 0) u = 0;
+                if (u > np - 1) u = np - 1;
+                while (u > 0 && row_start(u) > bi) --u;
+                while (u < np - 1 && row_start(u + 1) <= bi) ++u;
+                const int w = u + (bi - row_start(u));
                 const int p1 = pp[u], q1 = pq[u], p2 = pp[w], q2 = pq[w];
                 const double c1 = cs_c[u], s1 = cs_s[u], c2 = cs_c[w], s2 = cs_s[w];
                 const bool q1v = q1 < m, q2v = q2 < m;
