@@ -70,3 +70,13 @@ def test_product_does_not_link_the_oracle():
         assert "oracle" not in out and "nlsp_ref" not in out
         syms = subprocess.run(["nm", "-D", so], capture_output=True, text=True).stdout
         assert "orc_" not in syms and "ref_pcg" not in syms
+
+
+def test_null_handle_queries_are_safe():
+    """Handle queries need no device: a null operator has no schedule (-1) and
+    zero dimensions."""
+    lib = L.gpu_lib()
+    assert lib.nlsp_twolevel_cycle(None) == -1
+    n, k = C.c_uint64(7), C.c_uint64(7)
+    lib.nlsp_twolevel_dims(None, C.byref(n), C.byref(k))
+    assert n.value == 0 and k.value == 0
