@@ -1637,6 +1637,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_prolong_onepass(SolveArgs a, co
 constexpr int kOpTR = NLSP_OP_TR;  // rows per tile (64 or 128)
 static_assert(kOpTR == 64 || kOpTR == 128, "one-pass tiles are 64 or 128 rows");
 constexpr int kOpWWarps = 8;   // W-product warps
+// The W-product warps split into op_wh(PPL) groups taking alternate tiles (the
+// ring depth S must then be a multiple of it as well): two groups for k <= 48,
+// whose tiles are short (measured: C3 prolongation 317 -> 292 us, C2 83 -> 78 us;
+// at k = 64 one group is faster, C4 -3.7 %, C5 -3 % with two).
+__host__ __device__ constexpr int op_wh(int ppl) { return ppl <= 3 ? 2 : 1; }
 constexpr int kOpSPairs = 4;   // at most this many stencil warp pairs (tile i -> pair i % P)
 constexpr int kOpMaxStages = 8;
 // Stencil pair p waits only on tiles i = p (mod P). With S a multiple of P it
@@ -1689,7 +1694,7 @@ __global__ void __launch_bounds__(kOpThreads, 1) k_prolong_onepass_tma(SolveArgs
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&asr[s], 2);
-            mbar_init(&empty[s], kOpWWarps);
+            mbar_init(&empty[s], kOpWWarps / op_wh(PPL));
         }
         fence_barrier_init();
     }
@@ -1819,8 +1824,11 @@ __global__ void __launch_bounds__(kOpThreads, 1) k_prolong_onepass_tma(SolveArgs
         }
     } else {
         // ---- W-product warps: 8 lanes per row, 2 rows per group per tile
+        constexpr int kOpWH = op_wh(PPL);
+        constexpr int WPG = kOpWWarps / kOpWH;  // warps per W group
         const int cw = warp - 1 - 2 * P;
-        const int grp = (cw * 32 + lane) >> 3, l = lane & (kGroup - 1);
+        const int wgrp = cw / WPG;
+        const int grp = ((cw % WPG) * 32 + lane) >> 3, l = lane & (kGroup - 1);
         double ev[2 * PPL];
 #pragma unroll
         for (int t = 0; t < PPL; ++t) {
@@ -1828,8 +1836,8 @@ __global__ void __launch_bounds__(kOpThreads, 1) k_prolong_onepass_tma(SolveArgs
             ev[2 * t] = pi < pairs ? a.e[2 * pi] : 0.0;
             ev[2 * t + 1] = pi < pairs ? a.e[2 * pi + 1] : 0.0;
         }
-        int i = 0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+        int i = wgrp;
+        for (int tile = blockIdx.x + wgrp * gridDim.x; tile < ntiles; tile += kOpWH * gridDim.x, i += kOpWH) {
             const int stg = i % S;
             mbar_wait(&full[stg], (i / S) & 1);
             mbar_wait(&asr[stg], (i / S) & 1);
@@ -1839,8 +1847,8 @@ __global__ void __launch_bounds__(kOpThreads, 1) k_prolong_onepass_tma(SolveArgs
             const double* rs = reinterpret_cast<const double*>(base + r_off);
             const double* as = reinterpret_cast<const double*>(base + as_off);
 #pragma unroll
-            for (int u = 0; u < kOpTR / (kOpWWarps * 4); ++u) {
-                const int lr = grp + kOpWWarps * 4 * u;
+            for (int u = 0; u < kOpTR / (WPG * 4); ++u) {
+                const int lr = grp + WPG * 4 * u;
                 const bool ok = lr < rows;  // every lane still runs the group shuffles
                 const double* wrow = reinterpret_cast<const double*>(base) + lr * ld;
                 const double rr = ok ? rs[lr] : 0.0, ar = ok ? as[lr] : 0.0;
@@ -2562,6 +2570,12 @@ static void prolong_onepass_ppl(const LaunchCtx& c, const SolveArgs& a, const do
         S -= S % P;  // the ring depth must be a multiple of P (see kOpSPairs)
         if (S < P) S = P;
         if (S > fit) S = fit, P = 1;
+    }
+    {
+        // ... and of the W-product warp groups
+        const int q = (P % op_wh(PPL) == 0) ? P : P * op_wh(PPL);
+        S -= S % q;
+        if (S < q) { S = q; }
     }
     const size_t sm = 256 + (size_t)S * op_stage_bytes(ld, tnz);
     if (NLSP_OP_TMA && fit >= 2) {
