@@ -1637,13 +1637,21 @@ __global__ void __launch_bounds__(kThreads, 2) k_prolong_onepass(SolveArgs a, co
 constexpr int kOpTR = NLSP_OP_TR;  // rows per tile (64 or 128)
 static_assert(kOpTR == 64 || kOpTR == 128, "one-pass tiles are 64 or 128 rows");
 constexpr int kOpWWarps = 8;   // W-product warps
+constexpr int kOpSPairs = 4;   // at most this many stencil warp pairs (tile i -> pair i % P)
+constexpr int kOpMaxStages = 8;
 // The W-product warps split into op_wh(PPL) groups taking alternate tiles (the
 // ring depth S must then be a multiple of it as well): two groups for k <= 48,
 // whose tiles are short (measured: C3 prolongation 317 -> 292 us, C2 83 -> 78 us;
 // at k = 64 one group is faster, C4 -3.7 %, C5 -3 % with two).
+// (16 W-product warps in two groups with 2 stencil pairs at k = 64 measured
+// slower too: C4 -7 %, C5 -6 %)
 __host__ __device__ constexpr int op_wh(int ppl) { return ppl <= 3 ? 2 : 1; }
-constexpr int kOpSPairs = 4;   // at most this many stencil warp pairs (tile i -> pair i % P)
-constexpr int kOpMaxStages = 8;
+// W-product warps per group (k <= 48: 4, k = 64: 8)
+__host__ __device__ constexpr int op_wpg(int ppl) { return ppl <= 3 ? 4 : 8; }
+__host__ __device__ constexpr int op_threads_max(int ppl) {
+    return 32 * (1 + 2 * kOpSPairs + op_wpg(ppl) * op_wh(ppl));
+}
+
 // Stencil pair p waits only on tiles i = p (mod P). With S a multiple of P it
 // always sees the stages p, p + P, ... and waits their phases in order, so an
 // mbarrier parity wait can never alias a phase two ahead (S % P == 0 is required).
@@ -1661,7 +1669,7 @@ __host__ __device__ constexpr unsigned op_stage_bytes(int ld, int tile_nnz = -1)
 }
 
 template <int PPL, int MAXD, bool RV>
-__global__ void __launch_bounds__(kOpThreads, 1) k_prolong_onepass_tma(SolveArgs a, const double* sv,
+__global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(SolveArgs a, const double* sv,
                                                                       double* zout,
                                                                       cudaGraphConditionalHandle h,
                                                                       int ctl, int S, int P, int rsel) {
@@ -1694,7 +1702,7 @@ __global__ void __launch_bounds__(kOpThreads, 1) k_prolong_onepass_tma(SolveArgs
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&asr[s], 2);
-            mbar_init(&empty[s], kOpWWarps / op_wh(PPL));
+            mbar_init(&empty[s], op_wpg(PPL));
         }
         fence_barrier_init();
     }
@@ -1825,7 +1833,7 @@ __global__ void __launch_bounds__(kOpThreads, 1) k_prolong_onepass_tma(SolveArgs
     } else {
         // ---- W-product warps: 8 lanes per row, 2 rows per group per tile
         constexpr int kOpWH = op_wh(PPL);
-        constexpr int WPG = kOpWWarps / kOpWH;  // warps per W group
+        constexpr int WPG = op_wpg(PPL);  // warps per W group
         const int cw = warp - 1 - 2 * P;
         const int wgrp = cw / WPG;
         const int grp = ((cw % WPG) * 32 + lane) >> 3, l = lane & (kGroup - 1);
@@ -1878,7 +1886,7 @@ __global__ void __launch_bounds__(kOpThreads, 1) k_prolong_onepass_tma(SolveArgs
         }
     }
     {
-        __shared__ double cs[(kOpThreads / 32) * 2 * kGroup * PPL];
+        __shared__ double cs[(op_threads_max(PPL) / 32) * 2 * kGroup * PPL];
         const long long G = gridDim.x;
         cta_columns<PPL>(au, cs, ld, a.opart);
         cta_columns<PPL>(av, cs, ld, a.opart + ld * G);
@@ -2580,7 +2588,7 @@ static void prolong_onepass_ppl(const LaunchCtx& c, const SolveArgs& a, const do
     const size_t sm = 256 + (size_t)S * op_stage_bytes(ld, tnz);
     if (NLSP_OP_TMA && fit >= 2) {
         const long long nt = (a.n + kOpTR - 1) / kOpTR;
-        const int threads = 32 * (1 + 2 * P + kOpWWarps);
+        const int threads = 32 * (1 + 2 * P + op_wpg(PPL) * op_wh(PPL));
 #define NLSP_P2(D, R) launch_op_tma(c, k_prolong_onepass_tma<PPL, D, R>, nt, sm, threads, a, sv, zout, h, ctl, S, P, rsel)
         const bool rv = a.dia.kind == 2;
         if (!a.dia.kind) NLSP_P2(0, false);
