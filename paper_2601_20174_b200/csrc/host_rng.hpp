@@ -53,37 +53,55 @@ inline void normal_stream(std::uint64_t seed, std::uint64_t count, double* out) 
     auto uni = [&]() { return static_cast<double>(gen() >> 11) * 0x1.0p-53; };
     const std::uint64_t pairs_total = (count + 1) / 2;
     const std::uint64_t chunk = 1ull << 22;
-    std::vector<double> u1(std::min(chunk, pairs_total)), u2(std::min(chunk, pairs_total));
+    const std::uint64_t cap = std::min(chunk, pairs_total);
+    // the sequential uniform stream of chunk c + 1 is drawn while the worker
+    // threads run the Box-Muller transforms of chunk c (double-buffered); the
+    // per-element arithmetic, and so every output bit, is that of a serial loop
+    std::vector<double> u1[2] = {std::vector<double>(cap), std::vector<double>(cap)};
+    std::vector<double> u2[2] = {std::vector<double>(cap), std::vector<double>(cap)};
     const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-    for (std::uint64_t base = 0; base < pairs_total; base += chunk) {
-        const std::uint64_t np = std::min(chunk, pairs_total - base);
+    auto draw = [&](std::uint64_t np, int buf) {
         for (std::uint64_t p = 0; p < np; ++p) {
             double a = uni();
             const double b = uni();
             while (a <= 0.0) a = uni();
-            u1[p] = a;
-            u2[p] = b;
+            u1[buf][p] = a;
+            u2[buf][p] = b;
         }
-        auto work = [&, base](std::uint64_t lo, std::uint64_t hi) {
-            for (std::uint64_t p = lo; p < hi; ++p) {
-                const double r = std::sqrt(-2.0 * std::log(u1[p]));
-                const double a = 2.0 * 3.141592653589793 * u2[p];
-                const std::uint64_t o = 2 * (base + p);
-                out[o] = r * std::cos(a);
-                if (o + 1 < count) out[o + 1] = r * std::sin(a);
-            }
-        };
+    };
+    auto transform = [&](std::uint64_t base, int buf, std::uint64_t lo, std::uint64_t hi) {
+        for (std::uint64_t p = lo; p < hi; ++p) {
+            const double r = std::sqrt(-2.0 * std::log(u1[buf][p]));
+            const double a = 2.0 * 3.141592653589793 * u2[buf][p];
+            const std::uint64_t o = 2 * (base + p);
+            out[o] = r * std::cos(a);
+            if (o + 1 < count) out[o + 1] = r * std::sin(a);
+        }
+    };
+    if (pairs_total == 0) return;
+    std::uint64_t np = std::min(chunk, pairs_total);
+    draw(np, 0);
+    int buf = 0;
+    for (std::uint64_t base = 0; base < pairs_total;) {
+        const std::uint64_t next = base + np;
+        const std::uint64_t np_next = next < pairs_total ? std::min(chunk, pairs_total - next) : 0;
         if (np < 65536 || hw == 1) {
-            work(0, np);
+            transform(base, buf, 0, np);
+            if (np_next) draw(np_next, buf ^ 1);
         } else {
             std::vector<std::thread> th;
-            const std::uint64_t per = (np + hw - 1) / hw;
-            for (unsigned t = 0; t < hw; ++t) {
+            const unsigned workers = hw > 1 ? hw - 1 : 1;  // this thread draws the next chunk
+            const std::uint64_t per = (np + workers - 1) / workers;
+            for (unsigned t = 0; t < workers; ++t) {
                 const std::uint64_t lo = t * per, hi = std::min(np, lo + per);
-                if (lo < hi) th.emplace_back(work, lo, hi);
+                if (lo < hi) th.emplace_back(transform, base, buf, lo, hi);
             }
+            if (np_next) draw(np_next, buf ^ 1);
             for (auto& x : th) x.join();
         }
+        base = next;
+        np = np_next;
+        buf ^= 1;
     }
 }
 
