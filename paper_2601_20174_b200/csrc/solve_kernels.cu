@@ -1,21 +1,26 @@
 // paper_2601_20174_b200/csrc/solve_kernels.cu — the PCG hot loop on sm_100a.
 //
-// One PCG iteration of two_level.hpp:141-191 with the two-level operator of
-// two_level.hpp:60-81 (nu1 = nu2 = 1) is five kernels, each a single pass over
-// HBM with its reductions finished by the last CTA to arrive (deterministic
-// fixed-order sums, no fp64 atomics):
+// Three schedules of one PCG iteration (two_level.hpp:141-191) with the
+// two-level operator (two_level.hpp:60-81), all applying the same operator
+// (DESIGN.md §3); every reduction is finished in a fixed order by the last CTA
+// to arrive (deterministic, no fp64 atomics):
 //
-//   k_spmv_p    p = z + beta p  (fused into the gather), q = A p, p.q -> alpha
-//   k_update    x += alpha p, r -= alpha q, ||r|| -> history, convergence test
-//   k_restrict  res = r - A (w D^-1 r), c = P^T res, last CTA: L L^T e = c
-//   k_prolong   z2 = w D^-1 r + P e
-//   k_sweep     z = z2 + w D^-1 (r - A z2), r.z -> beta            (post-sweep)
+//   one-pass (default, nu1 = nu2, k <= 64), three kernels at nu = 1/1:
+//     k_spmv_dia / k_spmv_tma <OpSpmvP>     p = z + beta p in the gather, q = A p, p.q -> alpha
+//     k_spmv_dia / k_spmv_tma <OpUpdSweep>  x, r' = r - alpha q (in the gather), s = S_2(r'),
+//                                           ||r'|| -> convergence; last CTA: c by its
+//                                           recurrence, e = A_c^-1 c
+//     k_prolong_onepass_tma                 z = s + W e with u = W^T r, v = W^T A s in the
+//                                           same pass over W; r.z -> beta, loop control
+//   folded (NLSP_CYCLE=folded): W1^T r fused with the x/r update, sweeps,
+//     z = s + W2 e (two passes over W) — k_update_restrict_tma, k_prolong
+//   literal (NLSP_CYCLE=literal): the reference's op-by-op order — k_update,
+//     k_restrict, k_prolong, k_sweep, k_loop_ctl
 //
-// plus a one-thread k_loop_ctl that advances the iteration and drives the CUDA
-// graph WHILE node. CSR rows and basis rows are handled by groups of 8 lanes
-// (4 rows per warp): the 8 lanes read a row's nonzeros as one coalesced run and
-// the row's k basis entries as 16-B loads, so the SpMV result of a row is
-// already in the registers of the lanes that stream that row of P.
+// The matrix is read in its diagonal form when the upload detected one
+// (k_spmv_dia, one thread per row) and otherwise from TMA-staged CSR row tiles
+// (k_spmv_tma); the row kernels of the literal schedule use groups of 8 lanes
+// per CSR / basis row.
 #include <cstdlib>
 #include <mutex>
 #include <type_traits>
