@@ -241,3 +241,51 @@ def test_onepass_cycle_matches_folded_midsize(nlsp, cfg, nx):
     # deterministic: a second solve is bitwise the first
     r3 = nlsp.pcg(a, pb.rhs, m1, c.delta, 10 * pb.n)
     assert np.array_equal(r1.solution, r3.solution)
+
+
+def test_shared_handles_concurrent_contexts(nlsp):
+    """Handles are immutable after build and may be shared read-only across
+    contexts: four host threads, each with its own context (stream,
+    workspace, one-pass partials, PCG state), solve different right-hand sides
+    with ONE uploaded matrix and ONE two-level operator at the same time, on the
+    graph loop (n > 65 536). Each result is bitwise the one of a serial solve."""
+    import ctypes as C
+    import threading
+
+    from paper_2601_20174_b200 import _lib as L
+    from paper_2601_20174_b200 import problems
+    c = problems.C4.scaled(nx=48)
+    pb = problems.generate(c)
+    a = pb.csr()
+    sv = nlsp.generate_smoothed_vectors(a, None, c.m, c.s1, c.omega, c.s0_seed)
+    p, _, _ = nlsp.svd_basis(sv.s, c.k)
+    m = nlsp.TwoLevelPreconditioner(a, p, c.omega, c.nu1, c.nu2)
+    assert m.cycle() == "onepass" and pb.n > 65536
+    dev = a.device(m.ctx)
+    rng = np.random.default_rng(3)
+    rhs = [rng.standard_normal(pb.n) for _ in range(4)]
+    lib = L.gpu_lib()
+
+    def solve(ctx, b):
+        x = np.empty(pb.n)
+        rep = L.SolveReportC()
+        st = lib.nlsp_pcg(ctx.handle, dev.handle, L.PRECOND_TWOLEVEL, m.handle, L.dptr(b), c.delta,
+                          10 * pb.n, L.dptr(x), C.byref(rep), None)
+        assert st == 0, lib.nlsp_last_error(ctx.handle)
+        return x, int(rep.iterations)
+
+    serial = [solve(m.ctx, b) for b in rhs]
+    ctxs = [nlsp.Context(0) for _ in rhs]
+    out = [None] * len(rhs)
+
+    def worker(i):
+        for _ in range(3):
+            out[i] = solve(ctxs[i], rhs[i])
+
+    th = [threading.Thread(target=worker, args=(i,)) for i in range(len(rhs))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for (x, it), (xs, its) in zip(out, serial):
+        assert it == its and np.array_equal(x, xs)
