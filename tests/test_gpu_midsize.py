@@ -1,0 +1,37 @@
+"""bench_single's SVD row at mid size against the reference's own run
+(tests/golden/make_mid_golden.py): the C4 and C3 families beyond the
+single-cluster solver (n = 262 144 and 102 400, the BASELINE k, m, nu), so the
+whole pipeline — smoothing, SVD basis, two-level build, and PCG on the graph
+loop with the one-pass schedule — is checked against the reference's outputs
+with the north-star tolerances."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from paper_2601_20174_b200 import problems
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", ["mid_C4", "mid_C3"])
+def test_midsize_pipeline_matches_reference(nlsp, name):
+    d = golden(name)
+    cfg = problems.CONFIGS[name[4:]].scaled(nx=int(d["nx"]))
+    pb = problems.generate(cfg)
+    assert pb.n == int(d["n"]) and pb.n > 65536
+    a = pb.csr()
+    sv = nlsp.generate_smoothed_vectors(a, None, cfg.m, cfg.s1, cfg.omega, cfg.s0_seed)
+    p, sig, _ = nlsp.svd_basis(sv.s, cfg.k)
+    sref = np.asarray(d["sigma"])
+    assert np.abs(np.asarray(sig) - sref[: len(sig)]).max() <= 1e-10 * sref[0]
+    m = nlsp.TwoLevelPreconditioner(a, p, cfg.omega, cfg.nu1, cfg.nu2)
+    assert m.cycle() == "onepass"
+    res = nlsp.pcg(a, pb.rhs, m, cfg.delta, 10 * pb.n)
+    rep = res.report
+    assert rep.converged and rep.kernel_launches > 2  # the graph loop, not the cluster solver
+    assert abs(rep.iterations - int(d["iterations"])) <= 2, (rep.iterations, int(d["iterations"]))
+    assert rep.residual_history[-1] < cfg.delta and rep.true_relative_residual < 10 * cfg.delta
+    x = np.asarray(d["x"])
+    assert np.linalg.norm(res.solution - x) <= 1e-9 * np.linalg.norm(x)
