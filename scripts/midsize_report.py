@@ -5,9 +5,10 @@ import sys, numpy as np
 sys.path.insert(0, '.'); sys.path.insert(0, 'tests')
 from conftest import golden
 from paper_2601_20174_b200 import problems, nlsp
-for name in ["mid_C4", "mid_C3"]:
+for name in ["mid_C4", "mid_C3", "mid_C2", "mid_C5"]:
     d = golden(name); cfg = problems.CONFIGS[name[4:]].scaled(nx=int(d["nx"])); pb = problems.generate(cfg); a = pb.csr()
-    sv = nlsp.generate_smoothed_vectors(a, None, cfg.m, cfg.s1, cfg.omega, cfg.s0_seed)
+    mask = pb.mask if pb.mask.any() else None
+    sv = nlsp.generate_smoothed_vectors(a, mask, cfg.m, cfg.s1, cfg.omega, cfg.s0_seed)
     p, sig, _ = nlsp.svd_basis(sv.s, cfg.k)
     m = nlsp.TwoLevelPreconditioner(a, p, cfg.omega, cfg.nu1, cfg.nu2)
     r = nlsp.pcg(a, pb.rhs, m, cfg.delta, 10 * pb.n)

@@ -29,16 +29,21 @@ OUT = os.path.dirname(os.path.abspath(__file__))
 MID = {
     "mid_C4": problems.C4.scaled(nx=64),    # n = 262 144, k = 64, m = 128, nu = 1/1
     "mid_C3": problems.C3.scaled(nx=320),   # n = 102 400, k = 48, m = 96, nu = 2/2
+    "mid_C2": problems.C2.scaled(nx=320),   # n = 102 400, k = 32, m = 64, s1 = 20 (per-row values)
+    "mid_C5": problems.C5.scaled(nx=192),   # n = 74 498, k = 64, m = 128 (CSR, clamped edge)
 }
 
 
-def main():
+def main(names=None):
     ref = Reference(strict=False)
     for name, cfg in MID.items():
+        if names and name not in names:
+            continue
         t0 = time.perf_counter()
         pb = problems.generate(cfg)
         a = (pb.n, pb.row_ptr, pb.col_idx, pb.values)
-        s = ref.generate_smoothed_vectors(a, None, cfg.m, cfg.s1, cfg.omega, cfg.s0_seed)
+        mask = pb.mask if pb.mask.any() else None
+        s = ref.generate_smoothed_vectors(a, mask, cfg.m, cfg.s1, cfg.omega, cfg.s0_seed)
         u, sig, _, sweeps = ref.svd(s)
         p = np.ascontiguousarray(u[:, : cfg.k])
         t = ref.twolevel(a, p, cfg.omega, cfg.nu1, cfg.nu2)
@@ -52,4 +57,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:])

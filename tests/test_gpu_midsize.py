@@ -1,6 +1,6 @@
 """bench_single's SVD row at mid size against the reference's own run
-(tests/golden/make_mid_golden.py): the C4 and C3 families beyond the
-single-cluster solver (n = 262 144 and 102 400, the BASELINE k, m, nu), so the
+(tests/golden/make_mid_golden.py): the C2–C5 families beyond the
+single-cluster solver (n = 74 498 to 262 144, the BASELINE k, m, nu), so the
 whole pipeline — smoothing, SVD basis, two-level build, and PCG on the graph
 loop with the one-pass schedule — is checked against the reference's outputs
 with the north-star tolerances."""
@@ -15,14 +15,15 @@ from paper_2601_20174_b200 import problems
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("name", ["mid_C4", "mid_C3"])
+@pytest.mark.parametrize("name", ["mid_C4", "mid_C3", "mid_C2", "mid_C5"])
 def test_midsize_pipeline_matches_reference(nlsp, name):
     d = golden(name)
     cfg = problems.CONFIGS[name[4:]].scaled(nx=int(d["nx"]))
     pb = problems.generate(cfg)
     assert pb.n == int(d["n"]) and pb.n > 65536
     a = pb.csr()
-    sv = nlsp.generate_smoothed_vectors(a, None, cfg.m, cfg.s1, cfg.omega, cfg.s0_seed)
+    mask = pb.mask if pb.mask.any() else None
+    sv = nlsp.generate_smoothed_vectors(a, mask, cfg.m, cfg.s1, cfg.omega, cfg.s0_seed)
     p, sig, _ = nlsp.svd_basis(sv.s, cfg.k)
     sref = np.asarray(d["sigma"])
     assert np.abs(np.asarray(sig) - sref[: len(sig)]).max() <= 1e-10 * sref[0]
