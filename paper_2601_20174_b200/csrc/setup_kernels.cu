@@ -295,6 +295,34 @@ __global__ void __launch_bounds__(1024) k_eigh(EighArgs args, int use_shared) {
     if (tid == 0) total_s = sqrt(t);
     __syncthreads();
     const double total = total_s;
+    // the (u, w) 2x2 blocks of every round are the same for a thread: decode
+    // them once (up to kEighBlk per thread; larger m decodes per round)
+    constexpr int kEighBlk = 4;
+    const int np_ = mp / 2;
+    const int nblocks_ = np_ * (np_ + 1) / 2;
+    const bool pre_blk = nblocks_ <= kEighBlk * nt;
+    auto decode = [&](int bi, int& u, int& w) {
+        // row u of the upper triangle starts at u np - u (u - 1) / 2 (closed
+        // form, then a +-1 fix-up)
+        const double b2 = 2.0 * np_ + 1.0;
+        u = (int)((b2 - sqrt(b2 * b2 - 8.0 * bi)) * 0.5);
+        auto row_start = [&](int uu) { return uu * np_ - (uu * (uu - 1)) / 2; };
+        if (u < 0) u = 0;
+        if (u > np_ - 1) u = np_ - 1;
+        while (u > 0 && row_start(u) > bi) --u;
+        while (u < np_ - 1 && row_start(u + 1) <= bi) ++u;
+        w = u + (bi - row_start(u));
+    };
+    int blk_u[kEighBlk], blk_w[kEighBlk];
+#pragma unroll
+    for (int j = 0; j < kEighBlk; ++j) {
+        blk_u[j] = blk_w[j] = -1;
+        const int bi = tid + j * nt;
+        if (pre_blk && bi < nblocks_) decode(bi, blk_u[j], blk_w[j]);
+    }
+    // V update mapping: a fixed rotation w per thread when nt is a multiple of np
+    const bool v_fixed = (nt % np_) == 0;
+    const int v_w = tid % np_, v_i0 = tid / np_, v_step = nt / np_;
     int sweeps = 0;
     int status = isfinite(total) ? 0 : kErrValidation;  // svd.hpp:156 all_finite gate
     for (; status == 0;) {
@@ -343,22 +371,12 @@ __global__ void __launch_bounds__(1024) k_eigh(EighArgs args, int use_shared) {
             // A <- J^T A J on 2x2 blocks (pair u rows, pair w cols), u <= w
             const int np = mp / 2;
             const int nblocks = np * (np + 1) / 2;
-            for (int bi = tid; bi < nblocks; bi += nt) {
-                // decode bi -> (u, w) with u <= w: row u of the upper triangle
-                // starts at u np - u (u - 1) / 2 (closed form, then a +-1 fix-up)
-                const double b2 = 2.0 * np + 1.0;
-                int u = (int)((b2 - sqrt(b2 * b2 - 8.0 * bi)) * 0.5);
-                auto row_start = [&](int uu) { return uu * np - (uu * (uu - 1)) / 2; };
-                if (u < 0) u = 0;
-                if (u > np - 1) u = np - 1;
-                while (u > 0 && row_start(u) > bi) --u;
-                while (u < np - 1 && row_start(u + 1) <= bi) ++u;
-                const int w = u + (bi - row_start(u));
+            auto block = [&](int u, int w) {
                 const int p1 = pp[u], q1 = pq[u], p2 = pp[w], q2 = pq[w];
                 const double c1 = cs_c[u], s1 = cs_s[u], c2 = cs_c[w], s2 = cs_s[w];
                 const bool q1v = q1 < m, q2v = q2 < m;
                 if (u == w) {
-                    if (!q1v) continue;
+                    if (!q1v) return;
                     const double xpp = a[pidx(p1, p1, m)], xpq = a[pidx(p1, q1, m)],
                                  xqq = a[pidx(q1, q1, m)];
                     // columns: y(., p) = c x(., p) - s x(., q); y(., q) = s x(., p) + c x(., q)
@@ -381,16 +399,39 @@ __global__ void __launch_bounds__(1024) k_eigh(EighArgs args, int use_shared) {
                     if (q1v) pel(a, q1, p2, m) = s1 * ypp + c1 * yqp;
                     if (q1v && q2v) pel(a, q1, q2, m) = s1 * ypq + c1 * yqq;
                 }
+            };
+            if (pre_blk) {
+#pragma unroll
+                for (int j = 0; j < kEighBlk; ++j)
+                    if (blk_u[j] >= 0) block(blk_u[j], blk_w[j]);
+            } else {
+                for (int bi = tid; bi < nblocks; bi += nt) {
+                    int u, w;
+                    decode(bi, u, w);
+                    block(u, w);
+                }
             }
             // V <- V J (svd.hpp:61-65)
-            for (int idx = tid; idx < m * np; idx += nt) {
-                const int i = idx / np, w = idx % np;
-                const int p = pp[w], q = pq[w];
-                if (q >= m) continue;
-                const double c = cs_c[w], s = cs_s[w];
-                const double vip = v[i * m + p], viq = v[i * m + q];
-                v[i * m + p] = c * vip - s * viq;
-                v[i * m + q] = s * vip + c * viq;
+            if (v_fixed) {
+                const int p = pp[v_w], q = pq[v_w];
+                if (q < m) {
+                    const double c = cs_c[v_w], s = cs_s[v_w];
+                    for (int i = v_i0; i < m; i += v_step) {
+                        const double vip = v[i * m + p], viq = v[i * m + q];
+                        v[i * m + p] = c * vip - s * viq;
+                        v[i * m + q] = s * vip + c * viq;
+                    }
+                }
+            } else {
+                for (int idx = tid; idx < m * np; idx += nt) {
+                    const int i = idx / np, w = idx % np;
+                    const int p = pp[w], q = pq[w];
+                    if (q >= m) continue;
+                    const double c = cs_c[w], s = cs_s[w];
+                    const double vip = v[i * m + p], viq = v[i * m + q];
+                    v[i * m + p] = c * vip - s * viq;
+                    v[i * m + q] = s * vip + c * viq;
+                }
             }
             __syncthreads();
         }
