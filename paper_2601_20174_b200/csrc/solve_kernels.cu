@@ -1651,8 +1651,8 @@ constexpr int kOpMaxStages = 8;
 // (16 W-product warps in two groups with 2 stencil pairs at k = 64 measured
 // slower too: C4 -7 %, C5 -6 %)
 __host__ __device__ constexpr int op_wh(int ppl) { return ppl <= 3 ? 2 : 1; }
-// W-product warps per group (k <= 48: 4, k = 64: 8)
-__host__ __device__ constexpr int op_wpg(int ppl) { return ppl <= 3 ? 4 : 8; }
+// W-product warps per group (kOpWWarps in all: k <= 48: 2 x 4, k = 64: 1 x 8)
+__host__ __device__ constexpr int op_wpg(int ppl) { return kOpWWarps / op_wh(ppl); }
 __host__ __device__ constexpr int op_threads_max(int ppl) {
     return 32 * (1 + 2 * kOpSPairs + op_wpg(ppl) * op_wh(ppl));
 }
@@ -1660,7 +1660,6 @@ __host__ __device__ constexpr int op_threads_max(int ppl) {
 // Stencil pair p waits only on tiles i = p (mod P). With S a multiple of P it
 // always sees the stages p, p + P, ... and waits their phases in order, so an
 // mbarrier parity wait can never alias a phase two ahead (S % P == 0 is required).
-constexpr int kOpThreads = 32 * (1 + 2 * kOpSPairs + kOpWWarps);
 constexpr unsigned kOpVec = kOpTR * 8;  // bytes of one staged vector slice
 
 // CSR matrices also stage the tile's row_ptr slice and its runs of values and
