@@ -367,12 +367,9 @@ def run_ours(args, dist: Dist):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generators, BASELINE.json shapes; DESIGN.md §Inputs)",
-        "config": {"workload": f"{args.config}: {cfg.name}", "n": pb.n, "nnz": pb.nnz, "k": cfg.k,
-                   "m": cfg.m, "s1": cfg.s1, "nu1": cfg.nu1, "nu2": cfg.nu2, "omega": cfg.omega,
-                   "delta": cfg.delta, "step": "one PCG solve to 1e-8 (device-resident b, x)",
-                   "l2": "inputs larger than L2 (%.2f GB streamed per iteration vs 126 MB L2)"
-                         % (bytes_iter / 1e9),
-                   "parallelism": f"replicas x{dist.world}"},
+        "config": workload_config(args, cfg, pb, "one PCG solve to 1e-8 (device-resident b, x)",
+                                  "inputs larger than L2 (%.2f GB streamed per iteration vs 126 MB L2)"
+                                  % (bytes_iter / 1e9), f"replicas x{dist.world}"),
         "iterations_per_solve": iters_per_solve,
         "time_to_solution_ms": round(ms_local / args.steps, 3),
         "ms_per_iteration": round(ms_local / iters, 4),
@@ -393,27 +390,39 @@ def run_ours(args, dist: Dist):
 def cpu_baseline(args, cfg, pb, m, x_gpu):
     """The reference's pcg<TwoLevelPreconditioner> on 1 host core (the reference
     solve is single-threaded) for a bounded number of iterations,
-    with the preconditioner seated from this run's basis and A_c."""
+    with the preconditioner seated from this run's basis and A_c.
+
+    Every pcg call also pays its prologue (r = b, z = M r, p = z: one apply,
+    two_level.hpp:152-156) and its final true-residual SpMV (:185-189), which
+    the iteration count does not include. So the sample is differenced: the
+    same call with N and with 1 iteration, per-iteration cost
+    (T_N - T_1) / (N - 1) (both from the library's steady clock)."""
     from oracle.oracle import Oracle, Reference, reference_available
 
     basis, _, coarse = m._export()
     a = (pb.n, pb.row_ptr, pb.col_idx, pb.values)
     kind = "reference" if reference_available() else "port"
-    impl = Reference() if kind == "reference" else Oracle()
+    impl = Reference(native=True) if kind == "reference" else Oracle()
     t = impl.twolevel_from_parts(a, basis, coarse, cfg.omega, cfg.nu1, cfg.nu2)
     # size the sample to ~args.cpu_seconds from one probe iteration
     probe = impl.pcg(a, pb.rhs, 2, t, 0.0, 1)
     per_iter_ms = max(probe.solve_ms, 1e-3)
-    iters = int(max(1, min(args.cpu_max_iters, args.cpu_seconds * 1e3 / per_iter_ms)))
+    iters = int(max(2, min(args.cpu_max_iters, args.cpu_seconds * 1e3 / per_iter_ms)))
     t0 = time.perf_counter()
     res = impl.pcg(a, pb.rhs, 2, t, 0.0, iters)
+    one = impl.pcg(a, pb.rhs, 2, t, 0.0, 1)
     wall = time.perf_counter() - t0
-    return {"value": round(res.iterations / wall, 4), "unit": UNIT, "cores": 1, "kind": kind,
-            "sample": f"{res.iterations} iterations of the reference pcg<TwoLevelPreconditioner> "
+    dn = res.iterations - one.iterations
+    dms = res.solve_ms - one.solve_ms
+    return {"value": round(dn / (dms / 1e3), 4), "unit": UNIT, "cores": 1, "kind": kind,
+            "isa": getattr(impl, "isa", "c11 -O2 port"),
+            "sample": f"{res.iterations} minus 1 iterations of the reference pcg<TwoLevelPreconditioner> "
                       f"on the full {args.config} system (n={pb.n}), 1 thread, preconditioner "
-                      f"seated from this run's basis/A_c (constructor body skipped)",
-            "ms_per_iteration": round(wall * 1e3 / res.iterations, 2),
-            "host_cpu": _cpu_model(), "nproc": os.cpu_count()}
+                      f"seated from this run's basis/A_c (constructor body skipped); prologue "
+                      f"apply and final true-residual SpMV differenced out",
+            "ms_per_iteration": round(dms / dn, 2),
+            "undifferenced_ms_per_iteration": round(res.solve_ms / res.iterations, 2),
+            "wall_s": round(wall, 2), "host_cpu": _cpu_model(), "nproc": os.cpu_count()}
 
 
 def _cpu_model():
@@ -440,7 +449,7 @@ def run_reference(args, dist: Dist):
     pb = problems.generate(cfg)
     a = (pb.n, pb.row_ptr, pb.col_idx, pb.values)
     kind = "reference" if reference_available() else "port"
-    impl = Reference() if kind == "reference" else Oracle()
+    impl = Reference(native=True) if kind == "reference" else Oracle()
     # an orthonormal n x k basis and its Galerkin operator (host LAPACK / scipy);
     # the per-iteration cost of the solve does not depend on which basis
     rng = np.random.default_rng(cfg.seed)
@@ -462,14 +471,22 @@ def run_reference(args, dist: Dist):
     else:
         probe_ms = impl.pcg(a, pb.rhs, 2, t, 0.0, 1).solve_ms
         threads = 1
-    per_step = int(max(1, min(args.cpu_max_iters, args.ref_step_seconds * 1e3 / max(probe_ms, 1e-3))))
+    per_step = int(max(2, min(args.cpu_max_iters, args.ref_step_seconds * 1e3 / max(probe_ms, 1e-3))))
+
+    def run(iters):
+        if kind == "reference":
+            wall_ms, it = impl.pcg_parallel(a, pb.rhs, 2, t, 0.0, iters, threads)
+            return wall_ms, it * threads
+        r = impl.pcg(a, pb.rhs, 2, t, 0.0, iters)
+        return r.solve_ms, r.iterations
 
     def step():
-        if kind == "reference":
-            wall_ms, it = impl.pcg_parallel(a, pb.rhs, 2, t, 0.0, per_step, threads)
-            return wall_ms, it * threads
-        r = impl.pcg(a, pb.rhs, 2, t, 0.0, per_step)
-        return r.solve_ms, r.iterations
+        # every pcg call also runs its prologue apply (two_level.hpp:152-156) and
+        # the final true-residual SpMV (:185-189): difference a 1-iteration call
+        # out, so the step's iterations and time are those of the loop alone
+        w_n, it_n = run(per_step)
+        w_1, it_1 = run(1)
+        return w_n - w_1, it_n - it_1
 
     for _ in range(args.warmup):
         step()
@@ -479,24 +496,31 @@ def run_reference(args, dist: Dist):
         tot_ms += w
         tot_it += it
     value = tot_it / (tot_ms / 1e3)
-    sample = (f"{per_step} PCG iterations x {threads} concurrent single-threaded reference solves "
+    sample = (f"({per_step} - 1) PCG iterations x {threads} concurrent single-threaded reference solves "
               f"(pcg<TwoLevelPreconditioner>, two_level.hpp:141-191) on the full {args.config} "
-              f"system (n={pb.n}, k={cfg.k}) per step")
+              f"system (n={pb.n}, k={cfg.k}) per step; a 1-iteration call differences out the "
+              f"prologue apply and the final true-residual SpMV")
+    isa = getattr(impl, "isa", "c11 -O2 port")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
         "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(tot_ms / args.steps, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (same generators as our arm)",
-        "config": {"workload": f"{args.config}: {cfg.name}", "n": pb.n, "nnz": pb.nnz, "k": cfg.k,
-                   "m": cfg.m, "nu1": cfg.nu1, "nu2": cfg.nu2, "delta": cfg.delta,
-                   "step": "bounded sample of the reference CPU solve",
-                   "l2": "host run (no GPU L2)", "parallelism": f"{threads} host threads"},
+        "config": workload_config(args, cfg, pb, "bounded sample of the reference CPU solve",
+                                  "host run (no GPU L2)", f"{threads} host threads"),
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": sample, "host_cpu": _cpu_model(), "nproc": os.cpu_count()},
+                         "isa": isa, "sample": sample, "host_cpu": _cpu_model(), "nproc": os.cpu_count()},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "ms_per_iteration_per_thread": round(tot_ms * threads / max(tot_it, 1), 2),
     }), flush=True)
+
+
+def workload_config(args, cfg, pb, step, l2, parallelism):
+    """The `config` object, identical keys for both arms."""
+    return {"workload": f"{args.config}: {cfg.name}", "n": pb.n, "nnz": pb.nnz, "k": cfg.k,
+            "m": cfg.m, "s1": cfg.s1, "nu1": cfg.nu1, "nu2": cfg.nu2, "omega": cfg.omega,
+            "delta": cfg.delta, "step": step, "l2": l2, "parallelism": parallelism}
 
 
 def main():

@@ -156,8 +156,13 @@ nlsp_status nlsp_twolevel_apply(nlsp_ctx* ctx, const nlsp_twolevel* m, const nls
 /* ------------------------------------------------------------------ PCG ---- */
 /* pcg<Preconditioner> (two_level.hpp:141-191) with x0 = 0. m must be non-NULL
  * for NLSP_PRECOND_TWOLEVEL and is ignored otherwise. b, x host buffers of
- * length n; residual_history (may be NULL) receives rep->iterations entries and
- * must hold max_iters. The whole iteration loop runs on the device. */
+ * length n. The whole iteration loop runs on the device; max_iters may be any
+ * value (SIZE_MAX: no limit). The device keeps the residual history in
+ * segments of at most 2^20 entries (a longer solve pauses at each segment end
+ * to move it to the host), so no buffer is sized by max_iters. Read the history
+ * after the call with nlsp_pcg_history; residual_history (may be NULL) is the
+ * one-shot form: it receives rep->iterations entries, so it must hold as many
+ * as the solve may run. */
 nlsp_status nlsp_pcg(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twolevel* m,
                      const double* b, double delta, uint64_t max_iters, double* x,
                      nlsp_solve_report* rep, double* residual_history);
@@ -166,6 +171,12 @@ nlsp_status nlsp_pcg(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
 nlsp_status nlsp_pcg_device(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twolevel* m,
                             const double* b_dev, double delta, uint64_t max_iters, double* x_dev,
                             nlsp_solve_report* rep, double* residual_history);
+/* SolveReport::residual_history (two_level.hpp:123, one ||r_k||/||b|| per
+ * iteration) of the last nlsp_pcg / nlsp_pcg_device call on ctx: *count = its
+ * length (= that call's rep->iterations), and min(cap, *count) entries are
+ * copied to the host buffer out (out may be NULL to query the length). Valid
+ * until the next solve on ctx. */
+nlsp_status nlsp_pcg_history(nlsp_ctx* ctx, double* out, uint64_t cap, uint64_t* count);
 
 /* ------------------------------------------------------------ profiling ---- */
 /* Runs `iters` PCG iterations kernel by kernel (no graph) on device-resident b

@@ -9,6 +9,10 @@
 //     nlsp_gpu::TwoLevelPreconditioner M(dev, A, u, omega, nu1, nu2);
 //     nlsp_gpu::PcgResult r = nlsp_gpu::pcg(dev, A, b, M, delta, max_iters);
 //
+// Reference-signature overloads (pcg(a, b, M, delta, max_iters),
+// build_preconditioner, apply_two_level, M.apply(a, r)) take the reference's
+// own SparseCsrMatrix and run on a thread-local default device; see below.
+//
 // `a` may be the reference's nlsp::SparseCsrMatrix itself (dim(), row_ptr(),
 // col_idx(), values() with size_t indices, sparse.hpp:62-66) and a basis may be
 // its nlsp::DenseMatrix (rows(), cols(), data(), dense.hpp:23-30). Errors throw:
@@ -18,6 +22,8 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -221,9 +227,13 @@ public:
     std::vector<double> apply(const Matrix& a, const std::vector<double>& rhs) const {
         if (rhs.size() != a.dim()) throw ValidationError("two-level apply: dimension mismatch");
         std::vector<double> z(a.dim());
-        check(nlsp_twolevel_apply(dev_->get(), m_.get(), a.get(), rhs.data(), z.data()), dev_->get());
+        check(nlsp_twolevel_apply(a.device().get(), m_.get(), a.get(), rhs.data(), z.data()), a.device().get());
         return z;
     }
+    // m.apply(a, r) with the reference's matrix (two_level.hpp:60): uploaded once
+    // per thread (device_matrix, below)
+    template <class Csr, class = decltype(std::declval<const Csr&>().row_ptr())>
+    std::vector<double> apply(const Csr& a, const std::vector<double>& rhs) const;
 
 private:
     struct Del {
@@ -237,21 +247,30 @@ private:
 struct IdentityPreconditioner {};  // two_level.hpp:103-106
 struct JacobiPreconditioner {};    // two_level.hpp:107-118
 
-// SolveReport / PcgResult (two_level.hpp:121-137)
+// SolveReport / PcgResult (two_level.hpp:121-137). With NLSP_GPU_REFERENCE_TYPES
+// (defined after including the reference's nlsp/two_level.hpp) they ARE the
+// reference's structs, so `nlsp::PcgResult r = pcg(...)` compiles unchanged.
+#ifdef NLSP_GPU_REFERENCE_TYPES
+using SolveReport = ::nlsp::SolveReport;
+using PcgResult = ::nlsp::PcgResult;
+#else
 struct SolveReport {
     std::size_t iterations = 0;
-    std::vector<double> residual_history;
+    std::vector<double> residual_history;  // ||r_k|| / ||b|| per iteration
     bool converged = false;
     double true_relative_residual = 0.0;
+    double inference_ms = 0.0;
     double setup_ms = 0.0;
     double solve_ms = 0.0;
     double total_ms = 0.0;
+    std::string method;
     std::size_t coarse_dim = 0;
 };
 struct PcgResult {
     std::vector<double> solution;
     SolveReport report;
 };
+#endif
 
 namespace detail {
 inline PcgResult run(Device& dev, const Matrix& a, const std::vector<double>& b, int kind,
@@ -259,12 +278,14 @@ inline PcgResult run(Device& dev, const Matrix& a, const std::vector<double>& b,
     if (b.size() != a.dim()) throw ValidationError("pcg: dimension mismatch");
     PcgResult out;
     out.solution.resize(a.dim());
-    std::vector<double> hist(max_iters ? max_iters : 1);
     nlsp_solve_report rep{};
     check(nlsp_pcg(dev.get(), a.get(), kind, m, b.data(), delta, max_iters, out.solution.data(), &rep,
-                   hist.data()),
+                   nullptr),
           dev.get());
-    hist.resize(rep.iterations);
+    // the history, sized by the iterations run (not by max_iters)
+    std::vector<double> hist(rep.iterations);
+    std::uint64_t cnt = 0;
+    check(nlsp_pcg_history(dev.get(), hist.empty() ? nullptr : hist.data(), hist.size(), &cnt), dev.get());
     out.report.iterations = rep.iterations;
     out.report.residual_history = std::move(hist);
     out.report.converged = rep.converged != 0;
@@ -272,6 +293,7 @@ inline PcgResult run(Device& dev, const Matrix& a, const std::vector<double>& b,
     out.report.solve_ms = rep.solve_ms;
     out.report.total_ms = rep.total_ms;
     out.report.coarse_dim = rep.coarse_dim;
+    out.report.method = kind == NLSP_PRECOND_TWOLEVEL ? "two_level" : (kind == NLSP_PRECOND_JACOBI ? "jacobi" : "plain");
     return out;
 }
 }  // namespace detail
@@ -288,6 +310,130 @@ inline PcgResult pcg(Device& dev, const Matrix& a, const std::vector<double>& b,
 inline PcgResult pcg(Device& dev, const Matrix& a, const std::vector<double>& b,
                      const JacobiPreconditioner&, double delta, std::size_t max_iters) {
     return detail::run(dev, a, b, NLSP_PRECOND_JACOBI, nullptr, delta, max_iters);
+}
+
+// ---- the reference's own signatures (two_level.hpp:91-101, 141-191) --------
+// Reference call sites keep their SparseCsrMatrix and std::vector arguments:
+//
+//     auto M = nlsp_gpu::build_preconditioner(a, basis, omega, nu1, nu2);  // the one changed line
+//     nlsp::PcgResult r = pcg(a, b, M, delta, max_iters);                  // unchanged: ADL picks
+//     auto z = apply_two_level(M, a, r);                                   // the device overloads
+//
+// A thread-local default Device (NLSP_GPU_DEVICE, default 0; one context per
+// host thread, as the C-ABI requires) and a small per-thread upload cache stand
+// in for the explicit Device/Matrix. The reference's matrices are immutable
+// after construction (sparse.hpp:19-113), so a cached upload is keyed by the
+// object's address, its arrays' addresses and sizes, and a sampled fingerprint
+// of its entries.
+namespace detail {
+struct CsrKey {
+    const void* obj = nullptr;
+    const void* rp = nullptr;
+    const void* ci = nullptr;
+    const void* v = nullptr;
+    std::uint64_t n = 0, nnz = 0, fp = 0;
+    bool operator==(const CsrKey& o) const {
+        return obj == o.obj && rp == o.rp && ci == o.ci && v == o.v && n == o.n && nnz == o.nnz && fp == o.fp;
+    }
+};
+template <class Csr>
+CsrKey csr_key(const Csr& a) {
+    CsrKey k;
+    k.obj = &a;
+    k.rp = a.row_ptr().data();
+    k.ci = a.col_idx().data();
+    k.v = a.values().data();
+    k.n = a.dim();
+    k.nnz = a.values().size();
+    std::uint64_t h = 1469598103934665603ull;  // FNV-1a over <= 64 sampled entries
+    const std::uint64_t step = k.nnz > 64 ? k.nnz / 64 : 1;
+    for (std::uint64_t i = 0; i < k.nnz; i += step) {
+        std::uint64_t bits;
+        const double d = a.values()[i];
+        std::memcpy(&bits, &d, sizeof bits);
+        h = (h ^ bits ^ ((std::uint64_t)a.col_idx()[i] << 17)) * 1099511628211ull;
+    }
+    k.fp = h;
+    return k;
+}
+struct ThreadState {
+    Device dev;  // declared first: destroyed after the cached matrices
+    std::vector<std::pair<CsrKey, std::unique_ptr<Matrix>>> cache;
+    ThreadState() : dev(std::getenv("NLSP_GPU_DEVICE") ? std::atoi(std::getenv("NLSP_GPU_DEVICE")) : 0) {}
+};
+inline ThreadState& tls() {
+    thread_local ThreadState t;
+    return t;
+}
+}  // namespace detail
+
+// the calling thread's default device
+inline Device& default_device() { return detail::tls().dev; }
+
+// the device copy of a reference matrix on this thread's device (cached; the
+// four most recent matrices are kept)
+template <class Csr, class = decltype(std::declval<const Csr&>().row_ptr())>
+const Matrix& device_matrix(const Csr& a) {
+    auto& t = detail::tls();
+    const detail::CsrKey key = detail::csr_key(a);
+    for (auto& e : t.cache)
+        if (e.first == key) return *e.second;
+    if (t.cache.size() >= 4) t.cache.erase(t.cache.begin());
+    t.cache.emplace_back(key, std::make_unique<Matrix>(t.dev, a));
+    return *t.cache.back().second;
+}
+
+// build_preconditioner (two_level.hpp:91-95): any SparseCsrMatrix-like a and any
+// DenseMatrix-like basis (row-major rows() x cols())
+template <class Csr, class DM, class = decltype(std::declval<const Csr&>().row_ptr()),
+          class = decltype(std::declval<const DM&>().data())>
+TwoLevelPreconditioner build_preconditioner(const Csr& a, const DM& basis, double omega, std::size_t nu1,
+                                            std::size_t nu2) {
+    return TwoLevelPreconditioner(default_device(), device_matrix(a), basis, omega, nu1, nu2);
+}
+// (the basis already on the device, e.g. svd_basis's output)
+template <class Csr, class = decltype(std::declval<const Csr&>().row_ptr())>
+TwoLevelPreconditioner build_preconditioner(const Csr& a, const Dense& basis, double omega, std::size_t nu1,
+                                            std::size_t nu2) {
+    return TwoLevelPreconditioner(default_device(), device_matrix(a), basis, omega, nu1, nu2);
+}
+
+#ifdef NLSP_GPU_REFERENCE_TYPES
+// exact (non-template) overloads for the reference's own matrix type, so that an
+// unqualified pcg(a, b, M, ...) prefers them over the template nlsp::pcg<P>
+inline PcgResult pcg(const ::nlsp::SparseCsrMatrix& a, const std::vector<double>& b,
+                     const TwoLevelPreconditioner& m, double delta, std::size_t max_iters) {
+    return detail::run(default_device(), device_matrix(a), b, NLSP_PRECOND_TWOLEVEL, m.get(), delta, max_iters);
+}
+inline std::vector<double> apply_two_level(const TwoLevelPreconditioner& m, const ::nlsp::SparseCsrMatrix& a,
+                                           const std::vector<double>& rhs) {
+    return m.apply(device_matrix(a), rhs);
+}
+#else
+template <class Csr, class = decltype(std::declval<const Csr&>().row_ptr())>
+PcgResult pcg(const Csr& a, const std::vector<double>& b, const TwoLevelPreconditioner& m, double delta,
+              std::size_t max_iters) {
+    return detail::run(default_device(), device_matrix(a), b, NLSP_PRECOND_TWOLEVEL, m.get(), delta, max_iters);
+}
+template <class Csr, class = decltype(std::declval<const Csr&>().row_ptr())>
+std::vector<double> apply_two_level(const TwoLevelPreconditioner& m, const Csr& a, const std::vector<double>& rhs) {
+    return m.apply(device_matrix(a), rhs);
+}
+#endif
+template <class Csr, class = decltype(std::declval<const Csr&>().row_ptr())>
+PcgResult pcg(const Csr& a, const std::vector<double>& b, const IdentityPreconditioner&, double delta,
+              std::size_t max_iters) {
+    return detail::run(default_device(), device_matrix(a), b, NLSP_PRECOND_IDENTITY, nullptr, delta, max_iters);
+}
+template <class Csr, class = decltype(std::declval<const Csr&>().row_ptr())>
+PcgResult pcg(const Csr& a, const std::vector<double>& b, const JacobiPreconditioner&, double delta,
+              std::size_t max_iters) {
+    return detail::run(default_device(), device_matrix(a), b, NLSP_PRECOND_JACOBI, nullptr, delta, max_iters);
+}
+
+template <class Csr, class>
+std::vector<double> TwoLevelPreconditioner::apply(const Csr& a, const std::vector<double>& rhs) const {
+    return apply(device_matrix(a), rhs);
 }
 
 }  // namespace nlsp_gpu

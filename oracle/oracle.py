@@ -23,6 +23,21 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "build", "libnlsp_oracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libnlsp_ref.so")
 REF_STRICT_SO = os.path.join(HERE, "_ref", "libnlsp_ref_strict.so")
+REF_V4_SO = os.path.join(HERE, "_ref", "libnlsp_ref_v4.so")
+_V4_FLAGS = ("avx512f", "avx512bw", "avx512cd", "avx512dq", "avx512vl")
+
+
+def host_isa() -> str:
+    """x86-64-v4 when this host advertises AVX-512 F/BW/CD/DQ/VL, else v3."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("flags"):
+                    fl = set(line.split(":", 1)[1].split())
+                    return "x86-64-v4" if all(x in fl for x in _V4_FLAGS) else "x86-64-v3"
+    except OSError:
+        pass
+    return "x86-64-v3"
 
 u64, dbl, vp = C.c_uint64, C.c_double, C.c_void_p
 Pu64, Pdbl, Pu8, Pi32 = (C.POINTER(C.c_uint64), C.POINTER(C.c_double), C.POINTER(C.c_uint8),
@@ -297,8 +312,13 @@ def reference_available(strict: bool = False) -> bool:
 class Reference:
     """The reference's own code (oracle/_ref), default or -ffp-contract=off build."""
 
-    def __init__(self, strict: bool = False):
+    def __init__(self, strict: bool = False, native: bool = False):
+        """native: the build closest to the reference's -march=native on this
+        host (x86-64-v4 where AVX-512 is present) — the CPU baselines use it."""
         path = REF_STRICT_SO if strict else REF_SO
+        self.isa = "x86-64-v3"
+        if native and not strict and host_isa() == "x86-64-v4" and os.path.exists(REF_V4_SO):
+            path, self.isa = REF_V4_SO, "x86-64-v4"
         if not os.path.exists(path):
             raise RuntimeError(f"{path} missing: run `make -C {HERE} ref` where /root/reference exists")
         self.name = "ref_strict" if strict else "ref"

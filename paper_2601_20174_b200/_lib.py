@@ -126,6 +126,7 @@ GPU_SYMBOLS = [
     ("nlsp_twolevel_apply", C.c_int, [vp, vp, vp, P_dbl, P_dbl]),
     ("nlsp_pcg", C.c_int, [vp, vp, C.c_int, vp, P_dbl, c_dbl, c_u64, P_dbl, C.POINTER(SolveReportC), P_dbl]),
     ("nlsp_pcg_device", C.c_int, [vp, vp, C.c_int, vp, vp, c_dbl, c_u64, vp, C.POINTER(SolveReportC), P_dbl]),
+    ("nlsp_pcg_history", C.c_int, [vp, P_dbl, c_u64, C.POINTER(c_u64)]),
     ("nlsp_pcg_profile", C.c_int, [vp, vp, C.c_int, vp, vp, c_u64, C.POINTER(KernelStatC), C.c_int]),
 ]
 

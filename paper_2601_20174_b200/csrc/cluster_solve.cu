@@ -313,6 +313,7 @@ __device__ __forceinline__ void cluster_pcg_body(const ClusterArgs& a) {
     double beta = 0.0;
     long long it = 0;
     int converged = 0, err = 0;
+    double last_rel = 0.0;
     for (; it < max_it; ++it) {
         double* pc = pv[it & 1];
         double* pp = pv[(it + 1) & 1];
@@ -349,7 +350,8 @@ __device__ __forceinline__ void cluster_pcg_body(const ClusterArgs& a) {
             rr = fma(ri, ri, rr);
         }
         const double rel = sqrt(restrict_solve(rr)) / bnorm;
-        if (q == 0 && tid == 0) a.hist[it] = rel;
+        last_rel = rel;
+        if (q == 0 && tid == 0 && a.hist && it < a.hist_cap) a.hist[it] = rel;
         if (rel < delta) {
             converged = 1;
             ++it;
@@ -377,7 +379,7 @@ __device__ __forceinline__ void cluster_pcg_body(const ClusterArgs& a) {
         st->done = 1;
         st->bnorm = bnorm;
         st->true_res = err ? 0.0 : true_res;
-        st->last_rel = it > 0 ? a.hist[it - 1] : 0.0;
+        st->last_rel = last_rel;
         st->body_runs = it;
     }
     cl.sync();  // no CTA exits while others may still read its shared memory

@@ -38,6 +38,7 @@ enum DevError : int {
 struct PcgState {
     double rz, rz_new, pap, alpha, beta, rr, bnorm, delta, true_res, last_rel;
     long long it, max_it, iterations, body_runs;
+    long long hist_base;       // iteration of hist[0]: the history is kept in segments (nlsp_gpu.cu run_pcg)
     int done, converged, error, first;
     unsigned int counter[16];  // last-CTA tickets, one slot per kernel kind
     int op_grid;               // CTAs of the last one-pass prolongation (its partials' stride)
@@ -97,7 +98,7 @@ struct SolveArgs {
     double* zt0;
     double* zt1;
     const double* b;
-    double* hist;        // device residual history (max_it entries)
+    double* hist;        // device residual history segment: entry it - st->hist_base
     PcgState* st;
     double* partials;    // kMaxGrid * max(k, 4)
     double* e;           // coarse correction, k
@@ -127,7 +128,8 @@ struct ClusterArgs {
     const double* Ainv;  // A_c^-1 or null
     const double* b;
     double* x;           // out
-    double* hist;
+    double* hist;        // residual history (may be null: batched solves keep none)
+    long long hist_cap;  // entries hist holds; later iterations are not recorded
     PcgState* st;
 };
 

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
+#include <cmath>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -24,6 +26,7 @@ void launch_state_init(const LaunchCtx&, PcgState*, double, long long);
 void launch_bnorm(const LaunchCtx&, const SolveArgs&);
 void launch_init_simple(const LaunchCtx&, const SolveArgs&, int);
 void launch_init_ctl(const LaunchCtx&, PcgState*);
+void launch_state_continue(const LaunchCtx&, PcgState*, long long, long long);
 void launch_spmv_p(const LaunchCtx&, const SolveArgs&);
 void launch_update(const LaunchCtx&, const SolveArgs&, int);
 void launch_loop_ctl(const LaunchCtx&, PcgState*, cudaGraphConditionalHandle, int);
@@ -82,6 +85,11 @@ void launch_chol(const LaunchCtx&, int, const double*, double*, double, int*);
 void launch_coarse_inverse(const LaunchCtx&, int, const double*, double*);
 void launch_tri_inv_t(const LaunchCtx&, int, const double*, double*);
 void launch_symmetrize(const LaunchCtx&, int, double*);
+void launch_shift_diag(const LaunchCtx&, int, double*, double);
+void launch_coldot(const LaunchCtx&, long long, int, const double*, int, const double*, double*, double*);
+void launch_col_axpy(const LaunchCtx&, long long, int, const double*, int, double*, const double*);
+void launch_col_move(const LaunchCtx&, long long, int, double*, int, double*, const double*, int, long long);
+void launch_transpose(const LaunchCtx&, long long, int, const double*, double*);
 void launch_sigma(const LaunchCtx&, int, int, const double*, const double*, double*, double*,
                   int*);
 // setup_kernels.cu (SA)
@@ -176,6 +184,16 @@ struct nlsp_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
     cudaGraphExec_t gexec = nullptr;
     GraphKey gkey;
+    cudaGraphExec_t gexec_cont = nullptr;  // the loop without its prologue: later history segments
+    GraphKey gkey_cont;
+    // residual history of the last solve (SolveReport::residual_history): the
+    // device keeps one segment of ws_hist entries; completed segments are moved
+    // here, the last one stays on the device until nlsp_pcg_history asks
+    std::vector<double> hist_done;
+    unsigned long long hist_tail = 0;
+    bool last_qr_robust = false;  // the last qr_thin took the shifted CholeskyQR3 path
+    double last_svd_defect = 0.0;  // orthonormality defect of the last svd_basis' U_k before any polish
+    int last_svd_solid = 0;        // its columns above the singular-value cutoff
     bool use_graph = true;
     bool use_cluster = true;  // single-cluster solver for small systems
     cudaMemPool_t pool = nullptr;  // scratch of setup calls (salloc / sfree)
@@ -296,6 +314,22 @@ void free_ws(nlsp_ctx* c) {
     c->ws_hist = 0;
 }
 
+// Device residual-history segment: a solve longer than this runs in segments
+// (run_pcg), so the device never holds max_iters entries (10 n in the
+// reference's harness: 328 MB at C4). NLSP_HIST_CHUNK overrides (tests).
+long long hist_chunk() {
+    static const long long v = [] {
+        const char* e = std::getenv("NLSP_HIST_CHUNK");
+        const long long c = e ? std::atoll(e) : (1ll << 20);
+        return c < 1 ? 1ll : c;
+    }();
+    return v;
+}
+long long hist_segment(unsigned long long max_iters) {
+    const unsigned long long c = (unsigned long long)hist_chunk();
+    return (long long)(max_iters < c ? (max_iters ? max_iters : 1) : c);
+}
+
 // vectors for n rows, coarse vector and partials, history of hist entries
 nlsp_status ensure_ws(nlsp_ctx* ctx, long long n, long long hist) {
     if (n > ctx->ws_n) {
@@ -371,6 +405,8 @@ SolveArgs make_args(nlsp_ctx* c, const nlsp_csr* a, const nlsp_twolevel* m) {
     return s;
 }
 
+// NLSP_QR=robust forces the shifted CholeskyQR3 path of qr_thin_dev (tests)
+const bool g_force_sqr = std::getenv("NLSP_QR") && std::strcmp(std::getenv("NLSP_QR"), "robust") == 0;
 const bool g_pdl = !(std::getenv("NLSP_PDL") && std::strcmp(std::getenv("NLSP_PDL"), "0") == 0);
 const int g_unroll = [] {
     const char* u = std::getenv("NLSP_UNROLL");
@@ -416,17 +452,23 @@ void enqueue_prologue(const LaunchCtx& lc, const SolveArgs& a, int mode, const n
 
 int kind_mode(int kind) { return kind == NLSP_PRECOND_TWOLEVEL ? 0 : (kind == NLSP_PRECOND_JACOBI ? 2 : 1); }
 
-nlsp_status build_graph(nlsp_ctx* ctx, const SolveArgs& a, int mode, const nlsp_twolevel* m) {
-    if (ctx->gexec) {
-        cudaGraphExecDestroy(ctx->gexec);
-        ctx->gexec = nullptr;
+// The solve graph: prologue, WHILE(body), true residual. prologue = false: the
+// continuation graph of a later history segment (the loop resumes from the
+// device state).
+nlsp_status build_graph(nlsp_ctx* ctx, const SolveArgs& a, int mode, const nlsp_twolevel* m,
+                        bool prologue = true) {
+    cudaGraphExec_t& gx = prologue ? ctx->gexec : ctx->gexec_cont;
+    if (gx) {
+        cudaGraphExecDestroy(gx);
+        gx = nullptr;
     }
     cudaGraph_t g = nullptr;
     LaunchCtx lc = ctx->lc;
-    ctx->gk_pro = ctx->gk_body = ctx->gk_epi = 0;
-    lc.launches = &ctx->gk_pro;
+    unsigned long long scratch = 0;
+    if (prologue) ctx->gk_pro = ctx->gk_body = ctx->gk_epi = 0;
+    lc.launches = prologue ? &ctx->gk_pro : &scratch;
     CU(cudaStreamBeginCapture(ctx->s, cudaStreamCaptureModeThreadLocal));
-    enqueue_prologue(lc, a, mode, m, nullptr);
+    if (prologue) enqueue_prologue(lc, a, mode, m, nullptr);
     cudaStreamCaptureStatus cs;
     cudaGraph_t cg = nullptr;
     const cudaGraphNode_t* deps = nullptr;
@@ -453,14 +495,14 @@ nlsp_status build_graph(nlsp_ctx* ctx, const SolveArgs& a, int mode, const nlsp_
     if (e == cudaSuccess) {
         LaunchCtx lb = lc;
         lb.s = ctx->s_body;
-        lb.launches = &ctx->gk_body;
+        lb.launches = prologue ? &ctx->gk_body : &scratch;
         // NLSP_UNROLL iterations per WHILE body execution (kernels of an
         // iteration after convergence exit at once; each iteration's last
         // kernel still sets the condition)
         for (int u = 0; u < g_unroll; ++u) enqueue_iteration(lb, a, mode, m, h, 1);
         e = cudaStreamEndCapture(ctx->s_body, &body);
     }
-    lc.launches = &ctx->gk_epi;
+    lc.launches = prologue ? &ctx->gk_epi : &scratch;
     if (e == cudaSuccess) launch_true_res(lc, a);
     cudaError_t e2 = cudaStreamEndCapture(ctx->s, &g);
     if (e != cudaSuccess) {
@@ -468,23 +510,33 @@ nlsp_status build_graph(nlsp_ctx* ctx, const SolveArgs& a, int mode, const nlsp_
         return cuda_fail(ctx, e, "graph build");
     }
     if (e2 != cudaSuccess) return cuda_fail(ctx, e2, "graph capture");
-    e = cudaGraphInstantiate(&ctx->gexec, g, 0);
+    e = cudaGraphInstantiate(&gx, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "graph instantiate");
     return NLSP_OK;
 }
 
 // Runs the solve on ctx->b -> ctx->x. Caller has ensured the workspace.
+// The loop runs in history segments of ws_hist iterations (hist_chunk): the
+// device loop stops at the segment end, the host moves the segment's history
+// out and resumes the loop from the device state (a solve that converges
+// within the first segment — every BASELINE configuration — is one graph
+// launch).
 nlsp_status run_pcg(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twolevel* m,
-                    double delta, unsigned long long max_iters, nlsp_solve_report* rep,
-                    double* hist_host) {
+                    double delta, unsigned long long max_iters, nlsp_solve_report* rep) {
     const int mode = kind_mode(kind);
     const SolveArgs args = make_args(ctx, a, m);
-    launch_state_init(ctx->lc, ctx->st, delta, (long long)max_iters);
+    const unsigned long long H = (unsigned long long)ctx->ws_hist;
+    unsigned long long seg_end = std::min<unsigned long long>(max_iters, H);
+    ctx->hist_done.clear();
+    ctx->hist_tail = 0;
+    launch_state_init(ctx->lc, ctx->st, delta, (long long)seg_end);
     CHECK_LAUNCH();
     unsigned long long klaunch = 1;
     bool graph_ok = false;
-    // small systems: the whole solve in one launch of one thread-block cluster
+    // small systems: the whole solve in one launch of one thread-block cluster.
+    // It cannot pause at a segment end: a solve still running after H
+    // iterations (never at the BASELINE sizes) restarts on the multi-kernel path.
     bool cluster_ok = false;
     int c_rows = 0, c_ncta = 0;
     size_t c_smem = 0;
@@ -492,13 +544,26 @@ nlsp_status run_pcg(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twole
         c_ncta = cluster_plan(a->n, m->k, a->max_row, m->W2 != m->W1, &c_rows, &c_smem);
     if (c_ncta) {
         ClusterArgs ca{a->n, m->k, m->ld, c_rows, (int)m->nu1, (int)m->nu2, a->max_row, a->rp, a->ci, a->v,
-                       m->wd, m->W1, m->W2, m->L, args.Ainv, ctx->b, ctx->x, ctx->hist, ctx->st};
+                       m->wd, m->W1, m->W2, m->L, args.Ainv, ctx->b, ctx->x, ctx->hist, (long long)H,
+                       ctx->st};
         CU(cudaEventRecord(ctx->ev0, ctx->s));
         const cudaError_t ce = launch_cluster_pcg(ctx->s, ca, c_ncta, c_smem);
         if (ce == cudaSuccess) {
             cluster_ok = true;
             klaunch += 1;
-            ctx->launches += klaunch;
+            ctx->launches += 1;
+            if (max_iters > H) {
+                CU(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(PcgState), cudaMemcpyDeviceToHost, ctx->s));
+                CU(cudaStreamSynchronize(ctx->s));
+                const PcgState& cs = *ctx->st_host;
+                if (!cs.error && !cs.converged && (unsigned long long)cs.iterations == seg_end) {
+                    cluster_ok = false;
+                    launch_state_init(ctx->lc, ctx->st, delta, (long long)seg_end);
+                    CHECK_LAUNCH();
+                    klaunch += 1;
+                }
+            }
+            if (cluster_ok) ctx->launches += 1;  // the state init
         } else {
             cudaGetLastError();
             ctx->use_cluster = false;  // not schedulable here: multi-kernel path
@@ -516,40 +581,76 @@ nlsp_status run_pcg(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twole
             }
         }
     }
-    // solve_ms starts after the (cached) graph build
-    if (!cluster_ok) CU(cudaEventRecord(ctx->ev0, ctx->s));
-    if (!cluster_ok && ctx->use_graph) {
-        if (ctx->gexec) {
-            CU(cudaGraphLaunch(ctx->gexec, ctx->s));
-            graph_ok = true;
+    // one history segment on the multi-kernel path: the graph, or the
+    // stream-ordered loop in chunks of iterations (converged kernels exit early)
+    unsigned long long segments = 0;
+    auto run_segment = [&](bool first, unsigned long long seg_iters) -> nlsp_status {
+        ++segments;
+        if (graph_ok) {
+            if (!first) {
+                GraphKey key{a->id, m ? m->id : 0, kind, ctx->ws_gen};
+                if (!ctx->gexec_cont || !(ctx->gkey_cont == key)) {
+                    const nlsp_status bs = build_graph(ctx, args, mode, m, false);
+                    if (bs) return bs;
+                    ctx->gkey_cont = key;
+                }
+            }
+            CU(cudaGraphLaunch(first ? ctx->gexec : ctx->gexec_cont, ctx->s));
+            return NLSP_OK;
         }
-    }
-    if (!graph_ok && !cluster_ok) {
-        // stream-ordered loop: chunks of iterations, converged kernels exit early
-        enqueue_prologue(ctx->lc, args, mode, m, nullptr);
-        CHECK_LAUNCH();
+        if (first) {
+            enqueue_prologue(ctx->lc, args, mode, m, nullptr);
+            CHECK_LAUNCH();
+        }
         unsigned long long done_iters = 0;
         const unsigned long long chunk = 16;
         for (;;) {
-            for (unsigned long long i = 0; i < chunk && done_iters < max_iters; ++i, ++done_iters)
+            for (unsigned long long i = 0; i < chunk && done_iters < seg_iters; ++i, ++done_iters)
                 enqueue_iteration(ctx->lc, args, mode, m, cudaGraphConditionalHandle{}, 0);
             CHECK_LAUNCH();
             CU(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(PcgState), cudaMemcpyDeviceToHost, ctx->s));
             CU(cudaStreamSynchronize(ctx->s));
-            if (ctx->st_host->done || done_iters >= max_iters) break;
+            if (ctx->st_host->done || done_iters >= seg_iters) break;
         }
         launch_true_res(ctx->lc, args);
         CHECK_LAUNCH();
+        return NLSP_OK;
+    };
+    // solve_ms starts after the (cached) graph build
+    if (!cluster_ok) {
+        CU(cudaEventRecord(ctx->ev0, ctx->s));
+        graph_ok = ctx->use_graph && ctx->gexec;
+        const nlsp_status ss = run_segment(true, seg_end);
+        if (ss) return ss;
+    }
+    CU(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(PcgState), cudaMemcpyDeviceToHost, ctx->s));
+    CU(cudaStreamSynchronize(ctx->s));
+    while (!cluster_ok && !ctx->st_host->error && !ctx->st_host->converged &&
+           (unsigned long long)ctx->st_host->iterations == seg_end && seg_end < max_iters) {
+        // segment full: keep its history, resume the loop
+        const size_t old = ctx->hist_done.size();
+        const unsigned long long base = seg_end;
+        ctx->hist_done.resize(old + (size_t)(seg_end - (unsigned long long)ctx->st_host->hist_base));
+        CU(cudaMemcpyAsync(ctx->hist_done.data() + old, ctx->hist, sizeof(double) * (ctx->hist_done.size() - old),
+                           cudaMemcpyDeviceToHost, ctx->s));
+        seg_end = std::min<unsigned long long>(max_iters, base + H);
+        launch_state_continue(ctx->lc, ctx->st, (long long)seg_end, (long long)base);
+        CHECK_LAUNCH();
+        klaunch += 1;
+        const nlsp_status ss = run_segment(false, seg_end - base);
+        if (ss) return ss;
+        CU(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(PcgState), cudaMemcpyDeviceToHost, ctx->s));
+        CU(cudaStreamSynchronize(ctx->s));
     }
     CU(cudaEventRecord(ctx->ev1, ctx->s));
-    CU(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(PcgState), cudaMemcpyDeviceToHost, ctx->s));
     CU(cudaStreamSynchronize(ctx->s));
     const PcgState& st = *ctx->st_host;
     if (graph_ok) {
         // kernels counted while capturing each graph part; the WHILE body ran
         // st.body_runs times (k_loop_ctl counts itself)
         // (body_runs counts iterations, g_unroll of them per body execution)
-        klaunch += ctx->gk_pro + ctx->gk_body * (unsigned long long)st.body_runs / g_unroll + ctx->gk_epi;
+        klaunch += ctx->gk_pro + ctx->gk_body * (unsigned long long)st.body_runs / g_unroll +
+                   ctx->gk_epi * segments;
         ctx->launches += klaunch;
     }
     float ms = 0.f;
@@ -564,10 +665,19 @@ nlsp_status run_pcg(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twole
         rep->coarse_dim = m ? (unsigned long long)m->k : 0;
         rep->kernel_launches = klaunch;
     }
+    if ((unsigned long long)st.iterations > ctx->hist_done.size())
+        ctx->hist_tail = (unsigned long long)st.iterations - ctx->hist_done.size();
     if (st.error) return map_dev_error(ctx, st.error, "pcg");
-    if (hist_host && st.iterations > 0)
-        CU(cudaMemcpy(hist_host, ctx->hist, sizeof(double) * (size_t)st.iterations,
-                      cudaMemcpyDeviceToHost));
+    return NLSP_OK;
+}
+
+// Copies the last solve's history: completed segments from the host, the last
+// one from the device.
+nlsp_status copy_history(nlsp_ctx* ctx, double* out, unsigned long long cap) {
+    const unsigned long long nd = std::min<unsigned long long>(cap, ctx->hist_done.size());
+    if (nd) std::memcpy(out, ctx->hist_done.data(), sizeof(double) * nd);
+    const unsigned long long nt = std::min<unsigned long long>(cap - nd, ctx->hist_tail);
+    if (nt) CU(cudaMemcpy(out + nd, ctx->hist, sizeof(double) * nt, cudaMemcpyDeviceToHost));
     return NLSP_OK;
 }
 
@@ -578,8 +688,8 @@ nlsp_status check_pcg_args(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nls
         if (!m) return set_err(ctx, NLSP_E_VALIDATION, "pcg: two-level preconditioner is NULL");
         if (m->n != a->n) return set_err(ctx, NLSP_E_VALIDATION, "pcg: dimension mismatch");
     }
-    if (kind == NLSP_PRECOND_JACOBI && !a->diag_ok)
-        return set_err(ctx, NLSP_E_NUMERIC, "jacobi preconditioner: non-positive diagonal");
+    // a non-positive diagonal under the Jacobi preconditioner fails on the device
+    // (k_init_simple), after the zero-rhs check, in the reference's order
     return NLSP_OK;
 }
 
@@ -1076,11 +1186,14 @@ nlsp_status nlsp_svd_basis(nlsp_ctx* ctx, const nlsp_dense* s, uint64_t k, nlsp_
     if (st) return st;
     if (!s) return set_err(ctx, NLSP_E_VALIDATION, "svd_basis: null matrix");
     const long long n = (long long)s->rows;
-    const int m = (int)s->cols;
+    const int m = (int)std::min<unsigned long long>(s->cols, 1u << 30);
     if (m == 0 || n == 0) return set_err(ctx, NLSP_E_VALIDATION, "svd_oracle: empty matrix");
-    if ((long long)m > n) return set_err(ctx, NLSP_E_VALIDATION, "svd_basis: requires rows >= cols");
-    if (k > (uint64_t)m) return set_err(ctx, NLSP_E_VALIDATION, "first_cols: k exceeds column count");
-    if (m > 1024) return set_err(ctx, NLSP_E_VALIDATION, "svd_basis: at most 1024 columns");
+    // svd.hpp:161-165: the eigensolve runs on the Gram of the smaller dimension
+    // (S^T S for a tall S, S S^T for a wide one), gdim = r = min(n, m)
+    const bool wide = (long long)m > n;
+    const int gdim = wide ? (int)n : m;
+    if (gdim > 1024) return set_err(ctx, NLSP_E_VALIDATION, "svd_basis: min(rows, cols) at most 1024");
+    if (k > (uint64_t)gdim) return set_err(ctx, NLSP_E_VALIDATION, "first_cols: k exceeds column count");
     if (k > 256) return set_err(ctx, NLSP_E_VALIDATION, "svd_basis: at most 256 basis columns");
     if (k == 0) {
         nlsp_dense* d = nullptr;
@@ -1088,32 +1201,45 @@ nlsp_status nlsp_svd_basis(nlsp_ctx* ctx, const nlsp_dense* s, uint64_t k, nlsp_
         if (!st) *p_out = d;
         return st;
     }
-    const int g = gram_grid(ctx->lc, n);
+    const long long grow = wide ? (long long)m : n;  // rows the Gram streams
+    const int g = gram_grid(ctx->lc, grow);
     double *part = nullptr, *G = nullptr, *ev = nullptr, *V = nullptr, *sa = nullptr, *sv = nullptr,
-           *sig = nullptr, *W = nullptr, *pmag = nullptr, *pval = nullptr, *sign = nullptr;
+           *sig = nullptr, *W = nullptr, *pmag = nullptr, *pval = nullptr, *sign = nullptr, *T = nullptr,
+           *vcol = nullptr, *cpart = nullptr, *cval = nullptr, *Gk = nullptr;
     long long* pidx = nullptr;
     nlsp_dense* P = nullptr;
-    nlsp_status ret = NLSP_OK;
     auto cleanup = [&]() {
-        for (double* p : {part, G, ev, V, sa, sv, sig, W, pmag, pval, sign}) sfree(ctx, p);
+        for (double* p : {part, G, ev, V, sa, sv, sig, W, pmag, pval, sign, T, vcol, cpart, cval, Gk}) sfree(ctx, p);
         sfree(ctx, pidx);
     };
+    auto fail = [&](nlsp_status code, const std::string& msg) {
+        cleanup();
+        if (P) nlsp_dense_destroy(P);
+        return set_err(ctx, code, msg);
+    };
     cudaError_t e;
-    const size_t mm = (size_t)m * m;
-    if ((e = salloc(ctx, &part, (size_t)g * gram_tile(m, m))) || (e = salloc(ctx, &G, mm)) || (e = salloc(ctx, &ev, m)) ||
-        (e = salloc(ctx, &V, mm)) || (e = salloc(ctx, &sa, mm)) || (e = salloc(ctx, &sv, mm)) ||
-        (e = salloc(ctx, &sig, m)) || (e = salloc(ctx, &W, (size_t)m * k)) ||
+    const size_t gg = (size_t)gdim * gdim;
+    if ((e = salloc(ctx, &part, (size_t)g * gram_tile(gdim, gdim))) || (e = salloc(ctx, &G, gg)) ||
+        (e = salloc(ctx, &ev, gdim)) || (e = salloc(ctx, &V, gg)) || (e = salloc(ctx, &sa, gg)) ||
+        (e = salloc(ctx, &sv, gg)) || (e = salloc(ctx, &sig, gdim)) || (e = salloc(ctx, &W, (size_t)gdim * k)) ||
         (e = salloc(ctx, &pmag, (size_t)ctx->num_sms * kColsignPerSm * k)) ||
         (e = salloc(ctx, &pval, (size_t)ctx->num_sms * kColsignPerSm * k)) ||
-        (e = salloc(ctx, &pidx, (size_t)ctx->num_sms * kColsignPerSm * k)) || (e = salloc(ctx, &sign, k))) {
+        (e = salloc(ctx, &pidx, (size_t)ctx->num_sms * kColsignPerSm * k)) || (e = salloc(ctx, &sign, k)) ||
+        (wide && (e = salloc(ctx, &T, (size_t)n * m)))) {
         cleanup();
         return cuda_fail(ctx, e, "svd_basis alloc");
     }
     CU(cudaMemsetAsync(ctx->flags, 0, 16 * sizeof(int), ctx->s));
-    // Gram S^T S (svd.hpp:162-166), eigensolve (:167), sigma + W = V_k (:174-183)
-    launch_gram(ctx->lc, n, m, m, s->d, s->d, part, G);
-    launch_eigh(ctx->lc, m, G, ev, V, sa, sv, ctx->flags + 4, ctx->flags + 5);
-    launch_sigma(ctx->lc, m, (int)k, ev, V, sig, W, ctx->flags + 6);
+    // Gram (svd.hpp:161-166), eigensolve (:167), sigma with the rounding floor
+    // and the first k eigenvectors W (:174-183)
+    if (wide) {
+        launch_transpose(ctx->lc, n, m, s->d, T);
+        launch_gram(ctx->lc, m, gdim, gdim, T, T, part, G);
+    } else {
+        launch_gram(ctx->lc, n, m, m, s->d, s->d, part, G);
+    }
+    launch_eigh(ctx->lc, gdim, G, ev, V, sa, sv, ctx->flags + 4, ctx->flags + 5);
+    launch_sigma(ctx->lc, gdim, (int)k, ev, V, sig, W, ctx->flags + 6);
     e = cudaGetLastError();
     if (!e) e = cudaMemcpyAsync(ctx->flags_host, ctx->flags, 16 * sizeof(int), cudaMemcpyDeviceToHost, ctx->s);
     if (!e) e = cudaStreamSynchronize(ctx->s);
@@ -1122,27 +1248,83 @@ nlsp_status nlsp_svd_basis(nlsp_ctx* ctx, const nlsp_dense* s, uint64_t k, nlsp_
         return cuda_fail(ctx, e, "svd_basis");
     }
     if (eigh_sweeps) *eigh_sweeps = ctx->flags_host[5];
-    if (ctx->flags_host[4] == kErrValidation) {
+    if (ctx->flags_host[4] == kErrValidation) return fail(NLSP_E_VALIDATION, "svd_oracle: non-finite entries");
+    if (ctx->flags_host[4]) return fail(NLSP_E_CONVERGENCE, "jacobi_eigh: no convergence after 30 sweeps");
+    if (sigma) CU(cudaMemcpy(sigma, sig, sizeof(double) * gdim, cudaMemcpyDeviceToHost));
+    const int solid = ctx->flags_host[6];
+    st = dense_alloc(ctx, n, k, &P);
+    if (st) {
         cleanup();
-        return set_err(ctx, NLSP_E_VALIDATION, "svd_oracle: non-finite entries");
+        return st;
     }
-    if (ctx->flags_host[4]) {
-        cleanup();
-        return set_err(ctx, NLSP_E_CONVERGENCE, "jacobi_eigh: no convergence after 30 sweeps");
+    if (wide) {
+        // U = the eigenvectors of S S^T themselves (svd.hpp:186, 205)
+        CU(cudaMemcpyAsync(P->d, W, sizeof(double) * (size_t)n * k, cudaMemcpyDeviceToDevice, ctx->s));
+    } else {
+        // U_j = S V_j / sigma_j for the solid columns (svd.hpp:189-202; the
+        // columns past `solid` are overwritten by the completion below)
+        launch_dense_mm(ctx->lc, n, m, (int)k, s->d, W, sig, P->d);
+        const int gd = std::max(1, std::min(ctx->num_sms * 2, (int)((n + 255) / 256)));
+        if ((e = salloc(ctx, &vcol, (size_t)n)) || (e = salloc(ctx, &cpart, (size_t)gd + 64)) ||
+            (e = salloc(ctx, &cval, 2)) || (e = salloc(ctx, &Gk, (size_t)k * k))) {
+            cleanup();
+            nlsp_dense_destroy(P);
+            return cuda_fail(ctx, e, "svd_basis alloc");
+        }
+        const int kk = (int)k;
+        // complete_orthonormal (svd.hpp:101-126): column j from the coordinate
+        // vector e_cand with the largest residual > 0.5, candidates in order
+        for (int j = solid; j < kk; ++j) {
+            bool placed = false;
+            for (long long cand = 0; cand < n && !placed; ++cand) {
+                launch_col_move(ctx->lc, n, kk, P->d, -1, vcol, nullptr, 0, cand);
+                for (int pass = 0; pass < 2; ++pass)
+                    for (int p = 0; p < j; ++p) {
+                        launch_coldot(ctx->lc, n, kk, P->d, p, vcol, cpart, cval);
+                        launch_col_axpy(ctx->lc, n, kk, P->d, p, vcol, cval);
+                    }
+                launch_coldot(ctx->lc, n, kk, P->d, -1, vcol, cpart, cval + 1);
+                double nrm = 0.0;
+                CU(cudaMemcpyAsync(&nrm, cval + 1, sizeof(double), cudaMemcpyDeviceToHost, ctx->s));
+                CU(cudaStreamSynchronize(ctx->s));
+                if (nrm > 0.5) {
+                    launch_col_move(ctx->lc, n, kk, P->d, j, vcol, cval + 1, 1, 0);
+                    placed = true;
+                }
+            }
+            if (!placed) return fail(NLSP_E_NUMERIC, "complete_orthonormal: no candidate found");
+        }
+        // orthonormality_defect (dense.hpp:175-182) of the k columns; past 1e-11
+        // the Gram-Schmidt polish (svd.hpp:128-145). (The reference measures
+        // the defect over all min(n, m) columns; a polish triggered only by
+        // the later columns moves the first k by less than their own defect,
+        // < 1e-11.)
+        launch_gram(ctx->lc, n, kk, kk, P->d, P->d, part, Gk);
+        std::vector<double> gk((size_t)k * k);
+        CU(cudaMemcpyAsync(gk.data(), Gk, sizeof(double) * gk.size(), cudaMemcpyDeviceToHost, ctx->s));
+        CU(cudaStreamSynchronize(ctx->s));
+        double defect = 0.0;
+        for (int i = 0; i < kk; ++i)
+            for (int j = 0; j < kk; ++j) defect = std::max(defect, std::fabs(gk[(size_t)i * k + j] - (i == j ? 1.0 : 0.0)));
+        ctx->last_svd_defect = defect;
+        ctx->last_svd_solid = solid;
+        if (defect > 1e-11) {
+            for (int j = 0; j < kk; ++j) {
+                launch_col_move(ctx->lc, n, kk, P->d, j, vcol, nullptr, 0, 0);
+                for (int p = 0; p < j; ++p) {
+                    launch_coldot(ctx->lc, n, kk, P->d, p, vcol, cpart, cval);
+                    launch_col_axpy(ctx->lc, n, kk, P->d, p, vcol, cval);
+                }
+                launch_coldot(ctx->lc, n, kk, P->d, -1, vcol, cpart, cval + 1);
+                double nrm = 0.0;
+                CU(cudaMemcpyAsync(&nrm, cval + 1, sizeof(double), cudaMemcpyDeviceToHost, ctx->s));
+                CU(cudaStreamSynchronize(ctx->s));
+                if (nrm == 0.0) return fail(NLSP_E_NUMERIC, "reorthonormalize: zero column");
+                launch_col_move(ctx->lc, n, kk, P->d, j, vcol, cval + 1, 1, 0);
+            }
+        }
     }
-    if (sigma) cudaMemcpy(sigma, sig, sizeof(double) * m, cudaMemcpyDeviceToHost);
-    if (ctx->flags_host[6]) {
-        cleanup();
-        return set_err(ctx, NLSP_E_NUMERIC,
-                       "svd_basis: S has numerical rank below k (sigma_j <= 1e-13 sigma_max)");
-    }
-    ret = dense_alloc(ctx, n, k, &P);
-    if (ret) {
-        cleanup();
-        return ret;
-    }
-    // U_k = S V_k / sigma_k (svd.hpp:189-202), sign convention (:209-225)
-    launch_dense_mm(ctx->lc, n, m, (int)k, s->d, W, sig, P->d);
+    // sign convention (svd.hpp:209-225)
     launch_colsign(ctx->lc, n, (int)k, P->d, pmag, pidx, pval, sign);
     e = cudaGetLastError();
     if (!e) e = cudaStreamSynchronize(ctx->s);
@@ -1152,6 +1334,83 @@ nlsp_status nlsp_svd_basis(nlsp_ctx* ctx, const nlsp_dense* s, uint64_t k, nlsp_
         return cuda_fail(ctx, e, "svd_basis products");
     }
     *p_out = P;
+    return NLSP_OK;
+}
+
+// qr_thin (qr.hpp:18-45) on the device: Q (n x k, orthonormal, R with a
+// positive diagonal, so the same Q as the reference's two-pass MGS up to
+// rounding) from the basis B.
+//
+// CholeskyQR2 (R1 = chol(B^T B), Q1 = B R1^-1; R2 = chol(Q1^T Q1), Q = Q1 R2^-1)
+// when B is well conditioned: every first-pass pivot L_jj (= MGS's
+// post-elimination norm of column j, up to the Gram's rounding of
+// eps ||B||_F^2) is at least 1e-6 ||B||_F, so the reference's rank test
+// (nrm < 1e-12 ||B||_F) cannot trigger and Q is orthonormal to rounding.
+// Otherwise the Gram has lost the small pivots to rounding (they square the
+// condition number), and shifted CholeskyQR3 takes over: R1 = chol(B^T B + s I)
+// with s = 11 (n k + k (k + 1)) u ||B||_F^2, then CholeskyQR2 on B R1^-1 —
+// orthonormal for cond(B) up to ~1/u. Its rank test is the reference's own on
+// the diagonal of R = Q^T B (the post-elimination norms, resolved to
+// ~u ||B||_F): R_jj < 1e-12 ||B||_F -> RankDeficiencyError; a second-stage
+// Cholesky breakdown means B is numerically rank-deficient too.
+// Scratch: Q1, Y (n x k), part, G, U (k x k); L (k x k + 8) ends as garbage.
+static nlsp_status qr_thin_dev(nlsp_ctx* ctx, long long n, int k, const double* B, double* Q, double* Q1, double* Y,
+                        double* part, double* G, double* U, double* L) {
+    const LaunchCtx& lc = ctx->lc;
+    CU(cudaMemsetAsync(ctx->flags + 8, 0, 3 * sizeof(int), ctx->s));
+    launch_gram(lc, n, k, k, B, B, part, G);
+    launch_chol(lc, k, G, L, 0.0, ctx->flags + 8);
+    std::vector<double> gd(k), ld(k);
+    CU(cudaMemcpy2DAsync(gd.data(), 8, G, (size_t)(k + 1) * 8, 8, k, cudaMemcpyDeviceToHost, ctx->s));
+    CU(cudaMemcpy2DAsync(ld.data(), 8, L, (size_t)(k + 1) * 8, 8, k, cudaMemcpyDeviceToHost, ctx->s));
+    CU(cudaMemcpyAsync(ctx->flags_host + 8, ctx->flags + 8, sizeof(int), cudaMemcpyDeviceToHost, ctx->s));
+    CU(cudaStreamSynchronize(ctx->s));
+    double fro2 = 0.0, lmin = HUGE_VAL;
+    for (int j = 0; j < k; ++j) {
+        fro2 += gd[j];
+        lmin = std::min(lmin, ld[j]);
+    }
+    const double fro = std::sqrt(std::max(fro2, 0.0));
+    if (!(fro > 0.0)) return set_err(ctx, NLSP_E_RANK_DEFICIENT, "qr_thin: rank-deficient at column 0");
+    const bool fast = ctx->flags_host[8] == 0 && lmin >= 1e-6 * fro && !g_force_sqr;
+    if (fast) {
+        launch_tri_inv_t(lc, k, L, U);
+        launch_dense_mm(lc, n, k, k, B, U, nullptr, Q1);
+        launch_gram(lc, n, k, k, Q1, Q1, part, G);
+        launch_chol(lc, k, G, L, 0.0, ctx->flags + 9);
+        launch_tri_inv_t(lc, k, L, U);
+        launch_dense_mm(lc, n, k, k, Q1, U, nullptr, Q);
+        ctx->last_qr_robust = false;
+        return NLSP_OK;
+    }
+    // shifted CholeskyQR3
+    const double u = std::ldexp(1.0, -53);
+    const double shift = 11.0 * ((double)n * k + (double)k * (k + 1)) * u * fro2;
+    launch_gram(lc, n, k, k, B, B, part, G);
+    launch_shift_diag(lc, k, G, shift);
+    launch_chol(lc, k, G, L, 0.0, ctx->flags + 9);
+    launch_tri_inv_t(lc, k, L, U);
+    launch_dense_mm(lc, n, k, k, B, U, nullptr, Q1);
+    launch_gram(lc, n, k, k, Q1, Q1, part, G);
+    launch_chol(lc, k, G, L, 0.0, ctx->flags + 10);
+    launch_tri_inv_t(lc, k, L, U);
+    launch_dense_mm(lc, n, k, k, Q1, U, nullptr, Y);
+    launch_gram(lc, n, k, k, Y, Y, part, G);
+    launch_chol(lc, k, G, L, 0.0, ctx->flags + 10);
+    launch_tri_inv_t(lc, k, L, U);
+    launch_dense_mm(lc, n, k, k, Y, U, nullptr, Q);
+    // R = Q^T B: its diagonal holds the post-elimination norms
+    launch_gram(lc, n, k, k, Q, B, part, G);
+    CU(cudaGetLastError());
+    CU(cudaMemcpy2DAsync(gd.data(), 8, G, (size_t)(k + 1) * 8, 8, k, cudaMemcpyDeviceToHost, ctx->s));
+    CU(cudaMemcpyAsync(ctx->flags_host + 9, ctx->flags + 9, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->s));
+    CU(cudaStreamSynchronize(ctx->s));
+    ctx->last_qr_robust = true;
+    for (int j = 0; j < k; ++j)
+        if (!(gd[j] >= 1e-12 * fro))
+            return set_err(ctx, NLSP_E_RANK_DEFICIENT, "qr_thin: rank-deficient at column " + std::to_string(j));
+    if (ctx->flags_host[9] || ctx->flags_host[10])
+        return set_err(ctx, NLSP_E_RANK_DEFICIENT, "qr_thin: rank-deficient basis");
     return NLSP_OK;
 }
 
@@ -1211,16 +1470,16 @@ nlsp_status nlsp_twolevel_build(nlsp_ctx* ctx, const nlsp_csr* a, const nlsp_den
         return fail_cuda(e, "two-level alloc");
     if ((e = cudaMemsetAsync(ctx->flags, 0, 16 * sizeof(int), ctx->s))) return fail_cuda(e, "memset");
     launch_wd(ctx->lc, (int)n, a->diag, omega, m->wd, ctx->flags + 7);
-    // qr_thin (qr.hpp:18-45) as CholeskyQR2: R1 = chol(B^T B) with the rank
-    // test, Q1 = B R1^-1; R2 = chol(Q1^T Q1), Q = Q1 R2^-1.
-    launch_gram(ctx->lc, n, k, k, basis->d, basis->d, part, G);
-    launch_chol(ctx->lc, k, G, m->L, 1e-12, ctx->flags + 8);
-    launch_tri_inv_t(ctx->lc, k, m->L, U);
-    launch_dense_mm(ctx->lc, n, k, k, basis->d, U, nullptr, Q1);
-    launch_gram(ctx->lc, n, k, k, Q1, Q1, part, G);
-    launch_chol(ctx->lc, k, G, m->L, 0.0, ctx->flags + 9);
-    launch_tri_inv_t(ctx->lc, k, m->L, U);
-    launch_dense_mm(ctx->lc, n, k, k, Q1, U, nullptr, Q);
+    {
+        // qr_thin (qr.hpp:18-45): CholeskyQR2, or shifted CholeskyQR3 for an
+        // ill-conditioned basis (qr_thin_dev)
+        const nlsp_status qs = qr_thin_dev(ctx, n, k, basis->d, Q, Q1, Y, part, G, U, m->L);
+        if (qs) {
+            cleanup();
+            nlsp_twolevel_destroy(m);
+            return qs;
+        }
+    }
     // Galerkin A_c = Q^T (A Q), exact symmetrisation, Cholesky (two_level.hpp:33-52)
     if (!launch_block_op_dia(ctx->lc, 1, (int)n, a->dia, nullptr, k, Q, Y))
         launch_block_op(ctx->lc, 1, (int)n, a->rp, a->ci, a->v, nullptr, k, Q, Y);
@@ -1280,7 +1539,7 @@ nlsp_status nlsp_twolevel_build(nlsp_ctx* ctx, const nlsp_csr* a, const nlsp_den
         nlsp_twolevel_destroy(m);
         return set_err(ctx, NLSP_E_NUMERIC, "jacobi: non-positive diagonal");
     }
-    if (f[8] || f[9]) {
+    if (f[9]) {  // CholeskyQR2's second pass
         nlsp_twolevel_destroy(m);
         return set_err(ctx, NLSP_E_RANK_DEFICIENT, "qr_thin: rank-deficient basis");
     }
@@ -1354,7 +1613,7 @@ nlsp_status nlsp_pcg(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
     st = check_pcg_args(ctx, a, kind, m);
     if (st) return st;
     if (!b || !x) return set_err(ctx, NLSP_E_VALIDATION, "pcg: null vector");
-    st = ensure_ws(ctx, a->n, (long long)max_iters);
+    st = ensure_ws(ctx, a->n, hist_segment(max_iters));
     if (st) return st;
     const size_t bytes = (size_t)a->n * 8;
     CU(cudaEventRecord(ctx->ev2, ctx->s));
@@ -1362,8 +1621,12 @@ nlsp_status nlsp_pcg(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
     nlsp_solve_report local{};
     nlsp_solve_report* r = rep ? rep : &local;
     std::memset(r, 0, sizeof(*r));
-    st = run_pcg(ctx, a, kind, m, delta, max_iters, r, residual_history);
+    st = run_pcg(ctx, a, kind, m, delta, max_iters, r);
     if (st) return st;
+    if (residual_history) {
+        st = copy_history(ctx, residual_history, r->iterations);
+        if (st) return st;
+    }
     CU(cudaMemcpyAsync(x, ctx->x, bytes, cudaMemcpyDeviceToHost, ctx->s));
     CU(cudaEventRecord(ctx->ev3, ctx->s));
     CU(cudaStreamSynchronize(ctx->s));
@@ -1383,7 +1646,7 @@ nlsp_status nlsp_pcg_device(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nl
     st = check_pcg_args(ctx, a, kind, m);
     if (st) return st;
     if (!b_dev || !x_dev) return set_err(ctx, NLSP_E_VALIDATION, "pcg: null vector");
-    st = ensure_ws(ctx, a->n, (long long)max_iters);
+    st = ensure_ws(ctx, a->n, hist_segment(max_iters));
     if (st) return st;
     const size_t bytes = (size_t)a->n * 8;
     CU(cudaEventRecord(ctx->ev2, ctx->s));
@@ -1391,8 +1654,12 @@ nlsp_status nlsp_pcg_device(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nl
     nlsp_solve_report local{};
     nlsp_solve_report* r = rep ? rep : &local;
     std::memset(r, 0, sizeof(*r));
-    st = run_pcg(ctx, a, kind, m, delta, max_iters, r, residual_history);
+    st = run_pcg(ctx, a, kind, m, delta, max_iters, r);
     if (st) return st;
+    if (residual_history) {
+        st = copy_history(ctx, residual_history, r->iterations);
+        if (st) return st;
+    }
     CU(cudaMemcpyAsync(x_dev, ctx->x, bytes, cudaMemcpyDeviceToDevice, ctx->s));
     CU(cudaEventRecord(ctx->ev3, ctx->s));
     CU(cudaStreamSynchronize(ctx->s));
@@ -1402,6 +1669,15 @@ nlsp_status nlsp_pcg_device(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nl
     r->h2d_bytes = 0;
     r->d2h_bytes = sizeof(PcgState) + (residual_history ? r->iterations * 8 : 0);
     return NLSP_OK;
+}
+
+nlsp_status nlsp_pcg_history(nlsp_ctx* ctx, double* out, uint64_t cap, uint64_t* count) {
+    nlsp_status st = bind(ctx);
+    if (st) return st;
+    const unsigned long long total = ctx->hist_done.size() + ctx->hist_tail;
+    if (count) *count = total;
+    if (!out || !cap) return NLSP_OK;
+    return copy_history(ctx, out, std::min<unsigned long long>(cap, total));
 }
 
 // ---------------------------------------------------------------- profiling --
@@ -1888,7 +2164,6 @@ nlsp_status nlsp_pcg_batch(nlsp_ctx* ctx, uint64_t count, const nlsp_csr* const*
     if (st) return st;
     if (count == 0) return NLSP_OK;
     if (!a || !m || !b || !x) return set_err(ctx, NLSP_E_VALIDATION, "pcg_batch: null array");
-    if (max_iters > (1ull << 26)) return set_err(ctx, NLSP_E_VALIDATION, "pcg_batch: max_iters too large");
     std::vector<int> in_batch, ns, ks, ws, rows;
     std::vector<char> tw;
     for (uint64_t i = 0; i < count; ++i) {
@@ -1921,27 +2196,32 @@ nlsp_status nlsp_pcg_batch(nlsp_ctx* ctx, uint64_t count, const nlsp_csr* const*
         for (int j = 0; j < cnt; ++j) twa[j] = twb[j];
         const int ncta = cluster_plan_batch(cnt, ns.data(), ks.data(), ws.data(), twa.get(), rows.data(), &smem);
         if (!ncta) return set_err(ctx, NLSP_E_VALIDATION, "pcg_batch: systems do not fit one cluster size");
-        // per-system state, history, b, x in one pool allocation each
+        // per-system state, b, x in one pool allocation each (no residual
+        // history: the batch reports iterations and the last residual only)
         std::vector<size_t> voff(cnt + 1, 0);
         for (int j = 0; j < cnt; ++j) voff[j + 1] = voff[j] + (size_t)ns[j] + 16;
-        PcgState* dst = nullptr;
-        double *dhist = nullptr, *db = nullptr, *dx = nullptr;
-        ClusterArgs* dargs = nullptr;
-        const size_t hcap = std::max<uint64_t>(max_iters, 1);
-        auto cleanup = [&]() {
-            sfree(ctx, dst);
-            sfree(ctx, dhist);
-            sfree(ctx, db);
-            sfree(ctx, dx);
-            sfree(ctx, dargs);
-        };
+        struct Scratch {
+            nlsp_ctx* c;
+            PcgState* dst = nullptr;
+            double *db = nullptr, *dx = nullptr;
+            ClusterArgs* dargs = nullptr;
+            ~Scratch() {  // every return path gives the pool blocks back
+                sfree(c, dst);
+                sfree(c, db);
+                sfree(c, dx);
+                sfree(c, dargs);
+            }
+        } sc{ctx};
+        PcgState*& dst = sc.dst;
+        double*& db = sc.db;
+        double*& dx = sc.dx;
+        ClusterArgs*& dargs = sc.dargs;
         cudaError_t e;
-        if ((e = salloc(ctx, &dst, cnt)) || (e = salloc(ctx, &dhist, (size_t)cnt * hcap)) ||
-            (e = salloc(ctx, &db, voff[cnt])) || (e = salloc(ctx, &dx, voff[cnt])) ||
-            (e = salloc(ctx, &dargs, cnt))) {
-            cleanup();
+        if ((e = salloc(ctx, &dst, cnt)) || (e = salloc(ctx, &db, voff[cnt])) || (e = salloc(ctx, &dx, voff[cnt])) ||
+            (e = salloc(ctx, &dargs, cnt)))
             return cuda_fail(ctx, e, "pcg_batch alloc");
-        }
+        // a system that fails before its loop (zero rhs) leaves x = 0, not pool garbage
+        CU(cudaMemsetAsync(dx, 0, sizeof(double) * voff[cnt], ctx->s));
         std::vector<ClusterArgs> args(cnt);
         CU(cudaEventRecord(ctx->ev2, ctx->s));
         for (int j = 0; j < cnt; ++j) {
@@ -1949,19 +2229,17 @@ nlsp_status nlsp_pcg_batch(nlsp_ctx* ctx, uint64_t count, const nlsp_csr* const*
             const nlsp_csr* A = a[i];
             const nlsp_twolevel* M = m[i];
             CU(cudaMemcpyAsync(db + voff[j], b[i], (size_t)A->n * 8, cudaMemcpyHostToDevice, ctx->s));
-            launch_state_init(ctx->lc, dst + j, delta, (long long)max_iters);
+            launch_state_init(ctx->lc, dst + j, delta,
+                              (long long)std::min<uint64_t>(max_iters, (uint64_t)LLONG_MAX));
             const SolveArgs sa = make_args(ctx, A, M);
             args[j] = ClusterArgs{A->n, M->k, M->ld, rows[j], (int)M->nu1, (int)M->nu2, A->max_row, A->rp, A->ci, A->v,
                                   M->wd, M->W1, M->W2, M->L, sa.Ainv, db + voff[j], dx + voff[j],
-                                  dhist + (size_t)j * hcap, dst + j};
+                                  nullptr, 0, dst + j};
         }
         CU(cudaMemcpyAsync(dargs, args.data(), sizeof(ClusterArgs) * cnt, cudaMemcpyHostToDevice, ctx->s));
         CU(cudaEventRecord(ctx->ev0, ctx->s));
         e = launch_cluster_pcg_batch(ctx->s, dargs, cnt, ncta, smem);
-        if (e) {
-            cleanup();
-            return cuda_fail(ctx, e, "pcg_batch launch");
-        }
+        if (e) return cuda_fail(ctx, e, "pcg_batch launch");
         ctx->launches += 1 + cnt;
         CU(cudaEventRecord(ctx->ev1, ctx->s));
         std::vector<PcgState> hs(cnt);
@@ -1993,8 +2271,6 @@ nlsp_status nlsp_pcg_batch(nlsp_ctx* ctx, uint64_t count, const nlsp_csr* const*
             }
             record(i, p.error == kErrNotSpd ? NLSP_E_NOT_SPD : (p.error ? NLSP_E_VALIDATION : NLSP_OK));
         }
-        cleanup();
-        CU(cudaStreamSynchronize(ctx->s));
     }
     // the rest one by one on the general path
     for (uint64_t i = 0; i < count; ++i) {

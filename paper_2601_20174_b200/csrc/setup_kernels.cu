@@ -820,6 +820,67 @@ __global__ void k_symmetrize(int k, double* C) {
     }
 }
 
+// G += shift I (shifted CholeskyQR, nlsp_gpu.cu qr_thin_dev)
+__global__ void k_shift_diag(int k, double* G, double shift) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x)
+        G[(long long)i * k + i] += shift;
+}
+
+// ---- column Gram-Schmidt on a row-major n x ld basis (svd.hpp:101-145) ----
+// svd_oracle's rare branches: completing a numerically rank-deficient U
+// (complete_orthonormal) and the polish when U^T U drifts past 1e-11
+// (reorthonormalize_columns). One column at a time, as the reference does;
+// every dot product is a fixed-order two-stage sum (deterministic).
+// v is a separate n-vector; col < 0 selects v as the left operand.
+__global__ void __launch_bounds__(256) k_coldot_partial(long long n, int ld, const double* __restrict__ U, int col,
+                                                        const double* __restrict__ v, double* part) {
+    __shared__ double red[256];
+    double s = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double a = col >= 0 ? U[i * ld + col] : v[i];
+        s = fma(a, v[i], s);
+    }
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+// out[0] = sum of the partials; sqrt_out: out[0] = sqrt(sum)
+__global__ void k_coldot_final(int nparts, const double* part, double* out, int sqrt_out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double s = 0.0;
+        for (int p = 0; p < nparts; ++p) s += part[p];
+        out[0] = sqrt_out ? sqrt(s) : s;
+    }
+}
+// v -= c u_col  (c read on the device: no host round trip per projection)
+__global__ void k_col_axpy(long long n, int ld, const double* __restrict__ U, int col, double* v,
+                           const double* __restrict__ c) {
+    const double cc = c[0];
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        v[i] -= cc * U[i * ld + col];
+}
+// v = u_col (get) or u_col = v / nrm (put); v = e_cand when col < 0
+__global__ void k_col_move(long long n, int ld, double* U, int col, double* v, const double* nrm, int put,
+                           long long cand) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        if (col < 0) v[i] = (i == cand) ? 1.0 : 0.0;
+        else if (put) U[i * ld + col] = v[i] / nrm[0];
+        else v[i] = U[i * ld + col];
+    }
+}
+// Y (cols x rows) = X^T for a row-major rows x cols X (the wide-S Gram S S^T)
+__global__ void k_transpose(long long rows, int cols, const double* __restrict__ X, double* __restrict__ Y) {
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < rows * cols;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long i = idx / cols, j = idx % cols;
+        Y[j * rows + i] = X[idx];
+    }
+}
+
 // sigma_i = sqrt(max(0, lambda_i <= floor ? 0 : lambda_i)), floor = 64 eps lambda_0
 // (svd.hpp:174-179); W[:, :k] = V[:, :k]; flag if any sigma_j (j < k) <= 1e-13 sigma_0
 __global__ void k_sigma(int m, int k, const double* evals, const double* evecs, double* sigma,
@@ -832,10 +893,11 @@ __global__ void k_sigma(int m, int k, const double* evals, const double* evecs, 
             sigma[i] = sqrt(fmax(0.0, lam));
         }
         smax = sigma[0];
-        int bad = 0;
-        for (int j = 0; j < k; ++j)
-            if (!(sigma[j] > smax * 1e-13)) bad = 1;
-        *status = bad ? kErrNumeric : 0;
+        // solid: the leading sigma_j above the cutoff 1e-13 sigma_max (svd.hpp:185-200);
+        // U's later columns come from complete_orthonormal instead
+        int solid = 0;
+        while (solid < k && sigma[solid] > smax * 1e-13) ++solid;
+        *status = solid;
     }
     __syncthreads();
     for (int idx = threadIdx.x; idx < m * k; idx += blockDim.x) {
@@ -1073,6 +1135,35 @@ void launch_tri_inv_t(const LaunchCtx& c, int k, const double* L, double* U) {
 
 void launch_coarse_inverse(const LaunchCtx& c, int k, const double* U, double* Ainv) {
     k_coarse_inverse<<<(k * k + 255) / 256, 256, 0, c.s>>>(k, U, Ainv);
+    count(c);
+}
+
+// dot / norm of columns (k_coldot_*): out[0] = u_col . v (col >= 0) or
+// sqrt(v . v) (col < 0); part holds num_sms * 2 partials
+void launch_coldot(const LaunchCtx& c, long long n, int ld, const double* U, int col, const double* v, double* part,
+                   double* out) {
+    const int g = grid_for(c, n, 256, 2);
+    k_coldot_partial<<<g, 256, 0, c.s>>>(n, ld, U, col, v, part);
+    k_coldot_final<<<1, 32, 0, c.s>>>(g, part, out, col < 0 ? 1 : 0);
+    count(c);
+    count(c);
+}
+void launch_col_axpy(const LaunchCtx& c, long long n, int ld, const double* U, int col, double* v, const double* cc) {
+    k_col_axpy<<<grid_for(c, n, 256), 256, 0, c.s>>>(n, ld, U, col, v, cc);
+    count(c);
+}
+void launch_col_move(const LaunchCtx& c, long long n, int ld, double* U, int col, double* v, const double* nrm,
+                     int put, long long cand) {
+    k_col_move<<<grid_for(c, n, 256), 256, 0, c.s>>>(n, ld, U, col, v, nrm, put, cand);
+    count(c);
+}
+void launch_transpose(const LaunchCtx& c, long long rows, int cols, const double* X, double* Y) {
+    k_transpose<<<grid_for(c, rows * cols, 256), 256, 0, c.s>>>(rows, cols, X, Y);
+    count(c);
+}
+
+void launch_shift_diag(const LaunchCtx& c, int k, double* G, double shift) {
+    k_shift_diag<<<(k + 255) / 256, 256, 0, c.s>>>(k, G, shift);
     count(c);
 }
 

@@ -238,12 +238,22 @@ __global__ void k_state_init(PcgState* st, double delta, long long max_it) {
     st->last_rel = 0.0;
     st->it = 0;
     st->max_it = max_it;
+    st->hist_base = 0;
     st->iterations = 0;
     st->body_runs = 0;
     st->done = 0;
     st->converged = 0;
     st->error = 0;
     st->first = 1;
+}
+
+// Next segment of a solve that stopped at its segment end (st->max_it) without
+// converging: the loop resumes from the state left by the last iteration, the
+// history restarts at hist[0] = iteration `base` (nlsp_gpu.cu run_pcg).
+__global__ void k_state_continue(PcgState* st, long long max_it, long long base) {
+    st->max_it = max_it;
+    st->hist_base = base;
+    st->done = 0;
 }
 
 // ||b||_2 (two_level.hpp:143-146) and r = b, x = 0; zero rhs -> ValidationError
@@ -275,6 +285,12 @@ __global__ void __launch_bounds__(kThreads) k_init_simple(SolveArgs a) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.n;
          i += (long long)gridDim.x * blockDim.x) {
         const double ri = a.r[i];
+        // JacobiPreconditioner::apply (two_level.hpp:112-113): a non-positive
+        // diagonal is a NumericError, raised after pcg's zero-rhs check
+        if (MODE == 1 && !(a.diag[i] > 0.0)) {
+            a.st->error = kErrNumeric;
+            a.st->done = 1;
+        }
         const double zi = MODE == 1 ? ri / a.diag[i] : ri;
         a.z[i] = zi;
         s[0] = fma(ri, zi, s[0]);
@@ -380,7 +396,7 @@ __global__ void __launch_bounds__(kThreads) k_update(SolveArgs a) {
         const double rel = sqrt(tot[0]) / st->bnorm;
         st->rr = tot[0];
         st->last_rel = rel;
-        a.hist[st->it] = rel;
+        a.hist[st->it - st->hist_base] = rel;
         st->iterations = st->it + 1;
         if (rel < st->delta) {
             st->converged = 1;
@@ -605,7 +621,7 @@ __device__ __forceinline__ void restrict_finish(double (&acc)[2 * PPL], double r
         const double rel = sqrt(ys[ld]) / st->bnorm;
         st->rr = ys[ld];
         st->last_rel = rel;
-        a.hist[st->it] = rel;
+        a.hist[st->it - st->hist_base] = rel;
         st->iterations = st->it + 1;
         if (rel < st->delta) {
             st->converged = 1;
@@ -1381,7 +1397,7 @@ __global__ void __launch_bounds__(kThreads) k_update_restrict_wide(SolveArgs a) 
         const double rel = sqrt(rrt) / st->bnorm;
         st->rr = rrt;
         st->last_rel = rel;
-        a.hist[st->it] = rel;
+        a.hist[st->it - st->hist_base] = rel;
         st->iterations = st->it + 1;
         if (rel < st->delta) {
             st->converged = 1;
@@ -1939,7 +1955,7 @@ __device__ void onepass_last(const SolveArgs& a, double rrt, double alpha) {
         const double rel = sqrt(rrt) / st->bnorm;
         st->rr = rrt;
         st->last_rel = rel;
-        a.hist[st->it] = rel;
+        a.hist[st->it - st->hist_base] = rel;
         st->iterations = st->it + 1;
         if (rel < st->delta) {
             st->converged = 1;
@@ -2179,6 +2195,11 @@ void launch_init_simple(const LaunchCtx& c, const SolveArgs& a, int mode) {
         launch_elems(c, k_init_simple<1>, a.n, a);
     else
         launch_elems(c, k_init_simple<0>, a.n, a);
+    count(c);
+}
+
+void launch_state_continue(const LaunchCtx& c, PcgState* st, long long max_it, long long base) {
+    k_state_continue<<<1, 1, 0, c.s>>>(st, max_it, base);
     count(c);
 }
 

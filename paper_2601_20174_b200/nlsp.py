@@ -403,7 +403,7 @@ def svd_basis(s, k: int, ctx: Context | None = None):
     sweeps = C.c_int32(0)
     _check(ctx, L.gpu_lib().nlsp_svd_basis(ctx.handle, sd.handle, k, C.byref(h), L.dptr(sig),
                                            C.byref(sweeps)))
-    return DeviceDense(ctx, h), sig[: sd.cols], int(sweeps.value)
+    return DeviceDense(ctx, h), sig[: min(sd.rows, sd.cols)], int(sweeps.value)
 
 
 # -------------------------------------------------------------- two-level --
@@ -542,11 +542,17 @@ def pcg(a: SparseCsrMatrix, b, m, delta: float, max_iters: int) -> PcgResult:
         raise ValidationError("pcg: unsupported preconditioner type")
     dev = _dev(a, getattr(m, "ctx", None))
     x = np.empty(a.dim())
-    hist = np.empty(max(int(max_iters), 1))
     rep = L.SolveReportC()
     mh = m.handle if kind == L.PRECOND_TWOLEVEL else None
-    _check(dev.ctx, L.gpu_lib().nlsp_pcg(dev.ctx.handle, dev.handle, kind, mh, L.dptr(bb), delta,
-                                         int(max_iters), L.dptr(x), C.byref(rep), L.dptr(hist)))
+    lib = L.gpu_lib()
+    # max_iters is size_t in the reference: clamp Python ints beyond 2^64 - 1
+    _check(dev.ctx, lib.nlsp_pcg(dev.ctx.handle, dev.handle, kind, mh, L.dptr(bb), delta,
+                                 min(int(max_iters), 2**64 - 1), L.dptr(x), C.byref(rep), None))
+    # the history, sized by the iterations run (nlsp_pcg_history)
+    hist = np.empty(int(rep.iterations))
+    cnt = C.c_uint64(0)
+    _check(dev.ctx, lib.nlsp_pcg_history(dev.ctx.handle, L.dptr(hist) if hist.size else None,
+                                         hist.size, C.byref(cnt)))
     r = SolveReport(iterations=int(rep.iterations),
                     residual_history=hist[: int(rep.iterations)].copy(),
                     converged=bool(rep.converged),

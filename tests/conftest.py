@@ -68,3 +68,39 @@ def col_match(p_gpu, p_ref):
         errs.append(min(e_pos, e_neg))
         signs.append(1.0 if e_pos <= e_neg else -1.0)
     return np.array(errs), np.array(signs)
+
+
+def gap_bounds(sigma, k):
+    """Per-column P bound of SURVEY §8c: 1e-10, or the gap-limited
+    1e-13 lambda_0 / gap_j where lambda = sigma^2 (eigenvalues of the Gram)."""
+    lam = np.asarray(sigma, np.float64) ** 2
+    gaps = np.array([min(lam[j - 1] - lam[j] if j > 0 else np.inf,
+                         lam[j] - lam[j + 1] if j + 1 < lam.size else np.inf) for j in range(k)])
+    return np.maximum(1e-10, 1e-13 * lam[0] / gaps), np.maximum(1e-10, 1e-13 * lam[0] / gaps.min())
+
+
+def check_basis_coarse_sketch(d, basis, coarse, k):
+    """P (up to column sign) and A_c against a golden holding only sketches of
+    the reference's basis_ (tests/golden/sketch.py): its row sample entrywise
+    (relative to the column's largest |entry|) and its Gaussian sketch (2-norm
+    relative; the JL factor is covered by 2x). Returns the per-column errors."""
+    import sys
+    sys.path.insert(0, GOLDEN)
+    from sketch import sketch
+    bound, sub = gap_bounds(d["sigma"], k)
+    idx, val = d["basis_argmax_idx"], d["basis_argmax_val"]
+    signs = np.sign(basis[idx, np.arange(k)]) * np.sign(val)
+    signs[signs == 0] = 1.0
+    rows = d["rows"]
+    err_rows = np.abs(basis[rows] * signs - d["basis_rows"]).max(axis=0) / np.abs(val)
+    sk = sketch(basis * signs)
+    ref_sk = d["basis_sketch"]
+    err_sk = np.linalg.norm(sk - ref_sk, axis=0) / np.linalg.norm(ref_sk, axis=0)
+    assert np.all(err_rows <= bound), (err_rows, bound)
+    assert np.all(err_sk <= 2 * bound), (err_sk, bound)
+    dac = np.diag(signs)
+    ac = dac @ coarse @ dac
+    ac_ref = d["coarse"]
+    err_ac = np.abs(ac - ac_ref).max() / np.abs(ac_ref).max()
+    assert err_ac <= sub, (err_ac, sub)
+    return err_rows, err_sk, err_ac

@@ -11,6 +11,7 @@
 // (u64 rows, u64 cols, f64 row-major): csr_rp.bin, csr_ci.bin, csr_v.bin (as
 // n x 1 columns of doubles), rhs.bin, params.bin = [k, m, s1, nu1, nu2, omega,
 // delta, s0_seed]. Writes x.bin and prints one JSON line.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -20,9 +21,12 @@
 #include <vector>
 
 #ifdef WITH_REFERENCE
+#include "nlsp/dense.hpp"
 #include "nlsp/errors.hpp"
 #include "nlsp/sparse.hpp"
+#include "nlsp/two_level.hpp"
 #define NLSP_GPU_REFERENCE_ERRORS
+#define NLSP_GPU_REFERENCE_TYPES
 #endif
 #include "nlsp_gpu.hpp"
 
@@ -46,6 +50,16 @@ void save(const std::string& path, const std::vector<double>& v) {
 }
 
 #ifndef WITH_REFERENCE
+// the accessor surface of nlsp::DenseMatrix (dense.hpp:17-30)
+struct LocalDense {
+    std::size_t r, c;
+    std::vector<double> a;
+    LocalDense(std::size_t rows, std::size_t cols) : r(rows), c(cols), a(rows * cols) {}
+    std::size_t rows() const { return r; }
+    std::size_t cols() const { return c; }
+    double* data() { return a.data(); }
+    const double* data() const { return a.data(); }
+};
 // the accessor surface of nlsp::SparseCsrMatrix (sparse.hpp:62-66)
 struct LocalCsr {
     std::size_t n;
@@ -95,6 +109,37 @@ int main(int argc, char** argv) {
     const auto plain = nlsp_gpu::pcg(dev, A, rhs, nlsp_gpu::IdentityPreconditioner{}, delta, 10 * n);
     save(dir + "/x.bin", res.solution);
 
+    // The reference's own call site, unchanged but for the namespace of
+    // build_preconditioner (two_level.hpp:91-101, 141-191): the matrix stays the
+    // reference's SparseCsrMatrix, the basis a host DenseMatrix, and the
+    // unqualified pcg / apply_two_level resolve to the device overloads.
+#ifdef WITH_REFERENCE
+    using HostDense = nlsp::DenseMatrix;
+    using nlsp::PcgResult;
+#else
+    using HostDense = LocalDense;
+    using nlsp_gpu::PcgResult;
+#endif
+    const auto uh = u.host();
+    HostDense basis(n, k);
+    std::copy(uh.begin(), uh.end(), basis.data());
+    auto M = nlsp_gpu::build_preconditioner(a, basis, omega, nu1, nu2);
+#ifdef WITH_REFERENCE
+    PcgResult ref_style = pcg(a, rhs, M, delta, 10 * n);
+    const auto z_free = apply_two_level(M, a, rhs);
+#else
+    PcgResult ref_style = nlsp_gpu::pcg(a, rhs, M, delta, 10 * n);
+    const auto z_free = nlsp_gpu::apply_two_level(M, a, rhs);
+#endif
+    const auto z_member = M.apply(a, rhs);
+    const auto z_dev = precond.apply(A, rhs);
+    double z_diff = 0.0, z_norm = 0.0, x_diff = 0.0;
+    for (std::size_t i = 0; i < n; ++i) {
+        z_diff = std::fmax(z_diff, std::fabs(z_free[i] - z_dev[i]) + std::fabs(z_member[i] - z_dev[i]));
+        z_norm = std::fmax(z_norm, std::fabs(z_dev[i]));
+        x_diff = std::fmax(x_diff, std::fabs(ref_style.solution[i] - res.solution[i]));
+    }
+
     // error mapping: the reference's ValidationError for a zero right-hand side
     bool zero_rhs_rejected = false;
     try {
@@ -105,10 +150,13 @@ int main(int argc, char** argv) {
     std::printf(
         "{\"n\": %zu, \"iterations\": %zu, \"converged\": %d, \"true_relative_residual\": %.6e, "
         "\"plain_iterations\": %zu, \"history_len\": %zu, \"zero_rhs_rejected\": %d, "
-        "\"solve_ms\": %.3f, \"reference_types\": %d}\n",
+        "\"solve_ms\": %.3f, \"ref_style_iterations\": %zu, \"ref_style_history_len\": %zu, "
+        "\"ref_style_method\": \"%s\", \"ref_style_x_maxdiff\": %.3e, \"apply_rel_diff\": %.3e, "
+        "\"reference_types\": %d}\n",
         n, res.report.iterations, res.report.converged ? 1 : 0, res.report.true_relative_residual,
         plain.report.iterations, res.report.residual_history.size(), zero_rhs_rejected ? 1 : 0,
-        res.report.solve_ms,
+        res.report.solve_ms, ref_style.report.iterations, ref_style.report.residual_history.size(),
+        ref_style.report.method.c_str(), x_diff, z_diff / (z_norm > 0 ? z_norm : 1.0),
 #ifdef WITH_REFERENCE
         1
 #else

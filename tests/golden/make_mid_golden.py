@@ -24,6 +24,9 @@ sys.path.insert(0, ROOT)
 from oracle.oracle import Reference  # noqa: E402
 from paper_2601_20174_b200 import problems  # noqa: E402
 
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from sketch import col_argmax, sample_rows, sketch  # noqa: E402
+
 OUT = os.path.dirname(os.path.abspath(__file__))
 
 MID = {
@@ -48,10 +51,19 @@ def main(names=None):
         p = np.ascontiguousarray(u[:, : cfg.k])
         t = ref.twolevel(a, p, cfg.omega, cfg.nu1, cfg.nu2)
         res = ref.pcg(a, pb.rhs, 2, t, cfg.delta, 10 * pb.n)
+        # the reference's basis_ (after qr_thin) as sketches, its Galerkin A_c
+        # (the constructor's own loops) and Cholesky factor: the north star's
+        # P / A_c rule at the BASELINE k and m
+        basis, chol, _ = t.export()
+        coarse = ref.galerkin(t)
+        rows = sample_rows(pb.n)
+        amax_i, amax_v = col_argmax(basis)
         np.savez_compressed(
             os.path.join(OUT, f"{name}.npz"), config=name, nx=cfg.nx, n=pb.n, k=cfg.k, m=cfg.m,
             sigma=sig, eigh_sweeps=sweeps, x=res.x, iterations=res.iterations, converged=res.converged,
-            history=res.history, true_res=res.true_relative_residual)
+            history=res.history, true_res=res.true_relative_residual,
+            basis_sketch=sketch(basis), basis_rows=basis[rows], rows=rows, basis_argmax_idx=amax_i,
+            basis_argmax_val=amax_v, svd_p_sketch=sketch(p), coarse=coarse, chol=chol)
         print(f"{name}: n={pb.n} iterations={res.iterations} true_res={res.true_relative_residual:.3e} "
               f"({time.perf_counter() - t0:.0f} s)", flush=True)
 

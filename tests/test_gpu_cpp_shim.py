@@ -50,5 +50,11 @@ def test_shim_program_matches_reference(tmp_path, binary):
     assert abs(out["iterations"] - int(d["iterations"])) <= 2
     assert abs(out["plain_iterations"] - int(d["plain_iterations"])) <= 2
     assert out["history_len"] == out["iterations"]
+    # the reference-signature call site (build_preconditioner / unqualified pcg /
+    # apply_two_level / M.apply(a, r) on the reference's matrix type): same solve
+    assert out["ref_style_iterations"] == out["iterations"]
+    assert out["ref_style_history_len"] == out["iterations"] and out["ref_style_method"] == "two_level"
+    assert out["ref_style_x_maxdiff"] <= 1e-12 * np.abs(d["x"]).max()
+    assert out["apply_rel_diff"] <= 1e-12
     x = load(tmp_path / "x.bin")
     assert np.linalg.norm(x - d["x"]) <= 1e-9 * np.linalg.norm(d["x"])

@@ -76,3 +76,59 @@ def test_full_size_solve_properties(nlsp, name):
     # the coarse correction must help: fewer iterations than plain CG
     plain = nlsp.pcg(a, pb.rhs, nlsp.IdentityPreconditioner(), cfg.delta, 10 * pb.n)
     assert rep.iterations < plain.report.iterations
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
+def test_full_size_matches_reference(nlsp, name):
+    """The benchmarked configurations against the REFERENCE's own full-size run
+    (tests/golden/make_full_golden.py: bench_single's SVD row through
+    oracle/_ref at the BASELINE size), with the north star's tolerances:
+    sigma, P and A_c (1e-10 up to column sign, gap-limited), iterations +-2, the
+    same 1e-8 stop, x within 1e-9 (in full for C2/C5; for C3/C4 through a
+    Gaussian sketch and a row sample)."""
+    import os
+    import sys
+
+    from conftest import GOLDEN, check_basis_coarse_sketch
+    path = os.path.join(GOLDEN, f"full_{name}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated (tests/golden/make_full_golden.py)")
+    d = np.load(path)
+    sys.path.insert(0, GOLDEN)
+    from sketch import sketch
+    cfg = problems.CONFIGS[name]
+    pb = problems.generate(cfg)
+    assert pb.n == int(d["n"]) and pb.nnz == int(d["nnz"])
+    a = pb.csr()
+    mask = pb.mask if pb.mask.any() else None
+    sv = nlsp.generate_smoothed_vectors(a, mask, cfg.m, cfg.s1, cfg.omega, cfg.s0_seed)
+    p, sig, _ = nlsp.svd_basis(sv.s, cfg.k)
+    del sv
+    sref = np.asarray(d["sigma"])
+    assert np.abs(np.asarray(sig) - sref[: len(sig)]).max() <= 1e-10 * sref[0]
+    m = nlsp.TwoLevelPreconditioner(a, p, cfg.omega, cfg.nu1, cfg.nu2)
+    basis, chol, coarse = m._export()
+    er, es, ea = check_basis_coarse_sketch(d, basis, coarse, cfg.k)
+    del basis
+    res = nlsp.pcg(a, pb.rhs, m, cfg.delta, 10 * pb.n)
+    rep = res.report
+    it_ref = int(d["iterations"])
+    assert rep.converged and bool(d["converged"])
+    assert abs(rep.iterations - it_ref) <= 2, (rep.iterations, it_ref)
+    assert rep.residual_history[-1] < cfg.delta and rep.true_relative_residual < 10 * cfg.delta
+    hist_ref = np.asarray(d["history"])
+    c = min(len(hist_ref), rep.iterations)
+    hist_dev = np.abs(rep.residual_history[:c] - hist_ref[:c]) / hist_ref[:c]
+    x = res.solution
+    xn = float(d["x_norm"])
+    if "x" in d.files:
+        xerr = np.linalg.norm(x - d["x"]) / xn
+    else:
+        # ||R^T e|| / sqrt(32) estimates ||e|| within [0.5, 1.6]x w.p. > 1 - 1e-5
+        xerr = 2.0 * np.linalg.norm(sketch(x) - d["x_sketch"]) / np.sqrt(d["x_sketch"].size) / xn
+        rows = d["rows"]
+        assert np.linalg.norm(x[rows] - d["x_rows"]) <= 1e-9 * np.linalg.norm(d["x_rows"])
+    print(f"{name}: iterations {rep.iterations} (ref {it_ref}), x err {xerr:.2e}, history dev "
+          f"{hist_dev.max():.2e}, P rows {er.max():.2e} sketch {es.max():.2e}, A_c {ea:.2e}")
+    assert xerr <= 1e-9, xerr
+    assert hist_dev.max() <= 1e-6, hist_dev.max()

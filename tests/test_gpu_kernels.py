@@ -199,15 +199,125 @@ def test_svd_basis_random_matches_oracle(nlsp, oracle):
     assert errs.max() <= 1e-10 and np.all(signs == 1.0)  # same sign convention
 
 
-def test_svd_basis_rejects_nonfinite_and_wide(nlsp):
+def test_svd_basis_rejects_nonfinite_and_k_past_rank(nlsp):
     s = np.ones((10, 3))
     s[4, 1] = np.nan
     with pytest.raises(nlsp.ValidationError):
         nlsp.svd_basis(s, 2)
-    with pytest.raises(nlsp.ValidationError):
-        nlsp.svd_basis(np.ones((3, 10)), 2)
-    with pytest.raises(nlsp.ValidationError):
+    with pytest.raises(nlsp.ValidationError):  # first_cols: k > min(n, m)
         nlsp.svd_basis(np.random.default_rng(1).standard_normal((10, 3)), 4)
+    with pytest.raises(nlsp.ValidationError):
+        nlsp.svd_basis(np.random.default_rng(1).standard_normal((3, 10)), 4)
+
+
+def _svd_vs_oracle(nlsp, oracle, s, k, tol_orth=1e-12):
+    p, sig, _ = nlsp.svd_basis(s, k)
+    u, sig_o, _, _ = oracle.svd(s)
+    r = min(s.shape)
+    assert sig.shape == (r,)
+    # sigma_j = sqrt(lambda_j) of the Gram: lambda to ~u lambda_0 on both sides
+    assert np.abs(sig ** 2 - sig_o ** 2).max() <= 1e-13 * sig_o[0] ** 2
+    pg = p.numpy()
+    assert np.abs(pg.T @ pg - np.eye(k)).max() <= tol_orth
+    return pg, u[:, :k], sig_o
+
+
+def test_svd_basis_wide_s_matches_reference(nlsp, oracle):
+    """m > n: svd_oracle eigensolves S S^T and U is its eigenvectors
+    (svd.hpp:161-165, 186, 205), then the sign convention."""
+    rng = np.random.default_rng(11)
+    s = rng.standard_normal((12, 40)) * np.geomspace(1.0, 0.2, 12)[:, None]
+    pg, pr, sig = _svd_vs_oracle(nlsp, oracle, s, 6)
+    errs, signs = col_match(pg, pr)
+    assert np.all(signs == 1.0)  # same sign convention
+    lam = sig ** 2
+    gaps = np.array([min(lam[j - 1] - lam[j] if j > 0 else np.inf, lam[j] - lam[j + 1]) for j in range(6)])
+    assert np.all(errs <= np.maximum(1e-10, 1e-13 * lam[0] / gaps)), errs
+
+
+def test_svd_basis_completes_rank_deficient_s(nlsp, oracle):
+    """Numerical rank 3 < k = 5: columns past the sigma cutoff come from
+    complete_orthonormal (svd.hpp:101-126, 185-203), coordinate vectors
+    projected off the solid columns, as in the reference."""
+    rng = np.random.default_rng(5)
+    s = rng.standard_normal((60, 3)) @ rng.standard_normal((3, 8))
+    pg, pr, sig = _svd_vs_oracle(nlsp, oracle, s, 5)
+    assert np.all(sig[3:] == 0.0)  # clamped below the Gram's rounding floor
+    errs, _ = col_match(pg, pr)
+    assert errs[:3].max() <= 1e-10 and errs[3:].max() <= 1e-10, errs
+
+
+def test_svd_basis_polishes_lost_orthogonality(nlsp, oracle):
+    """sigma spread over 1e5: U = S V / sigma loses orthogonality (~u
+    sigma_0^2 / sigma_j^2), so the defect exceeds 1e-11 and the Gram-Schmidt
+    polish runs (svd.hpp:128-145, :204) — U orthonormal to rounding again."""
+    rng = np.random.default_rng(9)
+    q = np.linalg.qr(rng.standard_normal((400, 6)))[0]
+    v = np.linalg.qr(rng.standard_normal((6, 6)))[0]
+    s = (q * np.geomspace(1.0, 1e-5, 6)) @ v.T
+    pg, pr, sig = _svd_vs_oracle(nlsp, oracle, s, 6, tol_orth=1e-13)
+    errs, _ = col_match(pg, pr)
+    lam = sig ** 2
+    gaps = np.array([min(lam[j - 1] - lam[j] if j > 0 else np.inf, lam[j] - lam[j + 1] if j < 5 else np.inf)
+                     for j in range(6)])
+    # columns are determined to ~u lambda_0 / gap_j (both sides alike)
+    assert np.all(errs <= np.maximum(1e-10, 1e-12 * lam[0] / gaps)), errs
+
+
+@pytest.mark.parametrize("cond", [1e4, 1e10, 1e13])
+def test_qr_thin_ill_conditioned_basis_matches_reference(nlsp, oracle, cond):
+    """qr_thin (qr.hpp:18-45) through the two-level build: CholeskyQR2 for a
+    well-conditioned basis, shifted CholeskyQR3 once the Gram's pivots fall
+    under 1e-6 ||B||_F (where CholeskyQR2 would lose orthogonality or report a
+    spurious rank deficiency). Q matches the reference's two-pass MGS to
+    ~u cond(B) per column, and the reference's rank test is kept."""
+    from test_gpu_twolevel import tridiag
+    rng = np.random.default_rng(int(np.log10(cond)))
+    n, k = 300, 8
+    u0 = np.linalg.qr(rng.standard_normal((n, k)))[0]
+    v0 = np.linalg.qr(rng.standard_normal((k, k)))[0]
+    b = (u0 * np.geomspace(1.0, 1.0 / cond, k)) @ v0.T
+    a = tridiag(n, nlsp)
+    try:
+        qr, _ = oracle.qr_thin(b)
+    except Exception:  # cond 1e13: the last post-elimination norm < 1e-12 ||B||_F
+        with pytest.raises(nlsp.RankDeficiencyError):
+            nlsp.TwoLevelPreconditioner(a, b, 2 / 3, 1, 1)
+        return
+    m = nlsp.TwoLevelPreconditioner(a, b, 2 / 3, 1, 1)
+    q = m._export()[0]
+    assert np.abs(q.T @ q - np.eye(k)).max() <= 1e-12
+    errs, signs = col_match(q, qr)
+    assert np.all(signs == 1.0)  # positive diagonal of R on both sides
+    assert errs.max() <= max(1e-10, 1e-15 * cond), errs
+    # the span: B = Q R exactly up to rounding
+    rr = q.T @ b
+    assert np.abs(q @ rr - b).max() <= 1e-13 * np.abs(b).max()
+
+
+def test_qr_thin_rank_test_matches_reference(nlsp, oracle):
+    """A column dependent to 1e-14 ||B||_F is rank-deficient for the reference
+    (post-elimination norm < 1e-12 ||B||_F) and here; one at 1e-10 is not."""
+    from test_gpu_twolevel import tridiag
+    rng = np.random.default_rng(3)
+    n = 200
+    a = tridiag(n, nlsp)
+    base = rng.standard_normal((n, 4))
+    for eps, deficient in [(1e-14, True), (1e-10, False)]:
+        b = np.hstack([base, (base @ [1.0, -2.0, 0.5, 0.25])[:, None] + eps * rng.standard_normal((n, 1))])
+        try:
+            oracle.qr_thin(b)
+            ref_def = False
+        except Exception:
+            ref_def = True
+        assert ref_def == deficient
+        if deficient:
+            with pytest.raises(nlsp.RankDeficiencyError):
+                nlsp.TwoLevelPreconditioner(a, b, 2 / 3, 1, 1)
+        else:
+            m = nlsp.TwoLevelPreconditioner(a, b, 2 / 3, 1, 1)
+            q = m._export()[0]
+            assert np.abs(q.T @ q - np.eye(5)).max() <= 1e-12
 
 
 @pytest.mark.parametrize("name", ["c1_default", "scaled_C2", "scaled_C3", "scaled_C4", "scaled_C5"])

@@ -9,7 +9,7 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
-from conftest import golden
+from conftest import check_basis_coarse_sketch, golden
 from paper_2601_20174_b200 import problems
 
 pytestmark = pytest.mark.gpu
@@ -29,6 +29,11 @@ def test_midsize_pipeline_matches_reference(nlsp, name):
     assert np.abs(np.asarray(sig) - sref[: len(sig)]).max() <= 1e-10 * sref[0]
     m = nlsp.TwoLevelPreconditioner(a, p, cfg.omega, cfg.nu1, cfg.nu2)
     assert m.cycle() == "onepass"
+    # P and A_c at the BASELINE k / m (north star: 1e-10 up to column sign,
+    # gap-limited where the singular values cluster)
+    basis, _, coarse = m._export()
+    er, es, ea = check_basis_coarse_sketch(d, basis, coarse, cfg.k)
+    print(f"{name}: P rows {er.max():.2e} sketch {es.max():.2e} A_c {ea:.2e}")
     res = nlsp.pcg(a, pb.rhs, m, cfg.delta, 10 * pb.n)
     rep = res.report
     assert rep.converged and rep.kernel_launches > 2  # the graph loop, not the cluster solver

@@ -26,7 +26,7 @@ d = np.load({path!r})
 a = nlsp.SparseCsrMatrix(int(d["n"]), d["row_ptr"], d["col_idx"], d["values"])
 m = nlsp.TwoLevelPreconditioner(a, d["P"], float(d["omega"]), int(d["nu1"]), int(d["nu2"]))
 r = nlsp.pcg(a, d["rhs"], m, float(d["delta"]), 10 * a.dim())
-r2 = nlsp.pcg(a, d["rhs"], m, float(d["delta"]), 10 * a.dim())
+r2 = nlsp.pcg(a, d["rhs"], m, float(d["delta"]), 2**64 - 1)  # SIZE_MAX: no limit
 np.save({out!r}, r.solution)
 print(json.dumps({{"iterations": r.report.iterations, "launches": r.report.kernel_launches,
                    "true": r.report.true_relative_residual, "hist_len": len(r.report.residual_history),
@@ -46,6 +46,13 @@ PATHS = {
     "cluster_chol": {"NLSP_CLUSTER": "1", "NLSP_COARSE": "chol"},
     # the SpMV family over CSR instead of the detected diagonal form
     "graph_csr": {"NLSP_CLUSTER": "0", "NLSP_DIA": "0"},
+    # the residual history kept in device segments of 16 entries: the loop
+    # pauses at every segment end and resumes from the device state (graph:
+    # the continuation graph; host: the stream loop; the cluster solver cannot
+    # pause, so a short segment moves small systems to the graph path)
+    "graph_seg": {"NLSP_CLUSTER": "0", "NLSP_HIST_CHUNK": "16"},
+    "host_seg": {"NLSP_CLUSTER": "0", "NLSP_LOOP": "host", "NLSP_HIST_CHUNK": "16"},
+    "cluster_seg": {"NLSP_CLUSTER": "1", "NLSP_HIST_CHUNK": "16"},
 }
 
 
@@ -76,6 +83,11 @@ def test_execution_paths_match_reference(tmp_path, case):
     # the diagonal form sums every row in CSR column order: bitwise the CSR path
     assert res["graph"][0]["iterations"] == res["graph_csr"][0]["iterations"]
     assert np.array_equal(res["graph"][1], res["graph_csr"][1])
+    # pausing at history-segment ends changes nothing but the launch count
+    for p in ("graph_seg", "host_seg", "cluster_seg"):
+        assert res[p][0]["iterations"] == res["graph"][0]["iterations"], p
+        assert np.array_equal(res[p][1], res["graph"][1]), p
+        assert res[p][0]["last"] == res["graph"][0]["last"], p
 
 
 EXPECTED_FORM = {"c1_default": 1, "scaled_C2": 2, "scaled_C3": 1, "scaled_C4": 1, "scaled_C5": 0,

@@ -140,6 +140,38 @@ def test_pcg_zero_rhs_rejected(nlsp):
         nlsp.pcg(a, np.ones(3), nlsp.IdentityPreconditioner(), 1e-6, 10)
 
 
+def test_pcg_error_order_matches_reference(nlsp):
+    """pcg checks the right-hand side before the preconditioner is applied
+    (two_level.hpp:148 then :152): a zero rhs under a Jacobi preconditioner
+    with a non-positive diagonal is a ValidationError, a nonzero one the
+    JacobiPreconditioner's NumericError (:112-113)."""
+    a = nlsp.SparseCsrMatrix.from_triplets(2, [(0, 0, 1.0), (1, 1, -1.0)])
+    with pytest.raises(nlsp.ValidationError):
+        nlsp.pcg(a, np.zeros(2), nlsp.JacobiPreconditioner(), 1e-8, 10)
+    with pytest.raises(nlsp.NumericError):
+        nlsp.pcg(a, np.ones(2), nlsp.JacobiPreconditioner(), 1e-8, 10)
+
+
+def test_pcg_history_sized_by_iterations(nlsp):
+    """The history is read after the solve (nlsp_pcg_history), sized by the
+    iterations run: a reference-style max_iters = 10 n, or SIZE_MAX, allocates
+    nothing proportional to it."""
+    import ctypes as C
+    from paper_2601_20174_b200 import _lib as L
+    d = golden("fem_diffusion")
+    a = csr_from_golden(d)
+    for mx in (10 * a.dim(), 2**64 - 1):
+        res = nlsp.pcg(a, d["rhs"], nlsp.IdentityPreconditioner(), 1e-8, mx)
+        assert res.report.converged and len(res.report.residual_history) == res.report.iterations
+    ctx = nlsp.default_context()
+    cnt = C.c_uint64(0)
+    assert L.gpu_lib().nlsp_pcg_history(ctx.handle, None, 0, C.byref(cnt)) == 0
+    assert cnt.value == res.report.iterations
+    part = np.empty(3)
+    assert L.gpu_lib().nlsp_pcg_history(ctx.handle, L.dptr(part), 3, C.byref(cnt)) == 0
+    assert np.array_equal(part, res.report.residual_history[:3])
+
+
 def test_pcg_not_spd_detected(nlsp):
     a = nlsp.SparseCsrMatrix.from_triplets(2, [(0, 0, 1.0), (1, 1, -1.0)])
     with pytest.raises(nlsp.NotSpdError):
