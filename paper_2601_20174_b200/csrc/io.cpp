@@ -177,6 +177,11 @@ struct Trip {
 
 // SparseCsrMatrix::from_triplets (sparse.hpp:24-53)
 void from_triplets(unsigned long long dim, const std::vector<Trip>& t, nlsp_host_csr* out) {
+    // a size line such as "-1 -1 0" parses to 2^64 - 1 (istream >> size_t
+    // wraps negatives): dim + 1 would wrap to an empty row_ptr. Dimensions past
+    // the device limit (nlsp_csr_upload: n < 2^31) are rejected before anything
+    // is allocated.
+    if (dim >= (1ull << 31)) throw ValidationError("matrix dimension exceeds 2^31 - 1");
     for (const Trip& e : t)
         if (e.i >= dim || e.j >= dim) throw ValidationError("triplet index out of range");
     std::vector<unsigned long long> start(dim + 1, 0);

@@ -113,3 +113,14 @@ def test_bad_manifest(tmp_path):
     (d / "manifest.txt").write_text("no equals sign here\n")
     with pytest.raises(nlsp.ValidationError, match="manifest: bad line"):
         io.load_instance(str(d))
+
+
+def test_wrapping_dimension_rejected_before_allocation(tmp_path):
+    """A size line of -1 (istream >> size_t wraps it to 2^64 - 1) or any
+    dimension past the device limit is a ValidationError, not a wrapped
+    row_ptr size (heap corruption in a naive from_triplets)."""
+    for line in ("-1 -1 0", "18446744073709551615 18446744073709551615 0", "2147483648 2147483648 1\n1 1 1.0"):
+        p = tmp_path / "big.mtx"
+        p.write_text("%%MatrixMarket matrix coordinate real symmetric\n" + line + "\n")
+        with pytest.raises(nlsp.ValidationError, match="dimension"):
+            io.load_matrix_market(str(p))
