@@ -62,6 +62,12 @@ typedef struct {
     uint64_t kernel_launches;      /* this library's kernels launched by the solve   */
     uint64_t h2d_bytes;            /* host->device bytes copied by the call          */
     uint64_t d2h_bytes;            /* device->host bytes copied by the call          */
+    double onepass_drift;          /* one-pass cycle guard: max over the solve of
+                                      |c_rec - W^T r|_inf / |W^T r|_inf, the restriction's
+                                      recurrence against its direct value */
+    int32_t cycle_fallback;        /* 1: the drift passed NLSP_DRIFT_TOL (default 1e-10)
+                                      and the solve was re-run on the folded cycle        */
+    int32_t reserved;
 } nlsp_solve_report;
 
 /* ------------------------------------------------------------ context ---- */
@@ -92,6 +98,12 @@ void nlsp_csr_dims(const nlsp_csr* a, uint64_t* n, uint64_t* nnz);
  * model of the roofline). Detected at nlsp_csr_upload; NLSP_DIA=0 keeps CSR.
  * Results are bitwise those of the CSR kernels (same per-row fma order). */
 nlsp_status nlsp_csr_format(const nlsp_csr* a, int* kind, int* offsets, uint64_t* pass_bytes);
+/* The structured-grid geometry of the diagonal form (no reference
+ * counterpart): every offset is dz * plane + d with dz in {-1, 0, 1},
+ * |d| <= halo (plane = 0: none). march = 1 when the PCG loop's gather kernels
+ * run as plane marches on ctx's device (march.cuh; NLSP_MARCH=0
+ * disables, =1 forces for any n). */
+nlsp_status nlsp_csr_geometry(nlsp_ctx* ctx, const nlsp_csr* a, uint64_t* plane, int* halo, int* march);
 /* spmv (sparse.hpp:116-128), y = A x; host buffers of length n */
 nlsp_status nlsp_spmv(nlsp_ctx* ctx, const nlsp_csr* a, const double* x, double* y);
 /* device-buffer variant (x, y device pointers of length n) */

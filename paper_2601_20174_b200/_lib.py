@@ -54,6 +54,9 @@ class SolveReportC(C.Structure):
         ("kernel_launches", c_u64),
         ("h2d_bytes", c_u64),
         ("d2h_bytes", c_u64),
+        ("onepass_drift", c_dbl),
+        ("cycle_fallback", c_i32),
+        ("reserved", c_i32),
     ]
 
 
@@ -98,6 +101,7 @@ GPU_SYMBOLS = [
     ("nlsp_csr_destroy", None, [vp]),
     ("nlsp_csr_dims", None, [vp, P_u64, P_u64]),
     ("nlsp_csr_format", c_i32, [vp, P_i32, P_i32, P_u64]),
+    ("nlsp_csr_geometry", c_i32, [vp, vp, P_u64, P_i32, P_i32]),
     ("nlsp_pcg_batch", c_i32, [vp, c_u64, C.POINTER(vp), C.POINTER(vp), C.POINTER(P_dbl), c_dbl, c_u64,
                                 C.POINTER(P_dbl), C.POINTER(SolveReportC), P_i32]),
     ("nlsp_sa_aggregate", c_i32, [c_u64, c_u64, P_u64, P_u64, P_dbl, c_dbl, P_u64, P_u64]),

@@ -43,6 +43,7 @@ struct PcgState {
     unsigned int counter[16];  // last-CTA tickets, one slot per kernel kind
     int op_grid;               // CTAs of the last one-pass prolongation (its partials' stride)
     double alpha_prev;         // alpha of the previous iteration (one-pass restriction)
+    double drift_max;          // max over the solve of |c_rec - W^T r| / |W^T r| (one-pass guard)
 };
 
 // Ticket slots (each kernel kind reuses its own counter; counters return to 0).
@@ -67,6 +68,10 @@ struct DiaArgs {
     double val[kMaxDia];
     const void* mask;  // n presence masks (bit t: offset t present)
     const double* rv;  // kind 2: d x n values (0 where absent)
+    // structured grid (march.cuh): every offset is dz * plane + d, dz in
+    // {-1, 0, 1}, |d| <= halo, n % plane == 0; plane == 0: none detected
+    long long plane;
+    int halo;
 };
 
 // Everything a solve kernel needs, passed by value.
@@ -103,7 +108,8 @@ struct SolveArgs {
     double* partials;    // kMaxGrid * max(k, 4)
     double* e;           // coarse correction, k
     // one-pass cycle (solve_kernels.cu): M = W^T A W (k x k),
-    // ow = [u_even | u_odd | v] column sums (3 ld), opart = per-CTA partials of
+    // ow = [u_even | u_odd | v | c] column sums (4 ld; c = the last recurrence
+    // value, for the drift guard), opart = per-CTA partials of
     // [u | v], column-major
     const double* M;
     double* ow;

@@ -90,6 +90,7 @@ void launch_coldot(const LaunchCtx&, long long, int, const double*, int, const d
 void launch_col_axpy(const LaunchCtx&, long long, int, const double*, int, double*, const double*);
 void launch_col_move(const LaunchCtx&, long long, int, double*, int, double*, const double*, int, long long);
 void launch_transpose(const LaunchCtx&, long long, int, const double*, double*);
+bool march_planned(const LaunchCtx&, const SolveArgs&);
 void launch_sigma(const LaunchCtx&, int, int, const double*, const double*, double*, double*,
                   int*);
 // setup_kernels.cu (SA)
@@ -340,7 +341,7 @@ nlsp_status ensure_ws(nlsp_ctx* ctx, long long n, long long hist) {
             CU(dalloc(p, (size_t)n + 16));  // padded for 16-B bulk copies of tile slices
         CU(dalloc(&ctx->e, (size_t)kMaxCoarse + 2));
         CU(dalloc(&ctx->partials, (size_t)kMaxGrid * 256));
-        CU(dalloc(&ctx->ow, (size_t)3 * (kOnePassK + 2)));
+        CU(dalloc(&ctx->ow, (size_t)4 * (kOnePassK + 2)));
         CU(dalloc(&ctx->opart, (size_t)kMaxGrid * 3 * (kOnePassK + 2)));
         // q feeds the one-pass partials of the PCG prologue (weighted by 0)
         CU(cudaMemsetAsync(ctx->q, 0, ((size_t)n + 16) * 8, ctx->s));
@@ -671,6 +672,40 @@ nlsp_status run_pcg(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twole
     return NLSP_OK;
 }
 
+// The one-pass cycle carries the restriction by a recurrence; its
+// drift against the direct W^T r is measured every iteration on the device.
+// Past NLSP_DRIFT_TOL (default 1e-10) the solve is re-run from x0 = 0 on the
+// folded cycle (W streamed twice, the restriction direct), which applies the
+// same operator without the recurrence.
+const double g_drift_tol = [] {
+    const char* e = std::getenv("NLSP_DRIFT_TOL");
+    return e ? std::atof(e) : 1e-10;
+}();
+
+nlsp_status run_pcg_guarded(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twolevel* m,
+                            double delta, unsigned long long max_iters, nlsp_solve_report* rep) {
+    nlsp_status st = run_pcg(ctx, a, kind, m, delta, max_iters, rep);
+    const double drift = ctx->st_host->drift_max;
+    if (rep) {
+        rep->onepass_drift = drift;
+        rep->cycle_fallback = 0;
+    }
+    if (st != NLSP_OK || kind != NLSP_PRECOND_TWOLEVEL || !m->onepass || !(drift > g_drift_tol)) return st;
+    nlsp_twolevel folded = *m;  // same device arrays, W streamed twice per iteration
+    folded.onepass = false;
+    folded.id = m->id | (1ull << 63);
+    const double ms0 = rep ? rep->solve_ms : 0.0;
+    const unsigned long long l0 = rep ? rep->kernel_launches : 0;
+    st = run_pcg(ctx, a, kind, &folded, delta, max_iters, rep);
+    if (rep) {
+        rep->onepass_drift = drift;
+        rep->cycle_fallback = 1;
+        rep->solve_ms += ms0;
+        rep->kernel_launches += l0;
+    }
+    return st;
+}
+
 // Copies the last solve's history: completed segments from the host, the last
 // one from the device.
 nlsp_status copy_history(nlsp_ctx* ctx, double* out, unsigned long long cap) {
@@ -846,6 +881,25 @@ static bool detect_dia(uint64_t n, uint64_t nnz, const uint64_t* rp, const uint6
         d.off[t] = (int)offs[t];
         d.val[t] = constant ? cv[t] : 0.0;
     }
+    // structured-grid geometry for the plane-march kernels (march.cuh): the
+    // plane stride P (a positive offset) for which every offset is dz P + dd
+    // with dz in {-1, 0, 1} and the smallest halo max |dd| (<= P / 4), P | n
+    for (int c = 0; c < D; ++c) {
+        const long long P = offs[c];
+        if (P < 2 || (long long)n % P != 0 || (long long)n / P < 3) continue;
+        long long h = 0;
+        for (int t = 0; t < D; ++t) {
+            const long long o = offs[t];
+            const long long dz = o > P / 2 ? 1 : (o < -P / 2 ? -1 : 0);
+            const long long r = o - dz * P;
+            h = std::max(h, r < 0 ? -r : r);
+            if (o > P + P / 2 || o < -P - P / 2) h = P;  // beyond the neighbouring planes
+        }
+        if (h >= 1 && 4 * h <= P && (d.plane == 0 || h < d.halo)) {
+            d.plane = P;
+            d.halo = (int)h;
+        }
+    }
     return true;
 }
 
@@ -929,7 +983,7 @@ nlsp_status nlsp_csr_upload(nlsp_ctx* ctx, uint64_t n, uint64_t nnz, const uint6
                 (e = cudaMemcpyAsync(a->dia_mask, mask.data(), mask.size(), cudaMemcpyHostToDevice, ctx->s)))
                 return fail(e, "csr_upload diagonal form");
             if (d.kind == 2) {
-                if ((e = dalloc(&a->dia_rv, rv.size())) ||
+                if ((e = dalloc(&a->dia_rv, rv.size() + 16)) ||
                     (e = cudaMemcpyAsync(a->dia_rv, rv.data(), rv.size() * 8, cudaMemcpyHostToDevice, ctx->s)))
                     return fail(e, "csr_upload diagonal values");
             }
@@ -976,6 +1030,19 @@ nlsp_status nlsp_csr_format(const nlsp_csr* a, int* kind, int* offsets, uint64_t
     if (kind) *kind = a->dia.kind;
     if (offsets) *offsets = a->dia.kind ? a->dia.d : 0;
     if (pass_bytes) *pass_bytes = a->pass_bytes;
+    return NLSP_OK;
+}
+
+nlsp_status nlsp_csr_geometry(nlsp_ctx* ctx, const nlsp_csr* a, uint64_t* plane, int* halo, int* march) {
+    if (!a) return NLSP_E_VALIDATION;
+    if (plane) *plane = a->dia.kind ? (uint64_t)a->dia.plane : 0;
+    if (halo) *halo = a->dia.kind ? a->dia.halo : 0;
+    if (march) {
+        SolveArgs s{};
+        s.n = a->n;
+        s.dia = a->dia;
+        *march = (ctx && march_planned(ctx->lc, s)) ? 1 : 0;
+    }
     return NLSP_OK;
 }
 
@@ -1621,7 +1688,7 @@ nlsp_status nlsp_pcg(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
     nlsp_solve_report local{};
     nlsp_solve_report* r = rep ? rep : &local;
     std::memset(r, 0, sizeof(*r));
-    st = run_pcg(ctx, a, kind, m, delta, max_iters, r);
+    st = run_pcg_guarded(ctx, a, kind, m, delta, max_iters, r);
     if (st) return st;
     if (residual_history) {
         st = copy_history(ctx, residual_history, r->iterations);
@@ -1654,7 +1721,7 @@ nlsp_status nlsp_pcg_device(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nl
     nlsp_solve_report local{};
     nlsp_solve_report* r = rep ? rep : &local;
     std::memset(r, 0, sizeof(*r));
-    st = run_pcg(ctx, a, kind, m, delta, max_iters, r);
+    st = run_pcg_guarded(ctx, a, kind, m, delta, max_iters, r);
     if (st) return st;
     if (residual_history) {
         st = copy_history(ctx, residual_history, r->iterations);

@@ -239,6 +239,7 @@ __global__ void k_state_init(PcgState* st, double delta, long long max_it) {
     st->it = 0;
     st->max_it = max_it;
     st->hist_base = 0;
+    st->drift_max = 0.0;
     st->iterations = 0;
     st->body_runs = 0;
     st->done = 0;
@@ -1976,11 +1977,44 @@ __device__ void onepass_last(const SolveArgs& a, double rrt, double alpha) {
     __syncthreads();
     coarse_apply_inverse(a.M, k, es, gs);  // M e_i
     __syncthreads();
+    // Guard: the previous iteration's c_i came from the recurrence; u_i = W^T r_i
+    // was then formed directly by the pass over W, so their gap is the one-step
+    // error of the recurrence. Its max |c - u| / max |u| over the
+    // solve is reported (nlsp_solve_report.onepass_drift); above the tolerance
+    // the host re-runs the solve on the folded cycle (run_pcg).
+    if (!first) {
+        __shared__ double dred[2][32];
+        double d = 0.0, um = 0.0;
+        for (int j = threadIdx.x; j < k; j += blockDim.x) {
+            const double u = __ldcg(a.ow + ucur + j);
+            d = fmax(d, fabs(__ldcg(a.ow + 3 * ld + j) - u));
+            um = fmax(um, fabs(u));
+        }
+        for (int o = 16; o; o >>= 1) {
+            d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+            um = fmax(um, __shfl_xor_sync(0xffffffffu, um, o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            dred[0][warp] = d;
+            dred[1][warp] = um;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+                d = fmax(d, dred[0][w]);
+                um = fmax(um, dred[1][w]);
+            }
+            const double drift = um > 0.0 ? d / um : 0.0;
+            st->drift_max = fmax(st->drift_max, drift);
+        }
+    }
     for (int j = threadIdx.x; j < k; j += blockDim.x) {
         const double u = __ldcg(a.ow + ucur + j);
         double g = __ldcg(a.ow + 2 * ld + j) + gs[j];  // v + M e
         if (!first) g = fma(beta, (__ldcg(a.ow + uprev + j) - u) / alpha_prev, g);  // + beta W^T q_{i-1}
-        cs[j] = fma(-alpha, g, u);                     // c = u - alpha g
+        const double c = fma(-alpha, g, u);            // c = u - alpha g
+        cs[j] = c;
+        a.ow[3 * ld + j] = c;  // compared with the direct u_{i+1} next iteration
     }
     __syncthreads();
     if (a.Ainv) coarse_apply_inverse(a.Ainv, k, cs, a.e);
@@ -2085,6 +2119,8 @@ struct OpUpdSweep {
     }
     __device__ __forceinline__ void finish(PcgState*, const double*) const {}
 };
+
+#include "march.cuh"
 
 // ======================================================== host launchers ==
 
@@ -2268,6 +2304,113 @@ void launch_dia_op(const LaunchCtx& c, const SolveArgs& a, const Op& op) {
 #undef NLSP_DIA_GO
 }
 
+// ---- plane-march kernels (march.cuh) --------------------------------------
+// NLSP_MARCH: 0 never, 1 whenever the diagonal form has a plane geometry,
+// default (auto) from n >= 2^18 rows (smaller systems keep the direct kernels,
+// whose grid-wide sums are bitwise those of the CSR path).
+static int march_mode() {
+    static const int m = [] {
+        const char* e = std::getenv("NLSP_MARCH");
+        return e ? std::atoi(e) : 2;
+    }();
+    return m;
+}
+constexpr unsigned kMarchBudget = 200 * 1024;
+constexpr int kMarchMinRing = 6;
+
+struct MarchPlan {
+    MarchGeom g;
+    size_t smem;
+};
+
+// Slab width C (a divisor of the plane P): the widest whose ring slot lets
+// kMarchMinRing planes in flight, and at most n / (SMs x 16) rows so every CTA
+// marches >= 16 plane-steps (the march's two halo planes amortised).
+static bool march_plan(const LaunchCtx& c, const SolveArgs& a, int nh, int no, MarchPlan* out) {
+    const int mode = march_mode();
+    if (mode == 0 || !a.dia.kind || a.dia.plane <= 0) return false;
+    if (mode == 2 && a.n < (1 << 18)) return false;
+    const long long P = a.dia.plane, n = a.n;
+    const int h = a.dia.halo, mb = a.dia.mbytes;
+    const long long cmax = std::max<long long>(16, n / ((long long)c.num_sms * 16));
+    for (long long k = 1; k <= P; ++k) {
+        if (P % k) continue;
+        const long long C = P / k;
+        if (C > cmax) continue;
+        const unsigned hcap = (unsigned)((((C + 2 * h) * 8 + 15) & ~15ll) + 32);
+        const unsigned ocap = (unsigned)(((C * 8 + 15) & ~15ll) + 32);
+        const unsigned mcap = (unsigned)(((C * mb + 15) & ~15ll) + 32);
+        const unsigned slot = nh * hcap + no * ocap + mcap;
+        const int R = (int)std::min<unsigned>(12, kMarchBudget / slot);
+        if (R < kMarchMinRing) continue;
+        MarchGeom g{};
+        g.P = P;
+        g.h = h;
+        g.C = (int)C;
+        g.S = (int)(P / C);
+        g.Z = (int)(n / P);
+        g.R = R;
+        g.slot = slot;
+        g.hcap = hcap;
+        g.ocap = ocap;
+        g.mcap = mcap;
+        out->g = g;
+        out->smem = 256 + (size_t)R * slot;
+        return true;
+    }
+    return false;
+}
+
+// whether spmv_p runs as a plane march on this matrix (nlsp_csr_geometry)
+bool march_planned(const LaunchCtx& c, const SolveArgs& a) {
+    MarchPlan pl;
+    return march_plan(c, a, MOpSpmvP::NH, MOpSpmvP::NO + (a.dia.kind == 2 ? a.dia.d : 0), &pl);
+}
+
+template <class Op>
+static bool launch_march_op(const LaunchCtx& c, const SolveArgs& a, const Op& op) {
+    const bool rv = a.dia.kind == 2;
+    MarchPlan pl;
+    if (!march_plan(c, a, Op::NH, Op::NO + (rv ? a.dia.d : 0), &pl)) return false;
+    if (Op::NH + Op::NO + (rv ? a.dia.d : 0) > kMarchMaxArrays) return false;
+    auto go = [&](auto kern) {
+        static std::mutex mu;
+        static std::unordered_map<unsigned long long, int> occ;
+        int nb = 1;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            const unsigned long long key = reinterpret_cast<unsigned long long>(reinterpret_cast<const void*>(kern)) *
+                                               1315423911ull ^ pl.smem;
+            auto it = occ.find(key);
+            if (it == occ.end()) {
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+                if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kMarchThreads, pl.smem) != cudaSuccess ||
+                    nb < 1)
+                    nb = 1;
+                cudaGetLastError();
+                occ[key] = nb;
+            } else {
+                nb = it->second;
+            }
+        }
+        long long g = (long long)c.num_sms * nb;
+        const long long T = (long long)pl.g.S * pl.g.Z;
+        if (g > T) g = T;
+        if (g > kMaxGrid) g = kMaxGrid;
+        klaunch(c, kern, (int)g, kMarchThreads, pl.smem, a, op, pl.g);
+    };
+#define NLSP_MARCH_GO(D, MT, EX) \
+    do { if (rv) go(k_march<Op, D, MT, true, EX>); else go(k_march<Op, D, MT, false, EX>); } while (0)
+    if (a.dia.d == 5) NLSP_MARCH_GO(5, unsigned char, true);
+    else if (a.dia.d == 7) NLSP_MARCH_GO(7, unsigned char, true);
+    else if (a.dia.d == 9) NLSP_MARCH_GO(9, unsigned short, true);
+    else if (a.dia.d <= 8) NLSP_MARCH_GO(8, unsigned char, false);
+    else if (a.dia.d <= 16 && !rv) go(k_march<Op, 16, unsigned short, false, false>);
+    else return false;
+#undef NLSP_MARCH_GO
+    return true;
+}
+
 // Staged tiles must fit in shared memory (227 KB per CTA); matrices with very
 // long rows (a tile's nonzeros beyond the budget) take the direct-load kernels.
 constexpr size_t kStageBudget = 200 * 1024;
@@ -2275,7 +2418,8 @@ bool spmv_tma_ok(const SolveArgs& a) { return NLSP_TMA && spmv_stage_smem(a) <= 
 bool restrict_tma_ok(const SolveArgs& a) { return NLSP_TMA && restrict_stage_smem(a) <= kStageBudget; }
 
 void launch_spmv_p(const LaunchCtx& c, const SolveArgs& a) {
-    if (a.dia.kind) launch_dia_op<1>(c, a, OpSpmvP{});
+    if (a.dia.kind && launch_march_op(c, a, MOpSpmvP{})) {
+    } else if (a.dia.kind) launch_dia_op<1>(c, a, OpSpmvP{});
     else if (spmv_tma_ok(a)) launch_spmv_op<1>(c, a, OpSpmvP{});
     else launch_rows<kU>(c, k_spmv_p, a.n, a);
     count(c);
@@ -2656,7 +2800,9 @@ bool update_sweep_ok(const SolveArgs& a, unsigned long long T) {
 // r' = r[(it + 1) & 1]
 static void launch_sweep_rpar(const LaunchCtx& c, const SolveArgs& a, const double* zin, double* zout) {
     const GPlain gp{zin};
-    if (a.dia.kind && a.wdc != 0.0)
+    if (a.dia.kind && a.wdc != 0.0 && launch_march_op(c, a, MOpSweep<true>{zin, nullptr, a.wd, zout, a.wdc})) {
+    } else if (a.dia.kind && a.wdc == 0.0 && launch_march_op(c, a, MOpSweep<false>{zin, nullptr, a.wd, zout, 0.0})) {
+    } else if (a.dia.kind && a.wdc != 0.0)
         launch_dia_op<1>(c, a, OpSweep<GPlain, false, true>{gp, a.r, a.wd, zout, a.wdc, true});
     else if (a.dia.kind)
         launch_dia_op<1>(c, a, OpSweep<GPlain, false>{gp, a.r, a.wd, zout, 0.0, true});
@@ -2672,7 +2818,9 @@ void launch_sweeps_rpar(const LaunchCtx& c, const SolveArgs& a, unsigned long lo
     }
 }
 void launch_update_sweep(const LaunchCtx& c, const SolveArgs& a) {
-    if (a.dia.kind && a.wdc != 0.0) launch_dia_op<1>(c, a, OpUpdSweep<true>{});
+    if (a.dia.kind && a.wdc != 0.0 && launch_march_op(c, a, MOpUpdSweep<true>{})) {
+    } else if (a.dia.kind && a.wdc == 0.0 && launch_march_op(c, a, MOpUpdSweep<false>{})) {
+    } else if (a.dia.kind && a.wdc != 0.0) launch_dia_op<1>(c, a, OpUpdSweep<true>{});
     else if (a.dia.kind) launch_dia_op<1>(c, a, OpUpdSweep<false>{});
     else launch_spmv_op<1>(c, a, OpUpdSweep<false>{});
     count(c);

@@ -243,6 +243,14 @@ class DeviceCsr:
         _check(self.ctx, L.gpu_lib().nlsp_csr_format(self.handle, C.byref(kind), C.byref(offs), C.byref(pb)))
         return int(kind.value), int(offs.value), int(pb.value)
 
+    def geometry(self):
+        """(plane, halo, march) of nlsp_csr_geometry: the structured-grid
+        geometry of the diagonal form and whether the loop runs plane marches."""
+        pl, h, mr = C.c_uint64(0), C.c_int32(0), C.c_int32(0)
+        _check(self.ctx, L.gpu_lib().nlsp_csr_geometry(self.ctx.handle, self.handle, C.byref(pl), C.byref(h),
+                                                       C.byref(mr)))
+        return int(pl.value), int(h.value), bool(mr.value)
+
     def __del__(self):
         try:
             if self.handle:
@@ -522,6 +530,8 @@ class SolveReport:
     method: str = ""
     coarse_dim: int = 0
     kernel_launches: int = 0
+    onepass_drift: float = 0.0   # one-pass guard: max |c_rec - W^T r| / |W^T r|
+    cycle_fallback: bool = False  # the solve was re-run on the folded cycle
 
 
 @dataclass
@@ -559,6 +569,7 @@ def pcg(a: SparseCsrMatrix, b, m, delta: float, max_iters: int) -> PcgResult:
                     true_relative_residual=float(rep.true_relative_residual),
                     solve_ms=float(rep.solve_ms), total_ms=float(rep.total_ms),
                     coarse_dim=int(rep.coarse_dim), kernel_launches=int(rep.kernel_launches),
+                    onepass_drift=float(rep.onepass_drift), cycle_fallback=bool(rep.cycle_fallback),
                     method={0: "plain", 1: "jacobi", 2: "two_level"}[kind])
     return PcgResult(x, r)
 

@@ -129,6 +129,8 @@ def test_full_size_matches_reference(nlsp, name):
         rows = d["rows"]
         assert np.linalg.norm(x[rows] - d["x_rows"]) <= 1e-9 * np.linalg.norm(d["x_rows"])
     print(f"{name}: iterations {rep.iterations} (ref {it_ref}), x err {xerr:.2e}, history dev "
-          f"{hist_dev.max():.2e}, P rows {er.max():.2e} sketch {es.max():.2e}, A_c {ea:.2e}")
+          f"{hist_dev.max():.2e}, P rows {er.max():.2e} sketch {es.max():.2e}, A_c {ea:.2e}, "
+          f"one-pass drift {rep.onepass_drift:.2e}")
+    assert rep.onepass_drift <= 1e-10 and not rep.cycle_fallback
     assert xerr <= 1e-9, xerr
     assert hist_dev.max() <= 1e-6, hist_dev.max()

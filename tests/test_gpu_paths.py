@@ -31,6 +31,7 @@ np.save({out!r}, r.solution)
 print(json.dumps({{"iterations": r.report.iterations, "launches": r.report.kernel_launches,
                    "true": r.report.true_relative_residual, "hist_len": len(r.report.residual_history),
                    "repeat_equal": bool(np.array_equal(r.solution, r2.solution)),
+                   "fallback": bool(r.report.cycle_fallback), "drift": r.report.onepass_drift,
                    "last": float(r.report.residual_history[-1])}}))
 """
 
@@ -53,6 +54,12 @@ PATHS = {
     "graph_seg": {"NLSP_CLUSTER": "0", "NLSP_HIST_CHUNK": "16"},
     "host_seg": {"NLSP_CLUSTER": "0", "NLSP_LOOP": "host", "NLSP_HIST_CHUNK": "16"},
     "cluster_seg": {"NLSP_CLUSTER": "1", "NLSP_HIST_CHUNK": "16"},
+    # the one-pass guard's fallback forced (any drift passes a negative
+    # tolerance): the solve is re-run on the folded cycle
+    "drift_fallback": {"NLSP_CLUSTER": "0", "NLSP_DRIFT_TOL": "-1"},
+    # the plane-march kernels of the structured grids (march.cuh), forced at
+    # these small sizes (tiny slabs, one- and two-plane marches, clamped halos)
+    "march": {"NLSP_CLUSTER": "0", "NLSP_MARCH": "1"},
 }
 
 
@@ -83,6 +90,14 @@ def test_execution_paths_match_reference(tmp_path, case):
     # the diagonal form sums every row in CSR column order: bitwise the CSR path
     assert res["graph"][0]["iterations"] == res["graph_csr"][0]["iterations"]
     assert np.array_equal(res["graph"][1], res["graph_csr"][1])
+    # the plane-march gather kernels (forced at this size): the same rows, the
+    # dot products summed in another order
+    assert abs(res["march"][0]["iterations"] - res["graph"][0]["iterations"]) <= 1
+    assert np.linalg.norm(res["march"][1] - res["graph"][1]) <= 1e-10 * np.linalg.norm(res["graph"][1])
+    # the forced guard fallback gives exactly the folded cycle's solve
+    assert res["drift_fallback"][0]["fallback"] and not res["graph"][0]["fallback"]
+    assert res["drift_fallback"][0]["iterations"] == res["folded"][0]["iterations"]
+    assert np.array_equal(res["drift_fallback"][1], res["folded"][1])
     # pausing at history-segment ends changes nothing but the launch count
     for p in ("graph_seg", "host_seg", "cluster_seg"):
         assert res[p][0]["iterations"] == res["graph"][0]["iterations"], p
@@ -108,6 +123,57 @@ def test_detected_matrix_form(nlsp, case):
         mb = 1 if offsets <= 8 else (2 if offsets <= 16 else 4)
         assert pass_bytes == n * (mb + (8 * offsets if kind == 2 else 0))
         assert pass_bytes < 12 * nnz + 4 * (n + 1)
+    # structured-grid geometry (march.cuh): 2D grids plane = nx, halo 1; 3D
+    # plane = nx ny, halo nx; small systems keep the direct kernels
+    plane, halo, march = a.device().geometry()
+    side = {"c1_default": 64, "scaled_C2": 48, "scaled_C3": 40, "scaled_C4": 14}.get(case)
+    if case == "scaled_C4":
+        assert (plane, halo) == (side * side, side)
+    elif side:
+        assert (plane, halo) == (side, 1)
+    else:
+        assert plane == 0
+    assert not march
+
+
+MARCH_SCRIPT = r"""
+import sys, json, numpy as np
+sys.path.insert(0, {root!r})
+from paper_2601_20174_b200 import nlsp, problems
+c = problems.CONFIGS[{cfg!r}].scaled(nx={nx})
+pb = problems.generate(c)
+a = pb.csr()
+sv = nlsp.generate_smoothed_vectors(a, None, c.m, c.s1, c.omega, c.s0_seed)
+p, _, _ = nlsp.svd_basis(sv.s, c.k)
+m = nlsp.TwoLevelPreconditioner(a, p, c.omega, c.nu1, c.nu2)
+r = nlsp.pcg(a, pb.rhs, m, c.delta, 10 * pb.n)
+r2 = nlsp.pcg(a, pb.rhs, m, c.delta, 10 * pb.n)
+np.save({out!r}, r.solution)
+print(json.dumps({{"iterations": r.report.iterations, "geometry": a.device().geometry(),
+                   "repeat_equal": bool(np.array_equal(r.solution, r2.solution)),
+                   "true": r.report.true_relative_residual}}))
+"""
+
+
+@pytest.mark.parametrize("cfg,nx", [("C2", 512), ("C3", 512), ("C4", 64)])
+def test_march_matches_direct_kernels(tmp_path, cfg, nx):
+    """The plane-march gather kernels against the direct ones on the same
+    mid-size system (n = 262 144): same iteration count, solutions within
+    rounding, both deterministic."""
+    res = {}
+    for mode in ("0", "1"):
+        out = str(tmp_path / f"x_{mode}.npy")
+        code = MARCH_SCRIPT.format(root=ROOT, cfg=cfg, nx=nx, out=out)
+        p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                           env=dict(os.environ, NLSP_MARCH=mode))
+        assert p.returncode == 0, p.stderr[-3000:]
+        res[mode] = (json.loads(p.stdout.strip().splitlines()[-1]), np.load(out))
+    (i0, x0), (i1, x1) = res["0"], res["1"]
+    assert i1["geometry"][2] and not i0["geometry"][2]
+    assert i0["repeat_equal"] and i1["repeat_equal"]
+    assert abs(i0["iterations"] - i1["iterations"]) <= 1
+    assert np.linalg.norm(x1 - x0) <= 1e-10 * np.linalg.norm(x0)
+    assert i1["true"] < 1e-7
 
 
 @pytest.fixture(scope="module")
@@ -224,14 +290,19 @@ def test_pcg_batch_matches_reference(nlsp):
     assert np.array_equal(res[0].solution, res[-1].solution)
 
 
-@pytest.mark.parametrize("cfg,nx", [("C2", 512), ("C3", 512), ("C4", 64), ("C5", 256)])
-def test_onepass_cycle_matches_folded_midsize(nlsp, cfg, nx):
+HARD = {"none": {}, "aniso_1e-4": {"epsilon": 1e-4}, "contrast_1e6": {"young_hi": 1e6}}
+
+
+@pytest.mark.parametrize("cfg,nx,hard", [("C2", 512, "none"), ("C3", 512, "none"), ("C4", 64, "none"),
+                                         ("C5", 256, "none"), ("C3", 512, "aniso_1e-4"),
+                                         ("C5", 256, "contrast_1e6")])
+def test_onepass_cycle_matches_folded_midsize(nlsp, cfg, nx, hard):
     """The one-pass cycle (W streamed once per iteration, the restriction by
     its recurrence) against the folded cycle on the same system,
     at sizes where every CTA cycles its stage ring many times: same iteration
     count, solutions within rounding, both below the tolerance."""
     from paper_2601_20174_b200 import problems
-    c = problems.CONFIGS[cfg].scaled(nx=nx)
+    c = problems.CONFIGS[cfg].scaled(nx=nx, **HARD[hard])
     pb = problems.generate(c)
     a = pb.csr()
     assert pb.n > 65536  # beyond the single-cluster solver: the multi-kernel graph loop
@@ -250,6 +321,11 @@ def test_onepass_cycle_matches_folded_midsize(nlsp, cfg, nx):
     assert abs(r1.report.iterations - r2.report.iterations) <= 1
     assert r1.report.true_relative_residual < 10 * c.delta
     assert np.linalg.norm(r1.solution - r2.solution) <= 1e-10 * np.linalg.norm(r2.solution)
+    # the recurrence guard: measured every iteration, well under its 1e-10
+    # tolerance, so no fallback; the folded cycle has no recurrence
+    print(f"{cfg}/{hard}: {r1.report.iterations} iterations, one-pass drift {r1.report.onepass_drift:.2e}")
+    assert 0.0 < r1.report.onepass_drift <= 1e-10 and not r1.report.cycle_fallback
+    assert r2.report.onepass_drift == 0.0
     # deterministic: a second solve is bitwise the first
     r3 = nlsp.pcg(a, pb.rhs, m1, c.delta, 10 * pb.n)
     assert np.array_equal(r1.solution, r3.solution)
