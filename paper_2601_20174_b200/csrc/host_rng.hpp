@@ -48,11 +48,18 @@ private:
     bool has_cached_ = false;
 };
 
-inline void normal_stream(std::uint64_t seed, std::uint64_t count, double* out) {
+// The normal stream of Rng(seed).normal() x count, produced chunk by chunk:
+// sink.buffer(base, np) gives the destination of pairs [base, base + np) (2 np
+// doubles, the last one dropped when count is odd and the chunk is last), and
+// sink.done(base, np) is called once they are written — in order, from this
+// thread — so a caller can ship each chunk (e.g. to the device) while the
+// next one is generated.
+template <class Sink>
+inline void normal_stream_chunks(std::uint64_t seed, std::uint64_t count, Sink& sink,
+                                 std::uint64_t chunk = 1ull << 22) {
     std::mt19937_64 gen(seed);
     auto uni = [&]() { return static_cast<double>(gen() >> 11) * 0x1.0p-53; };
     const std::uint64_t pairs_total = (count + 1) / 2;
-    const std::uint64_t chunk = 1ull << 22;
     const std::uint64_t cap = std::min(chunk, pairs_total);
     // the sequential uniform stream of chunk c + 1 is drawn while the worker
     // threads run the Box-Muller transforms of chunk c (double-buffered); the
@@ -69,13 +76,13 @@ inline void normal_stream(std::uint64_t seed, std::uint64_t count, double* out) 
             u2[buf][p] = b;
         }
     };
-    auto transform = [&](std::uint64_t base, int buf, std::uint64_t lo, std::uint64_t hi) {
+    auto transform = [&](double* out, std::uint64_t base, int buf, std::uint64_t lo, std::uint64_t hi) {
         for (std::uint64_t p = lo; p < hi; ++p) {
             const double r = std::sqrt(-2.0 * std::log(u1[buf][p]));
             const double a = 2.0 * 3.141592653589793 * u2[buf][p];
-            const std::uint64_t o = 2 * (base + p);
+            const std::uint64_t o = 2 * p;
             out[o] = r * std::cos(a);
-            if (o + 1 < count) out[o + 1] = r * std::sin(a);
+            if (2 * (base + p) + 1 < count) out[o + 1] = r * std::sin(a);
         }
     };
     if (pairs_total == 0) return;
@@ -85,8 +92,9 @@ inline void normal_stream(std::uint64_t seed, std::uint64_t count, double* out) 
     for (std::uint64_t base = 0; base < pairs_total;) {
         const std::uint64_t next = base + np;
         const std::uint64_t np_next = next < pairs_total ? std::min(chunk, pairs_total - next) : 0;
+        double* out = sink.buffer(base, np);
         if (np < 65536 || hw == 1) {
-            transform(base, buf, 0, np);
+            transform(out, base, buf, 0, np);
             if (np_next) draw(np_next, buf ^ 1);
         } else {
             std::vector<std::thread> th;
@@ -94,15 +102,35 @@ inline void normal_stream(std::uint64_t seed, std::uint64_t count, double* out) 
             const std::uint64_t per = (np + workers - 1) / workers;
             for (unsigned t = 0; t < workers; ++t) {
                 const std::uint64_t lo = t * per, hi = std::min(np, lo + per);
-                if (lo < hi) th.emplace_back(transform, base, buf, lo, hi);
+                if (lo < hi) th.emplace_back(transform, out, base, buf, lo, hi);
             }
             if (np_next) draw(np_next, buf ^ 1);
             for (auto& x : th) x.join();
         }
+        sink.done(base, np);
         base = next;
         np = np_next;
         buf ^= 1;
     }
+}
+
+// the whole stream into out (count doubles)
+inline void normal_stream(std::uint64_t seed, std::uint64_t count, double* out) {
+    struct ToArray {
+        double* out;
+        std::uint64_t count;
+        std::vector<double> scratch;  // an odd count's last pair: one value past the end
+        double* buffer(std::uint64_t base, std::uint64_t np) {
+            if (2 * (base + np) <= count) return out + 2 * base;
+            scratch.assign(2 * np, 0.0);
+            return scratch.data();
+        }
+        void done(std::uint64_t base, std::uint64_t np) {
+            if (2 * (base + np) > count)
+                std::copy(scratch.begin(), scratch.begin() + (count - 2 * base), out + 2 * base);
+        }
+    } sink{out, count, {}};
+    normal_stream_chunks(seed, count, sink);
 }
 
 // S^(0) of generate_smoothed_vectors before the sweeps (smoothing.hpp:84-92)

@@ -22,7 +22,7 @@
 // (Included inside namespace nlsp, after the row ops it builds on.)
 #pragma once
 
-constexpr int kMarchConsumers = 8;                       // consumer warps
+constexpr int kMarchConsumers = 10;                      // consumer warps
 constexpr int kMarchThreads = (kMarchConsumers + 1) * 32;  // + 1 producer warp
 constexpr int kMarchMaxArrays = 16;                     // staged arrays per plane (halo + own)
 
@@ -64,6 +64,16 @@ __device__ __forceinline__ unsigned stage_bytes(long long ws, long long we, long
     return (unsigned)(((b * es + 15) & ~15ll) - ((a * es) & ~15ll));
 }
 
+// shared loads by 32-bit address (plain loads: ordered by the barriers' memory
+// clobbers, free to interleave between rows)
+__device__ __forceinline__ double lds_f64(unsigned addr) {
+    return *static_cast<const double*>(__cvta_shared_to_generic(addr));
+}
+template <typename MT>
+__device__ __forceinline__ unsigned lds_mask(unsigned addr) {
+    return *static_cast<const MT*>(__cvta_shared_to_generic(addr));
+}
+
 __device__ __forceinline__ void consumer_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(kMarchConsumers * 32) : "memory");
 }
@@ -73,7 +83,7 @@ __device__ __forceinline__ void consumer_sync() {
 // window element, row(i, y, hc, oc, s) with the centre values of the halo
 // arrays and the own values; NV / TICKET / finish or CTA hooks as the row ops.
 template <class Op, int MAXD, typename MT, bool RV, bool EXACT>
-__global__ void __launch_bounds__(kMarchThreads, 1) k_march(SolveArgs a, Op op, MarchGeom g) {
+__global__ void __launch_bounds__(kMarchThreads, 2) k_march(SolveArgs a, Op op, MarchGeom g) {
     pdl_entry();
     PcgState* st = a.st;
     if (st->done) return;
@@ -177,6 +187,7 @@ __global__ void __launch_bounds__(kMarchThreads, 1) k_march(SolveArgs a, Op op, 
 #pragma unroll
             for (int j = 0; j < NH; ++j) hv[j] = reinterpret_cast<double*>(harea(sp, j) + lead);
             const int W = g.C + 2 * g.h;
+#pragma unroll 4
             for (int x = tid; x < W; x += kMarchConsumers * 32) op.convert(hv, x);
         };
         for (long long t = t0; t < t1;) {
@@ -190,49 +201,50 @@ __global__ void __launch_bounds__(kMarchThreads, 1) k_march(SolveArgs a, Op op, 
                 const long long cz = base + (z - za + 1);
                 convert(cz + 1, z + 1, sl);
                 consumer_sync();
-                unsigned char* sp[3] = {slot_of(cz - 1), slot_of(cz), slot_of(cz + 1)};
+                // 32-bit shared addresses (few live registers: two CTAs per SM)
+                const unsigned sp[3] = {smem_u32(slot_of(cz - 1)), smem_u32(slot_of(cz)), smem_u32(slot_of(cz + 1))};
                 const long long e0 = (long long)z * g.P + (long long)sl * g.C;
                 // window starts of planes z - 1, z, z + 1 differ by P: one lead
                 // per plane (P may be odd in rows)
-                const double* hp[3][NH];
+                unsigned hq[3];
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
                     const long long ws = e0 + (long long)(q - 1) * g.P - g.h;
-                    const unsigned lead = stage_pos(ws, ws, 8);
-#pragma unroll
-                    for (int j = 0; j < NH; ++j)
-                        hp[q][j] = reinterpret_cast<const double*>(harea(sp[q], j) + lead);
+                    hq[q] = sp[q] + stage_pos(ws, ws, 8);
                 }
-                const double* op_[NO > 0 ? NO : 1];
                 const unsigned olead = stage_pos(e0, e0, 8);
-#pragma unroll
-                for (int j = 0; j < NO; ++j) op_[j] = reinterpret_cast<const double*>(oarea(sp[1], j) + olead);
-                const MT* mk = reinterpret_cast<const MT*>(marea(sp[1]) + stage_pos(e0, e0, mb));
-                // the gathered quantity's window position of row c + offset t
-                const double* gp[MAXD];
+                const unsigned ob = sp[1] + NH * g.hcap + olead;
+                const unsigned mk = sp[1] + NH * g.hcap + NO * g.ocap + stage_pos(e0, e0, mb);
+                // the gathered quantity's window position of row 0 + offset t
+                unsigned ga[MAXD];
 #pragma unroll
                 for (int t = 0; t < MAXD; ++t)
-                    gp[t] = (dz[t] < 0 ? hp[0][0] : (dz[t] > 0 ? hp[2][0] : hp[1][0])) + g.h + dd[t];
+                    ga[t] = (dz[t] < 0 ? hq[0] : (dz[t] > 0 ? hq[2] : hq[1])) + 8u * (unsigned)(g.h + dd[t]);
                 const int rows = (int)min((long long)g.C, n - e0);
+                // two rows in flight per thread: their fma chains interleave
+#pragma unroll 2
                 for (int c = tid; c < rows; c += kMarchConsumers * 32) {
-                    const unsigned m = mk[c];
+                    const unsigned m = lds_mask<MT>(mk + (unsigned)c * mb);
+                    const unsigned c8 = 8u * (unsigned)c;
                     double gv[MAXD];
 #pragma unroll
-                    for (int t = 0; t < MAXD; ++t) gv[t] = t < d ? gp[t][c] : 0.0;
+                    for (int t = 0; t < MAXD; ++t) gv[t] = t < d ? lds_f64(ga[t] + c8) : 0.0;
                     double y = 0.0;
                     if (EXACT && m == kFull) {
 #pragma unroll
-                        for (int t = 0; t < MAXD; ++t) y = fma(RV ? op_[Op::NO + t][c] : a.dia.val[t], gv[t], y);
+                        for (int t = 0; t < MAXD; ++t)
+                            y = fma(RV ? lds_f64(ob + (Op::NO + t) * g.ocap + c8) : a.dia.val[t], gv[t], y);
                     } else {
 #pragma unroll
                         for (int t = 0; t < MAXD; ++t)
-                            if (t < d && ((m >> t) & 1u)) y = fma(RV ? op_[Op::NO + t][c] : a.dia.val[t], gv[t], y);
+                            if (t < d && ((m >> t) & 1u))
+                                y = fma(RV ? lds_f64(ob + (Op::NO + t) * g.ocap + c8) : a.dia.val[t], gv[t], y);
                     }
-                    double hc[NH], oc[NO > 0 ? NO : 1];
+                    double hc[NH], oc[Op::NO > 0 ? Op::NO : 1];
 #pragma unroll
-                    for (int j = 0; j < NH; ++j) hc[j] = hp[1][j][c + g.h];
+                    for (int j = 0; j < NH; ++j) hc[j] = lds_f64(hq[1] + j * g.hcap + 8u * (unsigned)g.h + c8);
 #pragma unroll
-                    for (int j = 0; j < Op::NO; ++j) oc[j] = op_[j][c];
+                    for (int j = 0; j < Op::NO; ++j) oc[j] = lds_f64(ob + j * g.ocap + c8);
                     op.row(e0 + c, y, hc, oc, s);
                 }
                 __syncwarp();

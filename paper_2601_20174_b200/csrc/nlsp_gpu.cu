@@ -91,6 +91,7 @@ void launch_col_axpy(const LaunchCtx&, long long, int, const double*, int, doubl
 void launch_col_move(const LaunchCtx&, long long, int, double*, int, double*, const double*, int, long long);
 void launch_transpose(const LaunchCtx&, long long, int, const double*, double*);
 bool march_planned(const LaunchCtx&, const SolveArgs&);
+void launch_s0_scatter(const LaunchCtx&, const double*, long long, long long, int, const int*, double*);
 void launch_sigma(const LaunchCtx&, int, int, const double*, const double*, double*, double*,
                   int*);
 // setup_kernels.cu (SA)
@@ -193,6 +194,10 @@ struct nlsp_ctx {
     std::vector<double> hist_done;
     unsigned long long hist_tail = 0;
     bool last_qr_robust = false;  // the last qr_thin took the shifted CholeskyQR3 path
+    // pinned staging of the host-drawn S^(0) (nlsp_generate_smoothed_vectors):
+    // two chunks of the normal stream in flight to the device
+    double* s0_pin[2] = {nullptr, nullptr};
+    cudaEvent_t s0_ev[2] = {nullptr, nullptr};
     double last_svd_defect = 0.0;  // orthonormality defect of the last svd_basis' U_k before any polish
     int last_svd_solid = 0;        // its columns above the singular-value cutoff
     bool use_graph = true;
@@ -795,6 +800,11 @@ void nlsp_ctx_destroy(nlsp_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->s) cudaStreamSynchronize(ctx->s);
     if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+    if (ctx->gexec_cont) cudaGraphExecDestroy(ctx->gexec_cont);
+    for (int b = 0; b < 2; ++b) {
+        if (ctx->s0_pin[b]) cudaFreeHost(ctx->s0_pin[b]);
+        if (ctx->s0_ev[b]) cudaEventDestroy(ctx->s0_ev[b]);
+    }
     free_ws(ctx);
     dfree(ctx->st);
     dfree(ctx->flags);
@@ -1221,6 +1231,13 @@ nlsp_status nlsp_smooth_vectors(nlsp_ctx* ctx, const nlsp_csr* a, nlsp_dense* s,
     return smooth_impl(ctx, a, s, sweeps, omega);
 }
 
+// S^(0) streams from the host generator to the device chunk by chunk (4 M
+// normal pairs = 64 MB): each chunk is Box-Muller-transformed into one of two
+// pinned staging buffers while the previous one is in flight (cudaMemcpyAsync
+// on ctx->s), so the 4.2 GB upload at C4 hides behind the sequential
+// mt19937_64 draw. Rows under the Dirichlet mask take no values from the
+// stream (smoothing.hpp:84-92): the live rows' chunk is scattered on the
+// device (k_s0_scatter).
 nlsp_status nlsp_generate_smoothed_vectors(nlsp_ctx* ctx, const nlsp_csr* a, const uint8_t* mask,
                                            uint64_t k, uint64_t sweeps, double omega,
                                            uint64_t seed, nlsp_dense** out) {
@@ -1230,11 +1247,78 @@ nlsp_status nlsp_generate_smoothed_vectors(nlsp_ctx* ctx, const nlsp_csr* a, con
     if (st) return st;
     if (!a) return set_err(ctx, NLSP_E_VALIDATION, "generate_smoothed_vectors: null matrix");
     if (k < 1) return set_err(ctx, NLSP_E_VALIDATION, "generate_smoothed_vectors: K must be positive");
-    std::vector<double> s0((size_t)a->n * k);
-    nlsp_host::smoothed_s0(seed, (uint64_t)a->n, k, mask, s0.data());
+    const unsigned long long n = (unsigned long long)a->n;
+    constexpr unsigned long long kChunkPairs = 1ull << 22;
+    for (int b = 0; b < 2; ++b) {
+        if (!ctx->s0_pin[b]) CU(cudaMallocHost(&ctx->s0_pin[b], sizeof(double) * 2 * kChunkPairs));
+        if (!ctx->s0_ev[b]) CU(cudaEventCreateWithFlags(&ctx->s0_ev[b], cudaEventDisableTiming));
+    }
     nlsp_dense* d = nullptr;
-    st = nlsp_dense_upload(ctx, a->n, k, s0.data(), &d);
+    st = dense_alloc(ctx, n, k, &d);
     if (st) return st;
+    std::vector<int> live;
+    unsigned long long nlive = n;
+    if (mask) {
+        for (unsigned long long i = 0; i < n; ++i)
+            if (!mask[i]) live.push_back((int)i);
+        nlive = live.size();
+    }
+    int* dlive = nullptr;
+    double* dstage[2] = {nullptr, nullptr};
+    auto cleanup = [&]() {
+        sfree(ctx, dlive);
+        sfree(ctx, dstage[0]);
+        sfree(ctx, dstage[1]);
+    };
+    cudaError_t e = cudaSuccess;
+    if (mask) {
+        if ((e = cudaMemsetAsync(d->d, 0, sizeof(double) * n * k, ctx->s)) ||
+            (e = salloc(ctx, &dlive, (size_t)std::max<unsigned long long>(nlive, 1))) ||
+            (nlive && (e = cudaMemcpyAsync(dlive, live.data(), sizeof(int) * nlive, cudaMemcpyHostToDevice, ctx->s))) ||
+            (e = salloc(ctx, &dstage[0], 2 * kChunkPairs)) || (e = salloc(ctx, &dstage[1], 2 * kChunkPairs))) {
+            cleanup();
+            nlsp_dense_destroy(d);
+            return cuda_fail(ctx, e, "generate_smoothed_vectors alloc");
+        }
+    }
+    struct DeviceSink {
+        nlsp_ctx* ctx;
+        double* dst;
+        int* live;
+        double* const* stage;
+        unsigned long long count, m;
+        int cur = 0;
+        bool used[2] = {false, false};
+        cudaError_t err = cudaSuccess;
+        double* buffer(unsigned long long, unsigned long long) {
+            if (used[cur] && !err) err = cudaEventSynchronize(ctx->s0_ev[cur]);
+            return ctx->s0_pin[cur];
+        }
+        void done(unsigned long long base, unsigned long long np) {
+            const unsigned long long e0 = 2 * base, cnt = std::min(2 * np, count - e0);
+            if (!err) {
+                if (!live) {
+                    err = cudaMemcpyAsync(dst + e0, ctx->s0_pin[cur], sizeof(double) * cnt, cudaMemcpyHostToDevice,
+                                          ctx->s);
+                } else {
+                    err = cudaMemcpyAsync(stage[cur], ctx->s0_pin[cur], sizeof(double) * cnt, cudaMemcpyHostToDevice,
+                                          ctx->s);
+                    if (!err) launch_s0_scatter(ctx->lc, stage[cur], (long long)e0, (long long)cnt, (int)m, live, dst);
+                }
+            }
+            if (!err) err = cudaEventRecord(ctx->s0_ev[cur], ctx->s);
+            used[cur] = true;
+            cur ^= 1;
+        }
+    } sink{ctx, d->d, mask ? dlive : nullptr, dstage, nlive * k, k};
+    nlsp_host::normal_stream_chunks(nlsp_host::mix_seed(seed, 0x736d6f6f), nlive * k, sink, kChunkPairs);
+    e = sink.err;
+    if (!e) e = cudaStreamSynchronize(ctx->s);  // the staging buffers are reused by the next call
+    cleanup();
+    if (e) {
+        nlsp_dense_destroy(d);
+        return cuda_fail(ctx, e, "generate_smoothed_vectors upload");
+    }
     st = smooth_impl(ctx, a, d, sweeps, omega);
     if (st) {
         nlsp_dense_destroy(d);

@@ -16,6 +16,8 @@
 // Rounding differs from the reference's sequential sums only in summation
 // order (fp64 products, fp64 accumulation); the parity tests bound P, sigma
 // and A_c against the reference at 1e-10 / 1e-12.
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace nlsp {
@@ -120,12 +122,100 @@ __global__ void __launch_bounds__(256) k_gram_dmma(long long rows, int bi, int b
         }
 }
 
+// The symmetric Gram X^T X (svd_oracle's S^T S, the CholeskyQR Grams): only the
+// 8x8 blocks on and above the diagonal are computed — NB (NB + 1) / 2 of the
+// NB^2 — and mirrored on the way out. Warp w < NB/2 owns block rows w and
+// NB - 1 - w, NB + 1 blocks each (balanced). NB = bi / 8 rounded up (12 or 16).
+template <int NB>
+__global__ void __launch_bounds__(256) k_gram_dmma_sym(long long rows, int bi, int lda, const double* __restrict__ X,
+                                                       double* __restrict__ part) {
+    constexpr int TM = NB * 8, RB = 16, LX = TM + 4;
+    extern __shared__ __align__(16) double sm[];
+    double* xs = sm;  // [2][RB][LX]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long tiles = (rows + RB - 1) / RB;
+    auto load = [&](long long tile, int stg) {
+        const long long r0 = tile * RB;
+        for (int idx = tid; idx < RB * TM; idx += 256) {
+            const int r = idx / TM, c = idx - r * TM;
+            const long long row = r0 + r;
+            const bool ok = row < rows && c < bi;
+            cp8(xs + stg * RB * LX + r * LX + c, ok ? X + row * lda + c : X, ok);
+        }
+        cp_commit();
+    };
+    const bool active = warp < NB / 2;
+    const int ra = warp, rb = NB - 1 - warp;  // this warp's two block rows
+    double acc0[NB][2], acc1[NB][2];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) acc0[c][0] = acc0[c][1] = acc1[c][0] = acc1[c][1] = 0.0;
+    long long tile = blockIdx.x;
+    if (tile < tiles) load(tile, 0);
+    for (int i = 0; tile < tiles; tile += gridDim.x, ++i) {
+        const int stg = i & 1;
+        const bool more = tile + gridDim.x < tiles;
+        if (more) load(tile + gridDim.x, stg ^ 1);
+        if (more) cp_wait<1>();
+        else cp_wait<0>();
+        __syncthreads();
+        if (active) {
+            const double* xb = xs + stg * RB * LX + (lane & 3) * LX + (lane >> 2);
+#pragma unroll
+            for (int kk = 0; kk < RB; kk += 4) {
+                double f[NB];
+#pragma unroll
+                for (int c = 0; c < NB; ++c) f[c] = c >= ra ? xb[kk * LX + c * 8] : 0.0;
+                const double fa = xb[kk * LX + ra * 8], fb = xb[kk * LX + rb * 8];
+#pragma unroll
+                for (int c = 0; c < NB; ++c) {
+                    if (c >= ra) dmma(acc0[c][0], acc0[c][1], fa, f[c]);
+                    if (c >= rb) dmma(acc1[c][0], acc1[c][1], fb, f[c]);
+                }
+            }
+        }
+        __syncthreads();  // this stage is refilled next-but-one iteration
+    }
+    if (!active) return;
+    double* out = part + (long long)blockIdx.x * bi * bi;
+    auto put = [&](int br, int c, const double (&acc)[NB][2]) {
+        const int row = br * 8 + (lane >> 2);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int col = c * 8 + 2 * (lane & 3) + h;
+            if (row < bi && col < bi) {
+                out[row * bi + col] = acc[c][h];
+                if (c != br) out[col * bi + row] = acc[c][h];  // the mirrored block
+            }
+        }
+    };
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+        if (c >= ra) put(ra, c, acc0);
+        if (c >= rb) put(rb, c, acc1);
+    }
+}
+
 // Tile configuration covering a bi x bj block (<= 128 x 128); returns false
 // when the block is larger.
 bool launch_gram_dmma(cudaStream_t s, int g, long long rows, int bi, int bj, int lda, int ldb,
                       const double* X, const double* Y, double* part) {
     const bool same = X == Y && bi == bj && lda == ldb;
     const int w = bi > bj ? bi : bj;
+    static const bool sym_on = !(std::getenv("NLSP_GRAM_SYM") && std::atoi(std::getenv("NLSP_GRAM_SYM")) == 0);
+    if (same && sym_on && bi > 64) {
+        // symmetric: half the DMMA blocks (k_gram_dmma_sym)
+        const int nb = (bi + 7) / 8;
+        if (nb <= 12) {
+            const size_t smem = 2 * 16 * (12 * 8 + 4) * 8;
+            cudaFuncSetAttribute(k_gram_dmma_sym<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_gram_dmma_sym<12><<<g, 256, smem, s>>>(rows, bi, lda, X, part);
+        } else {
+            const size_t smem = 2 * 16 * (16 * 8 + 4) * 8;
+            cudaFuncSetAttribute(k_gram_dmma_sym<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_gram_dmma_sym<16><<<g, 256, smem, s>>>(rows, bi, lda, X, part);
+        }
+        return true;
+    }
 #define NLSP_GD(WM, WN)                                                                           \
     do {                                                                                          \
         constexpr int TM = 4 * (WM) * 8, TN = 2 * (WN) * 8;                                       \

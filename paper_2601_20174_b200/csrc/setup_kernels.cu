@@ -117,10 +117,26 @@ __global__ void __launch_bounds__(256) k_block_sweep(int n, const int* __restric
 // loaded at once (clamped rows, no column-index load in front of them), then
 // each output entry accumulates the present offsets in ascending order (= the
 // CSR column order): bitwise the CSR kernel's result.
-template <int D, int T, int MODE>
+// HINT: S (the block being swept) is read with an L2 evict_last policy and the
+// output written with evict-first (st.global.cs): a row of S is read again
+// +-P rows (26 MB of S at C4) after its first use, and the streaming output
+// would otherwise push it out of L2 in between (2.2x S read from DRAM).
+__device__ __forceinline__ unsigned long long l2_keep_policy() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double ld_keep(const double* a, unsigned long long pol) {
+    double v;
+    asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+    return v;
+}
+
+template <int D, int T, int MODE, bool HINT>
 __global__ void __launch_bounds__(256) k_block_sweep_dia(int n, DiaArgs dia, const double* __restrict__ wd,
                                                          int m, const double* __restrict__ in,
                                                          double* __restrict__ out) {
+    const unsigned long long pol = HINT ? l2_keep_policy() : 0ull;
     const int lane = threadIdx.x & 31;
     const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
@@ -140,7 +156,7 @@ __global__ void __launch_bounds__(256) k_block_sweep_dia(int n, DiaArgs dia, con
 #pragma unroll
                 for (int u = 0; u < T; ++u) {
                     const int j = c0 + lane + 32 * u;
-                    xv[t][u] = j < m ? xr[j] : 0.0;
+                    xv[t][u] = j < m ? (HINT ? ld_keep(xr + j, pol) : xr[j]) : 0.0;
                 }
             }
             double acc[T];
@@ -157,8 +173,9 @@ __global__ void __launch_bounds__(256) k_block_sweep_dia(int n, DiaArgs dia, con
                 const int j = c0 + lane + 32 * u;
                 if (j < m) {
                     const long long o = row * m + j;
-                    if (MODE == 0) out[o] = fma(wd[row], 0.0 - acc[u], in[o]);
-                    else out[o] = acc[u];
+                    const double r = MODE == 0 ? fma(wd[row], 0.0 - acc[u], in[o]) : acc[u];
+                    if (HINT) __stcs(out + o, r);
+                    else out[o] = r;
                 }
             }
         }
@@ -820,6 +837,16 @@ __global__ void k_symmetrize(int k, double* C) {
     }
 }
 
+// S^(0) of a masked system: the stream's elements [e0, e0 + cnt) over the live
+// rows (row live[e / m], column e % m) into S (generate_smoothed_vectors)
+__global__ void k_s0_scatter(const double* __restrict__ src, long long e0, long long cnt, int m,
+                             const int* __restrict__ live, double* __restrict__ S) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < cnt; t += (long long)gridDim.x * blockDim.x) {
+        const long long e = e0 + t;
+        S[(long long)live[e / m] * m + e % m] = src[t];
+    }
+}
+
 // G += shift I (shifted CholeskyQR, nlsp_gpu.cu qr_thin_dev)
 __global__ void k_shift_diag(int k, double* G, double shift) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x)
@@ -956,6 +983,9 @@ void launch_block_op(const LaunchCtx& c, int mode, int n, const int* rp, const i
 bool launch_block_op_dia(const LaunchCtx& c, int mode, int n, const DiaArgs& dia, const double* wd, int m,
                          const double* in, double* out) {
     static const bool on = !(std::getenv("NLSP_BSWEEP_DIA") && std::atoi(std::getenv("NLSP_BSWEEP_DIA")) == 0);
+    // measured at C4: 26.8 -> 38.4 ms for the 10 sweeps with the hints, so
+    // they stay off unless NLSP_BSWEEP_HINT=1
+    static const bool hint = std::getenv("NLSP_BSWEEP_HINT") && std::atoi(std::getenv("NLSP_BSWEEP_HINT")) == 1;
     // measured: faster than the CSR kernel for constant coefficients and wide
     // blocks (C4 smoothing, m = 128: 3.66 -> 2.68 ms per sweep; C3, m = 96:
     // -10 %), slower for per-row values (C2 +57 %) and m <= 64 (the builds, +9 %)
@@ -963,8 +993,9 @@ bool launch_block_op_dia(const LaunchCtx& c, int mode, int n, const DiaArgs& dia
     const int g = grid_for(c, (long long)n * 32, 256, 8);
 #define NLSP_BD(D, T)                                                                                   \
     do {                                                                                                \
-        if (mode == 0) k_block_sweep_dia<D, T, 0><<<g, 256, 0, c.s>>>(n, dia, wd, m, in, out);          \
-        else k_block_sweep_dia<D, T, 1><<<g, 256, 0, c.s>>>(n, dia, wd, m, in, out);                    \
+        if (mode == 0 && hint) k_block_sweep_dia<D, T, 0, true><<<g, 256, 0, c.s>>>(n, dia, wd, m, in, out); \
+        else if (mode == 0) k_block_sweep_dia<D, T, 0, false><<<g, 256, 0, c.s>>>(n, dia, wd, m, in, out); \
+        else k_block_sweep_dia<D, T, 1, false><<<g, 256, 0, c.s>>>(n, dia, wd, m, in, out);             \
     } while (0)
 #define NLSP_BDT(D)                  \
     do {                             \
@@ -1159,6 +1190,12 @@ void launch_col_move(const LaunchCtx& c, long long n, int ld, double* U, int col
 }
 void launch_transpose(const LaunchCtx& c, long long rows, int cols, const double* X, double* Y) {
     k_transpose<<<grid_for(c, rows * cols, 256), 256, 0, c.s>>>(rows, cols, X, Y);
+    count(c);
+}
+
+void launch_s0_scatter(const LaunchCtx& c, const double* src, long long e0, long long cnt, int m, const int* live,
+                       double* S) {
+    k_s0_scatter<<<grid_for(c, cnt, 256), 256, 0, c.s>>>(src, e0, cnt, m, live, S);
     count(c);
 }
 

@@ -2305,18 +2305,21 @@ void launch_dia_op(const LaunchCtx& c, const SolveArgs& a, const Op& op) {
 }
 
 // ---- plane-march kernels (march.cuh) --------------------------------------
-// NLSP_MARCH: 0 never, 1 whenever the diagonal form has a plane geometry,
-// default (auto) from n >= 2^18 rows (smaller systems keep the direct kernels,
-// whose grid-wide sums are bitwise those of the CSR path).
+// NLSP_MARCH: 0 (default) never; 1 whenever the diagonal form has a plane
+// geometry; 2 from n >= 2^18 rows. Off by default: measured slower than the
+// direct kernels on every configuration ("plane march") — the
+// consumer warps are issue-bound at one or two CTAs per SM, where the direct
+// kernels keep 32 warps of independent gathers in flight.
 static int march_mode() {
     static const int m = [] {
         const char* e = std::getenv("NLSP_MARCH");
-        return e ? std::atoi(e) : 2;
+        return e ? std::atoi(e) : 0;
     }();
     return m;
 }
-constexpr unsigned kMarchBudget = 200 * 1024;
-constexpr int kMarchMinRing = 6;
+// two CTAs per SM (34 warps: the stencil phase is latency-bound at 17)
+constexpr unsigned kMarchBudget = 104 * 1024;
+constexpr int kMarchMinRing = 5;
 
 struct MarchPlan {
     MarchGeom g;
@@ -2333,15 +2336,19 @@ static bool march_plan(const LaunchCtx& c, const SolveArgs& a, int nh, int no, M
     const long long P = a.dia.plane, n = a.n;
     const int h = a.dia.halo, mb = a.dia.mbytes;
     const long long cmax = std::max<long long>(16, n / ((long long)c.num_sms * 16));
+    // prefer slabs that give every consumer thread the same number of rows
+    for (int pass = 0; pass < 2; ++pass)
     for (long long k = 1; k <= P; ++k) {
         if (P % k) continue;
         const long long C = P / k;
         if (C > cmax) continue;
+        const long long nt = kMarchConsumers * 32;
+        if (pass == 0 && 4 * C < 3 * ((C + nt - 1) / nt) * nt) continue;  // last row pass >= 75 % full
         const unsigned hcap = (unsigned)((((C + 2 * h) * 8 + 15) & ~15ll) + 32);
         const unsigned ocap = (unsigned)(((C * 8 + 15) & ~15ll) + 32);
         const unsigned mcap = (unsigned)(((C * mb + 15) & ~15ll) + 32);
         const unsigned slot = nh * hcap + no * ocap + mcap;
-        const int R = (int)std::min<unsigned>(12, kMarchBudget / slot);
+        const int R = (int)std::min<unsigned>(8, kMarchBudget / slot);
         if (R < kMarchMinRing) continue;
         MarchGeom g{};
         g.P = P;

@@ -179,6 +179,23 @@ def test_zero_sweeps_returns_raw_gaussians(nlsp, oracle):
     assert np.array_equal(s1, s2) and np.array_equal(s1, so)
 
 
+@pytest.mark.parametrize("cfg,nx", [("C4", 64), ("C5", 320)])
+def test_streamed_s0_matches_host_stream(nlsp, cfg, nx):
+    """nlsp_generate_smoothed_vectors streams S^(0) to the device in 8 M-value
+    chunks through pinned staging (several chunks here; C5's clamped edge
+    takes the masked scatter path): with no sweeps the device holds exactly
+    the reference's Rng stream (the host restatement, pinned to rng.npz)."""
+    from paper_2601_20174_b200 import problems
+    c = problems.CONFIGS[cfg].scaled(nx=nx)
+    pb = problems.generate(c)
+    a = pb.csr()
+    mask = pb.mask if pb.mask.any() else None
+    assert pb.n * c.m > 2 * (1 << 23) and (mask is not None) == (cfg == "C5")
+    s = nlsp.generate_smoothed_vectors(a, mask, c.m, 0, c.omega, c.s0_seed).s.numpy()
+    ref = problems.smoothed_s0(c.s0_seed, pb.n, c.m, mask)
+    assert np.array_equal(s, ref)
+
+
 # ------------------------------------------------------------------ svd.hpp --
 def test_svd_basis_diagonal_case(nlsp):
     s = np.zeros((3, 2))
