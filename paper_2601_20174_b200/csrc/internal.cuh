@@ -7,6 +7,8 @@
 //   state      one PcgState (scalars + flags) + per-CTA reduction partials
 #pragma once
 
+#include <cstdio>
+
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -138,6 +140,26 @@ struct ClusterArgs {
     long long hist_cap;  // entries hist holds; later iterations are not recorded
     PcgState* st;
 };
+
+// Checked builds (make -C paper_2601_20174_b200 checked -> variants/
+// libnlsp_gpu_checked.so, scripts/gpu_checked.sh): device-side bounds checks on
+// every staged copy and shared-memory window, in place of compute-sanitizer
+// (closed on this pool). A failed check prints its site and traps, so the call
+// returns a CUDA error and the test fails. Compiled out otherwise.
+#ifdef NLSP_CHECKED
+#define NLSP_CHECK(cond)                                                                             \
+    do {                                                                                             \
+        if (!(cond)) {                                                                               \
+            printf("NLSP_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                               \
+            __trap();                                                                                \
+        }                                                                                            \
+    } while (0)
+#else
+#define NLSP_CHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -54,6 +54,7 @@ __device__ __forceinline__ unsigned stage_range(unsigned char* dst, const void* 
     if (a >= b) return 0;
     const long long sb = (a * es) & ~15ll, se = (b * es + 15) & ~15ll;
     const long long base = floor16(ws * es);
+    NLSP_CHECK(sb - base >= 0 && se - base <= (we - ws) * es + 32);
     bulk_g2s(dst + (sb - base), static_cast<const unsigned char*>(src) + sb, (unsigned)(se - sb), bar);
     return (unsigned)(se - sb);
 }
@@ -218,8 +219,10 @@ __global__ void __launch_bounds__(kMarchThreads, 2) k_march(SolveArgs a, Op op, 
                 // the gathered quantity's window position of row 0 + offset t
                 unsigned ga[MAXD];
 #pragma unroll
-                for (int t = 0; t < MAXD; ++t)
+                for (int t = 0; t < MAXD; ++t) {
                     ga[t] = (dz[t] < 0 ? hq[0] : (dz[t] > 0 ? hq[2] : hq[1])) + 8u * (unsigned)(g.h + dd[t]);
+                    NLSP_CHECK(t >= d || (g.h + dd[t] >= 0 && g.h + dd[t] + g.C <= g.C + 2 * g.h));
+                }
                 const int rows = (int)min((long long)g.C, n - e0);
                 // two rows in flight per thread: their fma chains interleave
 #pragma unroll 2

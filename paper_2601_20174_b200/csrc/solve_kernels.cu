@@ -1747,6 +1747,7 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
                 const unsigned vb = round16(rows * 8);  // vectors are padded by 16 doubles
                 const unsigned wb = (unsigned)rows * ld * 8;
                 const unsigned mbb = round16(rows * mb);  // masks are padded by 16 B
+                NLSP_CHECK(rows > 0 && rows <= kOpTR && wb <= s_off && m_off + mbb <= as_off && as_off + kOpVec <= sbytes);
                 mbar_arrive_tx(&full[stg], wb + (sv ? vb : 0u) + vb + mbb);
                 bulk_g2s(base_s, a.P + (long long)r0 * ld, wb, &full[stg]);
                 if (sv) bulk_g2s(base_s + s_off, sv + r0, vb, &full[stg]);
@@ -1791,6 +1792,8 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
                     cvb = ((a1 - s0 + 1) & ~1) * 8;
                     ccb = ((a1 - c0 + 3) & ~3) * 4;
                 }
+                NLSP_CHECK(rows > 0 && rows <= kOpTR && a1 >= a0 && a1 - a0 <= tile_nnz);
+                NLSP_CHECK(MAXD != 0 || (rp_off + cb <= v_off && v_off + cvb <= c_off && c_off + ccb <= sbytes));
                 mbar_arrive_tx(&full[stg], wb + (sv ? vb : 0u) + vb + mbb + cb + cvb + ccb);
                 bulk_g2s(base_s, a.P + (long long)r0 * ld, wb, &full[stg]);
                 if (sv) bulk_g2s(base_s + s_off, sv + r0, vb, &full[stg]);
@@ -1827,6 +1830,7 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
                     const int* cs_ = reinterpret_cast<const int*>(base + c_off);
                     const int a0 = rps[0], s0 = a0 & ~1, c0 = a0 & ~3;
                     const int b = rps[lr], e = rps[lr + 1];
+                    NLSP_CHECK(b >= a0 && e >= b && e - s0 <= tile_nnz + 2 && e - c0 <= tile_nnz + 8);
                     for (int kk = b; kk < e; ++kk) y = fma(vs[kk - s0], sv[cs_[kk - c0]], y);
                 } else {
                     unsigned m;

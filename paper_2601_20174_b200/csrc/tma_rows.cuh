@@ -86,6 +86,9 @@ __device__ __forceinline__ void stage_tile(const int* __restrict__ rp, const int
     const unsigned vbytes = ((a1 - s0 + 1) & ~1) * 8;
     const unsigned cbytes = ((a1 - c0 + 3) & ~3) * 4;
     const unsigned pbytes = P ? (unsigned)rows * ld * 8 : 0u;
+    NLSP_CHECK(rows > 0 && rows <= TR && a0 >= 0 && a1 >= a0);
+    NLSP_CHECK(L.rp_off + rbytes <= L.v_off && L.v_off + vbytes <= L.c_off);
+    NLSP_CHECK(L.c_off + cbytes <= (P ? L.p_off : L.bytes) && (!P || L.p_off + pbytes <= L.bytes));
     mbar_arrive_tx(full, rbytes + vbytes + cbytes + pbytes);
     bulk_g2s(stage_base + L.rp_off, rp + r0, rbytes, full);
     if (vbytes) bulk_g2s(stage_base + L.v_off, v + s0, vbytes, full);
