@@ -9,7 +9,6 @@ LIB=paper_2601_20174_b200/variants/libnlsp_gpu_checked.so
 NLSP_GPU_LIB=$PWD/$LIB timeout ${TMO:-2400} python -m pytest ${TESTS:-tests -m gpu} -q -p no:cacheprovider \
   > gpurun_out/pytest_checked.log 2>&1
 echo "checked pytest exit=$?"; tail -3 gpurun_out/pytest_checked.log
-# the march kernels (off by default) under the checks too
-NLSP_MARCH=1 NLSP_GPU_LIB=$PWD/$LIB timeout 900 python -m pytest tests/test_gpu_paths.py -q -k "execution or march" \
-  > gpurun_out/pytest_checked_march.log 2>&1
-echo "checked march pytest exit=$?"; tail -3 gpurun_out/pytest_checked_march.log
+# (the march kernels run under the checks too: the forced "march" path of
+# test_execution_paths_match_reference and test_march_matches_direct_kernels
+# pass NLSP_MARCH to their subprocesses, which inherit NLSP_GPU_LIB)
