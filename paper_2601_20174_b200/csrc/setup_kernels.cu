@@ -182,50 +182,6 @@ __global__ void __launch_bounds__(256) k_block_sweep_dia(int n, DiaArgs dia, con
     }
 }
 
-// The same sweep in column halves (NLSP_BSWEEP_HALF, m = 128): a launch per
-// 64-column half, a half-warp per row (16 lanes x 4 columns), so each launch's
-// plane of S is 13 MB instead of 26 MB at C4 and a row's +-plane neighbour is
-// reused from L2 within half the distance. Same per-entry arithmetic.
-template <int D, int MODE>
-__global__ void __launch_bounds__(256) k_block_sweep_dia_half(int n, DiaArgs dia, const double* __restrict__ wd,
-                                                              int m, int c0, const double* __restrict__ in,
-                                                              double* __restrict__ out) {
-    constexpr int T = 4;
-    const int lane = threadIdx.x & 31, hl = lane & 15;
-    const long long hw = ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 4);
-    const long long nh = (gridDim.x * (long long)blockDim.x) >> 4;
-    const int mb = dia.mbytes;
-    for (long long row = hw; row < n; row += nh) {
-        unsigned msk;
-        if (mb == 1) msk = static_cast<const unsigned char*>(dia.mask)[row];
-        else if (mb == 2) msk = static_cast<const unsigned short*>(dia.mask)[row];
-        else msk = static_cast<const unsigned*>(dia.mask)[row];
-        double xv[D][T], av[D];
-#pragma unroll
-        for (int t = 0; t < D; ++t) {
-            const long long nb = min(max(row + dia.off[t], 0LL), (long long)n - 1);
-            av[t] = dia.kind == 2 ? dia.rv[(size_t)t * n + row] : dia.val[t];
-            const double* xr = in + nb * m + c0;
-#pragma unroll
-            for (int u = 0; u < T; ++u) xv[t][u] = xr[hl + 16 * u];
-        }
-        double acc[T];
-#pragma unroll
-        for (int u = 0; u < T; ++u) acc[u] = 0.0;
-#pragma unroll
-        for (int t = 0; t < D; ++t)
-            if ((msk >> t) & 1u) {
-#pragma unroll
-                for (int u = 0; u < T; ++u) acc[u] = fma(av[t], xv[t][u], acc[u]);
-            }
-#pragma unroll
-        for (int u = 0; u < T; ++u) {
-            const long long o = row * m + c0 + hl + 16 * u;
-            out[o] = MODE == 0 ? fma(wd[row], 0.0 - acc[u], in[o]) : acc[u];
-        }
-    }
-}
-
 // ------------------------------------------------------------------ Gram --
 // C = X^T Y for tall X (rows x ca), Y (rows x cb), row-major. 256 threads as a
 // 16 x 16 grid; thread (ti, tj) owns a TI x TJ block of C. Row tiles of X and Y
@@ -1035,23 +991,6 @@ bool launch_block_op_dia(const LaunchCtx& c, int mode, int n, const DiaArgs& dia
     // -10 %), slower for per-row values (C2 +57 %) and m <= 64 (the builds, +9 %)
     if (!on || dia.kind != 1 || m <= 64 || m > 128 || !(dia.d == 5 || dia.d == 7 || dia.d == 9)) return false;
     const int g = grid_for(c, (long long)n * 32, 256, 8);
-    static const bool half = std::getenv("NLSP_BSWEEP_HALF") && std::atoi(std::getenv("NLSP_BSWEEP_HALF")) == 1;
-    if (half && m == 128) {
-        for (int c0 = 0; c0 < 128; c0 += 64) {
-            if (dia.d == 5) {
-                if (mode == 0) k_block_sweep_dia_half<5, 0><<<g, 256, 0, c.s>>>(n, dia, wd, m, c0, in, out);
-                else k_block_sweep_dia_half<5, 1><<<g, 256, 0, c.s>>>(n, dia, wd, m, c0, in, out);
-            } else if (dia.d == 7) {
-                if (mode == 0) k_block_sweep_dia_half<7, 0><<<g, 256, 0, c.s>>>(n, dia, wd, m, c0, in, out);
-                else k_block_sweep_dia_half<7, 1><<<g, 256, 0, c.s>>>(n, dia, wd, m, c0, in, out);
-            } else {
-                if (mode == 0) k_block_sweep_dia_half<9, 0><<<g, 256, 0, c.s>>>(n, dia, wd, m, c0, in, out);
-                else k_block_sweep_dia_half<9, 1><<<g, 256, 0, c.s>>>(n, dia, wd, m, c0, in, out);
-            }
-            count(c);
-        }
-        return true;
-    }
 #define NLSP_BD(D, T)                                                                                   \
     do {                                                                                                \
         if (mode == 0 && hint) k_block_sweep_dia<D, T, 0, true><<<g, 256, 0, c.s>>>(n, dia, wd, m, in, out); \
