@@ -165,6 +165,7 @@ public:
     }
     const nlsp_dense* get() const { return d_.get(); }
     nlsp_dense* get() { return d_.get(); }
+    Device& device() const { return *dev_; }
 
 private:
     struct Del {
@@ -396,6 +397,19 @@ template <class Csr, class = decltype(std::declval<const Csr&>().row_ptr())>
 TwoLevelPreconditioner build_preconditioner(const Csr& a, const Dense& basis, double omega, std::size_t nu1,
                                             std::size_t nu2) {
     return TwoLevelPreconditioner(default_device(), device_matrix(a), basis, omega, nu1, nu2);
+}
+
+// generate_smoothed_vectors(A, boundary_mask, K, sweeps, omega, seed)
+// (smoothing.hpp:81-100) with the reference's arguments; S stays on the device
+template <class Csr, class = decltype(std::declval<const Csr&>().row_ptr())>
+Dense generate_smoothed_vectors(const Csr& a, const std::vector<bool>& boundary_mask, std::size_t k,
+                                std::size_t sweeps, double omega, std::uint64_t seed) {
+    return generate_smoothed_vectors(default_device(), device_matrix(a), boundary_mask, k, sweeps, omega, seed);
+}
+// first_cols(svd_oracle(S).left_vectors, k) (svd.hpp:155-227, dense.hpp:158-164)
+// on the device of S
+inline Dense svd_first_cols(const Dense& s, std::size_t k, std::vector<double>* singular_values = nullptr) {
+    return svd_basis(s.device(), s, k, singular_values);
 }
 
 #ifdef NLSP_GPU_REFERENCE_TYPES

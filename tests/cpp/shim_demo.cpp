@@ -120,7 +120,12 @@ int main(int argc, char** argv) {
     using HostDense = LocalDense;
     using nlsp_gpu::PcgResult;
 #endif
+    // the setup through the reference-signature helpers as well
+    auto s_ref = nlsp_gpu::generate_smoothed_vectors(a, std::vector<bool>{}, m, s1, omega, seed);
+    const auto u_ref = nlsp_gpu::svd_first_cols(s_ref, k).host();
     const auto uh = u.host();
+    double u_diff = 0.0;
+    for (std::size_t i = 0; i < uh.size(); ++i) u_diff = std::fmax(u_diff, std::fabs(u_ref[i] - uh[i]));
     HostDense basis(n, k);
     std::copy(uh.begin(), uh.end(), basis.data());
     auto M = nlsp_gpu::build_preconditioner(a, basis, omega, nu1, nu2);
@@ -152,11 +157,12 @@ int main(int argc, char** argv) {
         "\"plain_iterations\": %zu, \"history_len\": %zu, \"zero_rhs_rejected\": %d, "
         "\"solve_ms\": %.3f, \"ref_style_iterations\": %zu, \"ref_style_history_len\": %zu, "
         "\"ref_style_method\": \"%s\", \"ref_style_x_maxdiff\": %.3e, \"apply_rel_diff\": %.3e, "
+        "\"ref_style_basis_maxdiff\": %.3e, "
         "\"reference_types\": %d}\n",
         n, res.report.iterations, res.report.converged ? 1 : 0, res.report.true_relative_residual,
         plain.report.iterations, res.report.residual_history.size(), zero_rhs_rejected ? 1 : 0,
         res.report.solve_ms, ref_style.report.iterations, ref_style.report.residual_history.size(),
-        ref_style.report.method.c_str(), x_diff, z_diff / (z_norm > 0 ? z_norm : 1.0),
+        ref_style.report.method.c_str(), x_diff, z_diff / (z_norm > 0 ? z_norm : 1.0), u_diff,
 #ifdef WITH_REFERENCE
         1
 #else

@@ -56,5 +56,8 @@ def test_shim_program_matches_reference(tmp_path, binary):
     assert out["ref_style_history_len"] == out["iterations"] and out["ref_style_method"] == "two_level"
     assert out["ref_style_x_maxdiff"] <= 1e-12 * np.abs(d["x"]).max()
     assert out["apply_rel_diff"] <= 1e-12
+    # generate_smoothed_vectors / svd_first_cols with the reference's arguments:
+    # the same (deterministic) basis
+    assert out["ref_style_basis_maxdiff"] == 0.0
     x = load(tmp_path / "x.bin")
     assert np.linalg.norm(x - d["x"]) <= 1e-9 * np.linalg.norm(d["x"])
