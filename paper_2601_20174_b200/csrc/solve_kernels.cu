@@ -2741,7 +2741,14 @@ static void prolong_onepass_ppl(const LaunchCtx& c, const SolveArgs& a, const do
     const int ld = a.k + (a.k & 1);
     // as many stages as fit, a multiple of the stencil pair count P
     const int tnz = a.dia.kind ? -1 : (kOpTR == 64 ? a.tile_nnz64 : a.tile_nnz128);
-    int fit = (int)((kStageBudget - 256) / op_stage_bytes(ld, tnz));
+    // The ring may take 224 KB (of the 227 KB a CTA can have; the static
+    // shared arrays of the column sums and the grid reduction fit beside it):
+    // at C4 that is 6 stages instead of 4 (measured 371 -> 361 us per launch,
+    // 2 175 -> 2 223 iterations/s at the same capped clock).
+    // NLSP_OP_BUDGET (KB) overrides it for A/B runs.
+    static const size_t budget = std::getenv("NLSP_OP_BUDGET") ? (size_t)std::atoi(std::getenv("NLSP_OP_BUDGET")) * 1024
+                                                               : (size_t)224 * 1024;
+    int fit = (int)((budget - 256) / op_stage_bytes(ld, tnz));
     if (fit > kOpMaxStages) fit = kOpMaxStages;
     if (NLSP_OP_STAGES > 0 && fit > NLSP_OP_STAGES) fit = NLSP_OP_STAGES;
     int S, P;

@@ -17,5 +17,9 @@ if [ "${NCU:-1}" = "1" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches_$CFG.csv $SHORT > gpurun_out/ncu_list.log 2>&1; echo "ncu list exit=$?"
   for K in ${KERNELS:-k_update_restrict k_prolong}; do
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s ${SKIP:-20} -c 1 -o gpurun_out/prof_${CFG}_$K -f $SHORT > gpurun_out/ncu_full_$K.log 2>&1; echo "ncu full $K exit=$?"
+    # exports only (gpurun brings back at most 64 MiB)
+    ncu -i gpurun_out/prof_${CFG}_$K.ncu-rep --page raw --csv > gpurun_out/prof_${CFG}_$K.raw.csv 2>/dev/null
+    ncu -i gpurun_out/prof_${CFG}_$K.ncu-rep --page details > gpurun_out/prof_${CFG}_$K.details.txt 2>/dev/null
+    [ "${KEEP_REP:-0}" = "1" ] || rm -f gpurun_out/prof_${CFG}_$K.ncu-rep
   done
 fi
