@@ -129,12 +129,32 @@ nlsp_status nlsp_jacobi_sweeps(nlsp_ctx* ctx, const nlsp_csr* a, double omega, u
 /* homogeneous block sweeps on s in place (smoothing.hpp:50-60) */
 nlsp_status nlsp_smooth_vectors(nlsp_ctx* ctx, const nlsp_csr* a, nlsp_dense* s, uint64_t sweeps,
                                 double omega);
-/* generate_smoothed_vectors (smoothing.hpp:81-100): S^(0) drawn on the host
- * from the reference's Rng stream (bit-identical), uploaded, then swept on the
- * device. mask may be NULL (no Dirichlet rows). */
+/* generate_smoothed_vectors (smoothing.hpp:81-100): S^(0) drawn from the
+ * reference's Rng stream (rng.hpp:22-49), then swept on the device. mask may be
+ * NULL (no Dirichlet rows). Where S^(0) is drawn is a context setting:
+ *   NLSP_S0_DRAW_HOST (default): on the host cores, every thread jumping its own
+ *     mt19937_64 generator to its slice of the one stream, glibc's log / sin /
+ *     cos — bit-identical to the reference's serial loop; streamed to the device
+ *     through pinned chunks.
+ *   NLSP_S0_DRAW_DEVICE: on the device. The mt19937_64 words are the same bit
+ *     for bit (jump-ahead, csrc/s0_device.cu); the Box-Muller transform uses
+ *     CUDA's log / sincos, so a normal can differ from the reference's in its
+ *     last bits (<= 4 ulp) — no host draw, no 8 n k byte upload.
+ * The environment variable NLSP_S0_DRAW=device selects the device draw for
+ * contexts created afterwards. */
+enum { NLSP_S0_DRAW_HOST = 0, NLSP_S0_DRAW_DEVICE = 1 };
+nlsp_status nlsp_ctx_set_s0_draw(nlsp_ctx* ctx, int32_t mode);
+/* where the last nlsp_generate_smoothed_vectors of this context drew S^(0)
+ * (the device draw hands over to the host when the stream holds a zero
+ * uniform, which the reference redraws: probability 2^-53 per pair) */
+int32_t nlsp_ctx_last_s0_draw(const nlsp_ctx* ctx);
 nlsp_status nlsp_generate_smoothed_vectors(nlsp_ctx* ctx, const nlsp_csr* a, const uint8_t* mask,
                                            uint64_t k, uint64_t sweeps, double omega,
                                            uint64_t seed, nlsp_dense** out);
+/* the first `count` outputs of std::mt19937_64(seed), generated on the device
+ * by the jump tree of the device draw (a check of its integer part: they are
+ * bit for bit the host generator's) */
+nlsp_status nlsp_mt19937_64_words(nlsp_ctx* ctx, uint64_t seed, uint64_t count, uint64_t* out);
 
 /* ----------------------------------------------------------- SVD basis ---- */
 /* first_cols(svd_oracle(S).left_vectors, k) (svd.hpp:155-227, dense.hpp:158-164)

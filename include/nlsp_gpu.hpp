@@ -83,6 +83,10 @@ public:
     }
     nlsp_ctx* get() const { return ctx_.get(); }
     void* stream() const { return nlsp_ctx_stream(ctx_.get()); }
+    // where generate_smoothed_vectors draws S^(0): NLSP_S0_DRAW_HOST (default,
+    // bit-identical to the reference's Rng stream) or NLSP_S0_DRAW_DEVICE
+    void set_s0_draw(int mode) { check(nlsp_ctx_set_s0_draw(ctx_.get(), mode), ctx_.get()); }
+    int last_s0_draw() const { return nlsp_ctx_last_s0_draw(ctx_.get()); }
 
 private:
     struct Del {

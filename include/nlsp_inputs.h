@@ -66,6 +66,17 @@ const char* nlsp_inputs_last_error(void);
 uint64_t nlsp_mix_seed(uint64_t seed, uint64_t tag);
 void nlsp_rng_normal_fill(uint64_t seed, uint64_t count, double* out);
 void nlsp_rng_uniform_fill(uint64_t seed, uint64_t count, double lo, double hi, double* out);
+/* nlsp_rng_normal_fill produces the stream of Rng(seed).normal() on several
+ * threads, each jumping its own mt19937_64 to its slice (csrc/mt_jump.hpp).
+ * The checks of that: the plain serial loop; the threaded stream with its
+ * chunk size (pairs), widened u1 rejection and worker cap exposed; raw
+ * mt19937_64 outputs after `skip` words by discard and by jump-ahead (skip a
+ * multiple of 2^17; returns 0 on success). */
+void nlsp_rng_normal_serial(uint64_t seed, uint64_t count, double zero_below, double* out);
+void nlsp_rng_normal_chunks(uint64_t seed, uint64_t count, uint64_t chunk_pairs, double zero_below,
+                            uint32_t max_workers, double* out);
+void nlsp_mt19937_64_fill(uint64_t seed, uint64_t skip, uint64_t count, uint64_t* out);
+int nlsp_mt19937_64_jump_fill(uint64_t seed, uint64_t skip, uint64_t count, uint64_t* out);
 
 /* S^(0) exactly as generate_smoothed_vectors fills it before sweeping
  * (smoothing.hpp:88-96): Rng(mix_seed(seed, 0x736d6f6f)), row-major i outer /

@@ -39,6 +39,8 @@ NLSP_E_IO = 8  # nlsp::IoError (include/nlsp_io.h)
 PRECOND_IDENTITY = 0
 PRECOND_JACOBI = 1
 PRECOND_TWOLEVEL = 2
+NLSP_S0_DRAW_HOST = 0
+NLSP_S0_DRAW_DEVICE = 1
 
 
 class SolveReportC(C.Structure):
@@ -121,6 +123,9 @@ GPU_SYMBOLS = [
     ("nlsp_jacobi_sweeps", C.c_int, [vp, vp, c_dbl, c_u64, P_dbl, P_dbl]),
     ("nlsp_smooth_vectors", C.c_int, [vp, vp, vp, c_u64, c_dbl]),
     ("nlsp_generate_smoothed_vectors", C.c_int, [vp, vp, P_u8, c_u64, c_u64, c_dbl, c_u64, C.POINTER(vp)]),
+    ("nlsp_ctx_set_s0_draw", C.c_int, [vp, c_i32]),
+    ("nlsp_ctx_last_s0_draw", c_i32, [vp]),
+    ("nlsp_mt19937_64_words", C.c_int, [vp, c_u64, c_u64, P_u64]),
     ("nlsp_svd_basis", C.c_int, [vp, vp, c_u64, C.POINTER(vp), P_dbl, P_i32]),
     ("nlsp_twolevel_build", C.c_int, [vp, vp, vp, c_dbl, c_u64, c_u64, C.POINTER(vp)]),
     ("nlsp_twolevel_destroy", None, [vp]),
@@ -146,6 +151,10 @@ INPUT_SYMBOLS = [
     ("nlsp_mix_seed", c_u64, [c_u64, c_u64]),
     ("nlsp_rng_normal_fill", None, [c_u64, c_u64, P_dbl]),
     ("nlsp_rng_uniform_fill", None, [c_u64, c_u64, c_dbl, c_dbl, P_dbl]),
+    ("nlsp_rng_normal_serial", None, [c_u64, c_u64, c_dbl, P_dbl]),
+    ("nlsp_rng_normal_chunks", None, [c_u64, c_u64, c_u64, c_dbl, C.c_uint32, P_dbl]),
+    ("nlsp_mt19937_64_fill", None, [c_u64, c_u64, c_u64, P_u64]),
+    ("nlsp_mt19937_64_jump_fill", C.c_int, [c_u64, c_u64, c_u64, P_u64]),
     ("nlsp_smoothed_s0", None, [c_u64, c_u64, c_u64, P_u8, P_dbl]),
 ]
 

@@ -348,6 +348,62 @@ void nlsp_rng_normal_fill(std::uint64_t seed, std::uint64_t count, double* out) 
     normal_stream(seed, count, out);
 }
 
+// The serial loop over Rng(seed).normal() itself (std::mt19937_64, no jumps):
+// what nlsp_rng_normal_fill's threaded stream must reproduce bit for bit.
+// zero_below widens the rejection `while (u1 <= 0)` for tests of that path.
+void nlsp_rng_normal_serial(std::uint64_t seed, std::uint64_t count, double zero_below, double* out) {
+    std::mt19937_64 gen(seed);
+    auto uni = [&]() { return static_cast<double>(gen() >> 11) * 0x1.0p-53; };
+    for (std::uint64_t i = 0; i < count; i += 2) {
+        double u1 = uni();
+        const double u2 = uni();
+        while (u1 <= zero_below) u1 = uni();
+        const double r = std::sqrt(-2.0 * std::log(u1));
+        const double a = 2.0 * 3.141592653589793 * u2;
+        out[i] = r * std::cos(a);
+        if (i + 1 < count) out[i + 1] = r * std::sin(a);
+    }
+}
+
+// nlsp_rng_normal_fill with its knobs exposed: chunk size in pairs, the widened
+// rejection, and a cap on the worker threads (0: all)
+void nlsp_rng_normal_chunks(std::uint64_t seed, std::uint64_t count, std::uint64_t chunk_pairs,
+                            double zero_below, std::uint32_t max_workers, double* out) {
+    struct ToArray {
+        double* out;
+        std::uint64_t count;
+        std::vector<double> scratch;
+        double* buffer(std::uint64_t base, std::uint64_t np) {
+            if (2 * (base + np) <= count) return out + 2 * base;
+            scratch.assign(2 * np, 0.0);
+            return scratch.data();
+        }
+        void done(std::uint64_t base, std::uint64_t np) {
+            if (2 * (base + np) > count)
+                std::copy(scratch.begin(), scratch.begin() + (count - 2 * base), out + 2 * base);
+        }
+    } sink{out, count, {}};
+    nlsp_host::normal_stream_chunks(seed, count, sink, chunk_pairs, zero_below, max_workers);
+}
+
+// raw std::mt19937_64 outputs (the check of the jump-ahead generators)
+void nlsp_mt19937_64_fill(std::uint64_t seed, std::uint64_t skip, std::uint64_t count, std::uint64_t* out) {
+    std::mt19937_64 gen(seed);
+    gen.discard(skip);
+    for (std::uint64_t i = 0; i < count; ++i) out[i] = gen();
+}
+
+// the same words from a generator jumped `skip` words ahead (mt_jump.hpp);
+// skip must be a multiple of 2^17. Returns 0 on success.
+int nlsp_mt19937_64_jump_fill(std::uint64_t seed, std::uint64_t skip, std::uint64_t count, std::uint64_t* out) {
+    std::uint64_t w[nlsp_host::kMtN], j[nlsp_host::kMtN];
+    nlsp_host::mt64_seed(seed, w);
+    if (!nlsp_host::mt64_jump(w, skip, j)) return 1;
+    nlsp_host::Mt64 gen(j);
+    for (std::uint64_t i = 0; i < count; ++i) out[i] = gen();
+    return 0;
+}
+
 void nlsp_rng_uniform_fill(std::uint64_t seed, std::uint64_t count, double lo, double hi,
                            double* out) {
     Rng r(seed);

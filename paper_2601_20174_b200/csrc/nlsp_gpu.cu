@@ -92,6 +92,9 @@ void launch_col_move(const LaunchCtx&, long long, int, double*, int, double*, co
 void launch_transpose(const LaunchCtx&, long long, int, const double*, double*);
 bool march_planned(const LaunchCtx&, const SolveArgs&);
 void launch_s0_scatter(const LaunchCtx&, const double*, long long, long long, int, const int*, double*);
+void launch_mt_stream(const LaunchCtx&, unsigned long long*, long long, int, const unsigned long long*, int,
+                      unsigned long long, unsigned long long, unsigned long long*, unsigned long long*);
+void launch_box_muller(const LaunchCtx&, double*, unsigned long long, const unsigned long long*, int*);
 void launch_sigma(const LaunchCtx&, int, int, const double*, const double*, double*, double*,
                   int*);
 // setup_kernels.cu (SA)
@@ -198,6 +201,11 @@ struct nlsp_ctx {
     // two chunks of the normal stream in flight to the device
     double* s0_pin[2] = {nullptr, nullptr};
     cudaEvent_t s0_ev[2] = {nullptr, nullptr};
+    // S^(0) drawn on the device (nlsp_ctx_set_s0_draw; s0_device.cu): the jump
+    // polynomials of mt19937_64 (mt_jump_table.inc), uploaded on first use
+    int s0_draw = NLSP_S0_DRAW_HOST;
+    unsigned long long* mt_polys = nullptr;
+    int last_s0_draw = NLSP_S0_DRAW_HOST;  // where the last generate_smoothed_vectors drew S^(0)
     double last_svd_defect = 0.0;  // orthonormality defect of the last svd_basis' U_k before any polish
     int last_svd_solid = 0;        // its columns above the singular-value cutoff
     bool use_graph = true;
@@ -791,6 +799,8 @@ nlsp_status nlsp_ctx_create(int device, nlsp_ctx** out) {
     ctx->use_cluster = !(clu && std::strcmp(clu, "0") == 0);
     const char* co = std::getenv("NLSP_COARSE");
     ctx->coarse_inverse = !(co && std::strcmp(co, "chol") == 0);
+    const char* sd = std::getenv("NLSP_S0_DRAW");
+    ctx->s0_draw = (sd && std::strcmp(sd, "device") == 0) ? NLSP_S0_DRAW_DEVICE : NLSP_S0_DRAW_HOST;
     *out = ctx;
     return NLSP_OK;
 }
@@ -806,6 +816,7 @@ void nlsp_ctx_destroy(nlsp_ctx* ctx) {
         if (ctx->s0_ev[b]) cudaEventDestroy(ctx->s0_ev[b]);
     }
     free_ws(ctx);
+    dfree(ctx->mt_polys);
     dfree(ctx->st);
     dfree(ctx->flags);
     if (ctx->st_host) cudaFreeHost(ctx->st_host);
@@ -1231,6 +1242,90 @@ nlsp_status nlsp_smooth_vectors(nlsp_ctx* ctx, const nlsp_csr* a, nlsp_dense* s,
     return smooth_impl(ctx, a, s, sweeps, omega);
 }
 
+nlsp_status nlsp_ctx_set_s0_draw(nlsp_ctx* ctx, int32_t mode) {
+    if (!ctx) return NLSP_E_VALIDATION;
+    if (mode != NLSP_S0_DRAW_HOST && mode != NLSP_S0_DRAW_DEVICE)
+        return set_err(ctx, NLSP_E_VALIDATION, "set_s0_draw: unknown mode");
+    ctx->s0_draw = mode;
+    return NLSP_OK;
+}
+
+int32_t nlsp_ctx_last_s0_draw(const nlsp_ctx* ctx) { return ctx ? ctx->last_s0_draw : -1; }
+
+namespace {
+constexpr int kS0Log2B = 18;  // words per device substream (s0_device.cu)
+
+// The first `count` normals of Rng(stream_seed) into dst (device, count
+// doubles), drawn on the device. *redo is set when the stream holds a zero u1
+// (the reference would redraw it and shift every later value): the caller then
+// draws on the host. words_only: dst receives the raw mt19937_64 words instead.
+nlsp_status s0_draw_device(nlsp_ctx* ctx, std::uint64_t stream_seed, unsigned long long count, double* dst,
+                           bool* redo, bool words_only = false) {
+    *redo = false;
+    if (count == 0) return NLSP_OK;
+    const unsigned long long total = (count + 1) / 2 * 2;
+    const long long nsub = (long long)((total + (1ull << kS0Log2B) - 1) >> kS0Log2B);
+    int levels = 0;
+    while ((1ll << levels) < nsub) ++levels;
+    if (kS0Log2B + levels - 1 > nlsp_host::kMtJumpMaxLog2) {  // beyond the tabulated jumps
+        *redo = true;
+        return NLSP_OK;
+    }
+    if (!ctx->mt_polys) {
+        CU(cudaMalloc(&ctx->mt_polys, sizeof(nlsp_host::kMtJump)));
+        CU(cudaMemcpy(ctx->mt_polys, nlsp_host::kMtJump, sizeof(nlsp_host::kMtJump), cudaMemcpyHostToDevice));
+    }
+    unsigned long long* win = nullptr;
+    unsigned long long* tail = nullptr;
+    cudaError_t e = cudaSuccess;
+    auto cleanup = [&]() {
+        sfree(ctx, win);
+        sfree(ctx, tail);
+    };
+    std::uint64_t w0[nlsp_host::kMtN];
+    nlsp_host::mt64_seed(stream_seed, w0);
+    if ((e = salloc(ctx, &win, (size_t)nsub * nlsp_host::kMtN)) || (e = salloc(ctx, &tail, 2)) ||
+        (e = cudaMemcpyAsync(win, w0, sizeof(w0), cudaMemcpyHostToDevice, ctx->s)) ||
+        (e = cudaMemsetAsync(ctx->flags, 0, sizeof(int), ctx->s))) {
+        cleanup();
+        return cuda_fail(ctx, e, "s0 device draw alloc");
+    }
+    launch_mt_stream(ctx->lc, win, nsub, kS0Log2B, ctx->mt_polys, nlsp_host::kMtJumpMinLog2, total, count,
+                     reinterpret_cast<unsigned long long*>(dst), tail);
+    if (!words_only) launch_box_muller(ctx->lc, dst, count, tail, ctx->flags);
+    e = cudaGetLastError();
+    if (!e) e = cudaMemcpyAsync(ctx->flags_host, ctx->flags, sizeof(int), cudaMemcpyDeviceToHost, ctx->s);
+    if (!e) e = cudaStreamSynchronize(ctx->s);
+    cleanup();
+    if (e) return cuda_fail(ctx, e, "s0 device draw");
+    *redo = ctx->flags_host[0] != 0;
+    return NLSP_OK;
+}
+}  // namespace
+
+// test hook: the first `count` raw words of std::mt19937_64(seed), generated
+// on the device by the jump tree, copied to the host
+nlsp_status nlsp_mt19937_64_words(nlsp_ctx* ctx, uint64_t seed, uint64_t count, uint64_t* out) {
+    nlsp_status st = bind(ctx);
+    if (st) return st;
+    if (!out && count) return set_err(ctx, NLSP_E_VALIDATION, "mt19937_64_words: null out");
+    if (count == 0) return NLSP_OK;
+    double* d = nullptr;
+    const unsigned long long even = (count + 1) / 2 * 2;
+    cudaError_t e = salloc(ctx, &d, (size_t)even);
+    if (e) return cuda_fail(ctx, e, "mt19937_64_words alloc");
+    bool redo = false;
+    st = s0_draw_device(ctx, seed, even, d, &redo, true);
+    if (!st && redo) st = set_err(ctx, NLSP_E_VALIDATION, "mt19937_64_words: count beyond the tabulated jumps");
+    if (!st) {
+        e = cudaMemcpyAsync(out, d, sizeof(uint64_t) * count, cudaMemcpyDeviceToHost, ctx->s);
+        if (!e) e = cudaStreamSynchronize(ctx->s);
+        if (e) st = cuda_fail(ctx, e, "mt19937_64_words copy");
+    }
+    sfree(ctx, d);
+    return st;
+}
+
 // S^(0) streams from the host generator to the device chunk by chunk (4 M
 // normal pairs = 64 MB): each chunk is Box-Muller-transformed into one of two
 // pinned staging buffers while the previous one is in flight (cudaMemcpyAsync
@@ -1249,10 +1344,6 @@ nlsp_status nlsp_generate_smoothed_vectors(nlsp_ctx* ctx, const nlsp_csr* a, con
     if (k < 1) return set_err(ctx, NLSP_E_VALIDATION, "generate_smoothed_vectors: K must be positive");
     const unsigned long long n = (unsigned long long)a->n;
     constexpr unsigned long long kChunkPairs = 1ull << 22;
-    for (int b = 0; b < 2; ++b) {
-        if (!ctx->s0_pin[b]) CU(cudaMallocHost(&ctx->s0_pin[b], sizeof(double) * 2 * kChunkPairs));
-        if (!ctx->s0_ev[b]) CU(cudaEventCreateWithFlags(&ctx->s0_ev[b], cudaEventDisableTiming));
-    }
     nlsp_dense* d = nullptr;
     st = dense_alloc(ctx, n, k, &d);
     if (st) return st;
@@ -1265,6 +1356,59 @@ nlsp_status nlsp_generate_smoothed_vectors(nlsp_ctx* ctx, const nlsp_csr* a, con
     }
     int* dlive = nullptr;
     double* dstage[2] = {nullptr, nullptr};
+    ctx->last_s0_draw = NLSP_S0_DRAW_HOST;
+    if (ctx->s0_draw == NLSP_S0_DRAW_DEVICE) {
+        // the stream's nlive * k normals straight into S (or, under a mask, into
+        // a buffer of the live rows that is then scattered)
+        bool redo = false;
+        double* dlivebuf = nullptr;
+        cudaError_t de = cudaSuccess;
+        if (mask) {
+            if ((de = cudaMemsetAsync(d->d, 0, sizeof(double) * n * k, ctx->s)) ||
+                (de = salloc(ctx, &dlive, (size_t)std::max<unsigned long long>(nlive, 1))) ||
+                (nlive && (de = cudaMemcpyAsync(dlive, live.data(), sizeof(int) * nlive, cudaMemcpyHostToDevice, ctx->s))) ||
+                (de = salloc(ctx, &dlivebuf, (size_t)(nlive * k + 2)))) {
+                sfree(ctx, dlive);
+                sfree(ctx, dlivebuf);
+                nlsp_dense_destroy(d);
+                return cuda_fail(ctx, de, "generate_smoothed_vectors alloc");
+            }
+        }
+        st = s0_draw_device(ctx, nlsp_host::mix_seed(seed, 0x736d6f6f), nlive * k, mask ? dlivebuf : d->d, &redo);
+        if (!st && !redo && mask && nlive)
+            launch_s0_scatter(ctx->lc, dlivebuf, 0, (long long)(nlive * k), (int)k, dlive, d->d);
+        if (mask) {
+            if (!st) de = cudaStreamSynchronize(ctx->s);  // live (host vector) is read by the copy above
+            sfree(ctx, dlive);
+            sfree(ctx, dlivebuf);
+            dlive = nullptr;
+            if (!st && de) st = cuda_fail(ctx, de, "generate_smoothed_vectors scatter");
+        }
+        if (st) {
+            nlsp_dense_destroy(d);
+            return st;
+        }
+        if (!redo) {
+            ctx->last_s0_draw = NLSP_S0_DRAW_DEVICE;
+            st = smooth_impl(ctx, a, d, sweeps, omega);
+            if (st) {
+                nlsp_dense_destroy(d);
+                return st;
+            }
+            *out = d;
+            return NLSP_OK;
+        }
+        // a zero u1 in the stream (or a stream beyond the jump table): the host draw below
+    }
+    for (int b = 0; b < 2; ++b) {
+        cudaError_t pe = cudaSuccess;
+        if (!ctx->s0_pin[b]) pe = cudaMallocHost(&ctx->s0_pin[b], sizeof(double) * 2 * kChunkPairs);
+        if (!pe && !ctx->s0_ev[b]) pe = cudaEventCreateWithFlags(&ctx->s0_ev[b], cudaEventDisableTiming);
+        if (pe) {
+            nlsp_dense_destroy(d);
+            return cuda_fail(ctx, pe, "generate_smoothed_vectors staging");
+        }
+    }
     auto cleanup = [&]() {
         sfree(ctx, dlive);
         sfree(ctx, dstage[0]);

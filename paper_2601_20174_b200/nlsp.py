@@ -95,6 +95,24 @@ class Context:
     def synchronize(self):
         _check(self, L.gpu_lib().nlsp_ctx_synchronize(self.handle))
 
+    def set_s0_draw(self, where: str):
+        """Where generate_smoothed_vectors draws S^(0): "host" (default,
+        bit-identical to the reference's Rng stream) or "device" (the same
+        mt19937_64 words by jump-ahead, CUDA's log / sincos in Box-Muller)."""
+        modes = {"host": L.NLSP_S0_DRAW_HOST, "device": L.NLSP_S0_DRAW_DEVICE}
+        if where not in modes:
+            raise ValidationError("set_s0_draw: 'host' or 'device'")
+        _check(self, L.gpu_lib().nlsp_ctx_set_s0_draw(self.handle, modes[where]))
+
+    def last_s0_draw(self) -> str:
+        return "device" if L.gpu_lib().nlsp_ctx_last_s0_draw(self.handle) == L.NLSP_S0_DRAW_DEVICE else "host"
+
+    def mt19937_64_words(self, seed: int, count: int) -> np.ndarray:
+        """The first `count` outputs of std::mt19937_64(seed) from the device jump tree."""
+        out = np.empty(count, dtype=np.uint64)
+        _check(self, L.gpu_lib().nlsp_mt19937_64_words(self.handle, seed, count, L.u64ptr(out)))
+        return out
+
     def close(self):
         if self.handle:
             L.gpu_lib().nlsp_ctx_destroy(self.handle)
