@@ -152,7 +152,7 @@ def byte_model_literal(n, nnz, k, nu1, nu2):
     return (1 + nu1 + nu2) * csr + 16.0 * n * k + v * n
 
 
-def byte_model(n, nnz, k, nu1, nu2, pass_bytes=None, cycle="onepass", const_wd=False):
+def byte_model(n, nnz, k, nu1, nu2, pass_bytes=None, cycle="onepass", const_wd=False, fused_sweeps=False):
     """Algorithmic HBM bytes per PCG iteration of the schedule this library runs
     (DESIGN.md §3). Folded cycle: spmv_p (A + 32n), update+restriction through
     W1 (8nk + 48n), nu1+nu2-1 smoothing sweeps (A + 24n for the first, A + 32n
@@ -161,7 +161,9 @@ def byte_model(n, nnz, k, nu1, nu2, pass_bytes=None, cycle="onepass", const_wd=F
     pass over W that also gathers A s (8nk + A + 24n; 8nk + 16n without sweeps);
     the update and the first two sweeps are one kernel (A + 64n), later sweeps
     A + 32n. const_wd: the constant-coefficient diagonal form, whose w D^-1 is
-    one kernel parameter (8n less per sweep pass).
+    one kernel parameter (8n less per sweep pass). fused_sweeps: the update and
+    ALL the sweeps are one line-march kernel (A + 56n, lmarch.cuh: 2D
+    constant-coefficient stencils).
     A = the matrix bytes one pass streams: CSR 12 nnz + 4(n+1), or the diagonal
     form's own bytes when the upload detected one (nlsp_csr_format; SURVEY
     §8d's rule for stencil-specialised kernels)."""
@@ -174,6 +176,8 @@ def byte_model(n, nnz, k, nu1, nu2, pass_bytes=None, cycle="onepass", const_wd=F
     wd = 0.0 if const_wd else 8.0
     if cycle == "onepass":
         pro = 8.0 * n * ld + ((csr + 24.0 * n) if t >= 1 else 16.0 * n)
+        if t >= 2 and fused_sweeps:  # x, p, q, r; writes x, r', s_t
+            return (csr + 32.0 * n) + (csr + 56.0 * n) + pro
         if t >= 2:  # x/r update fused with two sweeps (x, p, q, r, w; writes x, r', s), then t - 2 sweeps
             return (csr + 32.0 * n) + (csr + (56.0 + wd) * n) + (t - 2) * (csr + (24.0 + wd) * n) + pro
         return (csr + 32.0 * n) + 48.0 * n + pro
@@ -373,7 +377,9 @@ def run_ours(args, dist: Dist):
     if cycle == "literal":
         bytes_iter = bytes_iter_csr = byte_model_literal(pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2)
     else:
-        bytes_iter = byte_model(pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2, pass_bytes, cycle, fmt_kind == 1)
+        fused_sweeps = "update_sweeps_fused" in kernels
+        bytes_iter = byte_model(pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2, pass_bytes, cycle, fmt_kind == 1,
+                                fused_sweeps)
         bytes_iter_csr = byte_model(pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2, None, cycle)
     iter_gbs = bytes_iter * iters / (ms_local / 1e3) / 1e9
     traffic = ncu_traffic(dominant, args.config)
@@ -384,6 +390,10 @@ def run_ours(args, dist: Dist):
                 "iteration": {"bytes_per_iter": bytes_iter, "achieved": round(iter_gbs, 1),
                               "frac": round(iter_gbs / peak, 4),
                               "cycle": cycle,
+                              "sweeps": "fused line march" if "update_sweeps_fused" in kernels else "separate kernels",
+                              "separate_sweeps_bytes_per_iter": byte_model(
+                                  pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2, pass_bytes, cycle, fmt_kind == 1)
+                              if cycle != "literal" else None,
                               "folded_cycle_bytes_per_iter": byte_model(
                                   pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2, pass_bytes, "folded", fmt_kind == 1),
                               "matrix_form": ["csr", "diagonal-constant", "diagonal-values"][fmt_kind],

@@ -91,6 +91,7 @@ void launch_col_axpy(const LaunchCtx&, long long, int, const double*, int, doubl
 void launch_col_move(const LaunchCtx&, long long, int, double*, int, double*, const double*, int, long long);
 void launch_transpose(const LaunchCtx&, long long, int, const double*, double*);
 bool march_planned(const LaunchCtx&, const SolveArgs&);
+bool launch_lfused(const LaunchCtx&, const SolveArgs&, unsigned long long);
 void launch_s0_scatter(const LaunchCtx&, const double*, long long, long long, int, const int*, double*);
 void launch_mt_stream(const LaunchCtx&, unsigned long long*, long long, int, const unsigned long long*, int,
                       unsigned long long, unsigned long long, unsigned long long*, unsigned long long*);
@@ -1995,7 +1996,7 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
     const double csr = 12.0 * nnz + 4.0 * (n + 1);
     const double pass = (double)a->pass_bytes;  // CSR, or the diagonal form when detected
     // algorithmic bytes per launch; slots by name below
-    enum { kSpmvP = 0, kUpd, kRes, kPro, kPost, kUR, kSmooth, kCtl, kUO, kPO, kUS, kSlots };
+    enum { kSpmvP = 0, kUpd, kRes, kPro, kPost, kUR, kSmooth, kCtl, kUO, kPO, kUS, kUSF, kSlots };
     const bool onepass = mode == 0 && m->onepass;
     const unsigned long long T = m ? m->nu1 + m->nu2 : 0;
     std::vector<Acc> acc = {
@@ -2013,6 +2014,8 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
         {"prolong_onepass", 8.0 * n * k + (T ? pass + 24.0 * n : 16.0 * n)},
         // x/r update fused with the T = 2 sweeps: A, x, p, q, r, w; writes x, r', s
         {"update_sweep", pass + (args.wdc != 0.0 ? 56.0 : 64.0) * n},
+        // ... fused with ALL T sweeps (lmarch.cuh): A, x, p, q, r; writes x, r', s_T
+        {"update_sweeps_fused", pass + 56.0 * n},
     };
     if ((int)acc.size() != kSlots) return -1;
     std::vector<cudaEvent_t> evs(2);
@@ -2031,7 +2034,22 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
     const bool simple_apply = mode == 0 && !folded && m->nu1 == 1 && m->nu2 == 1;
     for (uint64_t it = 0; it < iters; ++it) {
         timed(kSpmvP, [&] { launch_spmv_p(ctx->lc, args); });
+        bool fused = false;
         if (onepass && update_sweep_ok(args, T)) {
+            cudaEventRecord(evs[0], ctx->s);
+            fused = launch_lfused(ctx->lc, args, T);
+            if (fused) {
+                cudaEventRecord(evs[1], ctx->s);
+                cudaEventSynchronize(evs[1]);
+                float tf = 0.f;
+                cudaEventElapsedTime(&tf, evs[0], evs[1]);
+                acc[kUSF].ms += tf;
+                acc[kUSF].launches++;
+            }
+        }
+        if (fused) {
+            timed(kPO, [&] { launch_prolong_onepass(ctx->lc, args, ctx->zt0, ctx->z, 0, 1, 1); });
+        } else if (onepass && update_sweep_ok(args, T)) {
             timed(kUS, [&] { launch_update_sweep(ctx->lc, args); });
             double* cur = ctx->zt0;
             for (unsigned long long j = 3; j <= T; ++j) {

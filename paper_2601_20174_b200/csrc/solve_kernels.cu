@@ -1656,6 +1656,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_prolong_onepass(SolveArgs a, co
 #ifndef NLSP_OP_TR
 #define NLSP_OP_TR 64
 #endif
+#ifndef NLSP_LFUSED_DEFAULT
+#define NLSP_LFUSED_DEFAULT 1
+#endif
 constexpr int kOpTR = NLSP_OP_TR;  // rows per tile (64 or 128)
 static_assert(kOpTR == 64 || kOpTR == 128, "one-pass tiles are 64 or 128 rows");
 constexpr int kOpWWarps = 8;   // W-product warps
@@ -2125,6 +2128,7 @@ struct OpUpdSweep {
 };
 
 #include "march.cuh"
+#include "lmarch.cuh"
 
 // ======================================================== host launchers ==
 
@@ -2419,6 +2423,82 @@ static bool launch_march_op(const LaunchCtx& c, const SolveArgs& a, const Op& op
     else if (a.dia.d <= 16 && !rv) go(k_march<Op, 16, unsigned short, false, false>);
     else return false;
 #undef NLSP_MARCH_GO
+    return true;
+}
+
+// ---- fused line march (lmarch.cuh) -----------------------------------------
+static int lmarch_env(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+
+template <int PAT>
+static bool line_pattern_ok(const SolveArgs& a, long long Lw) {
+    using Pat = LinePat<PAT>;
+    if (a.dia.d != PAT) return false;
+    for (int t = 0; t < PAT; ++t)
+        if (a.dia.off[t] != Pat::dl(t) * Lw + Pat::dx(t)) return false;
+    return true;
+}
+
+// The x/r update and all T sweeps in one line march (k_lfused): 2D
+// constant-coefficient patterns, T = 2 or 4. NLSP_LFUSED=0 keeps the separate kernels.
+bool launch_lfused(const LaunchCtx& c, const SolveArgs& a, unsigned long long T) {
+    static const int on = lmarch_env("NLSP_LFUSED", NLSP_LFUSED_DEFAULT);
+    if (!on || a.dia.kind != 1 || a.wdc == 0.0 || (T != 2 && T != 4) || a.dia.plane <= 0 || a.dia.halo > 2) return false;
+    if (a.n < (1 << 16)) return false;
+    const long long Lw = a.dia.plane;
+    if (Lw < 128 || a.n % Lw) return false;
+    LineGeom g{};
+    g.Lw = (int)Lw;
+    g.NL = (int)(a.n / Lw);
+    int pat = 0;
+    if (line_pattern_ok<9>(a, Lw)) pat = 9;
+    else if (line_pattern_ok<5>(a, Lw)) pat = 5;
+    else return false;
+    const int NS = (int)T - 1;
+    // slabs of 128 columns, overlapping by pad columns on either side
+    g.C = 128;
+    g.pad = 4;  // >= NS: a slab's valid columns move in by one per stencil stage
+    g.Ci = g.C - 2 * g.pad;
+    g.S = (int)((Lw + g.Ci - 1) / g.Ci);
+    if (g.NL < 4 * NS + 4) return false;
+    static const int ctas = lmarch_env("NLSP_LFUSED_CTAS", 0);
+    const int mb = pat == 9 ? 2 : 1;
+    const size_t smem = (size_t)(NS * kFusedSSlots + kFusedSlots) * (g.C + 2) * sizeof(double) +
+                        (size_t)kFusedSlots * (g.C + 2) * mb;
+    auto go = [&](auto kern) {
+        static std::mutex mu;
+        static std::unordered_map<unsigned long long, int> occ;
+        int nb = 1;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            const unsigned long long key =
+                reinterpret_cast<unsigned long long>(reinterpret_cast<const void*>(kern)) * 1315423911ull ^ (unsigned)g.C;
+            auto it = occ.find(key);
+            if (it == occ.end()) {
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, g.C, smem) != cudaSuccess || nb < 1) nb = 1;
+                cudaGetLastError();
+                occ[key] = nb;
+            } else {
+                nb = it->second;
+            }
+        }
+        if (ctas > 0 && ctas < nb) nb = ctas;
+        long long G = (long long)c.num_sms * nb;
+        const long long TT = (long long)g.S * g.NL;
+        if (G > TT) G = TT;
+        if (G > kMaxGrid) G = kMaxGrid;
+        klaunch(c, kern, (int)G, g.C, smem, a, OpUpdSweep<true>{}, g);
+    };
+#define NLSP_LF_GO(PAT, MT, NSS) go(k_lfused<PAT, MT, NSS, 2>)
+    if (pat == 9 && NS == 3) NLSP_LF_GO(9, unsigned short, 3);
+    else if (pat == 9) NLSP_LF_GO(9, unsigned short, 1);
+    else if (NS == 3) NLSP_LF_GO(5, unsigned char, 3);
+    else NLSP_LF_GO(5, unsigned char, 1);
+#undef NLSP_LF_GO
+    count(c);
     return true;
 }
 
@@ -2870,6 +2950,10 @@ void launch_onepass_tail(const LaunchCtx& c, const SolveArgs& a, unsigned long l
 // one iteration after k_spmv_p: fused update + sweeps (T = 2) when possible
 void launch_onepass_iteration_tail(const LaunchCtx& c, const SolveArgs& a, unsigned long long T,
                                    cudaGraphConditionalHandle h, int ctl) {
+    if (update_sweep_ok(a, T) && launch_lfused(c, a, T)) {  // s_T -> zt0
+        launch_prolong_onepass(c, a, a.zt0, a.z, h, ctl, 1);
+        return;
+    }
     if (update_sweep_ok(a, T)) {
         launch_update_sweep(c, a);  // s_2 -> zt0
         double* cur = a.zt0;

@@ -176,6 +176,29 @@ def test_march_matches_direct_kernels(tmp_path, cfg, nx):
     assert i1["true"] < 1e-7
 
 
+@pytest.mark.parametrize("cfg,nx", [("C3", 512), ("C3", 360), ("C1", 512), ("C1", 300)])
+def test_fused_line_march_matches_separate_kernels(tmp_path, cfg, nx):
+    """The x/r update and all the sweeps in one line-march kernel (lmarch.cuh,
+    2D constant-coefficient stencils: C3 with nu = 2/2 chains three stencil
+    stages, the 5-point C1 family one) against the separate update + sweep
+    kernels (NLSP_LFUSED=0): the same rows bit for bit, ||r||^2 summed in another
+    order. 512: slabs of 120 columns with overlaps and a short last slab; 360
+    and 300: line widths that are no multiple of the slab width (nor of 32)."""
+    res = {}
+    for mode in ("0", "1"):
+        out = str(tmp_path / f"x_{mode}.npy")
+        code = MARCH_SCRIPT.format(root=ROOT, cfg=cfg, nx=nx, out=out)
+        p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                           env=dict(os.environ, NLSP_LFUSED=mode, NLSP_CLUSTER="0"))
+        assert p.returncode == 0, p.stderr[-3000:]
+        res[mode] = (json.loads(p.stdout.strip().splitlines()[-1]), np.load(out))
+    (i0, x0), (i1, x1) = res["0"], res["1"]
+    assert i0["repeat_equal"] and i1["repeat_equal"]
+    assert abs(i0["iterations"] - i1["iterations"]) <= 1
+    assert np.linalg.norm(x1 - x0) <= 1e-10 * np.linalg.norm(x0)
+    assert i1["true"] < 1e-7
+
+
 @pytest.fixture(scope="module")
 def graph_ctx(nlsp):
     os.environ["NLSP_CLUSTER"] = "0"
