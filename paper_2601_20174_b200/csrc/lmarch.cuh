@@ -122,6 +122,12 @@ __global__ void __launch_bounds__(128, NLSP_LFUSED_MINB) k_lfused(SolveArgs a, O
             lo[k] = max(la - (NS - k), 0);
             cnt[k] = (unsigned)max(min(lb + (NS - k), g.NL) - lo[k], 0);
         }
+        // this thread's own column of the three lines stage k reads (s_k of lines
+        // Ak - 1, Ak, Ak + 1): it wrote them itself, so they stay in registers
+        // and only the left and right neighbours come from the rings
+        double own[NS + 1][3];
+#pragma unroll
+        for (int k = 0; k <= NS; ++k) own[k][0] = own[k][1] = own[k][2] = 0.0;
         Raw rq[D];
 #pragma unroll
         for (int u = 0; u < D; ++u) load_line(rq[u], line_row(la - NS + u));
@@ -140,25 +146,16 @@ __global__ void __launch_bounds__(128, NLSP_LFUSED_MINB) k_lfused(SolveArgs a, O
                     for (int q = 0; q < 4; ++q) b4[q] = ((A0 + 64 + q) & (kFusedSSlots - 1)) * W + 1 + c;
 #pragma unroll
                     for (int k = 0; k <= NS; ++k) b8[k] = ((A0 + 64 - 2 * k) & (kFusedSlots - 1)) * W + 1 + c;
-                    // ---- stage 0: r' = r - alpha q, s_1 = w r', x' = x + alpha p
-                    if (j < n0) {
-                        const Raw v = rq[u];
-                        if (j + D < n0) load_line(rq[u], line_row(A0 + D));
-                        const double rn = fma(-alpha, v.q, v.r);
-                        ringS[b4[0]] = wc * rn;
-                        ringR[b8[0]] = rn;
-                        ringM[b8[0]] = (MT)v.m;
-                        if (evaluates && (unsigned)(A0 - la) < (unsigned)(lb - la)) {
-                            const int row = orow + 2 * NS * g.Lw;
-                            op.rn[row] = rn;
-                            op.x[row] = fma(alpha, v.p, v.x);
-                            s[0] = fma(rn, rn, s[0]);
-                        }
-                    }
-                    // ---- stencil stages: s_{k+1} of the line 2 k behind stage 0
+                    // this step's line of stage 0: take it from the prefetch ring, refill the ring
+                    Raw v = rq[u];
+                    if (j + D < n0) load_line(rq[u], line_row(A0 + D));
+                    // ---- stencil stages, last first: s_{k+1} of the line 2 k behind stage 0.
+                    // own[k - 1] then still holds s_k of lines Ak - 1, Ak, Ak + 1 (stage
+                    // k - 1 pushes this step's line after stage k has run)
 #pragma unroll
-                    for (int k = 1; k <= NS; ++k) {
+                    for (int k = NS; k >= 1; --k) {
                         const int Ak = A0 - 2 * k;
+                        double zo = 0.0;
                         if ((unsigned)(Ak - lo[k]) < cnt[k]) {
                             const double* in = ringS + (k - 1) * kFusedSSlots * W;
                             // lines Ak - 1, Ak, Ak + 1 = A0 + (-2 k - 1, -2 k, -2 k + 1)
@@ -167,7 +164,8 @@ __global__ void __launch_bounds__(128, NLSP_LFUSED_MINB) k_lfused(SolveArgs a, O
                             const unsigned m = ringM[b8[k]];
                             double gv[PAT];
 #pragma unroll
-                            for (int tt = 0; tt < PAT; ++tt) gv[tt] = in[b[Pat::dl(tt) + 1] + Pat::dx(tt)];
+                            for (int tt = 0; tt < PAT; ++tt)
+                                gv[tt] = Pat::dx(tt) == 0 ? own[k - 1][Pat::dl(tt) + 1] : in[b[Pat::dl(tt) + 1] + Pat::dx(tt)];
                             double y = 0.0;
                             if (m == kFull) {
 #pragma unroll
@@ -177,11 +175,32 @@ __global__ void __launch_bounds__(128, NLSP_LFUSED_MINB) k_lfused(SolveArgs a, O
                                 for (int tt = 0; tt < PAT; ++tt)
                                     if ((m >> tt) & 1u) y = fma(a.dia.val[tt], gv[tt], y);
                             }
-                            const double zo = fma(wc, ringR[b8[k]] - y, in[b[1]]);
-                            if (k < NS) {
-                                ringS[k * kFusedSSlots * W + b[1]] = zo;
-                            } else if (evaluates) {
-                                op.sout[orow] = zo;
+                            zo = fma(wc, ringR[b8[k]] - y, own[k - 1][1]);
+                            if (k < NS) ringS[k * kFusedSSlots * W + b4[(4 * NS - 2 * k) & 3]] = zo;
+                            else if (evaluates) op.sout[orow] = zo;
+                        }
+                        if (k < NS) {  // every step pushes (a line outside the stage's range: a placeholder)
+                            own[k][0] = own[k][1];
+                            own[k][1] = own[k][2];
+                            own[k][2] = zo;
+                        }
+                    }
+                    // ---- stage 0: r' = r - alpha q, s_1 = w r', x' = x + alpha p
+                    {
+                        const double rn = fma(-alpha, v.q, v.r);
+                        const double s1 = wc * rn;
+                        own[0][0] = own[0][1];
+                        own[0][1] = own[0][2];
+                        own[0][2] = s1;
+                        if (j < n0) {
+                            ringS[b4[0]] = s1;
+                            ringR[b8[0]] = rn;
+                            ringM[b8[0]] = (MT)v.m;
+                            if (evaluates && (unsigned)(A0 - la) < (unsigned)(lb - la)) {
+                                const int row = orow + 2 * NS * g.Lw;
+                                op.rn[row] = rn;
+                                op.x[row] = fma(alpha, v.p, v.x);
+                                s[0] = fma(rn, rn, s[0]);
                             }
                         }
                     }
