@@ -174,6 +174,13 @@ def byte_model(n, nnz, k, nu1, nu2, pass_bytes=None, cycle="onepass", const_wd=F
     if t >= 2:
         sweeps = (csr + 24.0 * n) + (t - 2) * (csr + 32.0 * n)
     wd = 0.0 if const_wd else 8.0
+    if cycle == "lean":
+        # lean one-pass cycle (t >= 2): q = A p in the gather with the x/r update
+        # (A, p, x, r; writes x, r: A + 40n), s = S_2(r) gathering r alone
+        # (A + 16n, + w when not constant), t - 2 later sweeps, and the pass over W
+        # that writes p = s + W e + beta p (W, A for A s, s, r, p; writes p)
+        pro = 8.0 * n * ld + csr + 32.0 * n
+        return (csr + 40.0 * n) + (csr + (16.0 + wd) * n) + (t - 2) * (csr + (24.0 + wd) * n) + pro
     if cycle == "onepass":
         pro = 8.0 * n * ld + ((csr + 24.0 * n) if t >= 1 else 16.0 * n)
         if t >= 2 and fused_sweeps:  # x, p, q, r; writes x, r', s_t

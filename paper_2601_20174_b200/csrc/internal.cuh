@@ -46,6 +46,10 @@ struct PcgState {
     int op_grid;               // CTAs of the last one-pass prolongation (its partials' stride)
     double alpha_prev;         // alpha of the previous iteration (one-pass restriction)
     double drift_max;          // max over the solve of |c_rec - W^T r| / |W^T r| (one-pass guard)
+    // lean one-pass cycle (solve_kernels.cu): c.e and e.Me of the
+    // current coarse correction, the p.Ap predicted after the pass over W, and
+    // the max over the solve of |predicted - direct| / direct (its guard)
+    double lean_ce, lean_eme, pap_pred, pap_drift;
 };
 
 // Ticket slots (each kernel kind reuses its own counter; counters return to 0).
@@ -110,9 +114,9 @@ struct SolveArgs {
     double* partials;    // kMaxGrid * max(k, 4)
     double* e;           // coarse correction, k
     // one-pass cycle (solve_kernels.cu): M = W^T A W (k x k),
-    // ow = [u_even | u_odd | v | c] column sums (4 ld; c = the last recurrence
-    // value, for the drift guard), opart = per-CTA partials of
-    // [u | v], column-major
+    // ow = [u_even | u_odd | v | c | M e] column sums (5 ld; c = the last
+    // recurrence value, for the drift guard; M e: lean cycle), opart = per-CTA
+    // partials of [u | v], column-major
     const double* M;
     double* ow;
     double* opart;

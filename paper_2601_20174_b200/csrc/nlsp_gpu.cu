@@ -46,7 +46,13 @@ void launch_folded_tail(const LaunchCtx&, const SolveArgs&, unsigned long long, 
 void launch_folded_apply(const LaunchCtx&, const SolveArgs&, unsigned long long, unsigned long long);
 bool onepass_supported(int k);
 void launch_prolong_onepass(const LaunchCtx&, const SolveArgs&, const double*, double*,
-                            cudaGraphConditionalHandle, int, int);
+                            cudaGraphConditionalHandle, int, int, int);
+bool lean_supported(const SolveArgs&, unsigned long long);
+void launch_spmv_upd(const LaunchCtx&, const SolveArgs&);
+const double* launch_lean_sweeps(const LaunchCtx&, const SolveArgs&, unsigned long long);
+void launch_lean_iteration(const LaunchCtx&, const LaunchCtx&, const SolveArgs&, unsigned long long,
+                           cudaGraphConditionalHandle, int);
+void launch_lean_apply(const LaunchCtx&, const SolveArgs&, unsigned long long);
 bool update_sweep_ok(const SolveArgs&, unsigned long long);
 void launch_sweeps_rpar(const LaunchCtx&, const SolveArgs&, unsigned long long, double**);
 void launch_update_sweep(const LaunchCtx&, const SolveArgs&);
@@ -156,6 +162,7 @@ struct nlsp_twolevel {
     double* W2;      // (I - w D^-1 A)^nu2 P, n x ld (aliases W1 when nu1 == nu2)
     bool folded;     // folded cycle (default) or the literal schedule (NLSP_CYCLE=literal)
     bool onepass;    // PCG streams W once per iteration (nu1 == nu2, k <= 64; NLSP_CYCLE=folded: twice)
+    bool lean;       // one-pass with beta before and alpha after the pass (NLSP_CYCLE=onepass: off)
     double* M;       // W^T A W, k x k (one-pass restriction recurrence)
 };
 
@@ -355,7 +362,7 @@ nlsp_status ensure_ws(nlsp_ctx* ctx, long long n, long long hist) {
             CU(dalloc(p, (size_t)n + 16));  // padded for 16-B bulk copies of tile slices
         CU(dalloc(&ctx->e, (size_t)kMaxCoarse + 2));
         CU(dalloc(&ctx->partials, (size_t)kMaxGrid * 256));
-        CU(dalloc(&ctx->ow, (size_t)4 * (kOnePassK + 2)));
+        CU(dalloc(&ctx->ow, (size_t)5 * (kOnePassK + 2)));
         CU(dalloc(&ctx->opart, (size_t)kMaxGrid * 3 * (kOnePassK + 2)));
         // q feeds the one-pass partials of the PCG prologue (weighted by 0)
         CU(cudaMemsetAsync(ctx->q, 0, ((size_t)n + 16) * 8, ctx->s));
@@ -432,6 +439,13 @@ const int g_unroll = [] {
 // One PCG iteration (the WHILE body). mode: 0 two-level, 1 identity, 2 Jacobi.
 void enqueue_iteration(const LaunchCtx& lc, const SolveArgs& a, int mode, const nlsp_twolevel* m,
                        cudaGraphConditionalHandle h, int use_cond) {
+    if (mode == 0 && m->lean) {
+        // every kernel after the first of an iteration is launched with PDL
+        LaunchCtx lp = lc;
+        lp.pdl = g_pdl;
+        launch_lean_iteration(lc, lp, a, m->nu1 + m->nu2, h, use_cond ? 2 : 1);
+        return;
+    }
     launch_spmv_p(lc, a);
     if (mode == 0 && m->onepass) {
         // x, r, ||r||, c by its recurrence, e (+ the sweeps when fused); prolongation.
@@ -458,7 +472,8 @@ void enqueue_prologue(const LaunchCtx& lc, const SolveArgs& a, int mode, const n
                       const double* params_dev) {
     (void)params_dev;
     launch_bnorm(lc, a);
-    if (mode == 0 && m->onepass) launch_onepass_apply(lc, a, m->nu1 + m->nu2);
+    if (mode == 0 && m->lean) launch_lean_apply(lc, a, m->nu1 + m->nu2);
+    else if (mode == 0 && m->onepass) launch_onepass_apply(lc, a, m->nu1 + m->nu2);
     else if (mode == 0 && m->folded) launch_folded_apply(lc, a, m->nu1, m->nu2);
     else if (mode == 0) launch_twolevel_apply(lc, a, m->nu1, m->nu2);
     else launch_init_simple(lc, a, mode == 2 ? 1 : 0);
@@ -699,7 +714,10 @@ const double g_drift_tol = [] {
 nlsp_status run_pcg_guarded(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twolevel* m,
                             double delta, unsigned long long max_iters, nlsp_solve_report* rep) {
     nlsp_status st = run_pcg(ctx, a, kind, m, delta, max_iters, rep);
-    const double drift = ctx->st_host->drift_max;
+    // the lean cycle's second guard: the predicted p.Ap against the direct one
+    const double drift = (m && m->lean && kind == NLSP_PRECOND_TWOLEVEL)
+                             ? std::max(ctx->st_host->drift_max, ctx->st_host->pap_drift)
+                             : ctx->st_host->drift_max;
     if (rep) {
         rep->onepass_drift = drift;
         rep->cycle_fallback = 0;
@@ -707,6 +725,7 @@ nlsp_status run_pcg_guarded(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nl
     if (st != NLSP_OK || kind != NLSP_PRECOND_TWOLEVEL || !m->onepass || !(drift > g_drift_tol)) return st;
     nlsp_twolevel folded = *m;  // same device arrays, W streamed twice per iteration
     folded.onepass = false;
+    folded.lean = false;
     folded.id = m->id | (1ull << 63);
     const double ms0 = rep ? rep->solve_ms : 0.0;
     const unsigned long long l0 = rep ? rep->kernel_launches : 0;
@@ -1843,6 +1862,11 @@ nlsp_status nlsp_twolevel_build(nlsp_ctx* ctx, const nlsp_csr* a, const nlsp_den
         nlsp_twolevel_destroy(m);
         return map_dev_error(ctx, f[10], "cholesky");
     }
+    {
+        const char* cyc = std::getenv("NLSP_CYCLE");
+        m->lean = m->onepass && !(cyc && std::strcmp(cyc, "onepass") == 0) &&
+                  lean_supported(make_args(ctx, a, m), nu1 + nu2);
+    }
     *out = m;
     return NLSP_OK;
 }
@@ -1857,7 +1881,7 @@ void nlsp_twolevel_destroy(nlsp_twolevel* m) {
 
 int nlsp_twolevel_cycle(const nlsp_twolevel* m) {
     if (!m) return -1;
-    return m->onepass ? 2 : (m->folded ? 1 : 0);
+    return m->lean ? 3 : (m->onepass ? 2 : (m->folded ? 1 : 0));
 }
 
 void nlsp_twolevel_dims(const nlsp_twolevel* m, uint64_t* n, uint64_t* k) {
@@ -1996,7 +2020,7 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
     const double csr = 12.0 * nnz + 4.0 * (n + 1);
     const double pass = (double)a->pass_bytes;  // CSR, or the diagonal form when detected
     // algorithmic bytes per launch; slots by name below
-    enum { kSpmvP = 0, kUpd, kRes, kPro, kPost, kUR, kSmooth, kCtl, kUO, kPO, kUS, kUSF, kSlots };
+    enum { kSpmvP = 0, kUpd, kRes, kPro, kPost, kUR, kSmooth, kCtl, kUO, kPO, kUS, kUSF, kSU, kSL, kPL, kSlots };
     const bool onepass = mode == 0 && m->onepass;
     const unsigned long long T = m ? m->nu1 + m->nu2 : 0;
     std::vector<Acc> acc = {
@@ -2016,6 +2040,12 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
         {"update_sweep", pass + (args.wdc != 0.0 ? 56.0 : 64.0) * n},
         // ... fused with ALL T sweeps (lmarch.cuh): A, x, p, q, r; writes x, r', s_T
         {"update_sweeps_fused", pass + 56.0 * n},
+        // lean cycle: A, p (gathered), x, r; writes x, r
+        {"spmv_update", pass + 40.0 * n},
+        // ... A, r (gathered), w; writes s
+        {"sweep_lean", pass + (args.wdc != 0.0 ? 16.0 : 24.0) * n},
+        // ... W, A (A s), s, r, p; writes p
+        {"prolong_lean", 8.0 * n * k + pass + 32.0 * n},
     };
     if ((int)acc.size() != kSlots) return -1;
     std::vector<cudaEvent_t> evs(2);
@@ -2032,7 +2062,19 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
     };
     const bool folded = mode == 0 && m->folded;
     const bool simple_apply = mode == 0 && !folded && m->nu1 == 1 && m->nu2 == 1;
+    const bool lean = mode == 0 && m->lean;
     for (uint64_t it = 0; it < iters; ++it) {
+        if (lean) {
+            timed(kSU, [&] { launch_spmv_upd(ctx->lc, args); });
+            const double* sv = nullptr;
+            if (T == 2) {
+                timed(kSL, [&] { sv = launch_lean_sweeps(ctx->lc, args, T); });
+            } else {  // the T - 1 sweep launches together
+                timed(kSmooth, [&] { sv = launch_lean_sweeps(ctx->lc, args, T); });
+            }
+            timed(kPL, [&] { launch_prolong_onepass(ctx->lc, args, sv, ctx->p0, 0, 1, 0, 1); });
+            continue;
+        }
         timed(kSpmvP, [&] { launch_spmv_p(ctx->lc, args); });
         bool fused = false;
         if (onepass && update_sweep_ok(args, T)) {
@@ -2048,7 +2090,7 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
             }
         }
         if (fused) {
-            timed(kPO, [&] { launch_prolong_onepass(ctx->lc, args, ctx->zt0, ctx->z, 0, 1, 1); });
+            timed(kPO, [&] { launch_prolong_onepass(ctx->lc, args, ctx->zt0, ctx->z, 0, 1, 1, 0); });
         } else if (onepass && update_sweep_ok(args, T)) {
             timed(kUS, [&] { launch_update_sweep(ctx->lc, args); });
             double* cur = ctx->zt0;
@@ -2057,7 +2099,7 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
                 timed(kSmooth, [&] { launch_sweeps_rpar(ctx->lc, args, 3, &c1); });  // one sweep
                 cur = c1;
             }
-            timed(kPO, [&] { launch_prolong_onepass(ctx->lc, args, cur, ctx->z, 0, 1, 1); });
+            timed(kPO, [&] { launch_prolong_onepass(ctx->lc, args, cur, ctx->z, 0, 1, 1, 0); });
         } else if (onepass) {
             timed(kUO, [&] { launch_update_onepass(ctx->lc, args); });
             double* cur = nullptr;
@@ -2066,7 +2108,7 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
                 timed(kSmooth, [&] { launch_sweep(ctx->lc, args, cur == nullptr, cur, nxt, false); });
                 cur = nxt;
             }
-            timed(kPO, [&] { launch_prolong_onepass(ctx->lc, args, cur, ctx->z, 0, 1, 0); });
+            timed(kPO, [&] { launch_prolong_onepass(ctx->lc, args, cur, ctx->z, 0, 1, 0, 0); });
         } else if (folded) {
             timed(kUR, [&] { launch_update_restrict(ctx->lc, args, true); });
             // launch_folded_tail, each launch timed on its own

@@ -240,6 +240,7 @@ __global__ void k_state_init(PcgState* st, double delta, long long max_it) {
     st->max_it = max_it;
     st->hist_base = 0;
     st->drift_max = 0.0;
+    st->lean_ce = st->lean_eme = st->pap_pred = st->pap_drift = 0.0;
     st->iterations = 0;
     st->body_runs = 0;
     st->done = 0;
@@ -413,6 +414,19 @@ __device__ __forceinline__ void loop_ctl_body(PcgState* st, cudaGraphConditional
     st->body_runs += 1;
     if (!st->done) {
         st->beta = st->rz_new / st->rz;
+        st->rz = st->rz_new;
+        st->first = 0;
+        st->it += 1;
+        if (st->it >= st->max_it) st->done = 1;
+    }
+    if (use_cond && st->done) cudaGraphSetConditional(h, 0);
+}
+
+// Lean cycle: beta and r.z were already advanced by the sweep kernel's last CTA
+// (beta is needed before the pass over W); the pass only moves r.z on.
+__device__ __forceinline__ void loop_ctl_lean(PcgState* st, cudaGraphConditionalHandle h, int use_cond) {
+    st->body_runs += 1;
+    if (!st->done) {
         st->rz = st->rz_new;
         st->first = 0;
         st->it += 1;
@@ -629,6 +643,11 @@ __device__ __forceinline__ void restrict_finish(double (&acc)[2 * PPL], double r
             st->done = 1;
         }
     }
+    // c itself: the lean cycle's prologue forms r.z = r.s + c.e from it
+    if (a.ow && a.k <= kOnePassK) {
+        for (int c = threadIdx.x; c < a.k; c += blockDim.x) a.ow[3 * ld + c] = ys[c];
+        __syncthreads();
+    }
     if (a.Ainv) {
         coarse_apply_inverse(a.Ainv, a.k, ys, a.e);
         if (threadIdx.x == 0) {
@@ -824,6 +843,7 @@ struct OpSweep {
     double* zout;
     double wc = 0.0;    // constant w D^-1 (see GWdr)
     bool rpar = false;  // r = the residual the fused update + sweep wrote (r[(it + 1) & 1])
+    bool lean_fin = false;  // lean cycle, last sweep: r.z = r.s + c.e -> beta (see lean_last)
     __device__ __forceinline__ double operator()(int j) const { return g(j); }
     struct Pre {
         double ri, wi, gi;
@@ -839,7 +859,13 @@ struct OpSweep {
         if (rpar) r = (a.st->it & 1) ? a.r : a.r1;
     }
     __device__ __forceinline__ void finish(PcgState* st, const double* tot) const {
-        st->rz_new = tot[0];
+        if (lean_fin) {
+            const double g = tot[0] + st->lean_ce;
+            st->beta = g / st->rz;
+            st->rz_new = g;
+        } else {
+            st->rz_new = tot[0];
+        }
     }
 };
 
@@ -1688,7 +1714,7 @@ __host__ __device__ constexpr unsigned op_csr_bytes(int tile_nnz) {
     return round16((kOpTR + 4) * 4) + round16((tile_nnz + 2) * 8) + round16((tile_nnz + 8) * 4);
 }
 __host__ __device__ constexpr unsigned op_stage_bytes(int ld, int tile_nnz = -1) {
-    return (unsigned)kOpTR * ld * 8 + 2 * kOpVec + round16(kOpTR * 4) + kOpVec +
+    return (unsigned)kOpTR * ld * 8 + 2 * kOpVec + round16(kOpTR * 4) + 2 * kOpVec +
            (tile_nnz >= 0 ? op_csr_bytes(tile_nnz) : 0u);
 }
 
@@ -1696,14 +1722,21 @@ template <int PPL, int MAXD, bool RV>
 __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(SolveArgs a, const double* sv,
                                                                       double* zout,
                                                                       cudaGraphConditionalHandle h,
-                                                                      int ctl, int S, int P, int rsel) {
+                                                                      int ctl, int S, int P, int rsel, int lean) {
     pdl_entry();
     PcgState* st = a.st;
     if (st->done) {
-        if (ctl && blockIdx.x == 0 && threadIdx.x == 0) loop_ctl_body(st, h, ctl == 2);
+        if (ctl && blockIdx.x == 0 && threadIdx.x == 0) {
+            if (lean) loop_ctl_lean(st, h, ctl == 2);
+            else loop_ctl_body(st, h, ctl == 2);
+        }
         return;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) st->op_grid = gridDim.x;
+    // lean (DESIGN.md §3 "lean cycle"): 1 writes p = s + W e + beta p in place of
+    // z (zout = p, its old rows staged with the tile), 2 the prologue's p = s + W e;
+    // both reduce s.As and (W e).(A s) instead of r.z
+    const double lbeta = lean == 1 ? st->beta : 0.0;
     // rsel: the residual the fused update + sweep wrote (r[(it + 1) & 1]), else r
     const double* rv = (rsel && !(st->it & 1)) ? a.r1 : a.r;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -1716,10 +1749,11 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
     const unsigned wbytes = (unsigned)kOpTR * ld * 8;
     const int tile_nnz = kOpTR == 64 ? a.tile_nnz64 : a.tile_nnz128;
     const unsigned sbytes = op_stage_bytes(ld, MAXD ? -1 : tile_nnz);
-    // stage layout: [W rows | s | r | mask | A s | CSR: row_ptr | values | columns]
+    // stage layout: [W rows | s | r | mask | A s | p | CSR: row_ptr | values | columns]
     const unsigned s_off = wbytes, r_off = wbytes + kOpVec, m_off = wbytes + 2 * kOpVec;
     const unsigned as_off = m_off + round16(kOpTR * 4);
-    const unsigned rp_off = as_off + kOpVec;
+    const unsigned p_off = as_off + kOpVec;
+    const unsigned rp_off = p_off + kOpVec;
     const unsigned v_off = rp_off + round16((kOpTR + 4) * 4);
     const unsigned c_off = v_off + round16((tile_nnz + 2) * 8);
     if (threadIdx.x == 0) {
@@ -1737,7 +1771,7 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
     double au[2 * PPL], av[2 * PPL];
 #pragma unroll
     for (int t = 0; t < 2 * PPL; ++t) au[t] = av[t] = 0.0;
-    double rz[1] = {0.0};
+    double rz[2] = {0.0, 0.0};
     if (warp == 0) {
         // ---- producer (diagonal form): lane 0 issues each tile's bulk copies
         if (MAXD != 0 && lane == 0) {
@@ -1750,11 +1784,12 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
                 const unsigned vb = round16(rows * 8);  // vectors are padded by 16 doubles
                 const unsigned wb = (unsigned)rows * ld * 8;
                 const unsigned mbb = round16(rows * mb);  // masks are padded by 16 B
-                NLSP_CHECK(rows > 0 && rows <= kOpTR && wb <= s_off && m_off + mbb <= as_off && as_off + kOpVec <= sbytes);
-                mbar_arrive_tx(&full[stg], wb + (sv ? vb : 0u) + vb + mbb);
+                NLSP_CHECK(rows > 0 && rows <= kOpTR && wb <= s_off && m_off + mbb <= as_off && p_off + kOpVec <= sbytes);
+                mbar_arrive_tx(&full[stg], wb + (sv ? vb : 0u) + vb + mbb + (lean == 1 ? vb : 0u));
                 bulk_g2s(base_s, a.P + (long long)r0 * ld, wb, &full[stg]);
                 if (sv) bulk_g2s(base_s + s_off, sv + r0, vb, &full[stg]);
                 bulk_g2s(base_s + r_off, rv + r0, vb, &full[stg]);
+                if (lean == 1) bulk_g2s(base_s + p_off, zout + r0, vb, &full[stg]);
                 bulk_g2s(base_s + m_off, static_cast<const unsigned char*>(a.dia.mask) + (long long)r0 * mb,
                          mbb, &full[stg]);
             }
@@ -1797,10 +1832,11 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
                 }
                 NLSP_CHECK(rows > 0 && rows <= kOpTR && a1 >= a0 && a1 - a0 <= tile_nnz);
                 NLSP_CHECK(MAXD != 0 || (rp_off + cb <= v_off && v_off + cvb <= c_off && c_off + ccb <= sbytes));
-                mbar_arrive_tx(&full[stg], wb + (sv ? vb : 0u) + vb + mbb + cb + cvb + ccb);
+                mbar_arrive_tx(&full[stg], wb + (sv ? vb : 0u) + vb + mbb + cb + cvb + ccb + (lean == 1 ? vb : 0u));
                 bulk_g2s(base_s, a.P + (long long)r0 * ld, wb, &full[stg]);
                 if (sv) bulk_g2s(base_s + s_off, sv + r0, vb, &full[stg]);
                 bulk_g2s(base_s + r_off, rv + r0, vb, &full[stg]);
+                if (lean == 1) bulk_g2s(base_s + p_off, zout + r0, vb, &full[stg]);
                 if (MAXD)
                     bulk_g2s(base_s + m_off, static_cast<const unsigned char*>(a.dia.mask) + (long long)r0 * mb,
                              mbb, &full[stg]);
@@ -1882,6 +1918,7 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
             const double* ss = reinterpret_cast<const double*>(base + s_off);
             const double* rs = reinterpret_cast<const double*>(base + r_off);
             const double* as = reinterpret_cast<const double*>(base + as_off);
+            const double* ps = reinterpret_cast<const double*>(base + p_off);
 #pragma unroll
             for (int u = 0; u < kOpTR / (WPG * 4); ++u) {
                 const int lr = grp + WPG * 4 * u;
@@ -1904,9 +1941,17 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
                 }
                 const double sum = group_sum(part);
                 if (ok && l == 0) {
-                    const double zi = (sv ? ss[lr] : 0.0) + sum;
-                    zout[r0 + lr] = zi;
-                    rz[0] = fma(rr, zi, rz[0]);
+                    const double si = sv ? ss[lr] : 0.0;
+                    const double zi = si + sum;
+                    if (lean) {
+                        // p = z + beta p (two_level.hpp:182, the fma of GPupd)
+                        zout[r0 + lr] = lean == 1 ? fma(lbeta, ps[lr], zi) : zi;
+                        rz[0] = fma(si, ar, rz[0]);   // s.As
+                        rz[1] = fma(sum, ar, rz[1]);  // (W e).(A s) = e.v
+                    } else {
+                        zout[r0 + lr] = zi;
+                        rz[0] = fma(rr, zi, rz[0]);
+                    }
                 }
             }
             __syncwarp();
@@ -1919,10 +1964,20 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
         cta_columns<PPL>(au, cs, ld, a.opart);
         cta_columns<PPL>(av, cs, ld, a.opart + ld * G);
     }
-    double tot[1];
-    if (grid_reduce<1>(rz, a.partials, &st->counter[kTkProlong], tot) && threadIdx.x == 0) {
-        st->rz_new = tot[0];
-        if (ctl) loop_ctl_body(st, h, ctl == 2);
+    double tot[2];
+    if (grid_reduce<2>(rz, a.partials, &st->counter[kTkProlong], tot) && threadIdx.x == 0) {
+        if (lean) {
+            // p.Ap = z.Az - beta r.z / alpha_prev (exact-arithmetic identities of CG:
+            // z_i.A p_{i-1} = -r.z_i / alpha_{i-1}, p_{i-1}.A p_{i-1} = r.z_{i-1} / alpha_{i-1})
+            const double zaz = tot[0] + 2.0 * tot[1] + st->lean_eme;
+            const double pap = lean == 1 ? zaz - lbeta * st->rz_new / st->alpha : zaz;
+            st->pap_pred = pap;
+            st->alpha = st->rz_new / pap;
+            if (ctl) loop_ctl_lean(st, h, ctl == 2);
+        } else {
+            st->rz_new = tot[0];
+            if (ctl) loop_ctl_body(st, h, ctl == 2);
+        }
     }
 }
 
@@ -2126,6 +2181,229 @@ struct OpUpdSweep {
     }
     __device__ __forceinline__ void finish(PcgState*, const double*) const {}
 };
+
+// ============================================================ lean cycle ==
+// The lean one-pass cycle: beta_{i+1} is known BEFORE the pass
+// over W (r.z = r.s + c.e with c by its recurrence), so the pass writes
+// p = s + W e + beta p directly, and alpha_{i+1} is known right AFTER it
+// (p.Ap = z.Az - beta r.z / alpha_i, z.Az = s.As + 2 (W e).(A s) + e.M e, the
+// Chronopoulos-Gear form), so q = A p is never stored and the smoother gathers
+// r alone. Three kernels per iteration at nu = 1/1:
+//   OpSpmvUpd     q = A p in the gather of p; x += alpha p, r -= alpha q (in
+//                 place), ||r||^2 -> convergence; p.q directly: the NotSpd test
+//                 and the guard of the predicted p.Ap
+//   OpSweepLean   s = S_2(r) gathering r alone; r.s; last CTA: c by its
+//                 recurrence, e = A_c^-1 c, M e, c.e, e.M e, beta
+//   k_prolong_onepass_tma (lean)  p = s + W e + beta p, u, v, s.As, (W e).(A s)
+//                 -> alpha, loop control
+// 88n + 3A vector/matrix bytes beside W instead of 112n + 3A, and 7 + 7 gathers
+// of one array per row instead of 14 + 14 of two.
+
+// x += alpha p, r -= alpha (A p) in place; tot = [p.Ap, ||r_new||^2]
+struct OpSpmvUpd {
+    static constexpr int NV = 2;
+    static constexpr int TICKET = kTkSpmvP;
+    const double* p;
+    double* x;
+    double* r;
+    double* a_hist;
+    double alpha;
+    __device__ __forceinline__ void init(const SolveArgs& a) {
+        p = a.p0;
+        x = a.x;
+        r = a.r;
+        a_hist = a.hist;
+        alpha = a.st->alpha;
+    }
+    __device__ __forceinline__ double operator()(int j) const { return p[j]; }
+    struct Pre {
+        double pi, xi, ri;
+    };
+    __device__ __forceinline__ Pre pre(int i) const { return Pre{p[i], x[i], r[i]}; }
+    __device__ __forceinline__ void row(int i, double y, double* s, const Pre& pr) const {
+        const double rn = fma(-alpha, y, pr.ri);
+        x[i] = fma(alpha, pr.pi, pr.xi);
+        r[i] = rn;
+        s[0] = fma(pr.pi, y, s[0]);
+        s[1] = fma(rn, rn, s[1]);
+    }
+    __device__ __forceinline__ void row(int i, double y, double* s) const { row(i, y, s, pre(i)); }
+    // two_level.hpp:159-176: p^T A p <= 0 -> NotSpdError; history entry and the
+    // convergence test on ||r_new|| / ||b||
+    __device__ __forceinline__ void finish(PcgState* st, const double* tot) const {
+        const double pap = tot[0];
+        st->pap = pap;
+        if (pap <= 0.0) {
+            st->error = kErrNotSpd;
+            st->done = 1;
+            return;
+        }
+        // guard: the alpha this kernel used came from the predicted p.Ap
+        double dev = fabs(st->pap_pred - pap) / pap;
+        if (!(dev == dev) || dev > 1e300) dev = 1e300;
+        if (dev > st->pap_drift) st->pap_drift = dev;
+        if (dev > 1e-6) {  // the prediction broke down: stop, the host re-runs on the folded cycle
+            st->done = 1;
+            return;
+        }
+        const double rel = sqrt(tot[1]) / st->bnorm;
+        st->rr = tot[1];
+        st->last_rel = rel;
+        a_hist[st->it - st->hist_base] = rel;
+        st->iterations = st->it + 1;
+        if (rel < st->delta) {
+            st->converged = 1;
+            st->done = 1;
+        }
+    }
+};
+
+// The last CTA of the lean sweep kernel (whole CTA; rs = r.s when this kernel
+// wrote the final s, `fin`): the one-pass restriction recurrence
+// c = u_i - alpha_i (v_i + M e_i + beta_i (u_{i-1} - u_i) / alpha_{i-1}) with its
+// guard (as onepass_last), e = A_c^-1 c, then M e, c.e and e.M e for the pass
+// that follows, and (fin) r.z = r.s + c.e -> beta.
+__device__ void lean_last(const SolveArgs& a, double rs, bool fin) {
+    PcgState* st = a.st;
+    __shared__ double es[kOnePassK + 2], gs[kOnePassK + 2], cs[kOnePassK + 2];
+    __shared__ double dots[2];
+    const int k = a.k, ld = a.k + (a.k & 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool first = st->first != 0;
+    const double alpha = st->alpha, beta = st->beta, alpha_prev = st->alpha_prev;
+    const int ucur = (int)(st->it & 1) * ld, uprev = ld - ucur;
+    __threadfence();
+    if (!first) {
+        __shared__ double dred[2][32];
+        double d = 0.0, um = 0.0;
+        for (int j = threadIdx.x; j < k; j += blockDim.x) {
+            const double u = __ldcg(a.ow + ucur + j);
+            d = fmax(d, fabs(__ldcg(a.ow + 3 * ld + j) - u));
+            um = fmax(um, fabs(u));
+        }
+        for (int o = 16; o; o >>= 1) {
+            d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+            um = fmax(um, __shfl_xor_sync(0xffffffffu, um, o));
+        }
+        if (lane == 0) {
+            dred[0][warp] = d;
+            dred[1][warp] = um;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+                d = fmax(d, dred[0][w]);
+                um = fmax(um, dred[1][w]);
+            }
+            const double drift = um > 0.0 ? d / um : 0.0;
+            st->drift_max = fmax(st->drift_max, drift);
+        }
+    }
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+        const double u = __ldcg(a.ow + ucur + j);
+        double g = __ldcg(a.ow + 2 * ld + j) + __ldcg(a.ow + 4 * ld + j);  // v + M e
+        if (!first) g = fma(beta, (__ldcg(a.ow + uprev + j) - u) / alpha_prev, g);  // + beta W^T q_{i-1}
+        const double c = fma(-alpha, g, u);                                 // c = u - alpha g
+        cs[j] = c;
+        gs[j] = c;  // the substitutions overwrite their right-hand side
+        a.ow[3 * ld + j] = c;  // compared with the direct u_{i+1} next iteration
+    }
+    __syncthreads();
+    if (a.Ainv) coarse_apply_inverse(a.Ainv, k, gs, es);
+    else if (warp == 0) coarse_solve_warp(a.L, k, gs, es);
+    __syncthreads();
+    for (int j = threadIdx.x; j < ld; j += blockDim.x) a.e[j] = j < k ? es[j] : 0.0;  // padded column = 0
+    coarse_apply_inverse(a.M, k, es, gs);  // M e_{i+1}
+    __syncthreads();
+    for (int j = threadIdx.x; j < k; j += blockDim.x) a.ow[4 * ld + j] = gs[j];
+    if (warp == 0) {
+        double ce = 0.0, eme = 0.0;
+        for (int j = lane; j < k; j += 32) {
+            ce = fma(cs[j], es[j], ce);
+            eme = fma(es[j], gs[j], eme);
+        }
+        ce = warp_sum(ce);
+        eme = warp_sum(eme);
+        if (lane == 0) {
+            st->lean_ce = ce;
+            st->lean_eme = eme;
+            st->alpha_prev = alpha;
+            if (fin) {
+                const double g = rs + ce;
+                st->beta = g / st->rz;
+                st->rz_new = g;
+            }
+        }
+    }
+}
+
+// s = S_2(r) = s1 + w D^-1 (r - A s1), s1 = w D^-1 r (the arithmetic of
+// OpUpdSweep on the residual OpSpmvUpd wrote), r.s, and the lean hooks
+template <bool CW>
+struct OpSweepLean {
+    static constexpr int NV = 1;
+    static constexpr int TICKET = kTkUpdate;
+    static constexpr bool CTA_HOOKS = true;
+    bool fin;  // T = 2: this s is the final one
+    const double* r;
+    const double* wd;
+    double* sout;
+    double wc;
+    __device__ __forceinline__ void init(const SolveArgs& a) {
+        r = a.r;
+        wd = a.wd;
+        wc = a.wdc;
+        sout = a.zt0;
+    }
+    __device__ __forceinline__ double operator()(int j) const { return (CW ? wc : wd[j]) * r[j]; }
+    struct Pre {
+        double ri, wi;
+    };
+    __device__ __forceinline__ Pre pre(int i) const { return Pre{r[i], CW ? wc : wd[i]}; }
+    __device__ __forceinline__ void row(int i, double y, double* s, const Pre& pr) const {
+        const double gi = pr.wi * pr.ri;
+        const double si = fma(pr.wi, pr.ri - y, gi);
+        sout[i] = si;
+        s[0] = fma(pr.ri, si, s[0]);
+    }
+    __device__ __forceinline__ void row(int i, double y, double* s) const { row(i, y, s, pre(i)); }
+    __device__ __forceinline__ void cta_pre(const SolveArgs& a) const { onepass_colsums(a); }
+    __device__ __forceinline__ void cta_last(const SolveArgs& a, const double* tot) const {
+        lean_last(a, tot[0], fin);
+    }
+    __device__ __forceinline__ void finish(PcgState*, const double*) const {}
+};
+
+// Lean prologue, after c = W^T r_0, e_0 (restrict_finish kept c in ow) and the
+// sweeps (r.s in st->rz_new when has_s): M e_0, c.e, e.M e; r.z = r.s + c.e;
+// beta = 0.
+__global__ void __launch_bounds__(kThreads) k_lean_init(SolveArgs a, int has_s) {
+    PcgState* st = a.st;
+    if (st->done) return;
+    __shared__ double es[kOnePassK + 2], gs[kOnePassK + 2];
+    const int k = a.k, ld = a.k + (a.k & 1);
+    for (int j = threadIdx.x; j < k; j += blockDim.x) es[j] = __ldcg(a.e + j);
+    __syncthreads();
+    coarse_apply_inverse(a.M, k, es, gs);
+    __syncthreads();
+    for (int j = threadIdx.x; j < k; j += blockDim.x) a.ow[4 * ld + j] = gs[j];
+    if (threadIdx.x < 32) {
+        double ce = 0.0, eme = 0.0;
+        for (int j = threadIdx.x; j < k; j += 32) {
+            ce = fma(__ldcg(a.ow + 3 * ld + j), es[j], ce);
+            eme = fma(es[j], gs[j], eme);
+        }
+        ce = warp_sum(ce);
+        eme = warp_sum(eme);
+        if (threadIdx.x == 0) {
+            st->lean_ce = ce;
+            st->lean_eme = eme;
+            st->rz_new = (has_s ? st->rz_new : 0.0) + ce;
+            st->beta = 0.0;
+            st->alpha_prev = 0.0;
+        }
+    }
+}
 
 #include "march.cuh"
 #include "lmarch.cuh"
@@ -2815,9 +3093,16 @@ static void launch_op_tma(const LaunchCtx& c, void (*f)(KArgs...), long long nti
     klaunch(c, f, (int)g, threads, smem, std::forward<Args>(args)...);
 }
 
+// stages of the one-pass prolongation's ring that fit the budget
+static int op_fit(const SolveArgs& a, size_t budget) {
+    const int ld = a.k + (a.k & 1);
+    const int tnz = a.dia.kind ? -1 : (kOpTR == 64 ? a.tile_nnz64 : a.tile_nnz128);
+    return (int)((budget - 256) / op_stage_bytes(ld, tnz));
+}
+
 template <int PPL>
 static void prolong_onepass_ppl(const LaunchCtx& c, const SolveArgs& a, const double* sv, double* zout,
-                                cudaGraphConditionalHandle h, int ctl, int rsel) {
+                                cudaGraphConditionalHandle h, int ctl, int rsel, int lean) {
     const int ld = a.k + (a.k & 1);
     // as many stages as fit, a multiple of the stencil pair count P
     const int tnz = a.dia.kind ? -1 : (kOpTR == 64 ? a.tile_nnz64 : a.tile_nnz128);
@@ -2856,7 +3141,7 @@ static void prolong_onepass_ppl(const LaunchCtx& c, const SolveArgs& a, const do
     if (NLSP_OP_TMA && fit >= 2) {
         const long long nt = (a.n + kOpTR - 1) / kOpTR;
         const int threads = 32 * (1 + 2 * P + op_wpg(PPL) * op_wh(PPL));
-#define NLSP_P2(D, R) launch_op_tma(c, k_prolong_onepass_tma<PPL, D, R>, nt, sm, threads, a, sv, zout, h, ctl, S, P, rsel)
+#define NLSP_P2(D, R) launch_op_tma(c, k_prolong_onepass_tma<PPL, D, R>, nt, sm, threads, a, sv, zout, h, ctl, S, P, rsel, lean)
         const bool rv = a.dia.kind == 2;
         if (!a.dia.kind) NLSP_P2(0, false);
         else if (a.dia.d <= 8) { if (rv) NLSP_P2(8, true); else NLSP_P2(8, false); }
@@ -2877,14 +3162,14 @@ static void prolong_onepass_ppl(const LaunchCtx& c, const SolveArgs& a, const do
 // z = s + W e with u, v, w partials (s = S_T(r) by T - 1 sweep launches, or
 // none for T = 0); ctl as launch_prolong
 void launch_prolong_onepass(const LaunchCtx& c, const SolveArgs& a, const double* sv, double* zout,
-                            cudaGraphConditionalHandle h, int ctl, int rsel) {
+                            cudaGraphConditionalHandle h, int ctl, int rsel, int lean) {
     SolveArgs b = a;
     b.P = a.W2;
     switch (ppl_for(a.k)) {
-        case 1: prolong_onepass_ppl<1>(c, b, sv, zout, h, ctl, rsel); break;
-        case 2: prolong_onepass_ppl<2>(c, b, sv, zout, h, ctl, rsel); break;
-        case 3: prolong_onepass_ppl<3>(c, b, sv, zout, h, ctl, rsel); break;
-        default: prolong_onepass_ppl<4>(c, b, sv, zout, h, ctl, rsel); break;
+        case 1: prolong_onepass_ppl<1>(c, b, sv, zout, h, ctl, rsel, lean); break;
+        case 2: prolong_onepass_ppl<2>(c, b, sv, zout, h, ctl, rsel, lean); break;
+        case 3: prolong_onepass_ppl<3>(c, b, sv, zout, h, ctl, rsel, lean); break;
+        default: prolong_onepass_ppl<4>(c, b, sv, zout, h, ctl, rsel, lean); break;
     }
     count(c);
 }
@@ -2944,21 +3229,21 @@ void launch_update_onepass(const LaunchCtx& c, const SolveArgs& a) {
 void launch_onepass_tail(const LaunchCtx& c, const SolveArgs& a, unsigned long long T,
                          cudaGraphConditionalHandle h, int ctl) {
     const double* sv = launch_onepass_sweeps(c, a, T);
-    launch_prolong_onepass(c, a, sv, a.z, h, ctl, 0);
+    launch_prolong_onepass(c, a, sv, a.z, h, ctl, 0, 0);
 }
 
 // one iteration after k_spmv_p: fused update + sweeps (T = 2) when possible
 void launch_onepass_iteration_tail(const LaunchCtx& c, const SolveArgs& a, unsigned long long T,
                                    cudaGraphConditionalHandle h, int ctl) {
     if (update_sweep_ok(a, T) && launch_lfused(c, a, T)) {  // s_T -> zt0
-        launch_prolong_onepass(c, a, a.zt0, a.z, h, ctl, 1);
+        launch_prolong_onepass(c, a, a.zt0, a.z, h, ctl, 1, 0);
         return;
     }
     if (update_sweep_ok(a, T)) {
         launch_update_sweep(c, a);  // s_2 -> zt0
         double* cur = a.zt0;
         launch_sweeps_rpar(c, a, T, &cur);
-        launch_prolong_onepass(c, a, cur, a.z, h, ctl, 1);
+        launch_prolong_onepass(c, a, cur, a.z, h, ctl, 1, 0);
         return;
     }
     launch_update_onepass(c, a);
@@ -2969,6 +3254,74 @@ void launch_onepass_iteration_tail(const LaunchCtx& c, const SolveArgs& a, unsig
 void launch_onepass_apply(const LaunchCtx& c, const SolveArgs& a, unsigned long long T) {
     launch_update_restrict(c, a, false);
     launch_onepass_tail(c, a, T, 0, 0);
+}
+
+// ---------------------------------------------------------- lean cycle host --
+// The lean cycle needs the warp-specialised pass (it stages p's old rows) and
+// a smoother (T >= 2) on the diagonal-form or TMA-staged SpMV kernels.
+bool lean_supported(const SolveArgs& a, unsigned long long T) {
+    static const bool off = std::getenv("NLSP_LEAN") && std::atoi(std::getenv("NLSP_LEAN")) == 0;
+    if (off || !NLSP_OP_TMA || a.k > kOnePassK || T < 2 || (T & 1)) return false;
+    if (!(a.dia.kind || spmv_tma_ok(a))) return false;
+    return op_fit(a, (size_t)224 * 1024) >= 2;
+}
+
+// K1: q = A p in the gather, x += alpha p, r -= alpha q, ||r|| and p.q
+void launch_spmv_upd(const LaunchCtx& c, const SolveArgs& a) {
+    if (a.dia.kind) launch_dia_op<1>(c, a, OpSpmvUpd{});
+    else launch_spmv_op<1>(c, a, OpSpmvUpd{});
+    count(c);
+}
+
+// K2 (+ the later sweeps of T > 2): s = S_T(r), r.s, the coarse step; returns s
+const double* launch_lean_sweeps(const LaunchCtx& c, const SolveArgs& a, unsigned long long T) {
+    const bool fin = T == 2;
+    if (a.dia.kind && a.wdc != 0.0) launch_dia_op<1>(c, a, OpSweepLean<true>{fin});
+    else if (a.dia.kind) launch_dia_op<1>(c, a, OpSweepLean<false>{fin});
+    else launch_spmv_op<1>(c, a, OpSweepLean<false>{fin});
+    count(c);
+    double* cur = a.zt0;
+    for (unsigned long long j = 3; j <= T; ++j) {
+        double* nxt = (cur == a.zt0) ? a.zt1 : a.zt0;
+        const GPlain gp{cur};
+        const bool last = j == T;
+        if (a.dia.kind && a.wdc != 0.0) {
+            if (last) launch_dia_op<1>(c, a, OpSweep<GPlain, true, true>{gp, a.r, a.wd, nxt, a.wdc, false, true});
+            else launch_dia_op<1>(c, a, OpSweep<GPlain, false, true>{gp, a.r, a.wd, nxt, a.wdc, false, false});
+        } else if (a.dia.kind) {
+            if (last) launch_dia_op<1>(c, a, OpSweep<GPlain, true>{gp, a.r, a.wd, nxt, 0.0, false, true});
+            else launch_dia_op<1>(c, a, OpSweep<GPlain, false>{gp, a.r, a.wd, nxt, 0.0, false, false});
+        } else {
+            if (last) launch_spmv_op<1>(c, a, OpSweep<GPlain, true>{gp, a.r, a.wd, nxt, 0.0, false, true});
+            else launch_spmv_op<1>(c, a, OpSweep<GPlain, false>{gp, a.r, a.wd, nxt, 0.0, false, false});
+        }
+        count(c);
+        cur = nxt;
+    }
+    return cur;
+}
+
+// one lean iteration: c0 launches its first kernel, c1 the rest (PDL)
+void launch_lean_iteration(const LaunchCtx& c0, const LaunchCtx& c1, const SolveArgs& a,
+                           unsigned long long T, cudaGraphConditionalHandle h, int ctl) {
+    launch_spmv_upd(c0, a);
+    const double* sv = launch_lean_sweeps(c1, a, T);
+    launch_prolong_onepass(c1, a, sv, a.p0, h, ctl, 0, 1);
+}
+
+// lean prologue: c = W^T r_0 directly, e_0, s = S_T(r_0) with r.s, the coarse
+// scalars, then the pass: p_0 = s + W e_0, u_0, v_0 -> alpha_0
+void launch_lean_apply(const LaunchCtx& c, const SolveArgs& a, unsigned long long T) {
+    launch_update_restrict(c, a, false);
+    double* cur = nullptr;
+    for (unsigned long long j = 2; j <= T; ++j) {
+        double* nxt = (cur == a.zt0) ? a.zt1 : a.zt0;
+        launch_sweep(c, a, cur == nullptr, cur, nxt, j == T);
+        cur = nxt;
+    }
+    k_lean_init<<<1, kThreads, 0, c.s>>>(a, cur != nullptr ? 1 : 0);
+    count(c);
+    launch_prolong_onepass(c, a, cur, a.p0, 0, 0, 0, 2);
 }
 
 }  // namespace nlsp

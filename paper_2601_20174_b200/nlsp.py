@@ -478,8 +478,9 @@ class TwoLevelPreconditioner:
 
     def cycle(self) -> str:
         """The PCG schedule of this operator (nlsp_twolevel_cycle): "literal",
-        "folded" or "onepass"."""
-        return {0: "literal", 1: "folded", 2: "onepass"}[L.gpu_lib().nlsp_twolevel_cycle(self.handle)]
+        "folded", "onepass" or "lean" (the one-pass cycle with beta known before
+        and alpha right after the pass over W)."""
+        return {0: "literal", 1: "folded", 2: "onepass", 3: "lean"}[L.gpu_lib().nlsp_twolevel_cycle(self.handle)]
 
     def nu1(self) -> int:
         return self._nu1

@@ -53,7 +53,7 @@ def test_full_size_solve_properties(nlsp, name):
     assert res2.report.iterations == rep.iterations and np.array_equal(res2.solution, res.solution)
     # the one-pass schedule (W streamed once per iteration) against the folded
     # one (W twice, restriction direct) on the full-size system
-    assert m.cycle() == "onepass"
+    assert m.cycle() in ("onepass", "lean")
     import os
     os.environ["NLSP_CYCLE"] = "folded"
     try:

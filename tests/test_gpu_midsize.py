@@ -28,7 +28,7 @@ def test_midsize_pipeline_matches_reference(nlsp, name):
     sref = np.asarray(d["sigma"])
     assert np.abs(np.asarray(sig) - sref[: len(sig)]).max() <= 1e-10 * sref[0]
     m = nlsp.TwoLevelPreconditioner(a, p, cfg.omega, cfg.nu1, cfg.nu2)
-    assert m.cycle() == "onepass"
+    assert m.cycle() in ("onepass", "lean")
     # P and A_c at the BASELINE k / m (north star: 1e-10 up to column sign,
     # gap-limited where the singular values cluster)
     basis, _, coarse = m._export()

@@ -42,6 +42,11 @@ PATHS = {
     "literal": {"NLSP_CLUSTER": "0", "NLSP_CYCLE": "literal"},
     # W streamed twice per iteration (the default graph path streams it once)
     "folded": {"NLSP_CLUSTER": "0", "NLSP_CYCLE": "folded"},
+    # the one-pass cycle without the lean scalars (alpha and beta by their own
+    # reductions: spmv_p, fused update + sweep, prolongation)
+    "onepass": {"NLSP_CLUSTER": "0", "NLSP_CYCLE": "onepass"},
+    "onepass_host": {"NLSP_CLUSTER": "0", "NLSP_CYCLE": "onepass", "NLSP_LOOP": "host"},
+    "onepass_csr": {"NLSP_CLUSTER": "0", "NLSP_CYCLE": "onepass", "NLSP_DIA": "0"},
     # coarse solve by the reference's triangular substitutions instead of A_c^-1
     "chol": {"NLSP_CLUSTER": "0", "NLSP_COARSE": "chol"},
     "cluster_chol": {"NLSP_CLUSTER": "1", "NLSP_COARSE": "chol"},
@@ -59,7 +64,7 @@ PATHS = {
     "drift_fallback": {"NLSP_CLUSTER": "0", "NLSP_DRIFT_TOL": "-1"},
     # the plane-march kernels of the structured grids (march.cuh), forced at
     # these small sizes (tiny slabs, one- and two-plane marches, clamped halos)
-    "march": {"NLSP_CLUSTER": "0", "NLSP_MARCH": "1"},
+    "march": {"NLSP_CLUSTER": "0", "NLSP_MARCH": "1", "NLSP_CYCLE": "onepass"},
 }
 
 
@@ -92,8 +97,16 @@ def test_execution_paths_match_reference(tmp_path, case):
     assert np.array_equal(res["graph"][1], res["graph_csr"][1])
     # the plane-march gather kernels (forced at this size): the same rows, the
     # dot products summed in another order
-    assert abs(res["march"][0]["iterations"] - res["graph"][0]["iterations"]) <= 1
-    assert np.linalg.norm(res["march"][1] - res["graph"][1]) <= 1e-10 * np.linalg.norm(res["graph"][1])
+    assert abs(res["march"][0]["iterations"] - res["onepass"][0]["iterations"]) <= 1
+    assert np.linalg.norm(res["march"][1] - res["onepass"][1]) <= 1e-10 * np.linalg.norm(res["onepass"][1])
+    # the one-pass cycle with alpha and beta by their own reductions: the same
+    # kernels on the stream and in the graph, the same rows in both matrix forms
+    assert np.array_equal(res["onepass"][1], res["onepass_host"][1])
+    assert res["onepass"][0]["iterations"] == res["onepass_csr"][0]["iterations"]
+    assert np.array_equal(res["onepass"][1], res["onepass_csr"][1])
+    # ... and the lean scalars (the default) change the solve by rounding only
+    assert abs(res["onepass"][0]["iterations"] - res["graph"][0]["iterations"]) <= 1
+    assert np.linalg.norm(res["onepass"][1] - res["graph"][1]) <= 1e-10 * np.linalg.norm(res["graph"][1])
     # the forced guard fallback gives exactly the folded cycle's solve
     assert res["drift_fallback"][0]["fallback"] and not res["graph"][0]["fallback"]
     assert res["drift_fallback"][0]["iterations"] == res["folded"][0]["iterations"]
@@ -236,7 +249,7 @@ def test_graph_loop_cycles_match_oracle(nlsp, oracle, graph_ctx, graph_chol_ctx,
     for nu1, nu2, k in [(1, 1, kmax), (2, 2, kmax), (1, 1, 7), (2, 2, 7), (0, 1, kmax), (3, 1, kmax - 1)]:
         p = np.ascontiguousarray(d["P"][:, :k])
         m = nlsp.TwoLevelPreconditioner(a, nlsp.DeviceDense.upload(p, ctx), 2 / 3, nu1, nu2)
-        assert m.cycle() == ("onepass" if nu1 == nu2 else "folded"), (nu1, nu2, k)
+        assert m.cycle() == (("lean" if nu1 >= 1 else "onepass") if nu1 == nu2 else "folded"), (nu1, nu2, k)
         t = oracle.twolevel(ao, p, 2 / 3, nu1, nu2)
         res = nlsp.pcg(a, d["rhs"], m, 1e-8, 10 * a.dim())
         ro = oracle.pcg(ao, d["rhs"], 2, t, 1e-8, 10 * a.dim())
@@ -255,7 +268,7 @@ def test_graph_loop_cycles_match_oracle(nlsp, oracle, graph_ctx, graph_chol_ctx,
         m2 = nlsp.TwoLevelPreconditioner(a, nlsp.DeviceDense.upload(p, ctx), 2 / 3, 0, 0)
     finally:
         os.environ.pop("NLSP_CYCLE", None)
-    assert m1.cycle() == "onepass" and m2.cycle() == "folded"
+    assert m1.cycle() in ("onepass", "lean") and m2.cycle() == "folded"
     r1 = nlsp.pcg(a, d["rhs"], m1, 1e-8, 3)
     r2 = nlsp.pcg(a, d["rhs"], m2, 1e-8, 3)
     assert r1.report.iterations == r2.report.iterations == 3
@@ -337,7 +350,7 @@ def test_onepass_cycle_matches_folded_midsize(nlsp, cfg, nx, hard):
         m2 = nlsp.TwoLevelPreconditioner(a, p, c.omega, c.nu1, c.nu2)
     finally:
         os.environ.pop("NLSP_CYCLE", None)
-    assert m1.cycle() == "onepass" and m2.cycle() == "folded"
+    assert m1.cycle() in ("onepass", "lean") and m2.cycle() == "folded"
     r1 = nlsp.pcg(a, pb.rhs, m1, c.delta, 10 * pb.n)
     r2 = nlsp.pcg(a, pb.rhs, m2, c.delta, 10 * pb.n)
     assert r1.report.converged and r2.report.converged
@@ -382,7 +395,7 @@ def test_shared_handles_concurrent_contexts(nlsp):
     sv = nlsp.generate_smoothed_vectors(a, None, c.m, c.s1, c.omega, c.s0_seed)
     p, _, _ = nlsp.svd_basis(sv.s, c.k)
     m = nlsp.TwoLevelPreconditioner(a, p, c.omega, c.nu1, c.nu2)
-    assert m.cycle() == "onepass" and pb.n > 65536
+    assert m.cycle() in ("onepass", "lean") and pb.n > 65536
     dev = a.device(m.ctx)
     rng = np.random.default_rng(3)
     rhs = [rng.standard_normal(pb.n) for _ in range(4)]
