@@ -362,7 +362,7 @@ nlsp_status ensure_ws(nlsp_ctx* ctx, long long n, long long hist) {
             CU(dalloc(p, (size_t)n + 16));  // padded for 16-B bulk copies of tile slices
         CU(dalloc(&ctx->e, (size_t)kMaxCoarse + 2));
         CU(dalloc(&ctx->partials, (size_t)kMaxGrid * 256));
-        CU(dalloc(&ctx->ow, (size_t)5 * (kOnePassK + 2)));
+        CU(dalloc(&ctx->ow, (size_t)6 * (kOnePassK + 2)));
         CU(dalloc(&ctx->opart, (size_t)kMaxGrid * 3 * (kOnePassK + 2)));
         // q feeds the one-pass partials of the PCG prologue (weighted by 0)
         CU(cudaMemsetAsync(ctx->q, 0, ((size_t)n + 16) * 8, ctx->s));
@@ -430,6 +430,9 @@ SolveArgs make_args(nlsp_ctx* c, const nlsp_csr* a, const nlsp_twolevel* m) {
 // NLSP_QR=robust forces the shifted CholeskyQR3 path of qr_thin_dev (tests)
 const bool g_force_sqr = std::getenv("NLSP_QR") && std::strcmp(std::getenv("NLSP_QR"), "robust") == 0;
 const bool g_pdl = !(std::getenv("NLSP_PDL") && std::strcmp(std::getenv("NLSP_PDL"), "0") == 0);
+// NLSP_PDL_FIRST=1: the first kernel of an unrolled iteration launched with PDL
+// too (off: measured slower, C4 443 -> 455 us, C3 413 -> 440 us per iteration)
+const bool g_pdl_first = std::getenv("NLSP_PDL_FIRST") && std::strcmp(std::getenv("NLSP_PDL_FIRST"), "1") == 0;
 const int g_unroll = [] {
     const char* u = std::getenv("NLSP_UNROLL");
     const int v = u ? std::atoi(u) : 4;  // measured: +1.4 % at C2, +1.8 % at C5 over 1
@@ -438,12 +441,14 @@ const int g_unroll = [] {
 
 // One PCG iteration (the WHILE body). mode: 0 two-level, 1 identity, 2 Jacobi.
 void enqueue_iteration(const LaunchCtx& lc, const SolveArgs& a, int mode, const nlsp_twolevel* m,
-                       cudaGraphConditionalHandle h, int use_cond) {
+                       cudaGraphConditionalHandle h, int use_cond, bool pdl_first = false) {
     if (mode == 0 && m->lean) {
-        // every kernel after the first of an iteration is launched with PDL
-        LaunchCtx lp = lc;
+        // every kernel after the first of an iteration is launched with PDL, and
+        // the first too when it follows another iteration of the same WHILE body
+        LaunchCtx lp = lc, l0 = lc;
         lp.pdl = g_pdl;
-        launch_lean_iteration(lc, lp, a, m->nu1 + m->nu2, h, use_cond ? 2 : 1);
+        l0.pdl = g_pdl && pdl_first;
+        launch_lean_iteration(l0, lp, a, m->nu1 + m->nu2, h, use_cond ? 2 : 1);
         return;
     }
     launch_spmv_p(lc, a);
@@ -529,7 +534,7 @@ nlsp_status build_graph(nlsp_ctx* ctx, const SolveArgs& a, int mode, const nlsp_
         // NLSP_UNROLL iterations per WHILE body execution (kernels of an
         // iteration after convergence exit at once; each iteration's last
         // kernel still sets the condition)
-        for (int u = 0; u < g_unroll; ++u) enqueue_iteration(lb, a, mode, m, h, 1);
+        for (int u = 0; u < g_unroll; ++u) enqueue_iteration(lb, a, mode, m, h, 1, u > 0 && g_pdl_first);
         e = cudaStreamEndCapture(ctx->s_body, &body);
     }
     lc.launches = prologue ? &ctx->gk_epi : &scratch;

@@ -843,7 +843,6 @@ struct OpSweep {
     double* zout;
     double wc = 0.0;    // constant w D^-1 (see GWdr)
     bool rpar = false;  // r = the residual the fused update + sweep wrote (r[(it + 1) & 1])
-    bool lean_fin = false;  // lean cycle, last sweep: r.z = r.s + c.e -> beta (see lean_last)
     __device__ __forceinline__ double operator()(int j) const { return g(j); }
     struct Pre {
         double ri, wi, gi;
@@ -859,13 +858,7 @@ struct OpSweep {
         if (rpar) r = (a.st->it & 1) ? a.r : a.r1;
     }
     __device__ __forceinline__ void finish(PcgState* st, const double* tot) const {
-        if (lean_fin) {
-            const double g = tot[0] + st->lean_ce;
-            st->beta = g / st->rz;
-            st->rz_new = g;
-        } else {
-            st->rz_new = tot[0];
-        }
+        st->rz_new = tot[0];
     }
 };
 
@@ -1535,8 +1528,10 @@ __device__ __forceinline__ double dia_row_dot(const SolveArgs& a, int i, const d
 
 // Per-lane column accumulators of one k-vector -> this CTA's column sums ->
 // dst[c * G + blockIdx.x] (column-major partials, G = gridDim.x).
+// ecol / dot: also *dot += sum_c (this CTA's column sum c) * ecol[c]
 template <int PPL>
-__device__ __forceinline__ void cta_columns(double (&acc)[2 * PPL], double* cs, int ld, double* dst) {
+__device__ __forceinline__ void cta_columns(double (&acc)[2 * PPL], double* cs, int ld, double* dst,
+                                            const double* ecol = nullptr, double* dot = nullptr) {
     constexpr int CW = 2 * kGroup * PPL;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int pairs = ld >> 1;
@@ -1560,6 +1555,7 @@ __device__ __forceinline__ void cta_columns(double (&acc)[2 * PPL], double* cs, 
         double t = 0.0;
         for (int w = 0; w < nw; ++w) t += cs[w * CW + c];
         dst[(long long)c * gridDim.x + blockIdx.x] = t;
+        if (ecol) *dot = fma(t, ecol[c], *dot);
     }
     __syncthreads();
 }
@@ -1718,6 +1714,134 @@ __host__ __device__ constexpr unsigned op_stage_bytes(int ld, int tile_nnz = -1)
            (tile_nnz >= 0 ? op_csr_bytes(tile_nnz) : 0u);
 }
 
+// The coarse step of the lean cycle, run redundantly by the 256 W-product
+// threads of EVERY CTA of the pass while its producer fills the stage ring (so
+// it is off the critical path; as the last CTA of the sweep kernel it cost
+// ~10 us per iteration): the one-pass restriction recurrence
+//   c = u_i - alpha_i (v_i + M e_i + beta_i (u_{i-1} - u_i) / alpha_{i-1})
+// from the column sums the sweep kernel left in ow, e = A_c^-1 c, M e, and the
+// scalars c.e, e.M e -> r.z = r.s + c.e, beta = r.z / r.z_prev. Every CTA gets
+// bitwise the same values; CTA 0 publishes them (a.e, ow, the drift guard).
+// t: thread index in [0, 256); sc: 5 (ld + 2) doubles of scratch; on return
+// sc[3 (ld + 2) ..] holds e and lsc = [e.Me, r.z, beta].
+__device__ __forceinline__ void lean_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+// (operands by value: a reference to the kernel's SolveArgs would move the
+// whole struct to local memory, and every a.* of the hot loops with it —
+// measured +34 us per pass at C4)
+struct LeanCoarse {
+    const double* Ainv;
+    const double* M;
+    const double* L;
+    double* ow;
+    double* e;
+    PcgState* st;
+    int k;
+};
+__device__ __noinline__ void lean_coarse_step(const LeanCoarse a, int t, double* sc, double* lsc) {
+    PcgState* st = a.st;
+    const int k = a.k, ld = a.k + (a.k & 1);
+    double* cs = sc;
+    double* ws = sc + (ld + 2);
+    double* es = sc + 3 * (ld + 2);
+    double* gs = sc + 4 * (ld + 2);
+    const int i = t >> 2, sub = t & 3, lane = t & 31, w = t >> 5;
+    // A_c^-1 and M rows (L2 resident): in flight with everything else
+    double ai[kOnePassK / 4], mi[kOnePassK / 4];
+#pragma unroll
+    for (int jj = 0; jj < kOnePassK / 4; ++jj) {
+        const int j = sub + 4 * jj;
+        const bool ok = i < k && j < k;
+        ai[jj] = (ok && a.Ainv) ? __ldg(a.Ainv + (long long)i * k + j) : 0.0;
+        mi[jj] = ok ? __ldg(a.M + (long long)i * k + j) : 0.0;
+    }
+    // both parities of the ping-pong slots, so no load waits on st->it
+    double o6[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) o6[q] = t < k ? __ldcg(a.ow + q * ld + t) : 0.0;
+    const bool first = st->first != 0;
+    const long long it = st->it;
+    const double alpha = st->alpha, alpha_prev = st->alpha_prev, beta = st->beta, gam = st->rz, rs = st->rz_new;
+    const bool odd = it & 1;
+    const int mnew = (4 + (int)((it + 1) & 1)) * ld;
+    double d = 0.0, um = 0.0;
+    if (t < k) {
+        const double u = odd ? o6[1] : o6[0], up = odd ? o6[0] : o6[1];
+        double g = o6[2] + (odd ? o6[5] : o6[4]);                  // v + M e
+        if (!first) g = fma(beta, (up - u) / alpha_prev, g);       // + beta W^T q_{i-1}
+        const double c = fma(-alpha, g, u);                        // c = u - alpha g
+        cs[t] = c;
+        ws[t] = c;  // the substitutions overwrite their right-hand side
+        if (blockIdx.x == 0) {
+            // guard: last iteration's recurrence value against the direct u_i
+            if (!first) {
+                d = fabs(o6[3] - u);
+                um = fabs(u);
+            }
+            a.ow[3 * ld + t] = c;
+        }
+    }
+    if (blockIdx.x == 0 && !first && w < 2) {
+        for (int o = 16; o; o >>= 1) {
+            d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+            um = fmax(um, __shfl_xor_sync(0xffffffffu, um, o));
+        }
+        if (lane == 0) {
+            lsc[4 + w] = d;
+            lsc[6 + w] = um;
+        }
+    }
+    lean_bar();
+    if (a.Ainv) {
+        double e = 0.0;
+#pragma unroll
+        for (int jj = 0; jj < kOnePassK / 4; ++jj)
+            if (sub + 4 * jj < k) e = fma(ai[jj], cs[sub + 4 * jj], e);
+        e += __shfl_xor_sync(0xffffffffu, e, 1);
+        e += __shfl_xor_sync(0xffffffffu, e, 2);
+        if (i < k && sub == 0) es[i] = e;
+    } else if (w == 0) {
+        coarse_solve_warp(a.L, k, ws, es);
+    }
+    if (t == 0 && (k & 1)) es[k] = 0.0;  // padded column
+    lean_bar();
+    {
+        double g = 0.0;
+#pragma unroll
+        for (int jj = 0; jj < kOnePassK / 4; ++jj)
+            if (sub + 4 * jj < k) g = fma(mi[jj], es[sub + 4 * jj], g);
+        g += __shfl_xor_sync(0xffffffffu, g, 1);
+        g += __shfl_xor_sync(0xffffffffu, g, 2);
+        if (i < k && sub == 0) gs[i] = g;
+    }
+    lean_bar();
+    if (w == 0) {
+        double ce = 0.0, eme = 0.0;
+        for (int j = lane; j < k; j += 32) {
+            ce = fma(cs[j], es[j], ce);
+            eme = fma(es[j], gs[j], eme);
+        }
+        ce = warp_sum(ce);
+        eme = warp_sum(eme);
+        if (lane == 0) {
+            const double g = rs + ce;
+            lsc[0] = eme;
+            lsc[1] = g;
+            lsc[2] = g / gam;
+            if (blockIdx.x == 0 && !first) {
+                const double dd = fmax(lsc[4], k > 32 ? lsc[5] : 0.0), uu = fmax(lsc[6], k > 32 ? lsc[7] : 0.0);
+                const double drift = uu > 0.0 ? dd / uu : 0.0;
+                st->drift_max = fmax(st->drift_max, drift);
+            }
+        }
+    }
+    if (blockIdx.x == 0 && t < ld) {
+        a.e[t] = es[t];
+        if (t < k) a.ow[mnew + t] = gs[t];
+    }
+    lean_bar();
+}
+
 template <int PPL, int MAXD, bool RV>
 __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(SolveArgs a, const double* sv,
                                                                       double* zout,
@@ -1736,7 +1860,9 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
     // lean (DESIGN.md §3 "lean cycle"): 1 writes p = s + W e + beta p in place of
     // z (zout = p, its old rows staged with the tile), 2 the prologue's p = s + W e;
     // both reduce s.As and (W e).(A s) instead of r.z
-    const double lbeta = lean == 1 ? st->beta : 0.0;
+    __shared__ double cs[(op_threads_max(PPL) / 32) * 2 * kGroup * PPL];  // column sums (cta_columns)
+    __shared__ double lsm[5 * (2 * kGroup * PPL + 2)];  // lean: the coarse step's vectors
+    __shared__ double lsc[8];  // lean: [e.Me, r.z, beta] of the coarse step (+ guard partials)
     // rsel: the residual the fused update + sweep wrote (r[(it + 1) & 1]), else r
     const double* rv = (rsel && !(st->it & 1)) ? a.r1 : a.r;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -1890,6 +2016,8 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
                 }
             }
             reinterpret_cast<double*>(base + as_off)[lr] = y;
+            // lean: s.As summed here (the W-product warps are the pass's critical path)
+            if (lean && sv && lr < rows) rz[0] = fma(reinterpret_cast<const double*>(base + s_off)[lr], y, rz[0]);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&asr[stg]);
@@ -1901,12 +2029,16 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
         const int cw = warp - 1 - 2 * P;
         const int wgrp = cw / WPG;
         const int grp = ((cw % WPG) * 32 + lane) >> 3, l = lane & (kGroup - 1);
+        // lean: c by its recurrence, e, M e and beta while the producer fills the ring
+        if (lean == 1) lean_coarse_step(LeanCoarse{a.Ainv, a.M, a.L, a.ow, a.e, st, a.k}, cw * 32 + lane, lsm, lsc);
+        const double* esrc = lean == 1 ? lsm + 3 * (ld + 2) : a.e;
+        const double lbeta = lean == 1 ? lsc[2] : 0.0;
         double ev[2 * PPL];
 #pragma unroll
         for (int t = 0; t < PPL; ++t) {
             const int pi = l + kGroup * t;
-            ev[2 * t] = pi < pairs ? a.e[2 * pi] : 0.0;
-            ev[2 * t + 1] = pi < pairs ? a.e[2 * pi + 1] : 0.0;
+            ev[2 * t] = pi < pairs ? esrc[2 * pi] : 0.0;
+            ev[2 * t + 1] = pi < pairs ? esrc[2 * pi + 1] : 0.0;
         }
         int i = wgrp;
         for (int tile = blockIdx.x + wgrp * gridDim.x; tile < ntiles; tile += kOpWH * gridDim.x, i += kOpWH) {
@@ -1944,10 +2076,10 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
                     const double si = sv ? ss[lr] : 0.0;
                     const double zi = si + sum;
                     if (lean) {
-                        // p = z + beta p (two_level.hpp:182, the fma of GPupd)
+                        // p = z + beta p (two_level.hpp:182, the fma of GPupd);
+                        // s.As is summed by the stencil warps, (W e).(A s) = e.v
+                        // from this CTA's column sums of v below
                         zout[r0 + lr] = lean == 1 ? fma(lbeta, ps[lr], zi) : zi;
-                        rz[0] = fma(si, ar, rz[0]);   // s.As
-                        rz[1] = fma(sum, ar, rz[1]);  // (W e).(A s) = e.v
                     } else {
                         zout[r0 + lr] = zi;
                         rz[0] = fma(rr, zi, rz[0]);
@@ -1959,20 +2091,28 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
         }
     }
     {
-        __shared__ double cs[(op_threads_max(PPL) / 32) * 2 * kGroup * PPL];
         const long long G = gridDim.x;
         cta_columns<PPL>(au, cs, ld, a.opart);
-        cta_columns<PPL>(av, cs, ld, a.opart + ld * G);
+        if (lean) cta_columns<PPL>(av, cs, ld, a.opart + ld * G, lean == 1 ? lsm + 3 * (ld + 2) : a.e, &rz[1]);
+        else cta_columns<PPL>(av, cs, ld, a.opart + ld * G);
     }
     double tot[2];
     if (grid_reduce<2>(rz, a.partials, &st->counter[kTkProlong], tot) && threadIdx.x == 0) {
         if (lean) {
             // p.Ap = z.Az - beta r.z / alpha_prev (exact-arithmetic identities of CG:
             // z_i.A p_{i-1} = -r.z_i / alpha_{i-1}, p_{i-1}.A p_{i-1} = r.z_{i-1} / alpha_{i-1})
-            const double zaz = tot[0] + 2.0 * tot[1] + st->lean_eme;
-            const double pap = lean == 1 ? zaz - lbeta * st->rz_new / st->alpha : zaz;
+            // the coarse step's scalars (this CTA's copy; the prologue: k_lean_init's)
+            const double eme = lean == 1 ? lsc[0] : st->lean_eme;
+            const double gnew = lean == 1 ? lsc[1] : st->rz_new;
+            const double bnew = lean == 1 ? lsc[2] : 0.0;
+            const double aold = st->alpha;
+            const double zaz = tot[0] + 2.0 * tot[1] + eme;
+            const double pap = lean == 1 ? zaz - bnew * gnew / aold : zaz;
             st->pap_pred = pap;
-            st->alpha = st->rz_new / pap;
+            st->alpha_prev = aold;
+            st->alpha = gnew / pap;
+            st->beta = bnew;
+            st->rz_new = gnew;
             if (ctl) loop_ctl_lean(st, h, ctl == 2);
         } else {
             st->rz_new = tot[0];
@@ -2208,12 +2348,22 @@ struct OpSpmvUpd {
     double* r;
     double* a_hist;
     double alpha;
+    // the last CTA's scalars, loaded at kernel start (not after the grid sum)
+    double pap_pred, bnorm, delta, drift0;
+    long long hidx, itv;
     __device__ __forceinline__ void init(const SolveArgs& a) {
         p = a.p0;
         x = a.x;
         r = a.r;
         a_hist = a.hist;
-        alpha = a.st->alpha;
+        const PcgState* st = a.st;
+        alpha = st->alpha;
+        pap_pred = st->pap_pred;
+        bnorm = st->bnorm;
+        delta = st->delta;
+        drift0 = st->pap_drift;
+        itv = st->it;
+        hidx = itv - st->hist_base;
     }
     __device__ __forceinline__ double operator()(int j) const { return p[j]; }
     struct Pre {
@@ -2239,103 +2389,24 @@ struct OpSpmvUpd {
             return;
         }
         // guard: the alpha this kernel used came from the predicted p.Ap
-        double dev = fabs(st->pap_pred - pap) / pap;
+        double dev = fabs(pap_pred - pap) / pap;
         if (!(dev == dev) || dev > 1e300) dev = 1e300;
-        if (dev > st->pap_drift) st->pap_drift = dev;
+        if (dev > drift0) st->pap_drift = dev;
         if (dev > 1e-6) {  // the prediction broke down: stop, the host re-runs on the folded cycle
             st->done = 1;
             return;
         }
-        const double rel = sqrt(tot[1]) / st->bnorm;
+        const double rel = sqrt(tot[1]) / bnorm;
         st->rr = tot[1];
         st->last_rel = rel;
-        a_hist[st->it - st->hist_base] = rel;
-        st->iterations = st->it + 1;
-        if (rel < st->delta) {
+        a_hist[hidx] = rel;
+        st->iterations = itv + 1;
+        if (rel < delta) {
             st->converged = 1;
             st->done = 1;
         }
     }
 };
-
-// The last CTA of the lean sweep kernel (whole CTA; rs = r.s when this kernel
-// wrote the final s, `fin`): the one-pass restriction recurrence
-// c = u_i - alpha_i (v_i + M e_i + beta_i (u_{i-1} - u_i) / alpha_{i-1}) with its
-// guard (as onepass_last), e = A_c^-1 c, then M e, c.e and e.M e for the pass
-// that follows, and (fin) r.z = r.s + c.e -> beta.
-__device__ void lean_last(const SolveArgs& a, double rs, bool fin) {
-    PcgState* st = a.st;
-    __shared__ double es[kOnePassK + 2], gs[kOnePassK + 2], cs[kOnePassK + 2];
-    __shared__ double dots[2];
-    const int k = a.k, ld = a.k + (a.k & 1);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const bool first = st->first != 0;
-    const double alpha = st->alpha, beta = st->beta, alpha_prev = st->alpha_prev;
-    const int ucur = (int)(st->it & 1) * ld, uprev = ld - ucur;
-    __threadfence();
-    if (!first) {
-        __shared__ double dred[2][32];
-        double d = 0.0, um = 0.0;
-        for (int j = threadIdx.x; j < k; j += blockDim.x) {
-            const double u = __ldcg(a.ow + ucur + j);
-            d = fmax(d, fabs(__ldcg(a.ow + 3 * ld + j) - u));
-            um = fmax(um, fabs(u));
-        }
-        for (int o = 16; o; o >>= 1) {
-            d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
-            um = fmax(um, __shfl_xor_sync(0xffffffffu, um, o));
-        }
-        if (lane == 0) {
-            dred[0][warp] = d;
-            dred[1][warp] = um;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
-                d = fmax(d, dred[0][w]);
-                um = fmax(um, dred[1][w]);
-            }
-            const double drift = um > 0.0 ? d / um : 0.0;
-            st->drift_max = fmax(st->drift_max, drift);
-        }
-    }
-    for (int j = threadIdx.x; j < k; j += blockDim.x) {
-        const double u = __ldcg(a.ow + ucur + j);
-        double g = __ldcg(a.ow + 2 * ld + j) + __ldcg(a.ow + 4 * ld + j);  // v + M e
-        if (!first) g = fma(beta, (__ldcg(a.ow + uprev + j) - u) / alpha_prev, g);  // + beta W^T q_{i-1}
-        const double c = fma(-alpha, g, u);                                 // c = u - alpha g
-        cs[j] = c;
-        gs[j] = c;  // the substitutions overwrite their right-hand side
-        a.ow[3 * ld + j] = c;  // compared with the direct u_{i+1} next iteration
-    }
-    __syncthreads();
-    if (a.Ainv) coarse_apply_inverse(a.Ainv, k, gs, es);
-    else if (warp == 0) coarse_solve_warp(a.L, k, gs, es);
-    __syncthreads();
-    for (int j = threadIdx.x; j < ld; j += blockDim.x) a.e[j] = j < k ? es[j] : 0.0;  // padded column = 0
-    coarse_apply_inverse(a.M, k, es, gs);  // M e_{i+1}
-    __syncthreads();
-    for (int j = threadIdx.x; j < k; j += blockDim.x) a.ow[4 * ld + j] = gs[j];
-    if (warp == 0) {
-        double ce = 0.0, eme = 0.0;
-        for (int j = lane; j < k; j += 32) {
-            ce = fma(cs[j], es[j], ce);
-            eme = fma(es[j], gs[j], eme);
-        }
-        ce = warp_sum(ce);
-        eme = warp_sum(eme);
-        if (lane == 0) {
-            st->lean_ce = ce;
-            st->lean_eme = eme;
-            st->alpha_prev = alpha;
-            if (fin) {
-                const double g = rs + ce;
-                st->beta = g / st->rz;
-                st->rz_new = g;
-            }
-        }
-    }
-}
 
 // s = S_2(r) = s1 + w D^-1 (r - A s1), s1 = w D^-1 r (the arithmetic of
 // OpUpdSweep on the residual OpSpmvUpd wrote), r.s, and the lean hooks
@@ -2344,7 +2415,6 @@ struct OpSweepLean {
     static constexpr int NV = 1;
     static constexpr int TICKET = kTkUpdate;
     static constexpr bool CTA_HOOKS = true;
-    bool fin;  // T = 2: this s is the final one
     const double* r;
     const double* wd;
     double* sout;
@@ -2368,8 +2438,9 @@ struct OpSweepLean {
     }
     __device__ __forceinline__ void row(int i, double y, double* s) const { row(i, y, s, pre(i)); }
     __device__ __forceinline__ void cta_pre(const SolveArgs& a) const { onepass_colsums(a); }
+    // r.s (of this s: the last sweep's r.s replaces it when T > 2)
     __device__ __forceinline__ void cta_last(const SolveArgs& a, const double* tot) const {
-        lean_last(a, tot[0], fin);
+        if (threadIdx.x == 0) a.st->rz_new = tot[0];
     }
     __device__ __forceinline__ void finish(PcgState*, const double*) const {}
 };
@@ -3093,6 +3164,9 @@ static void launch_op_tma(const LaunchCtx& c, void (*f)(KArgs...), long long nti
     klaunch(c, f, (int)g, threads, smem, std::forward<Args>(args)...);
 }
 
+// The ring may take what the 227 KB of a CTA leave beside the kernel's static
+// shared arrays (column sums, the lean coarse step, the grid reduction: < 12 KB).
+constexpr size_t kOpRingBudget = 215 * 1024;
 // stages of the one-pass prolongation's ring that fit the budget
 static int op_fit(const SolveArgs& a, size_t budget) {
     const int ld = a.k + (a.k & 1);
@@ -3106,13 +3180,13 @@ static void prolong_onepass_ppl(const LaunchCtx& c, const SolveArgs& a, const do
     const int ld = a.k + (a.k & 1);
     // as many stages as fit, a multiple of the stencil pair count P
     const int tnz = a.dia.kind ? -1 : (kOpTR == 64 ? a.tile_nnz64 : a.tile_nnz128);
-    // The ring may take 224 KB (of the 227 KB a CTA can have; the static
-    // shared arrays of the column sums and the grid reduction fit beside it):
-    // at C4 that is 6 stages instead of 4 (measured 371 -> 361 us per launch,
-    // 2 175 -> 2 223 iterations/s at the same capped clock).
+    // The ring may take kOpRingBudget (of the 227 KB a CTA can have, less the
+    // static shared arrays): at C4 that is 6 stages instead of the 4 of a
+    // 200 KB budget (measured 371 -> 361 us per launch, 2 175 -> 2 223
+    // iterations/s at the same capped clock).
     // NLSP_OP_BUDGET (KB) overrides it for A/B runs.
     static const size_t budget = std::getenv("NLSP_OP_BUDGET") ? (size_t)std::atoi(std::getenv("NLSP_OP_BUDGET")) * 1024
-                                                               : (size_t)224 * 1024;
+                                                               : kOpRingBudget;
     int fit = (int)((budget - 256) / op_stage_bytes(ld, tnz));
     if (fit > kOpMaxStages) fit = kOpMaxStages;
     if (NLSP_OP_STAGES > 0 && fit > NLSP_OP_STAGES) fit = NLSP_OP_STAGES;
@@ -3263,7 +3337,7 @@ bool lean_supported(const SolveArgs& a, unsigned long long T) {
     static const bool off = std::getenv("NLSP_LEAN") && std::atoi(std::getenv("NLSP_LEAN")) == 0;
     if (off || !NLSP_OP_TMA || a.k > kOnePassK || T < 2 || (T & 1)) return false;
     if (!(a.dia.kind || spmv_tma_ok(a))) return false;
-    return op_fit(a, (size_t)224 * 1024) >= 2;
+    return op_fit(a, kOpRingBudget) >= 2;
 }
 
 // K1: q = A p in the gather, x += alpha p, r -= alpha q, ||r|| and p.q
@@ -3275,10 +3349,9 @@ void launch_spmv_upd(const LaunchCtx& c, const SolveArgs& a) {
 
 // K2 (+ the later sweeps of T > 2): s = S_T(r), r.s, the coarse step; returns s
 const double* launch_lean_sweeps(const LaunchCtx& c, const SolveArgs& a, unsigned long long T) {
-    const bool fin = T == 2;
-    if (a.dia.kind && a.wdc != 0.0) launch_dia_op<1>(c, a, OpSweepLean<true>{fin});
-    else if (a.dia.kind) launch_dia_op<1>(c, a, OpSweepLean<false>{fin});
-    else launch_spmv_op<1>(c, a, OpSweepLean<false>{fin});
+    if (a.dia.kind && a.wdc != 0.0) launch_dia_op<1>(c, a, OpSweepLean<true>{});
+    else if (a.dia.kind) launch_dia_op<1>(c, a, OpSweepLean<false>{});
+    else launch_spmv_op<1>(c, a, OpSweepLean<false>{});
     count(c);
     double* cur = a.zt0;
     for (unsigned long long j = 3; j <= T; ++j) {
@@ -3286,14 +3359,14 @@ const double* launch_lean_sweeps(const LaunchCtx& c, const SolveArgs& a, unsigne
         const GPlain gp{cur};
         const bool last = j == T;
         if (a.dia.kind && a.wdc != 0.0) {
-            if (last) launch_dia_op<1>(c, a, OpSweep<GPlain, true, true>{gp, a.r, a.wd, nxt, a.wdc, false, true});
-            else launch_dia_op<1>(c, a, OpSweep<GPlain, false, true>{gp, a.r, a.wd, nxt, a.wdc, false, false});
+            if (last) launch_dia_op<1>(c, a, OpSweep<GPlain, true, true>{gp, a.r, a.wd, nxt, a.wdc});
+            else launch_dia_op<1>(c, a, OpSweep<GPlain, false, true>{gp, a.r, a.wd, nxt, a.wdc});
         } else if (a.dia.kind) {
-            if (last) launch_dia_op<1>(c, a, OpSweep<GPlain, true>{gp, a.r, a.wd, nxt, 0.0, false, true});
-            else launch_dia_op<1>(c, a, OpSweep<GPlain, false>{gp, a.r, a.wd, nxt, 0.0, false, false});
+            if (last) launch_dia_op<1>(c, a, OpSweep<GPlain, true>{gp, a.r, a.wd, nxt});
+            else launch_dia_op<1>(c, a, OpSweep<GPlain, false>{gp, a.r, a.wd, nxt});
         } else {
-            if (last) launch_spmv_op<1>(c, a, OpSweep<GPlain, true>{gp, a.r, a.wd, nxt, 0.0, false, true});
-            else launch_spmv_op<1>(c, a, OpSweep<GPlain, false>{gp, a.r, a.wd, nxt, 0.0, false, false});
+            if (last) launch_spmv_op<1>(c, a, OpSweep<GPlain, true>{gp, a.r, a.wd, nxt});
+            else launch_spmv_op<1>(c, a, OpSweep<GPlain, false>{gp, a.r, a.wd, nxt});
         }
         count(c);
         cur = nxt;
