@@ -180,6 +180,8 @@ def byte_model(n, nnz, k, nu1, nu2, pass_bytes=None, cycle="onepass", const_wd=F
         # (A + 16n, + w when not constant), t - 2 later sweeps, and the pass over W
         # that writes p = s + W e + beta p (W, A for A s, s, r, p; writes p)
         pro = 8.0 * n * ld + csr + 32.0 * n
+        if fused_sweeps:  # all t sweeps in one line march: A, r; writes s_t
+            return (csr + 40.0 * n) + (csr + 16.0 * n) + pro
         return (csr + 40.0 * n) + (csr + (16.0 + wd) * n) + (t - 2) * (csr + (24.0 + wd) * n) + pro
     if cycle == "onepass":
         pro = 8.0 * n * ld + ((csr + 24.0 * n) if t >= 1 else 16.0 * n)
@@ -381,10 +383,10 @@ def run_ours(args, dist: Dist):
     dk = kernels[dominant]
     fmt_kind, fmt_offsets, pass_bytes = dcsr.format()
     cycle = m.cycle()
+    fused_sweeps = "update_sweeps_fused" in kernels or "sweeps_fused_lean" in kernels
     if cycle == "literal":
         bytes_iter = bytes_iter_csr = byte_model_literal(pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2)
     else:
-        fused_sweeps = "update_sweeps_fused" in kernels
         bytes_iter = byte_model(pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2, pass_bytes, cycle, fmt_kind == 1,
                                 fused_sweeps)
         bytes_iter_csr = byte_model(pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2, None, cycle)
@@ -397,7 +399,7 @@ def run_ours(args, dist: Dist):
                 "iteration": {"bytes_per_iter": bytes_iter, "achieved": round(iter_gbs, 1),
                               "frac": round(iter_gbs / peak, 4),
                               "cycle": cycle,
-                              "sweeps": "fused line march" if "update_sweeps_fused" in kernels else "separate kernels",
+                              "sweeps": "fused line march" if fused_sweeps else "separate kernels",
                               "separate_sweeps_bytes_per_iter": byte_model(
                                   pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2, pass_bytes, cycle, fmt_kind == 1)
                               if cycle != "literal" else None,

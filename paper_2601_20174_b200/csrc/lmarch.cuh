@@ -69,7 +69,12 @@ constexpr int kFusedSSlots = 4;  // s_1 .. s_NS
 #ifndef NLSP_LFUSED_MINB
 #define NLSP_LFUSED_MINB 8
 #endif
-template <int PAT, typename MT, int NS, int D>
+// LEAN (the lean cycle, solve_kernels.cu): the residual was already updated by
+// OpSpmvUpd, so stage 0 only reads r and the mask and nothing but s_T is
+// written (16 n bytes per iteration where the separate lean sweeps move
+// 16 n + (T - 2) 24 n); the reduction is r.s_T, and the CTA hooks are
+// OpSweepLean's.
+template <int PAT, typename MT, int NS, int D, bool LEAN = false>
 __global__ void __launch_bounds__(128, NLSP_LFUSED_MINB) k_lfused(SolveArgs a, OpUpdSweep<true> op, LineGeom g) {
     static_assert(NS >= 1 && 2 * NS + 2 <= kFusedSlots, "ring depth");
     pdl_entry();
@@ -93,11 +98,14 @@ __global__ void __launch_bounds__(128, NLSP_LFUSED_MINB) k_lfused(SolveArgs a, O
         double r, q, x, p;
         unsigned m;
     };
+    const double* rsrc = LEAN ? a.r : op.rc;
     auto load_line = [&](Raw& v, int row) {
-        v.r = op.rc[row];
-        v.q = op.q[row];
-        v.x = op.x[row];
-        v.p = op.p[row];
+        v.r = rsrc[row];
+        if (!LEAN) {
+            v.q = op.q[row];
+            v.x = op.x[row];
+            v.p = op.p[row];
+        }
         v.m = mask[row];
     };
 
@@ -175,9 +183,13 @@ __global__ void __launch_bounds__(128, NLSP_LFUSED_MINB) k_lfused(SolveArgs a, O
                                 for (int tt = 0; tt < PAT; ++tt)
                                     if ((m >> tt) & 1u) y = fma(a.dia.val[tt], gv[tt], y);
                             }
-                            zo = fma(wc, ringR[b8[k]] - y, own[k - 1][1]);
+                            const double rk = ringR[b8[k]];
+                            zo = fma(wc, rk - y, own[k - 1][1]);
                             if (k < NS) ringS[k * kFusedSSlots * W + b4[(4 * NS - 2 * k) & 3]] = zo;
-                            else if (evaluates) op.sout[orow] = zo;
+                            else if (evaluates) {
+                                op.sout[orow] = zo;
+                                if (LEAN) s[0] = fma(rk, zo, s[0]);  // r.s_T
+                            }
                         }
                         if (k < NS) {  // every step pushes (a line outside the stage's range: a placeholder)
                             own[k][0] = own[k][1];
@@ -187,7 +199,7 @@ __global__ void __launch_bounds__(128, NLSP_LFUSED_MINB) k_lfused(SolveArgs a, O
                     }
                     // ---- stage 0: r' = r - alpha q, s_1 = w r', x' = x + alpha p
                     {
-                        const double rn = fma(-alpha, v.q, v.r);
+                        const double rn = LEAN ? v.r : fma(-alpha, v.q, v.r);
                         const double s1 = wc * rn;
                         own[0][0] = own[0][1];
                         own[0][1] = own[0][2];
@@ -196,7 +208,7 @@ __global__ void __launch_bounds__(128, NLSP_LFUSED_MINB) k_lfused(SolveArgs a, O
                             ringS[b4[0]] = s1;
                             ringR[b8[0]] = rn;
                             ringM[b8[0]] = (MT)v.m;
-                            if (evaluates && (unsigned)(A0 - la) < (unsigned)(lb - la)) {
+                            if (!LEAN && evaluates && (unsigned)(A0 - la) < (unsigned)(lb - la)) {
                                 const int row = orow + 2 * NS * g.Lw;
                                 op.rn[row] = rn;
                                 op.x[row] = fma(alpha, v.p, v.x);
@@ -212,6 +224,9 @@ __global__ void __launch_bounds__(128, NLSP_LFUSED_MINB) k_lfused(SolveArgs a, O
         t += lb - la;
     }
     double v[1] = {s[0]}, tot[1];
-    op.cta_pre(a);
-    if (grid_reduce<1>(v, a.partials, &st->counter[kTkUpdate], tot)) op.cta_last(a, tot);
+    op.cta_pre(a);  // the column sums of the last pass over W (both cycles)
+    if (grid_reduce<1>(v, a.partials, &st->counter[kTkUpdate], tot)) {
+        if (!LEAN) op.cta_last(a, tot);
+        else if (threadIdx.x == 0) st->rz_new = tot[0];
+    }
 }

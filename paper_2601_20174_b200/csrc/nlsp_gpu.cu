@@ -97,7 +97,8 @@ void launch_col_axpy(const LaunchCtx&, long long, int, const double*, int, doubl
 void launch_col_move(const LaunchCtx&, long long, int, double*, int, double*, const double*, int, long long);
 void launch_transpose(const LaunchCtx&, long long, int, const double*, double*);
 bool march_planned(const LaunchCtx&, const SolveArgs&);
-bool launch_lfused(const LaunchCtx&, const SolveArgs&, unsigned long long);
+bool launch_lfused(const LaunchCtx&, const SolveArgs&, unsigned long long, bool);
+int lfused_pattern(const SolveArgs&, unsigned long long);
 void launch_s0_scatter(const LaunchCtx&, const double*, long long, long long, int, const int*, double*);
 void launch_mt_stream(const LaunchCtx&, unsigned long long*, long long, int, const unsigned long long*, int,
                       unsigned long long, unsigned long long, unsigned long long*, unsigned long long*);
@@ -2025,7 +2026,7 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
     const double csr = 12.0 * nnz + 4.0 * (n + 1);
     const double pass = (double)a->pass_bytes;  // CSR, or the diagonal form when detected
     // algorithmic bytes per launch; slots by name below
-    enum { kSpmvP = 0, kUpd, kRes, kPro, kPost, kUR, kSmooth, kCtl, kUO, kPO, kUS, kUSF, kSU, kSL, kPL, kSlots };
+    enum { kSpmvP = 0, kUpd, kRes, kPro, kPost, kUR, kSmooth, kCtl, kUO, kPO, kUS, kUSF, kSU, kSL, kPL, kSLF, kSL1, kSlots };
     const bool onepass = mode == 0 && m->onepass;
     const unsigned long long T = m ? m->nu1 + m->nu2 : 0;
     std::vector<Acc> acc = {
@@ -2051,6 +2052,11 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
         {"sweep_lean", pass + (args.wdc != 0.0 ? 16.0 : 24.0) * n},
         // ... W, A (A s), s, r, p; writes p
         {"prolong_lean", 8.0 * n * k + pass + 32.0 * n},
+        // ... all T sweeps in one line march: A, r; writes s_T
+        {"sweeps_fused_lean", pass + 16.0 * n},
+        // ... separate kernels at T > 2: the T - 1 launches together
+        {"sweeps_lean", (double)(T > 1 ? T - 1 : 1) * pass + (args.wdc != 0.0 ? 16.0 : 24.0) * n +
+                            (double)(T > 2 ? T - 2 : 0) * (args.wdc != 0.0 ? 24.0 : 32.0) * n},
     };
     if ((int)acc.size() != kSlots) return -1;
     std::vector<cudaEvent_t> evs(2);
@@ -2072,11 +2078,8 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
         if (lean) {
             timed(kSU, [&] { launch_spmv_upd(ctx->lc, args); });
             const double* sv = nullptr;
-            if (T == 2) {
-                timed(kSL, [&] { sv = launch_lean_sweeps(ctx->lc, args, T); });
-            } else {  // the T - 1 sweep launches together
-                timed(kSmooth, [&] { sv = launch_lean_sweeps(ctx->lc, args, T); });
-            }
+            const int slot = (T > 2 && lfused_pattern(args, T)) ? kSLF : (T == 2 ? kSL : kSL1);
+            timed(slot, [&] { sv = launch_lean_sweeps(ctx->lc, args, T); });
             timed(kPL, [&] { launch_prolong_onepass(ctx->lc, args, sv, ctx->p0, 0, 1, 0, 1); });
             continue;
         }
@@ -2084,7 +2087,7 @@ int nlsp_pcg_profile(nlsp_ctx* ctx, const nlsp_csr* a, int kind, const nlsp_twol
         bool fused = false;
         if (onepass && update_sweep_ok(args, T)) {
             cudaEventRecord(evs[0], ctx->s);
-            fused = launch_lfused(ctx->lc, args, T);
+            fused = launch_lfused(ctx->lc, args, T, false);
             if (fused) {
                 cudaEventRecord(evs[1], ctx->s);
                 cudaEventSynchronize(evs[1]);

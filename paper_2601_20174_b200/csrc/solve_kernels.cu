@@ -2792,26 +2792,32 @@ static bool line_pattern_ok(const SolveArgs& a, long long Lw) {
 
 // The x/r update and all T sweeps in one line march (k_lfused): 2D
 // constant-coefficient patterns, T = 2 or 4. NLSP_LFUSED=0 keeps the separate kernels.
-bool launch_lfused(const LaunchCtx& c, const SolveArgs& a, unsigned long long T) {
+// whether the fused line march runs on this matrix (0, or its pattern: 5 / 9)
+int lfused_pattern(const SolveArgs& a, unsigned long long T) {
     static const int on = lmarch_env("NLSP_LFUSED", NLSP_LFUSED_DEFAULT);
-    if (!on || a.dia.kind != 1 || a.wdc == 0.0 || (T != 2 && T != 4) || a.dia.plane <= 0 || a.dia.halo > 2) return false;
-    if (a.n < (1 << 16)) return false;
+    if (!on || a.dia.kind != 1 || a.wdc == 0.0 || (T != 2 && T != 4) || a.dia.plane <= 0 || a.dia.halo > 2) return 0;
+    if (a.n < (1 << 16)) return 0;
     const long long Lw = a.dia.plane;
-    if (Lw < 128 || a.n % Lw) return false;
+    if (Lw < 128 || a.n % Lw) return 0;
+    if (a.n / Lw < 4 * ((long long)T - 1) + 4) return 0;
+    if (line_pattern_ok<9>(a, Lw)) return 9;
+    if (line_pattern_ok<5>(a, Lw)) return 5;
+    return 0;
+}
+
+bool launch_lfused(const LaunchCtx& c, const SolveArgs& a, unsigned long long T, bool lean) {
+    const int pat = lfused_pattern(a, T);
+    if (!pat) return false;
+    const long long Lw = a.dia.plane;
     LineGeom g{};
     g.Lw = (int)Lw;
     g.NL = (int)(a.n / Lw);
-    int pat = 0;
-    if (line_pattern_ok<9>(a, Lw)) pat = 9;
-    else if (line_pattern_ok<5>(a, Lw)) pat = 5;
-    else return false;
     const int NS = (int)T - 1;
     // slabs of 128 columns, overlapping by pad columns on either side
     g.C = 128;
     g.pad = 4;  // >= NS: a slab's valid columns move in by one per stencil stage
     g.Ci = g.C - 2 * g.pad;
     g.S = (int)((Lw + g.Ci - 1) / g.Ci);
-    if (g.NL < 4 * NS + 4) return false;
     static const int ctas = lmarch_env("NLSP_LFUSED_CTAS", 0);
     const int mb = pat == 9 ? 2 : 1;
     const size_t smem = (size_t)(NS * kFusedSSlots + kFusedSlots) * (g.C + 2) * sizeof(double) +
@@ -2841,7 +2847,7 @@ bool launch_lfused(const LaunchCtx& c, const SolveArgs& a, unsigned long long T)
         if (G > kMaxGrid) G = kMaxGrid;
         klaunch(c, kern, (int)G, g.C, smem, a, OpUpdSweep<true>{}, g);
     };
-#define NLSP_LF_GO(PAT, MT, NSS) go(k_lfused<PAT, MT, NSS, 2>)
+#define NLSP_LF_GO(PAT, MT, NSS) do { if (lean) go(k_lfused<PAT, MT, NSS, 2, true>); else go(k_lfused<PAT, MT, NSS, 2, false>); } while (0)
     if (pat == 9 && NS == 3) NLSP_LF_GO(9, unsigned short, 3);
     else if (pat == 9) NLSP_LF_GO(9, unsigned short, 1);
     else if (NS == 3) NLSP_LF_GO(5, unsigned char, 3);
@@ -3309,7 +3315,7 @@ void launch_onepass_tail(const LaunchCtx& c, const SolveArgs& a, unsigned long l
 // one iteration after k_spmv_p: fused update + sweeps (T = 2) when possible
 void launch_onepass_iteration_tail(const LaunchCtx& c, const SolveArgs& a, unsigned long long T,
                                    cudaGraphConditionalHandle h, int ctl) {
-    if (update_sweep_ok(a, T) && launch_lfused(c, a, T)) {  // s_T -> zt0
+    if (update_sweep_ok(a, T) && launch_lfused(c, a, T, false)) {  // s_T -> zt0
         launch_prolong_onepass(c, a, a.zt0, a.z, h, ctl, 1, 0);
         return;
     }
@@ -3349,6 +3355,9 @@ void launch_spmv_upd(const LaunchCtx& c, const SolveArgs& a) {
 
 // K2 (+ the later sweeps of T > 2): s = S_T(r), r.s, the coarse step; returns s
 const double* launch_lean_sweeps(const LaunchCtx& c, const SolveArgs& a, unsigned long long T) {
+    // all T sweeps in one line march: s_T -> zt0 (T = 2 stays the direct kernel:
+    // one sweep pair has nothing to chain, measured 290 vs 297 us at C1 2048^2)
+    if (T > 2 && launch_lfused(c, a, T, true)) return a.zt0;
     if (a.dia.kind && a.wdc != 0.0) launch_dia_op<1>(c, a, OpSweepLean<true>{});
     else if (a.dia.kind) launch_dia_op<1>(c, a, OpSweepLean<false>{});
     else launch_spmv_op<1>(c, a, OpSweepLean<false>{});
