@@ -64,7 +64,9 @@ typedef struct {
     uint64_t d2h_bytes;            /* device->host bytes copied by the call          */
     double onepass_drift;          /* one-pass cycle guard: max over the solve of
                                       |c_rec - W^T r|_inf / |W^T r|_inf, the restriction's
-                                      recurrence against its direct value */
+                                      recurrence against its direct value; on
+                                      the lean cycle the larger of that and
+                                      |p.Ap predicted - direct| / direct               */
     int32_t cycle_fallback;        /* 1: the drift passed NLSP_DRIFT_TOL (default 1e-10)
                                       and the solve was re-run on the folded cycle        */
     int32_t reserved;
@@ -176,7 +178,9 @@ void nlsp_twolevel_dims(const nlsp_twolevel* m, uint64_t* n, uint64_t* k);
  * different pass structure): 0 literal (two_level.hpp:60-81 op by op), 1 folded
  * (W1 = G^nu1 P, W2 = G^nu2 P streamed twice per iteration), 2 one-pass (nu1 ==
  * nu2, k <= 64: W streamed once per iteration, the restriction by its
- * recurrence). NLSP_CYCLE=literal|folded selects the first two. */
+ * recurrence), 3 lean one-pass (nu1 == nu2 >= 1: beta known before and alpha
+ * right after the pass, q = A p never stored; the default where it applies).
+ * NLSP_CYCLE=literal|folded|onepass selects the first three. */
 int nlsp_twolevel_cycle(const nlsp_twolevel* m);
 /* basis_ (n x k), Cholesky factor L (k x k, lower), A_c (k x k); any may be NULL */
 nlsp_status nlsp_twolevel_export(nlsp_ctx* ctx, const nlsp_twolevel* m, double* basis,
