@@ -997,8 +997,11 @@ __global__ void __launch_bounds__(kThreads, NLSP_DIA_MINB) k_spmv_dia(SolveArgs 
 // SKIP: 0 never, 1 when st->done (solve kernels), 2 when st->error (true residual)
 // G lanes per row (transposed mapping), U row steps per warp and tile:
 // TR = 8 warps * U * (32 / G) rows per staged tile.
+#ifndef NLSP_SPMV_MINB
+#define NLSP_SPMV_MINB 3
+#endif
 template <int G, int U, int S, int SKIP, int CHW, class Op>
-__global__ void __launch_bounds__(kTmaThreads) k_spmv_tma(SolveArgs a, Op op) {
+__global__ void __launch_bounds__(kTmaThreads, NLSP_SPMV_MINB) k_spmv_tma(SolveArgs a, Op op) {
     pdl_entry();
     constexpr int R = 32 / G;
     constexpr int TR = kConsumerWarps * U * R;
@@ -1036,13 +1039,23 @@ __global__ void __launch_bounds__(kTmaThreads) k_spmv_tma(SolveArgs a, Op op) {
             int lr[U];
             bool valid[U];
             double y[U];
+            // own-row operands in flight with the tile's gathers (lanes < R hold
+            // rows (warp U + u) R + lane, as staged_rows_dot numbers them)
+            typename Op::Pre pr[U];
+            if (lane < R) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int lrow = (warp * U + u) * R + lane;
+                    if (lrow < rows) pr[u] = op.pre(r0 + lrow);
+                }
+            }
             staged_rows_dot<G, U, CH>(stages + stg * L.bytes, L, rows, warp, lane, op, lr, valid, y);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stg]);
             if (lane < R) {
 #pragma unroll
                 for (int u = 0; u < U; ++u)
-                    if (valid[u]) op.row(r0 + lr[u], y[u], s);
+                    if (valid[u]) op.row(r0 + lr[u], y[u], s, pr[u]);
             }
         }
     }
@@ -1996,7 +2009,23 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
                     const int a0 = rps[0], s0 = a0 & ~1, c0 = a0 & ~3;
                     const int b = rps[lr], e = rps[lr + 1];
                     NLSP_CHECK(b >= a0 && e >= b && e - s0 <= tile_nnz + 2 && e - c0 <= tile_nnz + 8);
-                    for (int kk = b; kk < e; ++kk) y = fma(vs[kk - s0], sv[cs_[kk - c0]], y);
+                    // 8 nonzeros per step: their staged values / columns and the
+                    // gathers of s issued together, then the fma chain in column
+                    // order (a rolled loop waits one L2 latency per nonzero:
+                    // the stencil warps were the pass's bottleneck at C5)
+                    for (int kk = b; kk < e; kk += 8) {
+                        double vv[8], xx[8];
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) {
+                            const int q = kk + c;
+                            const bool on = q < e;
+                            vv[c] = on ? vs[q - s0] : 0.0;
+                            xx[c] = on ? sv[cs_[q - c0]] : 0.0;
+                        }
+#pragma unroll
+                        for (int c = 0; c < 8; ++c)
+                            if (kk + c < e) y = fma(vv[c], xx[c], y);
+                    }
                 } else {
                     unsigned m;
                     const unsigned char* ms = base + m_off;
@@ -2604,8 +2633,13 @@ void launch_init_ctl(const LaunchCtx& c, PcgState* st) {
 #ifndef NLSP_TMA
 #define NLSP_TMA 1
 #endif
+// 2 stages of 256-row tiles: two CTAs (16 consumer warps) per SM instead of one
+// with 3 stages — the staged SpMV family is latency-bound (ncu at C5: 14 %
+// occupancy, 65 % of the stalls on the gathers). Measured at C5, us per
+// iteration: 3 stages 141.6; 2 stages 125.1, with the register cap of 3 CTAs
+// 119.8; 2 lanes per row (128-row tiles) 122.0-123.9; 4 lanes 134.0.
 #ifndef NLSP_SPMV_STAGES
-#define NLSP_SPMV_STAGES 3
+#define NLSP_SPMV_STAGES 2
 #endif
 #ifndef NLSP_RESTRICT_STAGES
 #define NLSP_RESTRICT_STAGES 2
