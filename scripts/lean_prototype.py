@@ -108,10 +108,13 @@ def main(name="C3", nx=256, k=48, nu=2):
     x1, i1, h1 = folded()
     x2, i2, h2, dev, canc = lean()
     m = min(len(h1), len(h2))
+    out = {"n": n, "folded": i1, "lean": i2, "x_diff": float(np.linalg.norm(x2 - x1) / np.linalg.norm(x1)),
+           "hist_dev": float(np.max(np.abs(h2[:m] - h1[:m]) / h1[:m])), "pap_dev": float(dev), "cancellation": float(canc)}
     print(f"{name} n={n} iterations folded={i1} lean={i2} "
           f"rel x diff={np.linalg.norm(x2 - x1) / np.linalg.norm(x1):.2e} "
           f"history dev={np.max(np.abs(h2[:m] - h1[:m]) / h1[:m]):.2e} "
           f"max rel dev of p.Ap={dev:.2e} max cancellation={canc:.1f}")
+    return out
 
 
 if __name__ == "__main__":
