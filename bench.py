@@ -405,7 +405,7 @@ def run_ours(args, dist: Dist):
                               if cycle != "literal" else None,
                               "folded_cycle_bytes_per_iter": byte_model(
                                   pb.n, pb.nnz, cfg.k, cfg.nu1, cfg.nu2, pass_bytes, "folded", fmt_kind == 1),
-                              "matrix_form": ["csr", "diagonal-constant", "diagonal-values"][fmt_kind],
+                              "matrix_form": ["csr", "diagonal-constant", "diagonal-values", "csr-implicit-columns"][fmt_kind],
                               "matrix_offsets": fmt_offsets, "matrix_bytes_per_pass": pass_bytes,
                               "csr_model_bytes_per_iter": bytes_iter_csr,
                               "literal_schedule_bytes_per_iter": byte_model_literal(

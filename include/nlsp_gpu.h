@@ -95,9 +95,13 @@ void nlsp_csr_dims(const nlsp_csr* a, uint64_t* n, uint64_t* nnz);
 /* The device form the solve kernels stream (no reference
  * counterpart): kind 0 = CSR; 1 = diagonal form with one value per offset
  * (constant-coefficient stencil: per-row presence bits only); 2 = diagonal
- * form with per-row values. `offsets` = number of distinct column offsets
- * (kinds 1, 2), `pass_bytes` = matrix bytes one SpMV pass reads (the byte
- * model of the roofline). Detected at nlsp_csr_upload; NLSP_DIA=0 keeps CSR.
+ * form with per-row values; 3 = CSR rows with implicit columns (a banded
+ * matrix with too many absent offsets for kind 2: row_ptr and values as they
+ * are, one 32-bit presence mask per row in place of the column indices).
+ * `offsets` = number of distinct column offsets (kinds 1, 2, 3), `pass_bytes`
+ * = matrix bytes one SpMV pass of the PCG loop reads (the byte model of the
+ * roofline). Detected at nlsp_csr_upload; NLSP_DIA=0 keeps CSR; kind 3 is
+ * opt-in (NLSP_PACK=1: measured slower than explicit columns).
  * Results are bitwise those of the CSR kernels (same per-row fma order). */
 nlsp_status nlsp_csr_format(const nlsp_csr* a, int* kind, int* offsets, uint64_t* pass_bytes);
 /* The structured-grid geometry of the diagonal form (no reference

@@ -80,6 +80,20 @@ struct DiaArgs {
     int halo;
 };
 
+// Implicit-column form of a CSR matrix (nlsp_gpu.cu detect_dia): a banded
+// matrix whose stored entries sit at d <= 32 fixed offsets from the row, but
+// with varying values and too many absent offsets for the value slab of the
+// diagonal form to pay (C5: 13 of 21 offsets stored per row). The CSR row_ptr
+// and values stay as they are; the column indices (4 B per nonzero) are
+// replaced by one 32-bit presence mask per row: the j-th stored entry of row i
+// is at column i + off[t_j], t_j the j-th set bit. Same entries in the same
+// order, so every row sum is bitwise the CSR one. mask == nullptr: not in use.
+struct PackArgs {
+    int d;
+    int off[kMaxDia];
+    const unsigned* mask;
+};
+
 // Everything a solve kernel needs, passed by value.
 struct SolveArgs {
     int n;
@@ -121,6 +135,7 @@ struct SolveArgs {
     double* ow;
     double* opart;
     DiaArgs dia;         // diagonal form of A (dia.kind == 0: CSR kernels)
+    PackArgs pk;         // implicit-column form of the CSR arrays (pk.mask == nullptr: explicit columns)
 };
 
 constexpr int kColsignPerSm = 8;  // CTAs per SM of the column-sign scan

@@ -1000,8 +1000,11 @@ __global__ void __launch_bounds__(kThreads, NLSP_DIA_MINB) k_spmv_dia(SolveArgs 
 #ifndef NLSP_SPMV_MINB
 #define NLSP_SPMV_MINB 3
 #endif
-template <int G, int U, int S, int SKIP, int CHW, class Op>
+// MK: the implicit-column form (PackArgs; one lane per row): the producer stages
+// the rows' presence masks in place of the column indices
+template <int G, int U, int S, int SKIP, int CHW, class Op, bool MK = false>
 __global__ void __launch_bounds__(kTmaThreads, NLSP_SPMV_MINB) k_spmv_tma(SolveArgs a, Op op) {
+    static_assert(!MK || G == 1, "implicit columns: one lane per row");
     pdl_entry();
     constexpr int R = 32 / G;
     constexpr int TR = kConsumerWarps * U * R;
@@ -1016,6 +1019,8 @@ __global__ void __launch_bounds__(kTmaThreads, NLSP_SPMV_MINB) k_spmv_tma(SolveA
     unsigned long long* empty = full + S;
     unsigned char* stages = smem + 128;
     const StageLayout L(TR, tile_nnz_for(a, TR), 0, false);
+    __shared__ int pko[MK ? kMaxDia : 1];
+    if (MK && threadIdx.x < kMaxDia) pko[threadIdx.x] = a.pk.off[threadIdx.x];
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
@@ -1029,7 +1034,7 @@ __global__ void __launch_bounds__(kTmaThreads, NLSP_SPMV_MINB) k_spmv_tma(SolveA
     double s[Op::NV > 0 ? Op::NV : 1];
     for (int j = 0; j < (Op::NV > 0 ? Op::NV : 1); ++j) s[j] = 0.0;
     if (warp == kConsumerWarps) {
-        produce_tiles<S>(a.rp, a.ci, a.v, nullptr, 0, a.n, TR, stages, L, full, empty);
+        produce_tiles<S>(a.rp, a.ci, a.v, nullptr, 0, a.n, TR, stages, L, full, empty, MK ? a.pk.mask : nullptr);
     } else {
         int i = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
@@ -1049,7 +1054,8 @@ __global__ void __launch_bounds__(kTmaThreads, NLSP_SPMV_MINB) k_spmv_tma(SolveA
                     if (lrow < rows) pr[u] = op.pre(r0 + lrow);
                 }
             }
-            staged_rows_dot<G, U, CH>(stages + stg * L.bytes, L, rows, warp, lane, op, lr, valid, y);
+            if constexpr (MK) staged_rows_dot_masked<U, CH>(stages + stg * L.bytes, L, rows, r0, warp, lane, op, pko, lr, valid, y);
+            else staged_rows_dot<G, U, CH>(stages + stg * L.bytes, L, rows, warp, lane, op, lr, valid, y);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stg]);
             if (lane < R) {
@@ -1895,6 +1901,11 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
     const unsigned rp_off = p_off + kOpVec;
     const unsigned v_off = rp_off + round16((kOpTR + 4) * 4);
     const unsigned c_off = v_off + round16((tile_nnz + 2) * 8);
+    // CSR rows with implicit columns (PackArgs): the rows' masks are staged in
+    // the column region, the offsets sit in shared memory
+    const bool mk = MAXD == 0 && a.pk.mask != nullptr;
+    __shared__ int pko[MAXD == 0 ? kMaxDia : 1];
+    if (MAXD == 0 && mk && threadIdx.x < kMaxDia) pko[threadIdx.x] = a.pk.off[threadIdx.x];
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
@@ -1967,7 +1978,7 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
                     c0 = a0 & ~3;
                     cb = ((rows + 1 + 3) & ~3) * 4;
                     cvb = ((a1 - s0 + 1) & ~1) * 8;
-                    ccb = ((a1 - c0 + 3) & ~3) * 4;
+                    ccb = mk ? ((rows + 3) & ~3) * 4 : ((a1 - c0 + 3) & ~3) * 4;
                 }
                 NLSP_CHECK(rows > 0 && rows <= kOpTR && a1 >= a0 && a1 - a0 <= tile_nnz);
                 NLSP_CHECK(MAXD != 0 || (rp_off + cb <= v_off && v_off + cvb <= c_off && c_off + ccb <= sbytes));
@@ -1982,7 +1993,8 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
                 if (MAXD == 0) {
                     bulk_g2s(base_s + rp_off, a.rp + r0, cb, &full[stg]);
                     if (cvb) bulk_g2s(base_s + v_off, a.v + s0, cvb, &full[stg]);
-                    if (ccb) bulk_g2s(base_s + c_off, a.ci + c0, ccb, &full[stg]);
+                    if (ccb && mk) bulk_g2s(base_s + c_off, a.pk.mask + r0, ccb, &full[stg]);
+                    else if (ccb) bulk_g2s(base_s + c_off, a.ci + c0, ccb, &full[stg]);
                 }
             }
         }
@@ -2013,6 +2025,7 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
                     // gathers of s issued together, then the fma chain in column
                     // order (a rolled loop waits one L2 latency per nonzero:
                     // the stencil warps were the pass's bottleneck at C5)
+                    unsigned pm = mk ? reinterpret_cast<const unsigned*>(cs_)[lr] : 0u;
                     for (int kk = b; kk < e; kk += 8) {
                         double vv[8], xx[8];
 #pragma unroll
@@ -2020,7 +2033,16 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
                             const int q = kk + c;
                             const bool on = q < e;
                             vv[c] = on ? vs[q - s0] : 0.0;
-                            xx[c] = on ? sv[cs_[q - c0]] : 0.0;
+                            int col = 0;
+                            if (on) {
+                                if (mk) {  // the next set bit of the row's mask
+                                    col = row + pko[__ffs(pm) - 1];
+                                    pm &= pm - 1u;
+                                } else {
+                                    col = cs_[q - c0];
+                                }
+                            }
+                            xx[c] = on ? sv[col] : 0.0;
                         }
 #pragma unroll
                         for (int c = 0; c < 8; ++c)
@@ -2671,6 +2693,14 @@ void launch_spmv_op(const LaunchCtx& c, const SolveArgs& a, const Op& op) {
     const int need = (a.max_row + G - 1) / G;
     const long long nt = spmv_tiles(a);
     const size_t sm = spmv_stage_smem(a);
+    if constexpr (G == 1) {
+        if (a.pk.mask) {  // implicit columns
+            if (need <= 8) launch_tma(c, k_spmv_tma<G, U, S, SKIP, 8, Op, true>, nt, sm, a, op);
+            else if (need <= 12) launch_tma(c, k_spmv_tma<G, U, S, SKIP, 12, Op, true>, nt, sm, a, op);
+            else launch_tma(c, k_spmv_tma<G, U, S, SKIP, 16, Op, true>, nt, sm, a, op);
+            return;
+        }
+    }
     if (need <= 8) launch_tma(c, k_spmv_tma<G, U, S, SKIP, 8, Op>, nt, sm, a, op);
     else if (need <= 12) launch_tma(c, k_spmv_tma<G, U, S, SKIP, 12, Op>, nt, sm, a, op);
     else launch_tma(c, k_spmv_tma<G, U, S, SKIP, 16, Op>, nt, sm, a, op);

@@ -78,13 +78,15 @@ __device__ __forceinline__ void stage_tile(const int* __restrict__ rp, const int
                                            const double* __restrict__ v,
                                            const double* __restrict__ P, int ld, int n, int TR,
                                            int tile, int a0, int a1, unsigned char* stage_base,
-                                           const StageLayout& L, unsigned long long* full) {
+                                           const StageLayout& L, unsigned long long* full,
+                                           const unsigned* __restrict__ pmask = nullptr) {
     const int r0 = tile * TR;
     const int rows = min(TR, n - r0);
     const int s0 = a0 & ~1, c0 = a0 & ~3;
     const unsigned rbytes = ((rows + 1 + 3) & ~3) * 4;
     const unsigned vbytes = ((a1 - s0 + 1) & ~1) * 8;
-    const unsigned cbytes = ((a1 - c0 + 3) & ~3) * 4;
+    // implicit columns (PackArgs): the rows' presence masks go where the column indices would
+    const unsigned cbytes = pmask ? ((rows + 3) & ~3) * 4 : ((a1 - c0 + 3) & ~3) * 4;
     const unsigned pbytes = P ? (unsigned)rows * ld * 8 : 0u;
     NLSP_CHECK(rows > 0 && rows <= TR && a0 >= 0 && a1 >= a0);
     NLSP_CHECK(L.rp_off + rbytes <= L.v_off && L.v_off + vbytes <= L.c_off);
@@ -92,7 +94,10 @@ __device__ __forceinline__ void stage_tile(const int* __restrict__ rp, const int
     mbar_arrive_tx(full, rbytes + vbytes + cbytes + pbytes);
     bulk_g2s(stage_base + L.rp_off, rp + r0, rbytes, full);
     if (vbytes) bulk_g2s(stage_base + L.v_off, v + s0, vbytes, full);
-    if (cbytes) bulk_g2s(stage_base + L.c_off, ci + c0, cbytes, full);
+    if (cbytes) {
+        if (pmask) bulk_g2s(stage_base + L.c_off, pmask + r0, cbytes, full);
+        else bulk_g2s(stage_base + L.c_off, ci + c0, cbytes, full);
+    }
     if (pbytes) bulk_g2s(stage_base + L.p_off, P + (long long)r0 * ld, pbytes, full);
 }
 
@@ -105,7 +110,8 @@ __device__ __forceinline__ void produce_tiles(const int* __restrict__ rp, const 
                                               const double* __restrict__ v,
                                               const double* __restrict__ P, int ld, int n, int TR,
                                               unsigned char* stages, const StageLayout& L,
-                                              unsigned long long* full, unsigned long long* empty) {
+                                              unsigned long long* full, unsigned long long* empty,
+                                              const unsigned* __restrict__ pmask = nullptr) {
     const int lane = threadIdx.x & 31;
     const int ntiles = (n + TR - 1) / TR;
     for (int base = 0;; base += 32) {
@@ -127,7 +133,7 @@ __device__ __forceinline__ void produce_tiles(const int* __restrict__ rp, const 
                 const int stg = i % S;
                 if (i >= S) mbar_wait(&empty[stg], ((i / S) - 1) & 1);
                 stage_tile(rp, ci, v, P, ld, n, TR, (int)tile, a0, a1, stages + stg * L.bytes, L,
-                           &full[stg]);
+                           &full[stg], pmask);
             }
             __syncwarp();
         }
@@ -186,6 +192,57 @@ __device__ __forceinline__ void staged_rows_dot(const unsigned char* stage_base,
     for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int m = R; m < 32; m <<= 1) y[u] += __shfl_xor_sync(0xffffffffu, y[u], m);
+}
+
+// The same for the implicit-column form (PackArgs, internal.cuh; one lane per
+// row): the staged column region holds the rows' presence masks, the j-th
+// nonzero of row i is at column i + offs[t_j], t_j the j-th set bit of its mask.
+// offs: the offsets in shared memory. Same values in the same order: y is
+// bitwise the explicit-column result.
+template <int U, int CH, class Gat>
+__device__ __forceinline__ void staged_rows_dot_masked(const unsigned char* stage_base,
+                                                       const StageLayout& L, int rows, int r0, int warp,
+                                                       int lane, const Gat& g, const int* offs,
+                                                       int (&lr)[U], bool (&valid)[U], double (&y)[U]) {
+    const int* rps = reinterpret_cast<const int*>(stage_base + L.rp_off);
+    const double* vs = reinterpret_cast<const double*>(stage_base + L.v_off);
+    const unsigned* ms = reinterpret_cast<const unsigned*>(stage_base + L.c_off);
+    const int s0 = rps[0] & ~1;
+    int b[U], e[U];
+    unsigned m[U];
+    int len = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        lr[u] = (warp * U + u) * 32 + lane;
+        valid[u] = lr[u] < rows;
+        b[u] = valid[u] ? rps[lr[u]] : 0;
+        e[u] = valid[u] ? rps[lr[u] + 1] : 0;
+        m[u] = valid[u] ? ms[lr[u]] : 0u;
+        len = max(len, e[u] - b[u]);
+        y[u] = 0.0;
+    }
+    for (int off = 0; off < len; off += CH) {
+        double vv[U][CH], xv[U][CH];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                const int k = b[u] + off + c;
+                vv[u][c] = 0.0;
+                xv[u][c] = 0.0;
+                if (k < e[u]) {
+                    const int t = __ffs(m[u]) - 1;
+                    m[u] &= m[u] - 1u;
+                    NLSP_CHECK(t >= 0);
+                    vv[u][c] = vs[k - s0];
+                    xv[u][c] = g(r0 + lr[u] + offs[t]);
+                }
+            }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int c = 0; c < CH; ++c) y[u] = fma(vv[u][c], xv[u][c], y[u]);  // absent: + 0 * 0, as above
+    }
 }
 
 // Consumer side: y[u] = sum_k v_k g(col_k) for the U local rows lr[u] of this

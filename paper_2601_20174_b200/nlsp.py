@@ -256,7 +256,8 @@ class DeviceCsr:
 
     def format(self):
         """(kind, offsets, pass_bytes) of nlsp_csr_format: 0 CSR, 1 constant
-        diagonal form, 2 diagonal form with per-row values."""
+        diagonal form, 2 diagonal form with per-row values, 3 CSR with implicit
+        columns (one presence mask per row in place of the column indices)."""
         kind, offs, pb = C.c_int32(0), C.c_int32(0), C.c_uint64(0)
         _check(self.ctx, L.gpu_lib().nlsp_csr_format(self.handle, C.byref(kind), C.byref(offs), C.byref(pb)))
         return int(kind.value), int(offs.value), int(pb.value)

@@ -52,6 +52,8 @@ PATHS = {
     "cluster_chol": {"NLSP_CLUSTER": "1", "NLSP_COARSE": "chol"},
     # the SpMV family over CSR instead of the detected diagonal form
     "graph_csr": {"NLSP_CLUSTER": "0", "NLSP_DIA": "0"},
+    # CSR rows with implicit columns (opt-in; scaled_C5 and the banded FEM case qualify)
+    "graph_pack": {"NLSP_CLUSTER": "0", "NLSP_PACK": "1"},
     # the residual history kept in device segments of 16 entries: the loop
     # pauses at every segment end and resumes from the device state (graph:
     # the continuation graph; host: the stream loop; the cluster solver cannot
@@ -95,6 +97,9 @@ def test_execution_paths_match_reference(tmp_path, case):
     # the diagonal form sums every row in CSR column order: bitwise the CSR path
     assert res["graph"][0]["iterations"] == res["graph_csr"][0]["iterations"]
     assert np.array_equal(res["graph"][1], res["graph_csr"][1])
+    # implicit columns: the same entries in the same order
+    assert res["graph"][0]["iterations"] == res["graph_pack"][0]["iterations"]
+    assert np.array_equal(res["graph"][1], res["graph_pack"][1])
     # the plane-march gather kernels (forced at this size): the same rows, the
     # dot products summed in another order
     assert abs(res["march"][0]["iterations"] - res["onepass"][0]["iterations"]) <= 1
@@ -129,6 +134,14 @@ def test_detected_matrix_form(nlsp, case):
     a = csr_from_golden(d)
     kind, offsets, pass_bytes = a.device().format()
     assert kind == EXPECTED_FORM[case]
+    if case in ("scaled_C5", "fem_diffusion"):  # banded with varying values: implicit columns on request
+        os.environ["NLSP_PACK"] = "1"
+        try:
+            k3, o3, pb3 = csr_from_golden(d).device().format()
+        finally:
+            os.environ.pop("NLSP_PACK", None)
+        assert k3 == 3 and 0 < o3 <= 32
+        assert pb3 == 8 * a.nnz() + 4 * (a.dim() + 1) + 4 * a.dim() < pass_bytes
     n, nnz = a.dim(), a.nnz()
     if kind == 0:
         assert pass_bytes == 12 * nnz + 4 * (n + 1)
