@@ -1765,6 +1765,7 @@ __device__ __noinline__ void lean_coarse_step(const LeanCoarse a, int t, double*
     double* es = sc + 3 * (ld + 2);
     double* gs = sc + 4 * (ld + 2);
     const int i = t >> 2, sub = t & 3, lane = t & 31, w = t >> 5;
+    NLSP_CHECK(t >= 0 && t < 256 && k <= kOnePassK && 5 * (ld + 2) <= 5 * (kOnePassK + 2));
     // A_c^-1 and M rows (L2 resident): in flight with everything else
     double ai[kOnePassK / 4], mi[kOnePassK / 4];
 #pragma unroll
@@ -1982,6 +1983,7 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
                 }
                 NLSP_CHECK(rows > 0 && rows <= kOpTR && a1 >= a0 && a1 - a0 <= tile_nnz);
                 NLSP_CHECK(MAXD != 0 || (rp_off + cb <= v_off && v_off + cvb <= c_off && c_off + ccb <= sbytes));
+                NLSP_CHECK(p_off + vb <= rp_off && as_off + kOpVec <= p_off);
                 mbar_arrive_tx(&full[stg], wb + (sv ? vb : 0u) + vb + mbb + cb + cvb + ccb + (lean == 1 ? vb : 0u));
                 bulk_g2s(base_s, a.P + (long long)r0 * ld, wb, &full[stg]);
                 if (sv) bulk_g2s(base_s + s_off, sv + r0, vb, &full[stg]);
