@@ -1926,10 +1926,11 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
     if (warp == 0) {
         // ---- producer (diagonal form): lane 0 issues each tile's bulk copies
         if (MAXD != 0 && lane == 0) {
-            int i = 0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
-                const int stg = i % S;
-                if (i >= S) mbar_wait(&empty[stg], ((i / S) - 1) & 1);
+            // ring position by counters (i % S, i / S with a run-time S cost an
+            // emulated division per tile and warp)
+            int stg = 0, rnd = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                if (rnd > 0) mbar_wait(&empty[stg], (rnd - 1) & 1);
                 unsigned char* base_s = stages + stg * sbytes;
                 const int r0 = tile * kOpTR, rows = min(kOpTR, a.n - r0);
                 const unsigned vb = round16(rows * 8);  // vectors are padded by 16 doubles
@@ -1943,6 +1944,10 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
                 if (lean == 1) bulk_g2s(base_s + p_off, zout + r0, vb, &full[stg]);
                 bulk_g2s(base_s + m_off, static_cast<const unsigned char*>(a.dia.mask) + (long long)r0 * mb,
                          mbb, &full[stg]);
+                if (++stg == S) {
+                    stg = 0;
+                    ++rnd;
+                }
             }
         }
         // ---- producer (CSR): the 32 lanes load the row_ptr bounds of 32
@@ -2005,10 +2010,9 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
         // chain in column order (bitwise the SpMV family's row sums)
         const int pair = (warp - 1) >> 1;
         const int lr0 = ((warp - 1) & 1) * 32 + lane;
-        int i = pair;
-        for (int tile = blockIdx.x + pair * gridDim.x; tile < ntiles; tile += P * gridDim.x, i += P) {
-            const int stg = i % S;
-            mbar_wait(&full[stg], (i / S) & 1);
+        int stg = pair % S, rnd = pair / S;
+        for (int tile = blockIdx.x + pair * gridDim.x; tile < ntiles; tile += P * gridDim.x) {
+            mbar_wait(&full[stg], rnd & 1);
             unsigned char* base = stages + stg * sbytes;
             const int r0 = tile * kOpTR, rows = min(kOpTR, a.n - r0);
             for (int lr = lr0; lr < kOpTR; lr += 64) {
@@ -2074,6 +2078,11 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&asr[stg]);
+            stg += P;  // P <= S
+            if (stg >= S) {
+                stg -= S;
+                ++rnd;
+            }
         }
     } else {
         // ---- W-product warps: 8 lanes per row, 2 rows per group per tile
@@ -2093,11 +2102,10 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
             ev[2 * t] = pi < pairs ? esrc[2 * pi] : 0.0;
             ev[2 * t + 1] = pi < pairs ? esrc[2 * pi + 1] : 0.0;
         }
-        int i = wgrp;
-        for (int tile = blockIdx.x + wgrp * gridDim.x; tile < ntiles; tile += kOpWH * gridDim.x, i += kOpWH) {
-            const int stg = i % S;
-            mbar_wait(&full[stg], (i / S) & 1);
-            mbar_wait(&asr[stg], (i / S) & 1);
+        int stg = wgrp % S, rnd = wgrp / S;
+        for (int tile = blockIdx.x + wgrp * gridDim.x; tile < ntiles; tile += kOpWH * gridDim.x) {
+            mbar_wait(&full[stg], rnd & 1);
+            mbar_wait(&asr[stg], rnd & 1);
             const unsigned char* base = stages + stg * sbytes;
             const int r0 = tile * kOpTR, rows = min(kOpTR, a.n - r0);
             const double* ss = reinterpret_cast<const double*>(base + s_off);
@@ -2141,6 +2149,11 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stg]);
+            stg += kOpWH;  // kOpWH <= S
+            if (stg >= S) {
+                stg -= S;
+                ++rnd;
+            }
         }
     }
     {

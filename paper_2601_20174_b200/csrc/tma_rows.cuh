@@ -34,15 +34,31 @@ __device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, unsigned b
 __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
+// try_wait with a suspend-time hint (ns): the waiting thread is parked until
+// the phase completes or the hint runs out, instead of the short
+// system-dependent limit. ncu source counters of the lean pass at C4 without
+// it: 18.7 M SYNCS + 17.5 M YIELD for 1.2 M completed waits, a third of the
+// kernel's instructions spent polling. NLSP_MBAR_HINT=0 compiles the plain form.
+#ifndef NLSP_MBAR_HINT
+#define NLSP_MBAR_HINT 20000
+#endif
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned phase) {
     const unsigned addr = smem_u32(b);
     unsigned ok = 0;
     do {
+#if NLSP_MBAR_HINT > 0
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+            : "=r"(ok)
+            : "r"(addr), "r"(phase), "r"((unsigned)NLSP_MBAR_HINT)
+            : "memory");
+#else
         asm volatile(
             "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
             : "=r"(ok)
             : "r"(addr), "r"(phase)
             : "memory");
+#endif
     } while (!ok);
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
