@@ -2112,41 +2112,51 @@ __global__ void __launch_bounds__(op_threads_max(PPL), 1) k_prolong_onepass_tma(
             const double* rs = reinterpret_cast<const double*>(base + r_off);
             const double* as = reinterpret_cast<const double*>(base + as_off);
             const double* ps = reinterpret_cast<const double*>(base + p_off);
+            // FULL: a whole tile of full-width rows (ld = 16 PPL) — no row or column
+            // predicates and a compile-time row stride (the W-product warps are the
+            // pass's critical path at the power-capped clock: ncu counted ~190
+            // instructions per warp and tile with the predicated body for ~80 of work)
+            auto wtile = [&](auto full_c) {
+                constexpr bool FULL = decltype(full_c)::value;
+                const int ldr = FULL ? 2 * kGroup * PPL : ld;
 #pragma unroll
-            for (int u = 0; u < kOpTR / (WPG * 4); ++u) {
-                const int lr = grp + WPG * 4 * u;
-                const bool ok = lr < rows;  // every lane still runs the group shuffles
-                const double* wrow = reinterpret_cast<const double*>(base) + lr * ld;
-                const double rr = ok ? rs[lr] : 0.0, ar = ok ? as[lr] : 0.0;
-                double part = 0.0;
+                for (int u = 0; u < kOpTR / (WPG * 4); ++u) {
+                    const int lr = grp + WPG * 4 * u;
+                    const bool ok = FULL || lr < rows;  // every lane still runs the group shuffles
+                    const double* wrow = reinterpret_cast<const double*>(base) + lr * ldr;
+                    const double rr = ok ? rs[lr] : 0.0, ar = ok ? as[lr] : 0.0;
+                    double part = 0.0;
 #pragma unroll
-                for (int t = 0; t < PPL; ++t) {
-                    const int pi = l + kGroup * t;
-                    if (ok && pi < pairs) {
-                        const double2 w = *reinterpret_cast<const double2*>(wrow + 2 * pi);
-                        part = fma(w.x, ev[2 * t], part);
-                        part = fma(w.y, ev[2 * t + 1], part);
-                        au[2 * t] = fma(w.x, rr, au[2 * t]);
-                        au[2 * t + 1] = fma(w.y, rr, au[2 * t + 1]);
-                        av[2 * t] = fma(w.x, ar, av[2 * t]);
-                        av[2 * t + 1] = fma(w.y, ar, av[2 * t + 1]);
+                    for (int t = 0; t < PPL; ++t) {
+                        const int pi = l + kGroup * t;
+                        if (FULL || (ok && pi < pairs)) {
+                            const double2 w = *reinterpret_cast<const double2*>(wrow + 2 * pi);
+                            part = fma(w.x, ev[2 * t], part);
+                            part = fma(w.y, ev[2 * t + 1], part);
+                            au[2 * t] = fma(w.x, rr, au[2 * t]);
+                            au[2 * t + 1] = fma(w.y, rr, au[2 * t + 1]);
+                            av[2 * t] = fma(w.x, ar, av[2 * t]);
+                            av[2 * t + 1] = fma(w.y, ar, av[2 * t + 1]);
+                        }
+                    }
+                    const double sum = group_sum(part);
+                    if (ok && l == 0) {
+                        const double si = sv ? ss[lr] : 0.0;
+                        const double zi = si + sum;
+                        if (lean) {
+                            // p = z + beta p (two_level.hpp:182, the fma of GPupd);
+                            // s.As is summed by the stencil warps, (W e).(A s) = e.v
+                            // from this CTA's column sums of v below
+                            zout[r0 + lr] = lean == 1 ? fma(lbeta, ps[lr], zi) : zi;
+                        } else {
+                            zout[r0 + lr] = zi;
+                            rz[0] = fma(rr, zi, rz[0]);
+                        }
                     }
                 }
-                const double sum = group_sum(part);
-                if (ok && l == 0) {
-                    const double si = sv ? ss[lr] : 0.0;
-                    const double zi = si + sum;
-                    if (lean) {
-                        // p = z + beta p (two_level.hpp:182, the fma of GPupd);
-                        // s.As is summed by the stencil warps, (W e).(A s) = e.v
-                        // from this CTA's column sums of v below
-                        zout[r0 + lr] = lean == 1 ? fma(lbeta, ps[lr], zi) : zi;
-                    } else {
-                        zout[r0 + lr] = zi;
-                        rz[0] = fma(rr, zi, rz[0]);
-                    }
-                }
-            }
+            };
+            if (rows == kOpTR && pairs == kGroup * PPL) wtile(std::true_type{});
+            else wtile(std::false_type{});
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stg]);
             stg += kOpWH;  // kOpWH <= S
