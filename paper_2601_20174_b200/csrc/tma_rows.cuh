@@ -61,6 +61,22 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned phase)
 #endif
     } while (!ok);
 }
+// Wait of a warp that runs AHEAD of the critical path (the pass's stencil warps:
+// their tile's data arrives several tile-times before the W-product warps need
+// A s): sleep between polls instead of spinning (ncu: 9.9 M polls for 64 k waits).
+__device__ __forceinline__ void mbar_wait_relaxed(unsigned long long* b, unsigned phase, unsigned ns) {
+    const unsigned addr = smem_u32(b);
+    for (;;) {
+        unsigned ok = 0;
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(ok)
+            : "r"(addr), "r"(phase)
+            : "memory");
+        if (ok) break;
+        __nanosleep(ns);
+    }
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
                                          unsigned long long* bar) {
     asm volatile(
